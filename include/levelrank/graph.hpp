@@ -1,0 +1,98 @@
+// levelrank-b200 host API: graph core.
+//
+// Drop-in for the reference's proj/include/levelrank/graph.hpp:1-107 (same
+// names, argument meaning and exceptions), re-implemented for large inputs:
+// from_edges runs a multi-threaded count/scatter/sort-rows build instead of one
+// global std::sort.  Lives in levelrank::b200 (an inline namespace), so code
+// written against `levelrank::Graph` recompiles unchanged while the symbols
+// never collide with a reference build loaded in the same process.
+#pragma once
+
+#include <cstdint>
+#include <iosfwd>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace levelrank {
+inline namespace b200 {
+
+using VertexId = std::int32_t;
+using EdgeId = std::int64_t;
+
+/// graph.hpp:19 -- n = max id + 1 must fit in VertexId.
+inline constexpr VertexId kMaxVertexId = 2147483646;
+
+/// graph.hpp:23 -- Ignore drops self-loops from the walk; Keep walks them.
+enum class LoopPolicy { Ignore, Keep };
+
+class ParseError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class IoError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+/// Compressed out-adjacency, rows sorted and duplicate-free (graph.hpp:39-76).
+class Graph {
+ public:
+  Graph() = default;
+
+  /// graph.cpp:14-36 semantics: range check (std::invalid_argument), dedup,
+  /// sorted rows, loop flags.  Multi-threaded.
+  static Graph from_edges(VertexId n, std::vector<std::pair<VertexId, VertexId>> edges,
+                          LoopPolicy policy = LoopPolicy::Ignore);
+  /// Same, from two parallel arrays (no pair vector materialised).
+  static Graph from_edge_arrays(VertexId n, const VertexId* src, const VertexId* dst, EdgeId m,
+                                LoopPolicy policy = LoopPolicy::Ignore);
+  /// Adopts an existing CSR; rows must be sorted and duplicate-free
+  /// (checked, std::invalid_argument otherwise).
+  static Graph from_csr(VertexId n, std::vector<EdgeId> offsets, std::vector<VertexId> targets,
+                        LoopPolicy policy = LoopPolicy::Ignore);
+
+  [[nodiscard]] VertexId vertex_count() const noexcept { return n_; }
+  [[nodiscard]] EdgeId edge_count() const noexcept { return static_cast<EdgeId>(targets_.size()); }
+  [[nodiscard]] LoopPolicy loop_policy() const noexcept { return policy_; }
+
+  [[nodiscard]] std::span<const VertexId> out_neighbors(VertexId u) const {
+    return {targets_.data() + offsets_[u], targets_.data() + offsets_[u + 1]};
+  }
+  [[nodiscard]] VertexId out_degree(VertexId u) const {
+    return static_cast<VertexId>(offsets_[u + 1] - offsets_[u]);
+  }
+  [[nodiscard]] bool has_loop(VertexId u) const { return has_loop_[u] != 0; }
+  /// graph.hpp:61-65.
+  [[nodiscard]] VertexId walk_out_degree(VertexId u) const {
+    VertexId d = out_degree(u);
+    if (policy_ == LoopPolicy::Ignore && has_loop(u)) --d;
+    return d;
+  }
+
+  [[nodiscard]] const EdgeId* offsets_data() const noexcept { return offsets_.data(); }
+  [[nodiscard]] const VertexId* targets_data() const noexcept { return targets_.data(); }
+  [[nodiscard]] const std::uint8_t* loop_data() const noexcept { return has_loop_.data(); }
+
+ private:
+  VertexId n_ = 0;
+  std::vector<EdgeId> offsets_ = {0};
+  std::vector<VertexId> targets_;
+  std::vector<std::uint8_t> has_loop_;
+  LoopPolicy policy_ = LoopPolicy::Ignore;
+};
+
+/// graph.cpp:54-99: "src<TAB>dst" lines, '#' comments, LF/CRLF; dense ids or
+/// compaction in sorted order.  ParseError on malformed or empty input.
+Graph parse_edge_list(std::istream& in, bool dense_ids, LoopPolicy policy = LoopPolicy::Ignore);
+/// graph.cpp:101-105; IoError if the file cannot be opened.
+Graph load_edge_list(const std::string& path, bool dense_ids, LoopPolicy policy = LoopPolicy::Ignore);
+
+/// Worker threads used by the host builders (LR_THREADS env var, else
+/// hardware concurrency).
+int host_threads();
+
+}  // namespace b200
+}  // namespace levelrank

@@ -1,0 +1,574 @@
+// lr_ctx: device residency of one Layout and the stream-ordered level loop
+// (the GPU replacement of compute_pagerank's loop, proj/src/engine.cpp:126-158).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "lr_cuda.h"
+
+namespace lrerr {
+void set(const std::string& msg);
+}
+
+using namespace lrk;
+
+namespace {
+
+#define LR_CUDA_TRY(expr)                                                                          \
+  do {                                                                                             \
+    const cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) {                                                                       \
+      lrerr::set(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #expr);             \
+      return e_ == cudaErrorMemoryAllocation ? LR_ENOMEM : LR_ECUDA;                               \
+    }                                                                                              \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t count) {
+    reset();
+    n = count;
+    return cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+  }
+  cudaError_t upload(const T* src, size_t count, cudaStream_t s) {
+    cudaError_t e = alloc(count);
+    if (e != cudaSuccess || count == 0) return e;
+    return cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s);
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+struct LevelTasks {
+  int rb = 0, re = 0;
+  int cac_w0 = 0, cac_w1 = 0;  // warp-per-CAC tasks
+  int cac_b0 = 0, cac_b1 = 0;  // CTA-per-CAC tasks
+  int sm0 = 0, sm1 = 0, sm_max = 0;
+  int lc0 = 0, lc1 = 0, lc_max = 0;
+  int gu0 = 0, gu1 = 0;
+  int bk0 = 0, bk1 = 0;
+};
+
+}  // namespace
+
+struct lr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int n = 0;
+  int n_levels = 0;
+  int64_t n_units = 0;
+  bool loaded = false;
+  std::vector<LevelTasks> lt;
+  // layout
+  DevBuf<int> vertex_of, row_of, deg, xsrc, isrc, depth_ptr;
+  DevBuf<std::uint8_t> loop, rowkind;
+  DevBuf<long long> xptr, iptr;
+  // tasks
+  DevBuf<CacTask> cac;
+  DevBuf<SccTask> small, lcta;
+  DevBuf<GridUnitState> gstate;
+  DevBuf<SpmvBlock> blocks;
+  DevBuf<HeavyRow> heavy;
+  DevBuf<double> heavy_part;
+  DevBuf<int> heavy_cnt;
+  DevBuf<double> small_scratch;
+  int small_scratch_ld = 0;
+  // work
+  DevBuf<double> w, rank, s0, s1, pf, r3, r1, partial, total;
+  DevBuf<SolveParams> params;
+  DevBuf<DevStatus> status;
+  DevBuf<long long> unit_iters;
+  SolveParams* h_params = nullptr;
+  DevStatus* h_status = nullptr;
+  int nparts = 0;
+  std::vector<long long> gu_rows, gu_nnz;   // per grid unit
+  std::vector<cudaEvent_t> lev;              // per-launch event pairs (grid SpMV)
+  int64_t launches = 0;
+  int64_t spmv_launches = 0;
+
+  DeviceLayout dl() const {
+    DeviceLayout L;
+    L.n = n;
+    L.vertex_of = vertex_of.p;
+    L.row_of = row_of.p;
+    L.deg = deg.p;
+    L.loop = loop.p;
+    L.rowkind = rowkind.p;
+    L.xptr = xptr.p;
+    L.xsrc = xsrc.p;
+    L.iptr = iptr.p;
+    L.isrc = isrc.p;
+    return L;
+  }
+  ~lr_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : lev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (h_params) cudaFreeHost(h_params);
+    if (h_status) cudaFreeHost(h_status);
+  }
+};
+
+extern "C" {
+
+lr_status lr_ctx_create(int device, lr_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    lrerr::set("no CUDA device available (the levelrank-b200 solve has no CPU fallback)");
+    return LR_ECUDA;
+  }
+  if (device < 0 || device >= count) {
+    lrerr::set("CUDA device index out of range");
+    return LR_EINVAL;
+  }
+  auto* ctx = new lr_ctx;
+  ctx->device = device;
+  auto fail = [&](lr_status s) {
+    delete ctx;
+    return s;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) {
+    lrerr::set("cudaSetDevice failed");
+    return fail(LR_ECUDA);
+  }
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    lrerr::set(std::string("levelrank-b200 is built for sm_100a; found ") + prop.name);
+    return fail(LR_ECUDA);
+  }
+  if (configure_kernels() != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    lrerr::set("CUDA stream / kernel setup failed");
+    return fail(LR_ECUDA);
+  }
+  for (auto& e : ctx->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      lrerr::set("cudaEventCreate failed");
+      return fail(LR_ECUDA);
+    }
+  if (cudaMallocHost(&ctx->h_params, sizeof(SolveParams)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_status, sizeof(DevStatus)) != cudaSuccess ||
+      ctx->params.alloc(1) != cudaSuccess || ctx->status.alloc(1) != cudaSuccess) {
+    lrerr::set("CUDA allocation failed");
+    return fail(LR_ENOMEM);
+  }
+  *out = ctx;
+  return LR_OK;
+}
+
+void lr_ctx_free(lr_ctx* ctx) { delete ctx; }
+
+void* lr_ctx_stream(lr_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int64_t lr_ctx_device_bytes(const lr_ctx* c) {
+  if (!c) return 0;
+  return static_cast<int64_t>(c->vertex_of.bytes() + c->row_of.bytes() + c->deg.bytes() + c->xsrc.bytes() +
+                              c->isrc.bytes() + c->depth_ptr.bytes() + c->loop.bytes() + c->rowkind.bytes() +
+                              c->xptr.bytes() + c->iptr.bytes() + c->cac.bytes() + c->small.bytes() +
+                              c->lcta.bytes() + c->gstate.bytes() + c->blocks.bytes() + c->heavy.bytes() +
+                              c->heavy_part.bytes() + c->heavy_cnt.bytes() + c->small_scratch.bytes() +
+                              c->w.bytes() + c->rank.bytes() + c->s0.bytes() + c->s1.bytes() + c->pf.bytes() +
+                              c->r3.bytes() + c->r1.bytes() + c->partial.bytes() + c->unit_iters.bytes());
+}
+
+lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
+  if (!ctx || !L) {
+    lrerr::set("null context or layout");
+    return LR_EINVAL;
+  }
+  LR_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const int n = L->n;
+  ctx->loaded = false;
+  ctx->n = n;
+  ctx->n_levels = L->n_levels;
+  ctx->n_units = L->n_units;
+  const size_t nn = static_cast<size_t>(n);
+
+  // per-row kind
+  std::vector<std::uint8_t> rowkind(nn, kSingle);
+  std::vector<CacTask> cac_w, cac_b;
+  std::vector<SccTask> small, lcta;
+  std::vector<GridUnitState> gstate;
+  std::vector<SpmvBlock> blocks;
+  std::vector<HeavyRow> heavy;
+  long long heavy_parts = 0;
+  ctx->lt.assign(static_cast<size_t>(L->n_levels), LevelTasks{});
+  ctx->gu_rows.clear();
+  ctx->gu_nnz.clear();
+  int max_small = 0;
+  bool small_needs_scratch = false;
+  for (int li = 0; li < L->n_levels; ++li) {
+    LevelTasks& T = ctx->lt[static_cast<size_t>(li)];
+    T.rb = L->level_row_begin[li];
+    T.re = L->level_row_begin[li + 1];
+    std::vector<CacTask> lw, lb;
+    T.sm0 = static_cast<int>(small.size());
+    T.lc0 = static_cast<int>(lcta.size());
+    T.gu0 = static_cast<int>(gstate.size());
+    T.bk0 = static_cast<int>(blocks.size());
+    for (int u = L->level_unit_begin[li]; u < L->level_unit_begin[li + 1]; ++u) {
+      const int rb = L->unit_row_begin[u], re = L->unit_row_begin[u + 1];
+      const int m = re - rb;
+      const std::uint8_t kind = L->unit_kind[u];
+      std::uint8_t rk = kSingle;
+      if (kind == 1) {
+        rk = kCac;
+        const long long db = L->cac_depth_begin[u];
+        int nd = 0;
+        while (L->depth_ptr[db + nd] < re) ++nd;  // depth_ptr[db+nd] == re ends the unit
+        CacTask t{rb, re, db, nd, 0};
+        (m > kCacWarpMaxRows ? lb : lw).push_back(t);
+      } else if (kind == 2) {
+        rk = kSmall;
+        small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+        T.sm_max = std::max(T.sm_max, m);
+        max_small = std::max(max_small, m);
+        if (m > kSmallSmemMaxM) small_needs_scratch = true;
+      } else if (kind == 3) {
+        const long long nnz = L->iptr[re] - L->iptr[rb];
+        if (m <= kCtaLargeMaxRows && nnz <= kCtaLargeMaxNnz) {
+          rk = kLargeCta;
+          lcta.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+          T.lc_max = std::max(T.lc_max, m);
+        } else {
+          rk = kLargeGrid;
+          const int gu = static_cast<int>(gstate.size());
+          const size_t first_block = blocks.size();
+          int r = rb;
+          while (r < re) {
+            const long long len = L->iptr[r + 1] - L->iptr[r];
+            if (len > kSpmvNnz) {
+              const int nseg = static_cast<int>((len + kSpmvNnz - 1) / kSpmvNnz);
+              const int hid = static_cast<int>(heavy.size());
+              heavy.push_back(HeavyRow{r, nseg, heavy_parts});
+              heavy_parts += nseg;
+              for (int sg = 0; sg < nseg; ++sg) blocks.push_back(SpmvBlock{r, r + 1, gu, hid, sg});
+              ++r;
+              continue;
+            }
+            const int start = r;
+            long long acc = 0;
+            while (r < re && r - start < kSpmvRows) {
+              const long long l2 = L->iptr[r + 1] - L->iptr[r];
+              if (l2 > kSpmvNnz || acc + l2 > kSpmvNnz) break;
+              acc += l2;
+              ++r;
+            }
+            blocks.push_back(SpmvBlock{start, r, gu, -1, 0});
+          }
+          ctx->gu_rows.push_back(m);
+          ctx->gu_nnz.push_back(L->iptr[re] - L->iptr[rb]);
+          GridUnitState g{};
+          g.unit = u;
+          g.nblocks = static_cast<int>(blocks.size() - first_block);
+          g.edges = L->unit_edges[u];
+          gstate.push_back(g);
+        }
+      }
+      for (int r = rb; r < re; ++r) rowkind[static_cast<size_t>(r)] = rk;
+    }
+    T.cac_w0 = static_cast<int>(cac_w.size());
+    cac_w.insert(cac_w.end(), lw.begin(), lw.end());
+    T.cac_w1 = static_cast<int>(cac_w.size());
+    T.cac_b0 = static_cast<int>(cac_b.size());
+    cac_b.insert(cac_b.end(), lb.begin(), lb.end());
+    T.cac_b1 = static_cast<int>(cac_b.size());
+    T.sm1 = static_cast<int>(small.size());
+    T.lc1 = static_cast<int>(lcta.size());
+    T.gu1 = static_cast<int>(gstate.size());
+    T.bk1 = static_cast<int>(blocks.size());
+  }
+  // warp tasks first, then CTA tasks, in one array
+  const int nw = static_cast<int>(cac_w.size());
+  for (auto& T : ctx->lt) {
+    T.cac_b0 += nw;
+    T.cac_b1 += nw;
+  }
+  cac_w.insert(cac_w.end(), cac_b.begin(), cac_b.end());
+
+  LR_CUDA_TRY(ctx->vertex_of.upload(L->vertex_of, nn, s));
+  LR_CUDA_TRY(ctx->row_of.upload(L->row_of, nn, s));
+  LR_CUDA_TRY(ctx->deg.upload(L->deg, nn, s));
+  LR_CUDA_TRY(ctx->loop.upload(L->loop, nn, s));
+  LR_CUDA_TRY(ctx->rowkind.upload(rowkind.data(), nn, s));
+  LR_CUDA_TRY(ctx->xptr.upload(reinterpret_cast<const long long*>(L->xptr), nn + 1, s));
+  LR_CUDA_TRY(ctx->xsrc.upload(L->xsrc, static_cast<size_t>(L->nnz_cross), s));
+  LR_CUDA_TRY(ctx->iptr.upload(reinterpret_cast<const long long*>(L->iptr), nn + 1, s));
+  LR_CUDA_TRY(ctx->isrc.upload(L->isrc, static_cast<size_t>(L->nnz_intra), s));
+  LR_CUDA_TRY(ctx->depth_ptr.upload(L->depth_ptr, static_cast<size_t>(L->depth_ptr_len), s));
+  LR_CUDA_TRY(ctx->cac.upload(cac_w.data(), cac_w.size(), s));
+  LR_CUDA_TRY(ctx->small.upload(small.data(), small.size(), s));
+  LR_CUDA_TRY(ctx->lcta.upload(lcta.data(), lcta.size(), s));
+  LR_CUDA_TRY(ctx->gstate.upload(gstate.data(), gstate.size(), s));
+  LR_CUDA_TRY(ctx->blocks.upload(blocks.data(), blocks.size(), s));
+  LR_CUDA_TRY(ctx->heavy.upload(heavy.data(), heavy.size(), s));
+  LR_CUDA_TRY(ctx->heavy_part.alloc(static_cast<size_t>(heavy_parts)));
+  LR_CUDA_TRY(ctx->heavy_cnt.alloc(heavy.size()));
+  LR_CUDA_TRY(cudaMemsetAsync(ctx->heavy_cnt.p, 0, ctx->heavy_cnt.bytes(), s));
+  ctx->small_scratch.reset();
+  ctx->small_scratch_ld = max_small + 1;
+  if (small_needs_scratch) {
+    const size_t ld = static_cast<size_t>(max_small) + 1;
+    LR_CUDA_TRY(ctx->small_scratch.alloc(static_cast<size_t>(kSmallScratchBlocks) * ld * (ld + 2)));
+  }
+  LR_CUDA_TRY(ctx->w.alloc(nn));
+  LR_CUDA_TRY(ctx->rank.alloc(nn));
+  LR_CUDA_TRY(ctx->pf.alloc(nn));
+  LR_CUDA_TRY(ctx->r3.alloc(nn));
+  LR_CUDA_TRY(ctx->r1.alloc(nn));
+  const bool any_grid = !gstate.empty();
+  LR_CUDA_TRY(ctx->s0.alloc(any_grid ? nn : 0));
+  LR_CUDA_TRY(ctx->s1.alloc(any_grid ? nn : 0));
+  ctx->nparts = static_cast<int>((nn + kOutBlock - 1) / kOutBlock);
+  LR_CUDA_TRY(ctx->partial.alloc(static_cast<size_t>(std::max(ctx->nparts, 1))));
+  LR_CUDA_TRY(ctx->total.alloc(1));
+  LR_CUDA_TRY(ctx->unit_iters.alloc(static_cast<size_t>(L->n_units)));
+  LR_CUDA_TRY(cudaStreamSynchronize(s));
+  ctx->loaded = true;
+  return LR_OK;
+}
+
+static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, double tol, double* r3_dev,
+                                 double* r1_dev, lr_solve_info* info, int64_t* unit_iters) {
+  const lr_status pv = lr_validate_params(c, tol);
+  if (pv != LR_OK) return pv;
+  if (!ctx || !ctx->loaded) {
+    lrerr::set("context has no uploaded layout");
+    return LR_EINVAL;
+  }
+  LR_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const DeviceLayout L = ctx->dl();
+  ctx->h_params->c = c;
+  ctx->h_params->tol = tol;
+  ctx->h_params->cap = lr_iteration_cap(c, tol);
+  int64_t launches = 0, spmv_launches = 0;
+  float spmv_ms = 0.f;
+  double active_ms = 0.0;
+  int64_t active_launches = 0, spmv_bytes = 0, spmv_edges = 0;
+  LR_CUDA_TRY(cudaMemcpyAsync(ctx->params.p, ctx->h_params, sizeof(SolveParams), cudaMemcpyHostToDevice, s));
+  LR_CUDA_TRY(cudaMemsetAsync(ctx->status.p, 0, sizeof(DevStatus), s));
+  if (ctx->n_units > 0) LR_CUDA_TRY(cudaMemsetAsync(ctx->unit_iters.p, 0, ctx->unit_iters.bytes(), s));
+  LR_CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
+  launch_prep(L, w_dev, ctx->params.p, ctx->pf.p, ctx->status.p, s);
+  ++launches;
+  for (const LevelTasks& T : ctx->lt) {
+    launch_cross(L, T.rb, T.re, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, s);
+    ++launches;
+    if (T.cac_w1 > T.cac_w0) {
+      launch_cac(L, ctx->cac.p + T.cac_w0, T.cac_w1 - T.cac_w0, false, ctx->depth_ptr.p, ctx->params.p, ctx->rank.p, s);
+      ++launches;
+    }
+    if (T.cac_b1 > T.cac_b0) {
+      launch_cac(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, true, ctx->depth_ptr.p, ctx->params.p, ctx->rank.p, s);
+      ++launches;
+    }
+    if (T.sm1 > T.sm0) {
+      launch_small(L, ctx->small.p + T.sm0, T.sm1 - T.sm0, T.sm_max > kSmallSmemMaxM ? ctx->small_scratch_ld - 1 : T.sm_max,
+                   ctx->pf.p, ctx->rank.p, T.sm_max > kSmallSmemMaxM ? ctx->small_scratch.p : nullptr,
+                   ctx->status.p, s);
+      ++launches;
+    }
+    if (T.lc1 > T.lc0) {
+      launch_large_cta(L, ctx->lcta.p + T.lc0, T.lc1 - T.lc0, T.lc_max, ctx->params.p, ctx->pf.p, ctx->rank.p,
+                       ctx->unit_iters.p, ctx->status.p, s);
+      ++launches;
+    }
+    if (T.gu1 > T.gu0) {
+      launch_grid_reset(ctx->gstate.p + T.gu0, T.gu1 - T.gu0, ctx->status.p, s);
+      ++launches;
+      LR_CUDA_TRY(cudaEventRecord(ctx->ev[2], s));
+      long long k = 0;
+      const long long cap = ctx->h_params->cap;
+      int batch = 4;
+      for (;;) {
+        for (int j = 0; j < batch; ++j) {
+          ++k;
+          const double* sin = (k & 1) ? ctx->s0.p : ctx->s1.p;
+          double* sout = (k & 1) ? ctx->s1.p : ctx->s0.p;
+          while (ctx->lev.size() < static_cast<size_t>(2 * k)) {
+            cudaEvent_t e;
+            LR_CUDA_TRY(cudaEventCreate(&e));
+            ctx->lev.push_back(e);
+          }
+          LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 2)], s));
+          launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
+                           ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
+                           ctx->status.p, s);
+          LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 1)], s));
+          ++launches;
+          ++spmv_launches;
+        }
+        LR_CUDA_TRY(cudaMemcpyAsync(&ctx->h_status->active, &ctx->status.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LR_CUDA_TRY(cudaStreamSynchronize(s));
+        if (ctx->h_status->active <= 0 || k > cap + 2) break;
+        batch = std::min(16, batch * 2);
+      }
+      LR_CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
+      LR_CUDA_TRY(cudaEventSynchronize(ctx->ev[3]));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+      spmv_ms += ms;
+      // roofline bookkeeping: per-unit iteration counts of this level
+      const int ngu = T.gu1 - T.gu0;
+      std::vector<GridUnitState> gsh(static_cast<size_t>(ngu));
+      LR_CUDA_TRY(cudaMemcpy(gsh.data(), ctx->gstate.p + T.gu0, sizeof(GridUnitState) * ngu, cudaMemcpyDeviceToHost));
+      long long kmax = 0;
+      for (int i = 0; i < ngu; ++i) {
+        const long long it = gsh[static_cast<size_t>(i)].iterations;
+        kmax = std::max(kmax, it);
+        spmv_bytes += it * (12 * ctx->gu_nnz[static_cast<size_t>(T.gu0 + i)] + 32 * ctx->gu_rows[static_cast<size_t>(T.gu0 + i)]);
+        spmv_edges += it * ctx->gu_nnz[static_cast<size_t>(T.gu0 + i)];
+      }
+      for (long long j = 0; j < std::min(kmax, k); ++j) {
+        float lm = 0.f;
+        cudaEventElapsedTime(&lm, ctx->lev[static_cast<size_t>(2 * j)], ctx->lev[static_cast<size_t>(2 * j + 1)]);
+        active_ms += lm;
+      }
+      active_launches += std::min(kmax, k);
+    }
+  }
+  launch_output(L, ctx->rank.p, r3_dev, ctx->partial.p, ctx->nparts, s);
+  launch_normalize(r3_dev, r1_dev, ctx->n, ctx->partial.p, ctx->nparts, ctx->total.p, s);
+  launches += 2 + (r1_dev ? 1 : 0);
+  LR_CUDA_TRY(cudaGetLastError());
+  LR_CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
+  LR_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  if (unit_iters && ctx->n_units > 0)
+    LR_CUDA_TRY(cudaMemcpyAsync(unit_iters, ctx->unit_iters.p, ctx->unit_iters.bytes(), cudaMemcpyDeviceToHost, s));
+  LR_CUDA_TRY(cudaStreamSynchronize(s));
+  float dev_ms = 0.f;
+  cudaEventElapsedTime(&dev_ms, ctx->ev[0], ctx->ev[1]);
+  ctx->launches += launches;
+  ctx->spmv_launches += spmv_launches;
+  const DevStatus& st = *ctx->h_status;
+  if (info) {
+    info->total_iterations = st.total_iterations;
+    info->iterative_edge_work = st.iterative_edge_work;
+    info->all_weights_zero = st.wmax_bits == 0ull;
+    info->n_devices = 1;
+    info->device_ms = dev_ms;
+    info->spmv_ms = spmv_ms;
+    info->spmv_launches = spmv_launches;
+    info->kernel_launches = launches;
+    info->spmv_active_launches = active_launches;
+    info->spmv_active_ms = active_ms;
+    info->spmv_bytes = spmv_bytes;
+    info->spmv_edges = spmv_edges;
+  }
+  if (st.err & kErrNegW) {
+    lrerr::set("weights must be non-negative");
+    return LR_EINVAL;
+  }
+  if (st.err & kErrNoConv) {
+    lrerr::set("power series failed to converge");
+    return LR_ENOCONV;
+  }
+  if (st.err & kErrDegen) {
+    lrerr::set("dense solve degenerated numerically");
+    return LR_EDEGEN;
+  }
+  return LR_OK;
+}
+
+lr_status lr_solve_device(lr_ctx* ctx, const double* w_dev, double c, double tol, double* r3_dev, double* r1_dev,
+                          lr_solve_info* info, int64_t* unit_iters) {
+  return solve_on_device(ctx, w_dev, c, tol, r3_dev, r1_dev, info, unit_iters);
+}
+
+lr_status lr_solve(lr_ctx* ctx, const double* w, double c, double tol, double* r3, double* r1, lr_solve_info* info,
+                   int64_t* unit_iters) {
+  if (!ctx || !ctx->loaded) {
+    lrerr::set("context has no uploaded layout");
+    return LR_EINVAL;
+  }
+  LR_CUDA_TRY(cudaSetDevice(ctx->device));
+  const size_t bytes = static_cast<size_t>(ctx->n) * sizeof(double);
+  if (bytes) LR_CUDA_TRY(cudaMemcpyAsync(ctx->w.p, w, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const lr_status st = solve_on_device(ctx, ctx->w.p, c, tol, ctx->r3.p, ctx->r1.p, info, unit_iters);
+  if (st != LR_OK && st != LR_ENOCONV && st != LR_EDEGEN) return st;
+  if (bytes) {
+    LR_CUDA_TRY(cudaMemcpyAsync(r3, ctx->r3.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (r1) LR_CUDA_TRY(cudaMemcpyAsync(r1, ctx->r1.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LR_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  return st;
+}
+
+lr_status lr_propagate_weights(int device, const int32_t* src, const int32_t* dst, const int32_t* deg, int64_t m,
+                               const double* ranks, int64_t n, double c, double* weights) {
+  for (int64_t i = 0; i < m; ++i)
+    if (src[i] < 0 || src[i] >= n || dst[i] < 0 || dst[i] >= n || deg[i] <= 0) {
+      lrerr::set("cross edge out of range");
+      return LR_EINVAL;
+    }
+  // stable grouping by destination (input order kept within a destination)
+  std::vector<long long> cnt(static_cast<size_t>(n) + 1, 0);
+  for (int64_t i = 0; i < m; ++i) ++cnt[static_cast<size_t>(dst[i]) + 1];
+  for (int64_t v = 0; v < n; ++v) cnt[static_cast<size_t>(v) + 1] += cnt[static_cast<size_t>(v)];
+  std::vector<int> order(static_cast<size_t>(m));
+  {
+    std::vector<long long> cur(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < m; ++i) order[static_cast<size_t>(cur[static_cast<size_t>(dst[i])]++)] = static_cast<int>(i);
+  }
+  std::vector<long long> seg;
+  for (int64_t v = 0; v < n; ++v)
+    if (cnt[static_cast<size_t>(v) + 1] > cnt[static_cast<size_t>(v)]) seg.push_back(cnt[static_cast<size_t>(v)]);
+  seg.push_back(m);
+  lr_ctx* ctx = nullptr;
+  lr_status st = lr_ctx_create(device, &ctx);
+  if (st != LR_OK) return st;
+  cudaStream_t s = ctx->stream;
+  DevBuf<int> d_src, d_dst, d_deg, d_order;
+  DevBuf<long long> d_seg;
+  DevBuf<double> d_r, d_w;
+  auto run = [&]() -> lr_status {
+    LR_CUDA_TRY(d_src.upload(src, static_cast<size_t>(m), s));
+    LR_CUDA_TRY(d_dst.upload(dst, static_cast<size_t>(m), s));
+    LR_CUDA_TRY(d_deg.upload(deg, static_cast<size_t>(m), s));
+    LR_CUDA_TRY(d_order.upload(order.data(), order.size(), s));
+    LR_CUDA_TRY(d_seg.upload(seg.data(), seg.size(), s));
+    LR_CUDA_TRY(d_r.upload(ranks, static_cast<size_t>(n), s));
+    LR_CUDA_TRY(d_w.upload(weights, static_cast<size_t>(n), s));
+    launch_propagate(d_order.p, d_seg.p, static_cast<int>(seg.size()) - 1, d_src.p, d_dst.p, d_deg.p, d_r.p, c, d_w.p, s);
+    LR_CUDA_TRY(cudaGetLastError());
+    if (n) LR_CUDA_TRY(cudaMemcpyAsync(weights, d_w.p, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LR_CUDA_TRY(cudaStreamSynchronize(s));
+    return LR_OK;
+  };
+  st = run();
+  d_src.reset();
+  d_dst.reset();
+  d_deg.reset();
+  d_order.reset();
+  d_seg.reset();
+  d_r.reset();
+  d_w.reset();
+  lr_ctx_free(ctx);
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,554 @@
+// sm_100a kernels of the level-scheduled PageRank solve.  Everything here is
+// fp64 and HBM/latency bound; no tensor cores (nothing on the path is a dense
+// contraction).  Accumulation orders are chosen so that every term and every
+// summation order matches the reference's CPU loops wherever a row is summed
+// by one thread; the file is compiled with
+// --fmad=false so no multiply-add is contracted behind our back.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace lrk {
+namespace {
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide max; `red` holds blockDim/32 doubles.  All threads get the result.
+__device__ __forceinline__ double block_max(double v, double* red) {
+  v = warp_max(v);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[warp] = v;
+  __syncthreads();
+  double m = red[0];
+  for (int i = 1; i < nw; ++i) m = fmax(m, red[i]);
+  return m;
+}
+// Block-wide sum in a fixed order (deterministic).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[warp] = v;
+  __syncthreads();
+  double s = red[0];
+  for (int i = 1; i < nw; ++i) s += red[i];
+  return s;
+}
+
+// ----------------------------------------------------------------- prep
+// Weight checks of engine.cpp:94-97,112 (negative -> error bit, max == 0 ->
+// all_weights_zero) and the per-row push factor c / walk_out_degree
+// (solvers.cpp:136-138; 0 for dangling rows, which never push).
+__global__ void k_prep(DeviceLayout L, const double* __restrict__ w, const SolveParams* __restrict__ p,
+                       double* __restrict__ pf, DevStatus* st) {
+  __shared__ double red[32];
+  const double c = p->c;
+  double wmax = 0.0;
+  bool neg = false;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
+    const double x = w[i];
+    neg |= x < 0.0;
+    wmax = fmax(wmax, x);
+    const int d = L.deg[i];
+    pf[i] = d > 0 ? c / static_cast<double>(d) : 0.0;
+  }
+  if (__syncthreads_or(neg) && threadIdx.x == 0) atomicOr(&st->err, kErrNegW);
+  const double m = block_max(wmax, red);
+  if (threadIdx.x == 0 && m > 0.0) atomicMax(&st->wmax_bits, dbits(m));
+}
+
+// ---------------------------------------------------------------- cross
+// K1: start weights of one level = w + pushes from every higher level along
+// cross edges (propagate_weights, engine.cpp:83-87, in pull form; sources are
+// final).  Per row the terms are (c * r_src) / deg_src added in the
+// reference's order (source level desc, source id asc).  Singleton rows are
+// solved here (solve_singletons, solvers.cpp:23-35); SccLarge grid rows also
+// get their first pushed value s0 = pf * w (solvers.cpp:141-150).
+__global__ void k_cross(DeviceLayout L, int row_begin, int row_end, const double* __restrict__ w,
+                        const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
+                        double* __restrict__ s0) {
+  const int row = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= row_end) return;
+  const double c = p->c;
+  double acc = w[L.vertex_of[row]];
+  const long long e1 = L.xptr[row + 1];
+  for (long long e = L.xptr[row]; e < e1; ++e) {
+    const int s = __ldg(L.xsrc + e);
+    acc += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
+  }
+  const std::uint8_t k = L.rowkind[row];
+  if (k == kSingle && L.loop[row]) acc /= 1.0 - c / static_cast<double>(L.deg[row]);
+  rank[row] = acc;
+  if (k == kLargeGrid) s0[row] = pf[row] * acc;
+}
+
+// ------------------------------------------------------------------ CAC
+// K3: one-pass topological propagation (solve_cac, solvers.cpp:37-88) in pull
+// form, depth slice by depth slice.  A row's parents sit in earlier slices
+// and are summed in the reference's Kahn dequeue order; the kept-loop factor
+// is applied after all parents, as at dequeue time (solvers.cpp:71-74).
+template <bool kBlock>
+__global__ void k_cac(DeviceLayout L, const CacTask* __restrict__ tasks, int ntasks,
+                      const int* __restrict__ depth_ptr, const SolveParams* __restrict__ p, double* rank) {
+  int task, lane, width;
+  if (kBlock) {
+    task = blockIdx.x;
+    lane = threadIdx.x;
+    width = blockDim.x;
+  } else {
+    task = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    lane = threadIdx.x & 31;
+    width = 32;
+  }
+  if (task >= ntasks) return;
+  const CacTask t = tasks[task];
+  const double c = p->c;
+  const int* dp = depth_ptr + t.depth_begin;
+  for (int r = dp[0] + lane; r < dp[1]; r += width)
+    if (L.loop[r]) rank[r] /= 1.0 - c / static_cast<double>(L.deg[r]);
+  for (int d = 1; d < t.ndepth; ++d) {
+    if (kBlock) {
+      __syncthreads();
+    } else {
+      __threadfence_block();
+      __syncwarp();
+    }
+    const int r1 = dp[d + 1];
+    for (int r = dp[d] + lane; r < r1; r += width) {
+      double acc = rank[r];
+      const long long e1 = L.iptr[r + 1];
+      for (long long e = L.iptr[r]; e < e1; ++e) {
+        const int s = L.isrc[e];
+        acc += rank[s] * c / static_cast<double>(L.deg[s]);
+      }
+      if (L.loop[r]) acc /= 1.0 - c / static_cast<double>(L.deg[r]);
+      rank[r] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------ small SCC
+// K5: exact dense solve of (I - cA^T) r = w per SccSmall unit
+// (solve_dense_system, solvers.cpp:92-108).  The matrix is strictly
+// diagonally dominant by columns (column a holds 1 on the diagonal and at most
+// c < 1 of off-diagonal mass), so partial pivoting never swaps rows and the
+// reference's partialPivLu reduces to plain Gaussian elimination, done here in
+// shared memory.  Residual check of solvers.cpp:103-106 -> kErrDegen.
+__global__ void k_small(DeviceLayout L, const SccTask* __restrict__ tasks, int ntasks, int ld,
+                        const double* __restrict__ pf, double* rank, double* scratch, DevStatus* st) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  double* M = scratch ? scratch + static_cast<size_t>(blockIdx.x) * ld * (ld + 2) : sm;
+  double* rhs = M + static_cast<size_t>(ld) * ld;
+  double* fcol = rhs + ld;
+  const int tid = threadIdx.x, bs = blockDim.x;
+  for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+    const SccTask t = tasks[task];
+    const int rb = t.row_begin, m = t.row_end - t.row_begin;
+    __syncthreads();
+    for (int i = tid; i < m * ld; i += bs) M[i] = 0.0;
+    __syncthreads();
+    for (int b = tid; b < m; b += bs) {
+      M[b * ld + b] = 1.0;
+      rhs[b] = rank[rb + b];
+    }
+    __syncthreads();
+    for (int b = tid; b < m; b += bs) {
+      const long long e1 = L.iptr[rb + b + 1];
+      for (long long e = L.iptr[rb + b]; e < e1; ++e) {
+        const int s = L.isrc[e];
+        M[b * ld + (s - rb)] -= pf[s];
+      }
+    }
+    for (int k = 0; k < m; ++k) {
+      __syncthreads();
+      const double piv = M[k * ld + k];
+      for (int i = k + 1 + tid; i < m; i += bs) {
+        const double f = M[i * ld + k] / piv;
+        fcol[i] = f;
+        rhs[i] -= f * rhs[k];
+      }
+      __syncthreads();
+      const int w = m - k - 1;
+      for (int idx = tid; idx < w * w; idx += bs) {
+        const int i = k + 1 + idx / w, j = k + 1 + idx % w;
+        M[i * ld + j] -= fcol[i] * M[k * ld + j];
+      }
+    }
+    for (int i = m - 1; i >= 0; --i) {
+      __syncthreads();
+      const double xi = rhs[i] / M[i * ld + i];
+      __syncthreads();
+      if (tid == 0) rhs[i] = xi;
+      for (int r = tid; r < i; r += bs) rhs[r] -= M[r * ld + i] * xi;
+    }
+    __syncthreads();
+    double res = 0.0, wm = 0.0, xm = 0.0;
+    for (int b = tid; b < m; b += bs) {
+      const double wb = rank[rb + b];
+      double acc = rhs[b];
+      const long long e1 = L.iptr[rb + b + 1];
+      for (long long e = L.iptr[rb + b]; e < e1; ++e) {
+        const int s = L.isrc[e];
+        acc -= pf[s] * rhs[s - rb];
+      }
+      res = fmax(res, fabs(acc - wb));
+      wm = fmax(wm, fabs(wb));
+      xm = fmax(xm, fabs(rhs[b]));
+    }
+    res = block_max(res, red);
+    __syncthreads();
+    wm = block_max(wm, red);
+    __syncthreads();
+    xm = block_max(xm, red);
+    if (tid == 0 && !(res <= 1e-8 * (1.0 + wm + xm))) atomicOr(&st->err, kErrDegen);
+    for (int b = tid; b < m; b += bs) rank[rb + b] = rhs[b];
+  }
+}
+
+// ---------------------------------------------------------- SccLarge, CTA
+// K4a: the whole accumulated power series of one SccLarge unit inside one CTA
+// (solve_large_scc, solvers.cpp:128-162) when its rows fit in shared memory.
+// Pull form: y_i = sum_{j in in(i)} s_j with s_j = pf_j * inc_j, summed by one
+// thread in ascending source order -> bit-identical to the reference's push
+// scatter; rank += y; stop when max y < tol; cap -> kErrNoConv.
+__global__ void k_large_cta(DeviceLayout L, const SccTask* __restrict__ tasks, int ntasks, int maxrows,
+                            const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
+                            long long* unit_iters, DevStatus* st) {
+  extern __shared__ double sm[];
+  __shared__ double red[2][32];
+  const SccTask t = tasks[blockIdx.x];
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  double* sc = sm;
+  double* sn = sm + maxrows;
+  double* pl = sm + 2 * maxrows;
+  const double tol = p->tol;
+  const long long cap = p->cap;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    pl[i] = pf[rb + i];
+    sc[i] = pl[i] * rank[rb + i];
+  }
+  __syncthreads();
+  long long it = 0;
+  bool fail = false;
+  for (;;) {
+    double lmax = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const int row = rb + i;
+      double y = 0.0;
+      const long long e1 = L.iptr[row + 1];
+      for (long long e = L.iptr[row]; e < e1; ++e) y += sc[__ldg(L.isrc + e) - rb];
+      rank[row] += y;
+      sn[i] = pl[i] * y;
+      lmax = fmax(lmax, y);
+    }
+    const double mx = block_max(lmax, red[it & 1]);
+    double* tmp = sc;
+    sc = sn;
+    sn = tmp;
+    ++it;
+    if (it > cap) {
+      fail = true;
+      break;
+    }
+    if (!(mx >= tol)) break;
+  }
+  if (threadIdx.x == 0) {
+    unit_iters[t.unit] = it;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->iterative_edge_work),
+              static_cast<unsigned long long>(it * t.edges));
+    if (fail) atomicOr(&st->err, kErrNoConv);
+  }
+}
+
+// --------------------------------------------------------- SccLarge, grid
+__global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ngu) {
+    gs[i].max_bits = 0ull;
+    gs[i].blocks_left = gs[i].nblocks;
+    gs[i].iterations = 0;
+    gs[i].done = 0;
+  }
+  if (i == 0) st->active = ngu;
+}
+
+// K4b: one power-series iteration of every still-running grid SccLarge unit
+// of a level.  Each CTA owns a row block (<= kSpmvNnz in-edges): it stages the
+// gathered s values of its block in shared memory with all index and gather
+// loads in flight, then reduces rows (one thread per row up to kLongRow
+// in-edges -- bit-exact with the reference; one warp per longer row) and runs
+// the epilogue rank += y, s' = pf * y, max.  Heavy rows are split over several
+// CTAs whose partials are combined in segment order by the last one to finish.
+// The last CTA of a unit closes the iteration: stop test of solvers.cpp:160,
+// cap test of :159.
+constexpr int kLongRow = 32;
+
+__global__ void __launch_bounds__(kSpmvThreads)
+    k_grid_iter(DeviceLayout L, const SpmvBlock* __restrict__ blocks, GridUnitState* gs,
+                const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
+                const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
+                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters,
+                DevStatus* st) {
+  __shared__ double vals[kSpmvNnz];
+  __shared__ long long rp[kSpmvRows + 1];
+  __shared__ double red[kSpmvThreads / 32];
+  __shared__ int is_last;
+  const SpmvBlock b = blocks[blockIdx.x];
+  GridUnitState* u = gs + b.gunit;
+  if (*reinterpret_cast<volatile int*>(&u->done)) return;
+  const int tid = threadIdx.x;
+  double lmax = 0.0;
+  constexpr int kPer = kSpmvNnz / kSpmvThreads;
+  if (b.heavy < 0) {
+    const int nr = b.row_end - b.row_begin;
+    for (int i = tid; i <= nr; i += kSpmvThreads) rp[i] = L.iptr[b.row_begin + i];
+    __syncthreads();
+    const long long base = rp[0];
+    const int nnz = static_cast<int>(rp[nr] - base);
+    int idx[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = tid + k * kSpmvThreads;
+      idx[k] = e < nnz ? __ldg(L.isrc + base + e) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (idx[k] >= 0) vals[tid + k * kSpmvThreads] = __ldg(s_in + idx[k]);
+    __syncthreads();
+    for (int r = tid; r < nr; r += kSpmvThreads) {
+      const int lo = static_cast<int>(rp[r] - base), hi = static_cast<int>(rp[r + 1] - base);
+      if (hi - lo > kLongRow) continue;
+      double y = 0.0;
+      for (int k = lo; k < hi; ++k) y += vals[k];
+      const int row = b.row_begin + r;
+      rank[row] += y;
+      s_out[row] = pf[row] * y;
+      lmax = fmax(lmax, y);
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int r = warp; r < nr; r += kSpmvThreads / 32) {
+      const int lo = static_cast<int>(rp[r] - base), hi = static_cast<int>(rp[r + 1] - base);
+      if (hi - lo <= kLongRow) continue;
+      double y = 0.0;
+      for (int k = lo + lane; k < hi; k += 32) y += vals[k];
+      y = warp_sum(y);
+      if (lane == 0) {
+        const int row = b.row_begin + r;
+        rank[row] += y;
+        s_out[row] = pf[row] * y;
+        lmax = fmax(lmax, y);
+      }
+    }
+  } else {
+    const HeavyRow h = heavy[b.heavy];
+    const long long lo = L.iptr[h.row] + static_cast<long long>(b.seg) * kSpmvNnz;
+    const long long hi = min(lo + kSpmvNnz, L.iptr[h.row + 1]);
+    const int nnz = static_cast<int>(hi - lo);
+    int idx[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = tid + k * kSpmvThreads;
+      idx[k] = e < nnz ? __ldg(L.isrc + lo + e) : -1;
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (idx[k] >= 0) part += __ldg(s_in + idx[k]);
+    part = block_sum(part, red);
+    if (tid == 0) {
+      heavy_part[h.part_begin + b.seg] = part;
+      __threadfence();
+      is_last = atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1;
+    }
+    __syncthreads();
+    if (is_last && tid == 0) {
+      __threadfence();
+      double y = 0.0;
+      for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
+      heavy_cnt[b.heavy] = 0;
+      rank[h.row] += y;
+      s_out[h.row] = pf[h.row] * y;
+      lmax = fmax(lmax, y);
+    }
+  }
+  __syncthreads();
+  const double bm = block_max(lmax, red);
+  if (tid == 0) {
+    atomicMax(&u->max_bits, dbits(bm));
+    __threadfence();
+    if (atomicSub(&u->blocks_left, 1) == 1) {
+      __threadfence();
+      const double mx = bitsd(atomicAdd(&u->max_bits, 0ull));
+      const int it = u->iterations + 1;
+      u->iterations = it;
+      u->max_bits = 0ull;
+      u->blocks_left = u->nblocks;
+      bool stop = false;
+      if (it > p->cap) {
+        atomicOr(&st->err, kErrNoConv);
+        stop = true;
+      } else if (!(mx >= p->tol)) {
+        stop = true;
+      }
+      if (stop) {
+        u->done = 1;
+        unit_iters[u->unit] = it;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->iterative_edge_work),
+                  static_cast<unsigned long long>(static_cast<long long>(it) * u->edges));
+        atomicSub(&st->active, 1);
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- output
+// R3 back to vertex order and fixed-order partial sums for the R1 total.
+__global__ void k_output(DeviceLayout L, const double* __restrict__ rank, double* __restrict__ r3,
+                         double* __restrict__ partial) {
+  __shared__ double red[kOutBlock / 32];
+  const int v = blockIdx.x * kOutBlock + threadIdx.x;
+  double x = 0.0;
+  if (v < L.n) {
+    x = rank[L.row_of[v]];
+    r3[v] = x;
+  }
+  const double s = block_sum(x, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partial, int nparts, double* total) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *total = s;
+}
+
+// R1 = R3 / ||R3||_1 (r3 >= 0); zero when the total is zero.
+__global__ void k_scale(const double* __restrict__ r3, double* __restrict__ r1, int n, const double* total) {
+  const double t = *total;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    r1[v] = t > 0.0 ? r3[v] / t : 0.0;
+}
+
+// propagate_weights (engine.cpp:83-87) for the standalone API: one thread per
+// destination, its edges in input order.
+__global__ void k_propagate(const int* __restrict__ order, const long long* __restrict__ seg_ptr, int nseg,
+                            const int* __restrict__ src, const int* __restrict__ dst, const int* __restrict__ deg,
+                            const double* __restrict__ ranks, double c, double* weights) {
+  const int sgi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sgi >= nseg) return;
+  const long long e0 = seg_ptr[sgi], e1 = seg_ptr[sgi + 1];
+  const int d = dst[order[e0]];
+  double acc = weights[d];
+  for (long long e = e0; e < e1; ++e) {
+    const int k = order[e];
+    acc += c * ranks[src[k]] / static_cast<double>(deg[k]);
+  }
+  weights[d] = acc;
+}
+
+int blocks_for(long long n, int threads) { return static_cast<int>((n + threads - 1) / threads); }
+
+}  // namespace
+
+void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,
+                 cudaStream_t s) {
+  if (L.n == 0) return;
+  const int grid = blocks_for(L.n, 256) < 148 * 8 ? blocks_for(L.n, 256) : 148 * 8;
+  k_prep<<<grid, 256, 0, s>>>(L, w, p, pf, st);
+}
+
+void launch_cross(const DeviceLayout& L, int row_begin, int row_end, const double* w, const SolveParams* p,
+                  const double* pf, double* rank, double* s0, cudaStream_t s) {
+  if (row_end <= row_begin) return;
+  k_cross<<<blocks_for(row_end - row_begin, 256), 256, 0, s>>>(L, row_begin, row_end, w, p, pf, rank, s0);
+}
+
+void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool big, const int* depth_ptr,
+                const SolveParams* p, double* rank, cudaStream_t s) {
+  if (ntasks == 0) return;
+  if (big)
+    k_cac<true><<<ntasks, 512, 0, s>>>(L, tasks, ntasks, depth_ptr, p, rank);
+  else
+    k_cac<false><<<blocks_for(ntasks, 8), 256, 0, s>>>(L, tasks, ntasks, depth_ptr, p, rank);
+}
+
+void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_m, const double* pf,
+                  double* rank, double* scratch, DevStatus* st, cudaStream_t s) {
+  if (ntasks == 0) return;
+  const int ld = max_m + 1;
+  const size_t bytes = static_cast<size_t>(ld) * (ld + 2) * sizeof(double);
+  if (scratch == nullptr) {
+    k_small<<<ntasks, 256, bytes, s>>>(L, tasks, ntasks, ld, pf, rank, nullptr, st);
+  } else {
+    const int grid = ntasks < kSmallScratchBlocks ? ntasks : kSmallScratchBlocks;
+    k_small<<<grid, 256, 0, s>>>(L, tasks, ntasks, ld, pf, rank, scratch, st);
+  }
+}
+
+cudaError_t configure_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_large_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+}
+
+void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
+                      const double* pf, double* rank, long long* unit_iters, DevStatus* st, cudaStream_t s) {
+  if (ntasks == 0) return;
+  const size_t bytes = static_cast<size_t>(3) * max_rows * sizeof(double);
+  k_large_cta<<<ntasks, 256, bytes, s>>>(L, tasks, ntasks, max_rows, p, pf, rank, unit_iters, st);
+}
+
+void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s) {
+  k_grid_reset<<<blocks_for(ngu > 0 ? ngu : 1, 128), 128, 0, s>>>(gs, ngu, st);
+}
+
+void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, GridUnitState* gs,
+                      const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
+                      const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
+                      DevStatus* st, cudaStream_t s) {
+  if (nblocks == 0) return;
+  k_grid_iter<<<nblocks, kSpmvThreads, 0, s>>>(L, blocks, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in,
+                                               s_out, unit_iters, st);
+}
+
+void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
+                   cudaStream_t s) {
+  if (nparts == 0) return;
+  k_output<<<nparts, kOutBlock, 0, s>>>(L, rank, r3, partial);
+}
+
+void launch_normalize(const double* r3, double* r1, int n, const double* partial, int nparts, double* total,
+                      cudaStream_t s) {
+  k_sum_partials<<<1, 1024, 0, s>>>(partial, nparts, total);
+  if (r1 && n > 0) k_scale<<<blocks_for(n, 256) < 148 * 16 ? blocks_for(n, 256) : 148 * 16, 256, 0, s>>>(r3, r1, n, total);
+}
+
+void launch_propagate(const int* order, const long long* seg_ptr, int nseg, const int* src, const int* dst,
+                      const int* deg, const double* ranks, double c, double* weights, cudaStream_t s) {
+  if (nseg == 0) return;
+  k_propagate<<<blocks_for(nseg, 256), 256, 0, s>>>(order, seg_ptr, nseg, src, dst, deg, ranks, c, weights);
+}
+
+}  // namespace lrk

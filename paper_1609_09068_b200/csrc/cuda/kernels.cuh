@@ -1,0 +1,128 @@
+// Device kernels of the level-scheduled PageRank solve (sm_100a).  See
+// DESIGN.md "Kernels" for each kernel's roofline and algorithmic bytes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lrk {
+
+// per-row kind (uploaded once)
+enum RowKind : std::uint8_t { kSingle = 0, kCac = 1, kSmall = 2, kLargeCta = 3, kLargeGrid = 4 };
+
+// device-side error bits
+enum ErrBits : unsigned { kErrNoConv = 1u, kErrDegen = 2u, kErrNegW = 4u, kErrCycle = 8u };
+
+// Per-solve scalars, read by every kernel from global memory.
+struct SolveParams {
+  double c;
+  double tol;
+  long long cap;  // iteration_cap (solvers.cpp:17-21)
+};
+
+// Small device-side status block (one per context).
+struct DevStatus {
+  unsigned err;
+  int all_zero;            // max(w) == 0
+  unsigned long long wmax_bits;
+  long long total_iterations;
+  long long iterative_edge_work;
+  int active;              // grid SccLarge units still iterating on the current level
+  int pad;
+};
+
+// One SccLarge grid unit's iteration state.
+struct GridUnitState {
+  unsigned long long max_bits;  // max(y) of the running iteration (y >= 0)
+  int blocks_left;              // blocks not yet done with this iteration
+  int iterations;
+  int done;
+  int unit;                     // schedule unit index (for unit_iters)
+  int nblocks;
+  int pad;
+  long long edges;              // reference unit.edges.size()
+};
+
+// A row block of the grid SpMV: rows [row_begin, row_end) of one unit, or one
+// segment of a heavy row (heavy >= 0).
+struct SpmvBlock {
+  int row_begin;
+  int row_end;
+  int gunit;   // index into GridUnitState array
+  int heavy;   // heavy-row id or -1
+  int seg;     // segment index within the heavy row
+};
+
+struct HeavyRow {
+  int row;
+  int nseg;
+  long long part_begin;  // into heavy partial buffer
+};
+
+struct DeviceLayout {
+  int n;
+  const int* vertex_of;
+  const int* row_of;
+  const int* deg;
+  const std::uint8_t* loop;
+  const std::uint8_t* rowkind;
+  const long long* xptr;
+  const int* xsrc;
+  const long long* iptr;
+  const int* isrc;
+};
+
+// tasks: CAC unit = rows [row_begin,row_end) with depth slices
+struct CacTask {
+  int row_begin;
+  int row_end;
+  long long depth_begin;  // into depth_ptr
+  int ndepth;
+  int pad;
+};
+struct SccTask {
+  int row_begin;
+  int row_end;
+  int unit;
+  int pad;
+  long long edges;
+};
+
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvNnz = 2048;     // nnz staged per block
+constexpr int kSpmvRows = 512;     // max rows per block
+constexpr int kCtaLargeMaxRows = 4096;
+constexpr long long kCtaLargeMaxNnz = 1 << 16;
+constexpr int kMaxDynSmem = 227 * 1024;
+constexpr int kSmallSmemMaxM = 160;      // ld*(ld+2)*8 <= 227 KB
+constexpr int kSmallScratchBlocks = 296; // grid of the global-scratch small-SCC path
+constexpr int kCacWarpMaxRows = 2048;    // larger CACs get a whole CTA
+
+cudaError_t configure_kernels();
+
+// launch wrappers (stream-ordered)
+void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,
+                 cudaStream_t s);
+void launch_cross(const DeviceLayout& L, int row_begin, int row_end, const double* w, const SolveParams* p,
+                  const double* pf, double* rank, double* s0, cudaStream_t s);
+void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool big, const int* depth_ptr,
+                const SolveParams* p, double* rank, cudaStream_t s);
+void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_m, const double* pf,
+                  double* rank, double* scratch, DevStatus* st, cudaStream_t s);
+void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
+                      const double* pf, double* rank, long long* unit_iters, DevStatus* st, cudaStream_t s);
+void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s);
+void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, GridUnitState* gs,
+                      const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
+                      const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
+                      DevStatus* st, cudaStream_t s);
+void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
+                   cudaStream_t s);
+void launch_normalize(const double* r3, double* r1, int n, const double* partial, int nparts, double* total,
+                      cudaStream_t s);
+void launch_propagate(const int* dst_order, const long long* seg_ptr, int nseg, const int* src, const int* dst,
+                      const int* deg, const double* ranks, double c, double* weights, cudaStream_t s);
+
+constexpr int kOutBlock = 1024;  // rows per partial sum of the R1 normalisation
+
+}  // namespace lrk

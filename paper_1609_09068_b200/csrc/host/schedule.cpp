@@ -1,0 +1,453 @@
+// Level-major schedule (reference-shaped, proj/src/schedule.cpp:32-137) and the
+// device Layout the GPU path consumes.
+#include "levelrank/schedule.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <numeric>
+#include <stdexcept>
+
+#include "parallel.hpp"
+
+namespace levelrank {
+inline namespace b200 {
+namespace {
+
+// Stable counting sort, descending key (schedule.cpp:14-28).
+std::vector<VertexId> stable_desc(const std::vector<VertexId>& items, const std::vector<std::int32_t>& key,
+                                  std::int32_t max_key) {
+  std::vector<std::int64_t> slot(static_cast<std::size_t>(max_key) + 2, 0);
+  for (const VertexId it : items) ++slot[static_cast<std::size_t>(key[static_cast<std::size_t>(it)])];
+  std::int64_t acc = 0;
+  for (std::int32_t k = max_key; k >= 0; --k) {
+    const std::int64_t c = slot[static_cast<std::size_t>(k)];
+    slot[static_cast<std::size_t>(k)] = acc;
+    acc += c;
+  }
+  std::vector<VertexId> out(items.size());
+  for (const VertexId it : items) out[static_cast<std::size_t>(slot[static_cast<std::size_t>(key[static_cast<std::size_t>(it)])]++)] = it;
+  return out;
+}
+
+// Components in schedule order: level desc, size desc, id asc.
+std::vector<VertexId> ordered_components(const Partition& p, VertexId n) {
+  const VertexId k = static_cast<VertexId>(p.component_count());
+  std::vector<VertexId> comps(static_cast<std::size_t>(k));
+  std::iota(comps.begin(), comps.end(), 0);
+  std::vector<std::int32_t> size_key(p.sizes.begin(), p.sizes.end());
+  comps = stable_desc(comps, size_key, n);
+  return stable_desc(comps, p.levels, std::max(p.max_level, 0));
+}
+
+// Members of every component, ascending vertex id (CSR by component).
+void component_members(const Partition& p, std::vector<std::int64_t>& begin, std::vector<VertexId>& mem) {
+  const std::size_t k = p.component_count(), n = p.comp_of.size();
+  begin.assign(k + 1, 0);
+  for (const VertexId c : p.comp_of) ++begin[static_cast<std::size_t>(c) + 1];
+  for (std::size_t c = 0; c < k; ++c) begin[c + 1] += begin[c];
+  std::vector<std::int64_t> cur(begin.begin(), begin.end() - 1);
+  mem.resize(n);
+  for (std::size_t v = 0; v < n; ++v) mem[static_cast<std::size_t>(cur[static_cast<std::size_t>(p.comp_of[v])]++)] = static_cast<VertexId>(v);
+}
+
+// One unit of the plan: a multi-vertex component, or a level's singletons.
+struct UnitPlan {
+  UnitKind kind;
+  std::int32_t level;
+  VertexId comp;  // -1: singleton group
+  VertexId size;
+};
+
+// Units per level in schedule order, singleton group slotted so sizes stay
+// non-increasing (schedule.cpp:58-110).  Fills per-level begin offsets.
+std::vector<UnitPlan> plan_units(const Partition& p, const std::vector<VertexId>& comps, VertexId threshold,
+                                 std::vector<std::int32_t>& level_unit_begin,
+                                 std::vector<std::vector<VertexId>>& singles_of_level,
+                                 const std::vector<std::int64_t>& mbegin, const std::vector<VertexId>& mem) {
+  const std::int32_t nl = p.max_level + 1;
+  level_unit_begin.assign(static_cast<std::size_t>(nl) + 1, 0);
+  singles_of_level.assign(static_cast<std::size_t>(nl), {});
+  std::vector<UnitPlan> units;
+  std::size_t walk = 0;
+  while (walk < comps.size()) {
+    const std::int32_t level = p.levels[static_cast<std::size_t>(comps[walk])];
+    const std::size_t li = static_cast<std::size_t>(p.max_level - level);
+    level_unit_begin[li] = static_cast<std::int32_t>(units.size());
+    const std::size_t first = units.size();
+    auto& singles = singles_of_level[li];
+    while (walk < comps.size() && p.levels[static_cast<std::size_t>(comps[walk])] == level) {
+      const VertexId c = comps[walk++];
+      const VertexId sz = p.sizes[static_cast<std::size_t>(c)];
+      if (sz == 1) {
+        singles.push_back(mem[static_cast<std::size_t>(mbegin[static_cast<std::size_t>(c)])]);
+        continue;
+      }
+      const UnitKind kind = p.kinds[static_cast<std::size_t>(c)] == ComponentKind::Cac ? UnitKind::Cac
+                            : sz < threshold                                          ? UnitKind::SccSmall
+                                                                                      : UnitKind::SccLarge;
+      units.push_back({kind, level, c, sz});
+    }
+    if (!singles.empty()) {
+      std::sort(singles.begin(), singles.end());
+      const VertexId gs = static_cast<VertexId>(singles.size());
+      auto at = std::find_if(units.begin() + static_cast<std::ptrdiff_t>(first), units.end(),
+                             [&](const UnitPlan& u) { return u.size < gs; });
+      units.insert(at, UnitPlan{UnitKind::SingletonGroup, level, -1, gs});
+    }
+  }
+  level_unit_begin[static_cast<std::size_t>(nl)] = static_cast<std::int32_t>(units.size());
+  for (std::int32_t i = nl - 1; i >= 0; --i)
+    level_unit_begin[static_cast<std::size_t>(i)] =
+        std::min(level_unit_begin[static_cast<std::size_t>(i)], level_unit_begin[static_cast<std::size_t>(i) + 1]);
+  return units;
+}
+
+}  // namespace
+
+std::vector<VertexId> schedule_permutation(const Partition& p) {
+  const VertexId n = static_cast<VertexId>(p.comp_of.size());
+  std::vector<VertexId> perm(static_cast<std::size_t>(n), 0);
+  if (n == 0) return perm;
+  const auto comps = ordered_components(p, n);
+  std::vector<std::int64_t> mb;
+  std::vector<VertexId> mem;
+  component_members(p, mb, mem);
+  VertexId pos = 0;
+  for (const VertexId c : comps)
+    for (std::int64_t j = mb[static_cast<std::size_t>(c)]; j < mb[static_cast<std::size_t>(c) + 1]; ++j)
+      perm[static_cast<std::size_t>(mem[static_cast<std::size_t>(j)])] = pos++;
+  return perm;
+}
+
+Schedule build_schedule(const Graph& g, const Partition& p, VertexId small_threshold) {
+  if (small_threshold < 1) throw std::invalid_argument("small_threshold must be at least 1");
+  const VertexId n = g.vertex_count();
+  Schedule s;
+  if (n == 0) return s;
+  const auto comps = ordered_components(p, n);
+  std::vector<std::int64_t> mb;
+  std::vector<VertexId> mem;
+  component_members(p, mb, mem);
+  s.permutation = schedule_permutation(p);
+  std::vector<std::int32_t> lub;
+  std::vector<std::vector<VertexId>> singles;
+  const auto plan = plan_units(p, comps, small_threshold, lub, singles, mb, mem);
+  const std::size_t nl = static_cast<std::size_t>(p.max_level) + 1;
+  s.levels.resize(nl);
+  std::vector<std::pair<std::size_t, std::size_t>> unit_of_comp(p.component_count());
+  std::vector<VertexId> local_of(static_cast<std::size_t>(n));
+  for (std::size_t li = 0; li < nl; ++li) {
+    auto& L = s.levels[li];
+    L.level = p.max_level - static_cast<std::int32_t>(li);
+    for (std::int32_t ui = lub[li]; ui < lub[li + 1]; ++ui) {
+      const UnitPlan& up = plan[static_cast<std::size_t>(ui)];
+      SolveUnit u;
+      u.kind = up.kind;
+      u.level = up.level;
+      if (up.comp >= 0)
+        u.global_ids.assign(mem.begin() + mb[static_cast<std::size_t>(up.comp)],
+                            mem.begin() + mb[static_cast<std::size_t>(up.comp) + 1]);
+      else
+        u.global_ids = singles[li];
+      const std::size_t idx = L.units.size();
+      for (std::size_t i = 0; i < u.global_ids.size(); ++i) {
+        const VertexId v = u.global_ids[i];
+        local_of[static_cast<std::size_t>(v)] = static_cast<VertexId>(i);
+        unit_of_comp[static_cast<std::size_t>(p.comp_of[static_cast<std::size_t>(v)])] = {li, idx};
+      }
+      L.units.push_back(std::move(u));
+    }
+  }
+  for (VertexId u = 0; u < n; ++u) {
+    const VertexId cu = p.comp_of[static_cast<std::size_t>(u)];
+    const auto [li, ui] = unit_of_comp[static_cast<std::size_t>(cu)];
+    for (const VertexId v : g.out_neighbors(u)) {
+      if (u == v) {
+        if (g.loop_policy() == LoopPolicy::Keep) {
+          s.levels[li].units[ui].edges.emplace_back(local_of[static_cast<std::size_t>(u)], local_of[static_cast<std::size_t>(u)]);
+          ++s.intra_edge_count;
+        } else {
+          ++s.dropped_loop_count;
+        }
+        continue;
+      }
+      if (cu == p.comp_of[static_cast<std::size_t>(v)]) {
+        s.levels[li].units[ui].edges.emplace_back(local_of[static_cast<std::size_t>(u)], local_of[static_cast<std::size_t>(v)]);
+        ++s.intra_edge_count;
+      } else {
+        s.levels[li].cross_edges.push_back({u, v, g.walk_out_degree(u)});
+        ++s.cross_edge_count;
+      }
+    }
+  }
+  return s;
+}
+
+Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold) {
+  if (small_threshold < 1) throw std::invalid_argument("small_threshold must be at least 1");
+  const VertexId n = g.vertex_count();
+  const std::size_t nn = static_cast<std::size_t>(n);
+  const bool keep = g.loop_policy() == LoopPolicy::Keep;
+  Layout L;
+  L.n = n;
+  L.max_level = p.max_level;
+  L.keep_loops = keep;
+  L.level_row_begin.assign(1, 0);
+  L.level_unit_begin.assign(1, 0);
+  L.unit_row_begin.assign(1, 0);
+  L.xptr.assign(1, 0);
+  L.iptr.assign(1, 0);
+  if (n == 0) return L;
+  const EdgeId* off = g.offsets_data();
+  const VertexId* tgt = g.targets_data();
+  const std::uint8_t* lp = g.loop_data();
+  const auto& comp_of = p.comp_of;
+
+  const auto comps = ordered_components(p, n);
+  std::vector<std::int64_t> mb;
+  std::vector<VertexId> mem;
+  component_members(p, mb, mem);
+  std::vector<std::vector<VertexId>> singles;
+  const auto plan = plan_units(p, comps, small_threshold, L.level_unit_begin, singles, mb, mem);
+  const std::size_t nu = plan.size();
+  const std::int32_t nl = p.max_level + 1;
+
+  // unit of every vertex, local index (= position in ascending members)
+  std::vector<std::int32_t> unit_of(nn), local_of(nn);
+  std::vector<std::int64_t> unit_mem_begin(nu + 1, 0);  // into `umem`
+  std::vector<VertexId> umem(nn);
+  {
+    std::int64_t pos = 0;
+    for (std::int32_t li = 0; li < nl; ++li)
+      for (std::int32_t ui = L.level_unit_begin[static_cast<std::size_t>(li)];
+           ui < L.level_unit_begin[static_cast<std::size_t>(li) + 1]; ++ui) {
+        const UnitPlan& up = plan[static_cast<std::size_t>(ui)];
+        unit_mem_begin[static_cast<std::size_t>(ui)] = pos;
+        if (up.comp >= 0) {
+          for (std::int64_t j = mb[static_cast<std::size_t>(up.comp)]; j < mb[static_cast<std::size_t>(up.comp) + 1]; ++j)
+            umem[static_cast<std::size_t>(pos++)] = mem[static_cast<std::size_t>(j)];
+        } else {
+          for (const VertexId v : singles[static_cast<std::size_t>(li)]) umem[static_cast<std::size_t>(pos++)] = v;
+        }
+      }
+    unit_mem_begin[nu] = pos;
+  }
+  detail::parallel_chunks(static_cast<std::int64_t>(nu), [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t u = b; u < e; ++u)
+      for (std::int64_t j = unit_mem_begin[static_cast<std::size_t>(u)]; j < unit_mem_begin[static_cast<std::size_t>(u) + 1]; ++j) {
+        const VertexId v = umem[static_cast<std::size_t>(j)];
+        unit_of[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(u);
+        local_of[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(j - unit_mem_begin[static_cast<std::size_t>(u)]);
+      }
+  }, 1);
+
+  // CAC units: Kahn pass of solve_cac (solvers.cpp:43-83) to get each vertex's
+  // dequeue position and its depth (longest path from the unit's sources).
+  std::vector<std::int32_t> kahn_pos(nn, 0), depth(nn, 0);
+  std::vector<std::int32_t> unit_depths(nu, 0);
+  std::atomic<bool> cycle{false};
+  detail::parallel_dynamic(static_cast<std::int64_t>(nu), 64, [&](std::int64_t b, std::int64_t e) {
+    std::vector<std::int32_t> adj_off, adj, indeg, queue, dep;
+    for (std::int64_t u = b; u < e; ++u) {
+      if (plan[static_cast<std::size_t>(u)].kind != UnitKind::Cac) continue;
+      const std::int64_t m0 = unit_mem_begin[static_cast<std::size_t>(u)];
+      const std::int32_t m = static_cast<std::int32_t>(unit_mem_begin[static_cast<std::size_t>(u) + 1] - m0);
+      const VertexId c = comp_of[static_cast<std::size_t>(umem[static_cast<std::size_t>(m0)])];
+      adj_off.assign(static_cast<std::size_t>(m) + 1, 0);
+      indeg.assign(static_cast<std::size_t>(m), 0);
+      adj.clear();
+      for (std::int32_t a = 0; a < m; ++a) {
+        const VertexId ga = umem[static_cast<std::size_t>(m0 + a)];
+        for (EdgeId k = off[ga]; k < off[ga + 1]; ++k) {
+          const VertexId gb = tgt[k];
+          if (gb == ga || comp_of[static_cast<std::size_t>(gb)] != c) continue;
+          const std::int32_t lb = local_of[static_cast<std::size_t>(gb)];
+          adj.push_back(lb);
+          ++indeg[static_cast<std::size_t>(lb)];
+        }
+        adj_off[static_cast<std::size_t>(a) + 1] = static_cast<std::int32_t>(adj.size());
+      }
+      queue.clear();
+      dep.assign(static_cast<std::size_t>(m), 0);
+      for (std::int32_t a = 0; a < m; ++a)
+        if (indeg[static_cast<std::size_t>(a)] == 0) queue.push_back(a);
+      std::size_t head = 0;
+      while (head < queue.size()) {
+        const std::int32_t a = queue[head++];
+        for (std::int32_t k = adj_off[static_cast<std::size_t>(a)]; k < adj_off[static_cast<std::size_t>(a) + 1]; ++k) {
+          const std::int32_t bb = adj[static_cast<std::size_t>(k)];
+          dep[static_cast<std::size_t>(bb)] = std::max(dep[static_cast<std::size_t>(bb)], dep[static_cast<std::size_t>(a)] + 1);
+          if (--indeg[static_cast<std::size_t>(bb)] == 0) queue.push_back(bb);
+        }
+      }
+      if (static_cast<std::int32_t>(queue.size()) != m) {
+        cycle = true;
+        continue;
+      }
+      std::int32_t maxd = 0;
+      for (std::int32_t i = 0; i < m; ++i) {
+        const VertexId gv = umem[static_cast<std::size_t>(m0 + queue[static_cast<std::size_t>(i)])];
+        kahn_pos[static_cast<std::size_t>(gv)] = i;
+        depth[static_cast<std::size_t>(gv)] = dep[static_cast<std::size_t>(queue[static_cast<std::size_t>(i)])];
+        maxd = std::max(maxd, dep[static_cast<std::size_t>(queue[static_cast<std::size_t>(i)])]);
+      }
+      unit_depths[static_cast<std::size_t>(u)] = maxd + 1;
+    }
+  });
+
+  if (cycle) throw std::logic_error("cycle inside an acyclic component");
+
+  // rows: units in order; CAC rows by (depth, vertex)
+  L.vertex_of.resize(nn);
+  L.row_of.resize(nn);
+  L.unit_row_begin.assign(nu + 1, 0);
+  L.unit_kind.resize(nu);
+  L.unit_level.resize(nu);
+  L.cac_depth_begin.assign(nu, -1);
+  for (std::size_t u = 0; u < nu; ++u) {
+    L.unit_row_begin[u] = static_cast<std::int32_t>(unit_mem_begin[u]);
+    L.unit_kind[u] = static_cast<std::uint8_t>(plan[u].kind);
+    L.unit_level[u] = plan[u].level;
+    if (plan[u].kind == UnitKind::Cac) {
+      L.cac_depth_begin[u] = static_cast<std::int64_t>(L.depth_ptr.size());
+      L.depth_ptr.resize(L.depth_ptr.size() + static_cast<std::size_t>(unit_depths[u]) + 1, 0);
+    }
+  }
+  L.unit_row_begin[nu] = n;
+  detail::parallel_dynamic(static_cast<std::int64_t>(nu), 256, [&](std::int64_t b, std::int64_t e) {
+    for (std::int64_t uu = b; uu < e; ++uu) {
+      const std::size_t u = static_cast<std::size_t>(uu);
+      const std::int64_t m0 = unit_mem_begin[u], m1 = unit_mem_begin[u + 1];
+      VertexId* rows = L.vertex_of.data() + m0;
+      std::copy(umem.begin() + m0, umem.begin() + m1, rows);
+      if (plan[u].kind == UnitKind::Cac) {
+        std::stable_sort(rows, rows + (m1 - m0), [&](VertexId a, VertexId bb) {
+          return depth[static_cast<std::size_t>(a)] < depth[static_cast<std::size_t>(bb)];
+        });
+        std::int32_t* dp = L.depth_ptr.data() + L.cac_depth_begin[u];
+        for (std::int64_t r = m0; r < m1; ++r) ++dp[depth[static_cast<std::size_t>(L.vertex_of[static_cast<std::size_t>(r)])] + 1];
+        dp[0] = static_cast<std::int32_t>(m0);
+        for (std::int32_t d = 0; d < unit_depths[u]; ++d) dp[d + 1] += dp[d];
+      }
+      for (std::int64_t r = m0; r < m1; ++r) L.row_of[static_cast<std::size_t>(L.vertex_of[static_cast<std::size_t>(r)])] = static_cast<VertexId>(r);
+    }
+  });
+  L.level_row_begin.assign(static_cast<std::size_t>(nl) + 1, 0);
+  for (std::int32_t li = 0; li <= nl; ++li)
+    L.level_row_begin[static_cast<std::size_t>(li)] = L.unit_row_begin[static_cast<std::size_t>(L.level_unit_begin[static_cast<std::size_t>(li)])];
+
+  L.deg.resize(nn);
+  L.loop.assign(nn, 0);
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t r = b; r < e; ++r) {
+      const VertexId v = L.vertex_of[static_cast<std::size_t>(r)];
+      L.deg[static_cast<std::size_t>(r)] = g.walk_out_degree(v);
+      const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(v)])].kind;
+      L.loop[static_cast<std::size_t>(r)] = keep && lp[v] && (k == UnitKind::SingletonGroup || k == UnitKind::Cac);
+    }
+  });
+
+  // in-degree counts: intra (pull lists), cross, per-unit reference edge counts
+  std::vector<EdgeId> icnt(nn + 1, 0), xcnt(nn + 1, 0);
+  std::vector<EdgeId> uedges(nu, 0);
+  std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    EdgeId li = 0, lx = 0, ld = 0;
+    for (std::int64_t uu = b; uu < e; ++uu) {
+      const VertexId u = static_cast<VertexId>(uu);
+      const VertexId cu = comp_of[static_cast<std::size_t>(u)];
+      const std::size_t un = static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)]);
+      const bool scc = plan[un].kind == UnitKind::SccSmall || plan[un].kind == UnitKind::SccLarge;
+      EdgeId ue = 0;
+      for (EdgeId k = off[u]; k < off[u + 1]; ++k) {
+        const VertexId v = tgt[k];
+        if (v == u) {
+          if (keep) {
+            ++ue;
+            if (scc) std::atomic_ref<EdgeId>(icnt[static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)])]).fetch_add(1, std::memory_order_relaxed);
+          } else {
+            ++ld;
+          }
+          continue;
+        }
+        const std::size_t rv = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
+        if (comp_of[static_cast<std::size_t>(v)] == cu) {
+          ++ue;
+          std::atomic_ref<EdgeId>(icnt[rv]).fetch_add(1, std::memory_order_relaxed);
+        } else {
+          ++lx;
+          std::atomic_ref<EdgeId>(xcnt[rv]).fetch_add(1, std::memory_order_relaxed);
+        }
+      }
+      li += ue;
+      if (ue) std::atomic_ref<EdgeId>(uedges[un]).fetch_add(ue, std::memory_order_relaxed);
+    }
+    n_intra += li;
+    n_cross += lx;
+    n_dropped += ld;
+  });
+  L.intra_edge_count = n_intra;
+  L.cross_edge_count = n_cross;
+  L.dropped_loop_count = n_dropped;
+  L.unit_edges = std::move(uedges);
+  const EdgeId ti = detail::exclusive_scan_inplace(icnt.data(), static_cast<std::int64_t>(nn) + 1);
+  const EdgeId tx = detail::exclusive_scan_inplace(xcnt.data(), static_cast<std::int64_t>(nn) + 1);
+  L.isrc.resize(static_cast<std::size_t>(ti));
+  L.xsrc.resize(static_cast<std::size_t>(tx));
+  {
+    std::vector<EdgeId> icur(icnt.begin(), icnt.end() - 1), xcur(xcnt.begin(), xcnt.end() - 1);
+    detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t uu = b; uu < e; ++uu) {
+        const VertexId u = static_cast<VertexId>(uu);
+        const VertexId cu = comp_of[static_cast<std::size_t>(u)];
+        const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)])].kind;
+        const bool scc = k == UnitKind::SccSmall || k == UnitKind::SccLarge;
+        for (EdgeId q = off[u]; q < off[u + 1]; ++q) {
+          const VertexId v = tgt[q];
+          const std::size_t rv = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
+          if (v == u) {
+            if (keep && scc)
+              L.isrc[static_cast<std::size_t>(std::atomic_ref<EdgeId>(icur[rv]).fetch_add(1, std::memory_order_relaxed))] = u;
+            continue;
+          }
+          if (comp_of[static_cast<std::size_t>(v)] == cu)
+            L.isrc[static_cast<std::size_t>(std::atomic_ref<EdgeId>(icur[rv]).fetch_add(1, std::memory_order_relaxed))] = u;
+          else
+            L.xsrc[static_cast<std::size_t>(std::atomic_ref<EdgeId>(xcur[rv]).fetch_add(1, std::memory_order_relaxed))] = u;
+        }
+      }
+    });
+  }
+  // per-row ordering = the reference's accumulation order, then vertex -> row
+  std::vector<std::int32_t> level_idx_of(nn);
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v)
+      level_idx_of[static_cast<std::size_t>(v)] = p.max_level - p.levels[static_cast<std::size_t>(comp_of[static_cast<std::size_t>(v)])];
+  });
+  detail::parallel_dynamic(n, 2048, [&](std::int64_t b, std::int64_t e) {
+    for (std::int64_t r = b; r < e; ++r) {
+      const VertexId v = L.vertex_of[static_cast<std::size_t>(r)];
+      const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(v)])].kind;
+      VertexId* a = L.isrc.data() + icnt[static_cast<std::size_t>(r)];
+      VertexId* ae = L.isrc.data() + icnt[static_cast<std::size_t>(r) + 1];
+      if (k == UnitKind::Cac)
+        std::sort(a, ae, [&](VertexId x, VertexId y) { return kahn_pos[static_cast<std::size_t>(x)] < kahn_pos[static_cast<std::size_t>(y)]; });
+      else
+        std::sort(a, ae);
+      for (VertexId* q = a; q < ae; ++q) *q = L.row_of[static_cast<std::size_t>(*q)];
+      VertexId* x = L.xsrc.data() + xcnt[static_cast<std::size_t>(r)];
+      VertexId* xe = L.xsrc.data() + xcnt[static_cast<std::size_t>(r) + 1];
+      std::sort(x, xe, [&](VertexId s1, VertexId s2) {
+        const std::int32_t l1 = level_idx_of[static_cast<std::size_t>(s1)], l2 = level_idx_of[static_cast<std::size_t>(s2)];
+        return l1 != l2 ? l1 < l2 : s1 < s2;
+      });
+      for (VertexId* q = x; q < xe; ++q) *q = L.row_of[static_cast<std::size_t>(*q)];
+    }
+  });
+  L.iptr = std::move(icnt);
+  L.xptr = std::move(xcnt);
+  return L;
+}
+
+}  // namespace b200
+}  // namespace levelrank

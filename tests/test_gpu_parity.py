@@ -1,0 +1,72 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle."""
+import numpy as np
+import pytest
+
+from conftest import FIXTURE8, random_graph
+
+pytestmark = pytest.mark.gpu
+
+FIX8_RANKS = [1.0, 2.99670691547750, 1.425, 1.84906695938529, 1.605625, 3.81947320938530,
+              9.72636742121042, 9.26741230802886]  # proj/tests/test_engine.cpp:23-34
+
+
+def oracle_graph(oracle, g):
+    off, tgt, _, _ = g.csr()
+    return oracle.graph_from_csr(g.n, off, tgt)
+
+
+def test_fixture8_ranks(lr):
+    g = lr.Graph.from_edges(8, FIXTURE8)
+    res = lr.compute_pagerank(g, np.ones(8), lr.SolverParams(0.85, 1e-9))
+    np.testing.assert_allclose(res.ranks, FIX8_RANKS, rtol=1e-12)
+    assert res.report["components"] == 4 and res.report["level_count"] == 3
+    assert res.report["total_edge_work"] == 11 and res.report["cross_edge_count"] == 4
+
+
+def test_random_graphs_all_kinds(lr, oracle):
+    rng = np.random.default_rng(1003)
+    for trial in range(120):
+        n = int(rng.integers(2, 60))
+        keep = trial % 4 == 0
+        s, d = random_graph(rng, n, float(rng.uniform(0.02, 0.2)), loops=trial % 2 == 0)
+        g = lr.Graph.from_edges(n, src=s, dst=d, loop_policy=int(keep))
+        go = oracle.graph(n, s, d, keep)
+        w = rng.uniform(0.05, 5.0, n)
+        th = [1, 2, 100][trial % 3]
+        c = [0.5, 0.85, 0.99][(trial // 3) % 3]
+        ref = go.compute_pagerank(w, c, 1e-12, th)
+        res = lr.compute_pagerank(g, w, lr.SolverParams(c, 1e-12), small_threshold=th)
+        assert np.array_equal(res.unit_iters, ref.unit_iters), trial
+        rel = np.abs(res.ranks - ref.ranks) / np.maximum(np.abs(ref.ranks), 1e-300)
+        assert rel.max() <= 1e-10, (trial, rel.max())
+        for k in ("total_edge_work", "iterative_edge_work", "single_pass_edge_work", "large_scc_vertices",
+                  "components", "max_level", "total_iterations"):
+            assert res.report[k] == ref.report[k], (trial, k)
+
+
+@pytest.mark.parametrize("cfg,shrink", [(1, 1), (2, 4), (3, 6), (4, 5)])
+def test_config_recipes(lr, oracle, cfg, shrink):
+    g = lr.config_graph(cfg, shrink)
+    go = oracle_graph(oracle, g)
+    w = np.full(g.n, 1.0 / g.n)
+    ref = go.compute_pagerank(w, 0.85, 1e-12, 100)
+    res = lr.compute_pagerank(g, w, lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(res.unit_iters, ref.unit_iters)
+    rel = np.abs(res.ranks - ref.ranks) / np.abs(ref.ranks)
+    assert rel.max() <= 1e-10, rel.max()
+    np.testing.assert_allclose(res.r1, oracle.normalize_r1(ref.ranks), rtol=1e-10)
+    assert res.report["total_edge_work"] == ref.report["total_edge_work"]
+
+
+def test_engine_reuse_and_zero_weights(lr):
+    g = lr.config_graph(2, 8)
+    eng = lr.Engine(g)
+    r3a, r1a, _, _ = eng.solve(np.full(g.n, 1.0 / g.n), lr.SolverParams(0.85, 1e-12))
+    r3b, r1b, _, _ = eng.solve(np.full(g.n, 1.0 / g.n), lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(r3a, r3b) and np.array_equal(r1a, r1b)
+    z3, z1, info, _ = eng.solve(np.zeros(g.n), lr.SolverParams(0.85, 1e-9))
+    assert info["all_weights_zero"] == 1 and not z3.any() and not z1.any()
+    with pytest.raises(ValueError):
+        w = np.ones(g.n)
+        w[3] = -1
+        eng.solve(w, lr.SolverParams(0.85, 1e-9))
