@@ -159,8 +159,12 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
     lrerr::set(std::string("levelrank-b200 is built for sm_100a; found ") + prop.name);
     return fail(LR_ECUDA);
   }
-  if (configure_kernels() != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-    lrerr::set("CUDA stream / kernel setup failed");
+  if (const cudaError_t e = configure_kernels(); e != cudaSuccess) {
+    lrerr::set(std::string("kernel setup failed: ") + cudaGetErrorString(e));
+    return fail(LR_ECUDA);
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    lrerr::set("CUDA stream creation failed");
     return fail(LR_ECUDA);
   }
   for (auto& e : ctx->ev)

@@ -507,10 +507,24 @@ void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int m
   }
 }
 
-cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+template <typename K>
+static cudaError_t allow_dynamic_smem(K kernel, int optin) {
+  cudaFuncAttributes a{};
+  cudaError_t e = cudaFuncGetAttributes(&a, kernel);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_large_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - static_cast<int>(a.sharedSizeBytes));
+}
+
+cudaError_t configure_kernels() {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  e = allow_dynamic_smem(k_small, optin);
+  if (e != cudaSuccess) return e;
+  return allow_dynamic_smem(k_large_cta, optin);
 }
 
 void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
