@@ -124,7 +124,7 @@ class _Lib:
     prefix = ""
 
     def _err(self):
-        return self.lib[self.prefix + "last_error"]().decode()
+        return getattr(self.lib, self.prefix + "last_error")().decode()
 
     def _check(self, rc):
         if rc != 0:
