@@ -269,7 +269,11 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
               const int hid = static_cast<int>(heavy.size());
               heavy.push_back(HeavyRow{r, nseg, heavy_parts});
               heavy_parts += nseg;
-              for (int sg = 0; sg < nseg; ++sg) blocks.push_back(SpmvBlock{r, r + 1, gu, hid, sg});
+              for (int sg = 0; sg < nseg; ++sg) {
+                const long long nb = L->iptr[r] + static_cast<long long>(sg) * kSpmvNnz;
+                const int cnt = static_cast<int>(std::min<long long>(kSpmvNnz, L->iptr[r + 1] - nb));
+                blocks.push_back(SpmvBlock{nb, cnt, r, r + 1, gu, hid, sg});
+              }
               ++r;
               continue;
             }
@@ -281,7 +285,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
               acc += l2;
               ++r;
             }
-            blocks.push_back(SpmvBlock{start, r, gu, -1, 0});
+            blocks.push_back(SpmvBlock{L->iptr[start], static_cast<int>(acc), start, r, gu, -1, 0});
           }
           ctx->gu_rows.push_back(m);
           ctx->gu_nnz.push_back(L->iptr[re] - L->iptr[rb]);
@@ -419,7 +423,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
             ctx->lev.push_back(e);
           }
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 2)], s));
-          launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
+          launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
                            ctx->status.p, s);
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 1)], s));

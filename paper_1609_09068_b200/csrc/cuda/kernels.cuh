@@ -28,29 +28,29 @@ struct DevStatus {
   long long total_iterations;
   long long iterative_edge_work;
   int active;              // grid SccLarge units still iterating on the current level
-  int pad;
+  int ctas_done;           // CTAs finished with the running grid SpMV launch
 };
 
 // One SccLarge grid unit's iteration state.
 struct GridUnitState {
   unsigned long long max_bits;  // max(y) of the running iteration (y >= 0)
-  int blocks_left;              // blocks not yet done with this iteration
   int iterations;
   int done;
   int unit;                     // schedule unit index (for unit_iters)
   int nblocks;
-  int pad;
   long long edges;              // reference unit.edges.size()
 };
 
 // A row block of the grid SpMV: rows [row_begin, row_end) of one unit, or one
 // segment of a heavy row (heavy >= 0).
 struct SpmvBlock {
+  long long nnz_begin;  // first in-edge of the block (absolute, into isrc)
+  int nnz;              // in-edges in the block (<= kSpmvNnz)
   int row_begin;
   int row_end;
-  int gunit;   // index into GridUnitState array
-  int heavy;   // heavy-row id or -1
-  int seg;     // segment index within the heavy row
+  int gunit;            // index into GridUnitState array
+  int heavy;            // heavy-row id or -1
+  int seg;              // segment index within the heavy row
 };
 
 struct HeavyRow {
@@ -112,7 +112,8 @@ void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int m
 void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
                       const double* pf, double* rank, long long* unit_iters, DevStatus* st, cudaStream_t s);
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s);
-void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, GridUnitState* gs,
+int grid_iter_ctas();
+void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
                       DevStatus* st, cudaStream_t s);
