@@ -264,24 +264,28 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           int r = rb;
           while (r < re) {
             const long long len = L->iptr[r + 1] - L->iptr[r];
-            if (len > kSpmvNnz) {
-              const int nseg = static_cast<int>((len + kSpmvNnz - 1) / kSpmvNnz);
-              const int hid = static_cast<int>(heavy.size());
-              heavy.push_back(HeavyRow{r, nseg, heavy_parts});
-              heavy_parts += nseg;
-              for (int sg = 0; sg < nseg; ++sg) {
-                const long long nb = L->iptr[r] + static_cast<long long>(sg) * kSpmvNnz;
-                const int cnt = static_cast<int>(std::min<long long>(kSpmvNnz, L->iptr[r + 1] - nb));
-                blocks.push_back(SpmvBlock{nb, cnt, r, r + 1, gu, hid, sg});
+            if (len > kTileNnz) {
+              if (len <= kSegNnz) {
+                blocks.push_back(SpmvBlock{L->iptr[r], static_cast<int>(len), r, r + 1, gu, -1, 0});
+              } else {
+                const int nseg = static_cast<int>((len + kSegNnz - 1) / kSegNnz);
+                const int hid = static_cast<int>(heavy.size());
+                heavy.push_back(HeavyRow{r, nseg, heavy_parts});
+                heavy_parts += nseg;
+                for (int sg = 0; sg < nseg; ++sg) {
+                  const long long nb = L->iptr[r] + static_cast<long long>(sg) * kSegNnz;
+                  const int cnt = static_cast<int>(std::min<long long>(kSegNnz, L->iptr[r + 1] - nb));
+                  blocks.push_back(SpmvBlock{nb, cnt, r, r + 1, gu, hid, sg});
+                }
               }
               ++r;
               continue;
             }
             const int start = r;
             long long acc = 0;
-            while (r < re && r - start < kSpmvRows) {
+            while (r < re && r - start < kTileRows) {
               const long long l2 = L->iptr[r + 1] - L->iptr[r];
-              if (l2 > kSpmvNnz || acc + l2 > kSpmvNnz) break;
+              if (l2 > kTileNnz || acc + l2 > kTileNnz) break;
               acc += l2;
               ++r;
             }

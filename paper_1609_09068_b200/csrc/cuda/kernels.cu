@@ -279,176 +279,6 @@ __global__ void k_large_cta(DeviceLayout L, const SccTask* __restrict__ tasks, i
   }
 }
 
-// --------------------------------------------------------- SccLarge, grid
-__global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < ngu) {
-    gs[i].max_bits = 0ull;
-    gs[i].iterations = 0;
-    gs[i].done = 0;
-  }
-  if (i == 0) {
-    st->active = ngu;
-    st->ctas_done = 0;
-  }
-}
-
-// Closes one iteration of every grid unit of the level (run by the last CTA):
-// stop test of solvers.cpp:160 (max|inc| < tol), cap test of :159.
-__device__ void finish_iteration(GridUnitState* gs, int gu0, int ngu, const SolveParams* p,
-                                 long long* unit_iters, DevStatus* st) {
-  for (int i = gu0; i < gu0 + ngu; ++i) {
-    GridUnitState* u = gs + i;
-    if (u->done) continue;
-    const double mx = bitsd(atomicAdd(&u->max_bits, 0ull));
-    const int it = u->iterations + 1;
-    u->iterations = it;
-    u->max_bits = 0ull;
-    bool stop = false;
-    if (it > p->cap) {
-      atomicOr(&st->err, kErrNoConv);
-      stop = true;
-    } else if (!(mx >= p->tol)) {
-      stop = true;
-    }
-    if (stop) {
-      u->done = 1;
-      unit_iters[u->unit] = it;
-      atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&st->iterative_edge_work),
-                static_cast<unsigned long long>(static_cast<long long>(it) * u->edges));
-      atomicSub(&st->active, 1);
-    }
-  }
-  st->ctas_done = 0;
-}
-
-// K4b: one power-series iteration (solve_large_scc, solvers.cpp:146-160) of
-// every still-running grid SccLarge unit of a level.  Persistent CTAs walk a
-// precomputed list of row blocks (<= kSpmvNnz in-edges, <= kSpmvRows rows).
-// Per block, every index load, row-pointer load and epilogue operand load is
-// issued before the gathers are consumed; the gathered s values are staged in
-// shared memory, then rows are reduced (one thread per row up to kLongRow
-// in-edges -- the reference's own accumulation order, bit-exact; one warp per
-// longer row) and the epilogue rank += y, s' = pf * y, max runs.  Heavy rows
-// are split over several blocks whose partials are combined in segment order
-// by the last segment to finish.  One atomicMax per (CTA, unit) and one
-// completion counter per CTA; the last CTA closes the iteration.
-constexpr int kLongRow = 32;
-constexpr int kRowsPerThread = kSpmvRows / kSpmvThreads;
-
-__global__ void __launch_bounds__(kSpmvThreads)
-    k_grid_iter(DeviceLayout L, const SpmvBlock* __restrict__ blocks, int nblocks, int gu0, int ngu,
-                GridUnitState* gs, const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
-                const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
-                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st) {
-  __shared__ double vals[kSpmvNnz];
-  __shared__ int rp[kSpmvRows + 1];  // row offsets relative to the block's first in-edge
-  __shared__ double red[kSpmvThreads / 32];
-  __shared__ int flag;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int kPer = kSpmvNnz / kSpmvThreads;
-  int cur_unit = -1;
-  double lmax = 0.0;
-  auto flush_max = [&]() {
-    if (cur_unit < 0) return;
-    __syncthreads();
-    const double bm = block_max(lmax, red);
-    if (tid == 0 && bm > 0.0) atomicMax(&gs[cur_unit].max_bits, dbits(bm));
-    lmax = 0.0;
-  };
-  for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
-    const SpmvBlock b = blocks[bi];
-    if (b.gunit != cur_unit) {
-      flush_max();
-      cur_unit = b.gunit;
-    }
-    if (gs[b.gunit].done) continue;
-    int idx[kPer];
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = tid + k * kSpmvThreads;
-      idx[k] = e < b.nnz ? __ldg(L.isrc + b.nnz_begin + e) : -1;
-    }
-    if (b.heavy < 0) {
-      const int nr = b.row_end - b.row_begin;
-      // row offsets and the epilogue operands of this thread's rows, in flight with the gathers
-      for (int i = tid; i <= nr; i += kSpmvThreads) rp[i] = static_cast<int>(__ldg(L.iptr + b.row_begin + i) - b.nnz_begin);
-      double rk[kRowsPerThread], pfr[kRowsPerThread];
-#pragma unroll
-      for (int j = 0; j < kRowsPerThread; ++j) {
-        const int r = tid + j * kSpmvThreads;
-        rk[j] = r < nr ? rank[b.row_begin + r] : 0.0;
-        pfr[j] = r < nr ? __ldg(pf + b.row_begin + r) : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < kPer; ++k)
-        if (idx[k] >= 0) vals[tid + k * kSpmvThreads] = __ldg(s_in + idx[k]);
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < kRowsPerThread; ++j) {
-        const int r = tid + j * kSpmvThreads;
-        if (r >= nr) continue;
-        const int lo = rp[r], hi = rp[r + 1];
-        if (hi - lo > kLongRow) continue;
-        double y = 0.0;
-        for (int k = lo; k < hi; ++k) y += vals[k];
-        const int row = b.row_begin + r;
-        rank[row] = rk[j] + y;
-        s_out[row] = pfr[j] * y;
-        lmax = fmax(lmax, y);
-      }
-      for (int r = warp; r < nr; r += kSpmvThreads / 32) {
-        const int lo = rp[r], hi = rp[r + 1];
-        if (hi - lo <= kLongRow) continue;
-        double y = 0.0;
-        for (int k = lo + lane; k < hi; k += 32) y += vals[k];
-        y = warp_sum(y);
-        if (lane == 0) {
-          const int row = b.row_begin + r;
-          rank[row] += y;
-          s_out[row] = pf[row] * y;
-          lmax = fmax(lmax, y);
-        }
-      }
-      __syncthreads();  // vals / rp reuse by the next block
-    } else {
-      const HeavyRow h = heavy[b.heavy];
-      double part = 0.0;
-#pragma unroll
-      for (int k = 0; k < kPer; ++k)
-        if (idx[k] >= 0) part += __ldg(s_in + idx[k]);
-      part = block_sum(part, red);
-      if (tid == 0) {
-        heavy_part[h.part_begin + b.seg] = part;
-        __threadfence();
-        flag = atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1;
-      }
-      __syncthreads();
-      if (flag && tid == 0) {
-        __threadfence();
-        double y = 0.0;
-        for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
-        heavy_cnt[b.heavy] = 0;
-        rank[h.row] += y;
-        s_out[h.row] = pf[h.row] * y;
-        lmax = fmax(lmax, y);
-      }
-      __syncthreads();
-    }
-  }
-  flush_max();
-  if (tid == 0) {
-    __threadfence();
-    flag = atomicAdd(&st->ctas_done, 1) == static_cast<int>(gridDim.x) - 1;
-  }
-  __syncthreads();
-  if (flag && tid == 0) {
-    __threadfence();
-    finish_iteration(gs, gu0, ngu, p, unit_iters, st);
-  }
-}
-
 // --------------------------------------------------------------- output
 // R3 back to vertex order and fixed-order partial sums for the R1 total.
 __global__ void k_output(DeviceLayout L, const double* __restrict__ rank, double* __restrict__ r3,
@@ -562,31 +392,6 @@ void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, i
   k_large_cta<<<ntasks, 256, bytes, s>>>(L, tasks, ntasks, max_rows, p, pf, rank, unit_iters, st);
 }
 
-void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s) {
-  k_grid_reset<<<blocks_for(ngu > 0 ? ngu : 1, 128), 128, 0, s>>>(gs, ngu, st);
-}
-
-int grid_iter_ctas() {
-  static int ctas = 0;
-  if (ctas == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads, 0);
-    ctas = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  return ctas;
-}
-
-void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu,
-                      GridUnitState* gs, const HeavyRow* heavy, double* heavy_part, int* heavy_cnt,
-                      const SolveParams* p, const double* pf, double* rank, const double* s_in, double* s_out,
-                      long long* unit_iters, DevStatus* st, cudaStream_t s) {
-  if (nblocks == 0) return;
-  const int grid = nblocks < grid_iter_ctas() ? nblocks : grid_iter_ctas();
-  k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, blocks, nblocks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf,
-                                            rank, s_in, s_out, unit_iters, st);
-}
 
 void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
                    cudaStream_t s) {

@@ -89,8 +89,9 @@ struct SccTask {
 };
 
 constexpr int kSpmvThreads = 256;
-constexpr int kSpmvNnz = 2048;     // nnz staged per block
-constexpr int kSpmvRows = 512;     // max rows per block
+constexpr int kTileNnz = 256;      // in-edges of one warp tile
+constexpr int kTileRows = 64;      // max rows of one warp tile
+constexpr int kSegNnz = 1024;      // rows above this are split into segments
 constexpr int kCtaLargeMaxRows = 4096;
 constexpr long long kCtaLargeMaxNnz = 1 << 16;
 constexpr int kMaxDynSmem = 227 * 1024;
