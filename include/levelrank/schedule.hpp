@@ -56,8 +56,10 @@ Schedule build_schedule(const Graph& g, const Partition& p, VertexId small_thres
 /// Device layout of one graph (host copy; uploaded by lr_ctx_upload).
 /// Rows are vertices in level-major order: levels descending, then units in
 /// schedule order, then within a unit:
-///   SingletonGroup / SccSmall / SccLarge: ascending vertex id
+///   SingletonGroup / SccSmall: ascending vertex id
 ///     (= the reference's local ids, schedule.cpp:101-109)
+///   SccLarge: descending in-unit out-degree, then vertex id (gather
+///     locality; each row's in-edge list keeps the reference's order)
 ///   Cac: ascending (intra-CAC depth, vertex id); depth = longest path from
 ///     the CAC's in-degree-0 vertices, so each depth slice depends only on
 ///     earlier slices.

@@ -61,6 +61,8 @@ struct LevelTasks {
   int cac_b0 = 0, cac_b1 = 0;  // CTA-per-CAC tasks
   int sm0 = 0, sm1 = 0, sm_max = 0;
   int lc0 = 0, lc1 = 0, lc_max = 0;
+  int xh0 = 0, xh1 = 0;  // heavy cross-row tasks
+  int sl0 = 0, sl1 = 0;  // depth slices of large CACs (one launch each)
   int gu0 = 0, gu1 = 0;
   int bk0 = 0, bk1 = 0;
 };
@@ -88,6 +90,10 @@ struct lr_ctx {
   DevBuf<HeavyRow> heavy;
   DevBuf<double> heavy_part;
   DevBuf<int> heavy_cnt;
+  DevBuf<CrossTask> xheavy;
+  DevBuf<double> xparts;
+  DevBuf<int> xcnts;
+  std::vector<std::pair<int, int>> cac_slices;
   DevBuf<double> small_scratch;
   int small_scratch_ld = 0;
   // work
@@ -218,10 +224,14 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   std::vector<GridUnitState> gstate;
   std::vector<SpmvBlock> blocks;
   std::vector<HeavyRow> heavy;
+  std::vector<CrossTask> xheavy;
+  long long xparts = 0;
+  int n_xslots = 0;
   long long heavy_parts = 0;
   ctx->lt.assign(static_cast<size_t>(L->n_levels), LevelTasks{});
   ctx->gu_rows.clear();
   ctx->gu_nnz.clear();
+  ctx->cac_slices.clear();
   int max_small = 0;
   bool small_needs_scratch = false;
   for (int li = 0; li < L->n_levels; ++li) {
@@ -229,6 +239,21 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.rb = L->level_row_begin[li];
     T.re = L->level_row_begin[li + 1];
     std::vector<CacTask> lw, lb;
+    T.sl0 = static_cast<int>(ctx->cac_slices.size());
+    T.xh0 = static_cast<int>(xheavy.size());
+    for (int r = T.rb; r < T.re; ++r) {
+      const long long xd = L->xptr[r + 1] - L->xptr[r];
+      if (xd <= kCrossLight) continue;
+      const int nseg = static_cast<int>((xd + kCrossSeg - 1) / kCrossSeg);
+      const int slot = n_xslots++;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const long long e0 = L->xptr[r] + static_cast<long long>(sg) * kCrossSeg;
+        xheavy.push_back(CrossTask{e0, xparts, static_cast<int>(std::min<long long>(kCrossSeg, L->xptr[r + 1] - e0)),
+                                   r, sg, nseg, slot, 0});
+      }
+      xparts += nseg;
+    }
+    T.xh1 = static_cast<int>(xheavy.size());
     T.sm0 = static_cast<int>(small.size());
     T.lc0 = static_cast<int>(lcta.size());
     T.gu0 = static_cast<int>(gstate.size());
@@ -243,8 +268,13 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         const long long db = L->cac_depth_begin[u];
         int nd = 0;
         while (L->depth_ptr[db + nd] < re) ++nd;  // depth_ptr[db+nd] == re ends the unit
-        CacTask t{rb, re, db, nd, 0};
-        (m > kCacWarpMaxRows ? lb : lw).push_back(t);
+        if (m > kCacWarpMaxRows) {
+          // large CAC: one grid-wide launch per depth slice
+          for (int d = 0; d < nd; ++d)
+            ctx->cac_slices.emplace_back(L->depth_ptr[db + d], L->depth_ptr[db + d + 1]);
+        } else {
+          lw.push_back(CacTask{rb, re, db, nd, 0});
+        }
       } else if (kind == 2) {
         rk = kSmall;
         small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
@@ -308,6 +338,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.cac_b0 = static_cast<int>(cac_b.size());
     cac_b.insert(cac_b.end(), lb.begin(), lb.end());
     T.cac_b1 = static_cast<int>(cac_b.size());
+    T.sl1 = static_cast<int>(ctx->cac_slices.size());
     T.sm1 = static_cast<int>(small.size());
     T.lc1 = static_cast<int>(lcta.size());
     T.gu1 = static_cast<int>(gstate.size());
@@ -339,6 +370,10 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->heavy.upload(heavy.data(), heavy.size(), s));
   LR_CUDA_TRY(ctx->heavy_part.alloc(static_cast<size_t>(heavy_parts)));
   LR_CUDA_TRY(ctx->heavy_cnt.alloc(heavy.size()));
+  LR_CUDA_TRY(ctx->xheavy.upload(xheavy.data(), xheavy.size(), s));
+  LR_CUDA_TRY(ctx->xparts.alloc(static_cast<size_t>(xparts)));
+  LR_CUDA_TRY(ctx->xcnts.alloc(static_cast<size_t>(n_xslots)));
+  LR_CUDA_TRY(cudaMemsetAsync(ctx->xcnts.p, 0, ctx->xcnts.bytes(), s));
   LR_CUDA_TRY(cudaMemsetAsync(ctx->heavy_cnt.p, 0, ctx->heavy_cnt.bytes(), s));
   ctx->small_scratch.reset();
   ctx->small_scratch_ld = max_small + 1;
@@ -390,6 +425,16 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   for (const LevelTasks& T : ctx->lt) {
     launch_cross(L, T.rb, T.re, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, s);
     ++launches;
+    if (T.xh1 > T.xh0) {
+      launch_cross_heavy(L, ctx->xheavy.p + T.xh0, T.xh1 - T.xh0, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p,
+                         ctx->s0.p, ctx->xparts.p, ctx->xcnts.p, s);
+      ++launches;
+    }
+    for (int i = T.sl0; i < T.sl1; ++i) {
+      launch_cac_slice(L, ctx->cac_slices[static_cast<size_t>(i)].first, ctx->cac_slices[static_cast<size_t>(i)].second,
+                       ctx->params.p, ctx->rank.p, s);
+      ++launches;
+    }
     if (T.cac_w1 > T.cac_w0) {
       launch_cac(L, ctx->cac.p + T.cac_w0, T.cac_w1 - T.cac_w0, false, ctx->depth_ptr.p, ctx->params.p, ctx->rank.p, s);
       ++launches;

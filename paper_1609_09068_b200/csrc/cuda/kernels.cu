@@ -8,6 +8,7 @@
 
 #include <cstdint>
 
+#include "devutil.cuh"
 #include "kernels.cuh"
 
 namespace lrk {
@@ -86,9 +87,10 @@ __global__ void k_cross(DeviceLayout L, int row_begin, int row_end, const double
                         double* __restrict__ s0) {
   const int row = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= row_end) return;
+  const long long e1 = L.xptr[row + 1];
+  if (e1 - L.xptr[row] > kCrossLight) return;  // heavy rows: k_cross_heavy
   const double c = p->c;
   double acc = w[L.vertex_of[row]];
-  const long long e1 = L.xptr[row + 1];
   for (long long e = L.xptr[row]; e < e1; ++e) {
     const int s = __ldg(L.xsrc + e);
     acc += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
@@ -97,6 +99,48 @@ __global__ void k_cross(DeviceLayout L, int row_begin, int row_end, const double
   if (k == kSingle && L.loop[row]) acc /= 1.0 - c / static_cast<double>(L.deg[row]);
   rank[row] = acc;
   if (k == kLargeGrid) s0[row] = pf[row] * acc;
+}
+
+__device__ __forceinline__ void cross_finish(const DeviceLayout& L, int row, double acc, double c,
+                                             const double* __restrict__ pf, double* rank, double* s0) {
+  const std::uint8_t k = L.rowkind[row];
+  if (k == kSingle && L.loop[row]) acc /= 1.0 - c / static_cast<double>(L.deg[row]);
+  rank[row] = acc;
+  if (k == kLargeGrid) s0[row] = pf[row] * acc;
+}
+
+// K1 for rows with more than kCrossLight cross in-edges (R-MAT hubs): one warp
+// per kCrossSeg-edge slice; slices of one row combine in slice order in the
+// last one to finish.  Same terms as k_cross, tree-summed.
+__global__ void k_cross_heavy(DeviceLayout L, const CrossTask* __restrict__ tasks, int ntasks,
+                              const double* __restrict__ w, const SolveParams* __restrict__ p,
+                              const double* __restrict__ pf, double* rank, double* __restrict__ s0, double* parts,
+                              int* cnts) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= ntasks) return;
+  const CrossTask x = tasks[t];
+  const double c = p->c;
+  double sum = 0.0;
+  for (int i = lane; i < x.cnt; i += 32) {
+    const int s = __ldg(L.xsrc + x.e_begin + i);
+    sum += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
+  }
+  sum = dev::warp_sum(sum);
+  if (lane != 0) return;
+  if (x.nseg == 1) {
+    cross_finish(L, x.row, w[L.vertex_of[x.row]] + sum, c, pf, rank, s0);
+    return;
+  }
+  parts[x.part_begin + x.seg] = sum;
+  __threadfence();
+  if (atomicAdd(cnts + x.slot, 1) == x.nseg - 1) {
+    __threadfence();
+    double y = 0.0;
+    for (int k = 0; k < x.nseg; ++k) y += __ldcg(parts + x.part_begin + k);
+    cnts[x.slot] = 0;
+    cross_finish(L, x.row, w[L.vertex_of[x.row]] + y, c, pf, rank, s0);
+  }
 }
 
 // ------------------------------------------------------------------ CAC
@@ -142,6 +186,23 @@ __global__ void k_cac(DeviceLayout L, const CacTask* __restrict__ tasks, int nta
       rank[r] = acc;
     }
   }
+}
+
+// One depth slice of a large CAC across the whole grid (the slice's parents
+// are final: earlier slices ran in earlier launches).
+__global__ void k_cac_slice(DeviceLayout L, int row_begin, int row_end, const SolveParams* __restrict__ p,
+                            double* rank) {
+  const int r = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= row_end) return;
+  const double c = p->c;
+  double acc = rank[r];
+  const long long e1 = L.iptr[r + 1];
+  for (long long e = L.iptr[r]; e < e1; ++e) {
+    const int s = __ldg(L.isrc + e);
+    acc += rank[s] * c / static_cast<double>(__ldg(L.deg + s));
+  }
+  if (L.loop[r]) acc /= 1.0 - c / static_cast<double>(L.deg[r]);
+  rank[r] = acc;
 }
 
 // ------------------------------------------------------------ small SCC
@@ -341,6 +402,19 @@ void launch_cross(const DeviceLayout& L, int row_begin, int row_end, const doubl
                   const double* pf, double* rank, double* s0, cudaStream_t s) {
   if (row_end <= row_begin) return;
   k_cross<<<blocks_for(row_end - row_begin, 256), 256, 0, s>>>(L, row_begin, row_end, w, p, pf, rank, s0);
+}
+
+void launch_cross_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const double* w,
+                        const SolveParams* p, const double* pf, double* rank, double* s0, double* parts, int* cnts,
+                        cudaStream_t s) {
+  if (ntasks == 0) return;
+  k_cross_heavy<<<blocks_for(ntasks, 8), 256, 0, s>>>(L, tasks, ntasks, w, p, pf, rank, s0, parts, cnts);
+}
+
+void launch_cac_slice(const DeviceLayout& L, int row_begin, int row_end, const SolveParams* p, double* rank,
+                      cudaStream_t s) {
+  if (row_end <= row_begin) return;
+  k_cac_slice<<<blocks_for(row_end - row_begin, 256), 256, 0, s>>>(L, row_begin, row_end, p, rank);
 }
 
 void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool big, const int* depth_ptr,

@@ -88,6 +88,20 @@ struct SccTask {
   long long edges;
 };
 
+// A slice of one heavy row's cross in-edges (rows with more than kCrossLight).
+struct CrossTask {
+  long long e_begin;     // into xsrc
+  long long part_begin;  // partial slots of the row (nseg > 1)
+  int cnt;
+  int row;
+  int seg;
+  int nseg;
+  int slot;              // completion counter of the row
+  int pad;
+};
+
+constexpr int kCrossLight = 32;    // rows up to this many cross in-edges: one thread, reference order
+constexpr int kCrossSeg = 2048;    // cross in-edges per warp task of a heavy row
 constexpr int kSpmvThreads = 256;
 constexpr int kTileNnz = 256;      // in-edges of one warp tile
 constexpr int kTileRows = 64;      // max rows of one warp tile
@@ -106,8 +120,13 @@ void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, d
                  cudaStream_t s);
 void launch_cross(const DeviceLayout& L, int row_begin, int row_end, const double* w, const SolveParams* p,
                   const double* pf, double* rank, double* s0, cudaStream_t s);
+void launch_cross_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const double* w,
+                        const SolveParams* p, const double* pf, double* rank, double* s0, double* parts, int* cnts,
+                        cudaStream_t s);
 void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool big, const int* depth_ptr,
                 const SolveParams* p, double* rank, cudaStream_t s);
+void launch_cac_slice(const DeviceLayout& L, int row_begin, int row_end, const SolveParams* p, double* rank,
+                      cudaStream_t s);
 void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_m, const double* pf,
                   double* rank, double* scratch, DevStatus* st, cudaStream_t s);
 void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,

@@ -314,12 +314,30 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
     }
   }
   L.unit_row_begin[nu] = n;
+  // Large SCC units: rows (= gather columns) by descending in-unit out-degree,
+  // so the most-gathered s values sit together at the head of the unit.
+  std::vector<std::int32_t> unit_out(nn, 0);
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t uu = b; uu < e; ++uu) {
+      const VertexId u = static_cast<VertexId>(uu);
+      if (plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)])].kind != UnitKind::SccLarge) continue;
+      const VertexId cu = comp_of[static_cast<std::size_t>(u)];
+      std::int32_t k = 0;
+      for (EdgeId q = off[u]; q < off[u + 1]; ++q)
+        k += comp_of[static_cast<std::size_t>(tgt[q])] == cu && (tgt[q] != u || keep);
+      unit_out[static_cast<std::size_t>(u)] = k;
+    }
+  });
   detail::parallel_dynamic(static_cast<std::int64_t>(nu), 256, [&](std::int64_t b, std::int64_t e) {
     for (std::int64_t uu = b; uu < e; ++uu) {
       const std::size_t u = static_cast<std::size_t>(uu);
       const std::int64_t m0 = unit_mem_begin[u], m1 = unit_mem_begin[u + 1];
       VertexId* rows = L.vertex_of.data() + m0;
       std::copy(umem.begin() + m0, umem.begin() + m1, rows);
+      if (plan[u].kind == UnitKind::SccLarge)
+        std::stable_sort(rows, rows + (m1 - m0), [&](VertexId a, VertexId bb) {
+          return unit_out[static_cast<std::size_t>(a)] > unit_out[static_cast<std::size_t>(bb)];
+        });
       if (plan[u].kind == UnitKind::Cac) {
         std::stable_sort(rows, rows + (m1 - m0), [&](VertexId a, VertexId bb) {
           return depth[static_cast<std::size_t>(a)] < depth[static_cast<std::size_t>(bb)];
