@@ -67,6 +67,11 @@ struct LevelTasks {
   int bk0 = 0, bk1 = 0;
 };
 
+// One depth slice of a large CAC: rows [r0, r1), heavy-row tasks [h0, h1).
+struct CacSlice {
+  int r0, r1, h0, h1;
+};
+
 }  // namespace
 
 struct lr_ctx {
@@ -93,7 +98,7 @@ struct lr_ctx {
   DevBuf<CrossTask> xheavy;
   DevBuf<double> xparts;
   DevBuf<int> xcnts;
-  std::vector<std::pair<int, int>> cac_slices;
+  std::vector<CacSlice> cac_slices;
   DevBuf<double> small_scratch;
   int small_scratch_ld = 0;
   // work
@@ -270,8 +275,23 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         while (L->depth_ptr[db + nd] < re) ++nd;  // depth_ptr[db+nd] == re ends the unit
         if (m > kCacWarpMaxRows) {
           // large CAC: one grid-wide launch per depth slice
-          for (int d = 0; d < nd; ++d)
-            ctx->cac_slices.emplace_back(L->depth_ptr[db + d], L->depth_ptr[db + d + 1]);
+          for (int d = 0; d < nd; ++d) {
+            const int r0 = L->depth_ptr[db + d], r1 = L->depth_ptr[db + d + 1];
+            const int h0 = static_cast<int>(xheavy.size());
+            for (int r = r0; r < r1; ++r) {
+              const long long id = L->iptr[r + 1] - L->iptr[r];
+              if (id <= kCrossLight) continue;
+              const int nseg = static_cast<int>((id + kCrossSeg - 1) / kCrossSeg);
+              const int slot = n_xslots++;
+              for (int sg = 0; sg < nseg; ++sg) {
+                const long long e0 = L->iptr[r] + static_cast<long long>(sg) * kCrossSeg;
+                xheavy.push_back(CrossTask{e0, xparts, static_cast<int>(std::min<long long>(kCrossSeg, L->iptr[r + 1] - e0)),
+                                           r, sg, nseg, slot, 0});
+              }
+              xparts += nseg;
+            }
+            ctx->cac_slices.push_back(CacSlice{r0, r1, h0, static_cast<int>(xheavy.size())});
+          }
         } else {
           lw.push_back(CacTask{rb, re, db, nd, 0});
         }
@@ -431,9 +451,14 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       ++launches;
     }
     for (int i = T.sl0; i < T.sl1; ++i) {
-      launch_cac_slice(L, ctx->cac_slices[static_cast<size_t>(i)].first, ctx->cac_slices[static_cast<size_t>(i)].second,
-                       ctx->params.p, ctx->rank.p, s);
+      const CacSlice& sl = ctx->cac_slices[static_cast<size_t>(i)];
+      launch_cac_slice(L, sl.r0, sl.r1, ctx->params.p, ctx->rank.p, s);
       ++launches;
+      if (sl.h1 > sl.h0) {
+        launch_cac_heavy(L, ctx->xheavy.p + sl.h0, sl.h1 - sl.h0, ctx->params.p, ctx->rank.p, ctx->xparts.p,
+                         ctx->xcnts.p, s);
+        ++launches;
+      }
     }
     if (T.cac_w1 > T.cac_w0) {
       launch_cac(L, ctx->cac.p + T.cac_w0, T.cac_w1 - T.cac_w0, false, ctx->depth_ptr.p, ctx->params.p, ctx->rank.p, s);

@@ -109,36 +109,44 @@ __device__ __forceinline__ void cross_finish(const DeviceLayout& L, int row, dou
   if (k == kLargeGrid) s0[row] = pf[row] * acc;
 }
 
-// K1 for rows with more than kCrossLight cross in-edges (R-MAT hubs): one warp
-// per kCrossSeg-edge slice; slices of one row combine in slice order in the
-// last one to finish.  Same terms as k_cross, tree-summed.
-__global__ void k_cross_heavy(DeviceLayout L, const CrossTask* __restrict__ tasks, int ntasks,
-                              const double* __restrict__ w, const SolveParams* __restrict__ p,
-                              const double* __restrict__ pf, double* rank, double* __restrict__ s0, double* parts,
-                              int* cnts) {
+// Pull rows with many in-edges (R-MAT hubs): one warp per kCrossSeg-edge
+// slice; slices of one row combine in slice order in the last one to finish.
+// kCac = false: cross in-edges of K1 (base = w, finish = cross_finish);
+// kCac = true : intra in-edges of a large-CAC depth slice (base = rank).
+// Same terms as the one-thread paths, tree-summed.
+template <bool kCac>
+__global__ void k_pull_heavy(DeviceLayout L, const CrossTask* __restrict__ tasks, int ntasks,
+                             const double* __restrict__ w, const SolveParams* __restrict__ p,
+                             const double* __restrict__ pf, double* rank, double* __restrict__ s0, double* parts,
+                             int* cnts) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= ntasks) return;
   const CrossTask x = tasks[t];
   const double c = p->c;
+  const int* src = kCac ? L.isrc : L.xsrc;
   double sum = 0.0;
   for (int i = lane; i < x.cnt; i += 32) {
-    const int s = __ldg(L.xsrc + x.e_begin + i);
+    const int s = __ldg(src + x.e_begin + i);
     sum += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
   }
   sum = dev::warp_sum(sum);
   if (lane != 0) return;
-  if (x.nseg == 1) {
-    cross_finish(L, x.row, w[L.vertex_of[x.row]] + sum, c, pf, rank, s0);
-    return;
-  }
-  parts[x.part_begin + x.seg] = sum;
-  __threadfence();
-  if (atomicAdd(cnts + x.slot, 1) == x.nseg - 1) {
+  double y = sum;
+  if (x.nseg > 1) {
+    parts[x.part_begin + x.seg] = sum;
     __threadfence();
-    double y = 0.0;
+    if (atomicAdd(cnts + x.slot, 1) != x.nseg - 1) return;
+    __threadfence();
+    y = 0.0;
     for (int k = 0; k < x.nseg; ++k) y += __ldcg(parts + x.part_begin + k);
     cnts[x.slot] = 0;
+  }
+  if (kCac) {
+    double acc = rank[x.row] + y;
+    if (L.loop[x.row]) acc /= 1.0 - c / static_cast<double>(L.deg[x.row]);
+    rank[x.row] = acc;
+  } else {
     cross_finish(L, x.row, w[L.vertex_of[x.row]] + y, c, pf, rank, s0);
   }
 }
@@ -194,9 +202,10 @@ __global__ void k_cac_slice(DeviceLayout L, int row_begin, int row_end, const So
                             double* rank) {
   const int r = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= row_end) return;
+  const long long e1 = L.iptr[r + 1];
+  if (e1 - L.iptr[r] > kCrossLight) return;  // heavy rows: k_pull_heavy<true>
   const double c = p->c;
   double acc = rank[r];
-  const long long e1 = L.iptr[r + 1];
   for (long long e = L.iptr[r]; e < e1; ++e) {
     const int s = __ldg(L.isrc + e);
     acc += rank[s] * c / static_cast<double>(__ldg(L.deg + s));
@@ -408,7 +417,14 @@ void launch_cross_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntask
                         const SolveParams* p, const double* pf, double* rank, double* s0, double* parts, int* cnts,
                         cudaStream_t s) {
   if (ntasks == 0) return;
-  k_cross_heavy<<<blocks_for(ntasks, 8), 256, 0, s>>>(L, tasks, ntasks, w, p, pf, rank, s0, parts, cnts);
+  k_pull_heavy<false><<<blocks_for(ntasks, 8), 256, 0, s>>>(L, tasks, ntasks, w, p, pf, rank, s0, parts, cnts);
+}
+
+void launch_cac_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const SolveParams* p, double* rank,
+                      double* parts, int* cnts, cudaStream_t s) {
+  if (ntasks == 0) return;
+  k_pull_heavy<true><<<blocks_for(ntasks, 8), 256, 0, s>>>(L, tasks, ntasks, nullptr, p, nullptr, rank, nullptr,
+                                                           parts, cnts);
 }
 
 void launch_cac_slice(const DeviceLayout& L, int row_begin, int row_end, const SolveParams* p, double* rank,

@@ -127,6 +127,8 @@ void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool bi
                 const SolveParams* p, double* rank, cudaStream_t s);
 void launch_cac_slice(const DeviceLayout& L, int row_begin, int row_end, const SolveParams* p, double* rank,
                       cudaStream_t s);
+void launch_cac_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const SolveParams* p, double* rank,
+                      double* parts, int* cnts, cudaStream_t s);
 void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_m, const double* pf,
                   double* rank, double* scratch, DevStatus* st, cudaStream_t s);
 void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
