@@ -8,12 +8,17 @@
 //   long row  one row with kTileNnz < in-degree <= kSegNnz
 //   segment   kSegNnz in-edges of a heavier row; partials combined in segment
 //             order by whichever segment finishes last
-// Persistent CTAs; every warp walks its own strided slice of the task list and
-// never waits on another warp (no __syncthreads in the loop): a tile issues all
-// 8 index loads per lane, then its row offsets and epilogue operands, then the
-// 8 gathers, stages them in a warp-private shared buffer and reduces rows.
+// One persistent CTA per SM of kHeadWarps warps.  Random 8-byte gathers cost
+// one L1 wavefront per distinct 128-byte line, which bounds this kernel; the
+// layout orders a unit's rows by in-unit out-degree, so the most-gathered
+// pushed values sit at the head of the unit, and each CTA stages that head
+// (up to ~19.6k doubles) in shared memory once per launch: gathers that land
+// there cost a bank access instead of a line.  Every warp walks its own
+// strided slice of the task list and never waits on another warp: a tile
+// issues its 8 index loads per lane, its row offsets and epilogue operands,
+// then the 8 gathers, stages them in a warp-private buffer and reduces rows.
 // Rows up to kLongRow in-edges are summed by one lane in the reference's own
-// order (bit-exact with the CPU push scatter); longer rows use a warp butterfly.
+// order (bit-exact with the CPU push scatter); longer rows use a butterfly.
 #include <cuda_runtime.h>
 
 #include "devutil.cuh"
@@ -24,9 +29,11 @@ namespace {
 
 using namespace dev;
 
-constexpr int kWarps = kSpmvThreads / 32;
+constexpr int kHeadWarps = 32;                  // warps per persistent CTA
+constexpr int kHeadThreads = kHeadWarps * 32;
 constexpr int kPerLane = kTileNnz / 32;
 constexpr int kLongRow = 32;
+constexpr int kStageBytes = kHeadWarps * (kTileNnz * 8 + (kTileRows + 1) * 4 + 12);
 
 __global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,23 +85,45 @@ __device__ __forceinline__ void epilogue(int row, double y, double rk, double pf
   lmax = fmax(lmax, y);
 }
 
-__global__ void __launch_bounds__(kSpmvThreads)
+// s_in[i] through the shared head when i lies in [head_base, head_base + nhead).
+__device__ __forceinline__ double gather(const double* __restrict__ s_in, const double* head, int head_base,
+                                         int nhead, int i) {
+  const unsigned h = static_cast<unsigned>(i - head_base);
+  return h < static_cast<unsigned>(nhead) ? head[h] : __ldg(s_in + i);
+}
+
+__global__ void __launch_bounds__(kHeadThreads, 1)
     k_grid_iter(DeviceLayout L, const SpmvBlock* __restrict__ tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
-                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st) {
-  __shared__ double vals[kWarps][kTileNnz];
-  __shared__ int rp[kWarps][kTileRows + 1];
-  __shared__ int wunit[kWarps];
-  __shared__ double wmax[kWarps];
+                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
+                int head_base, int nhead) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* head = reinterpret_cast<double*>(smem);
+  double* vals = head + nhead;                                          // [kHeadWarps][kTileNnz]
+  int* rp = reinterpret_cast<int*>(vals + kHeadWarps * kTileNnz);       // [kHeadWarps][kTileRows + 1]
+  int* wunit = rp + kHeadWarps * (kTileRows + 1);
+  double* wmax = reinterpret_cast<double*>(wunit + kHeadWarps + (kHeadWarps & 1));
   __shared__ int last_cta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* v = vals[warp];
-  int* wr = rp[warp];
+  double* v = vals + warp * kTileNnz;
+  int* wr = rp + warp * (kTileRows + 1);
+
+  // stage the hot head of the pushed vector (read-only during this launch)
+  if (nhead > 0) {
+    const double2* src = reinterpret_cast<const double2*>(s_in + head_base);
+    double2* dst = reinterpret_cast<double2*>(head);
+    const bool aligned = (head_base & 1) == 0;
+    for (int i = threadIdx.x; i < (nhead >> 1); i += blockDim.x)
+      dst[i] = aligned ? __ldg(src + i) : make_double2(__ldg(s_in + head_base + 2 * i), __ldg(s_in + head_base + 2 * i + 1));
+    if ((nhead & 1) && threadIdx.x == 0) head[nhead - 1] = __ldg(s_in + head_base + nhead - 1);
+    __syncthreads();
+  }
+
   int cur_unit = -1;
   double lmax = 0.0;
-  const int stride = gridDim.x * kWarps;
-  for (int t = blockIdx.x * kWarps + warp; t < ntasks; t += stride) {
+  const int stride = gridDim.x * kHeadWarps;
+  for (int t = blockIdx.x * kHeadWarps + warp; t < ntasks; t += stride) {
     const SpmvBlock b = tasks[t];
     if (b.gunit != cur_unit) {
       if (cur_unit >= 0) {
@@ -123,7 +152,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
       }
 #pragma unroll
       for (int k = 0; k < kPerLane; ++k)
-        if (idx[k] >= 0) v[lane + 32 * k] = __ldg(s_in + idx[k]);
+        if (idx[k] >= 0) v[lane + 32 * k] = gather(s_in, head, head_base, nhead, idx[k]);
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < kTileRows / 32; ++j) {
@@ -156,7 +185,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
         }
 #pragma unroll
         for (int k = 0; k < kPerLane; ++k)
-          if (idx[k] >= 0) part += __ldg(s_in + idx[k]);
+          if (idx[k] >= 0) part += gather(s_in, head, head_base, nhead, idx[k]);
       }
       part = warp_sum(part);
       if (b.heavy < 0) {
@@ -182,10 +211,10 @@ __global__ void __launch_bounds__(kSpmvThreads)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < kHeadWarps; ++w) {
       if (wunit[w] < 0 || !(wmax[w] > 0.0)) continue;
       double mm = wmax[w];
-      while (w + 1 < kWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
+      while (w + 1 < kHeadWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
       atomicMax(&gs[wunit[w]].max_bits, dbits(mm));
     }
     __threadfence();
@@ -200,19 +229,33 @@ __global__ void __launch_bounds__(kSpmvThreads)
 
 int blocks_for(long long n, int threads) { return static_cast<int>((n + threads - 1) / threads); }
 
+int optin_smem() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, k_grid_iter);
+    v -= static_cast<int>(a.sharedSizeBytes);
+    cudaFuncSetAttribute(k_grid_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+  }
+  return v;
+}
+
 }  // namespace
 
 int grid_iter_ctas() {
   static int ctas = 0;
   if (ctas == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads, 0);
-    ctas = sms * (per_sm > 0 ? per_sm : 1);
+    cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev);
   }
   return ctas;
 }
+
+int grid_head_capacity() { return (optin_smem() - kStageBytes - 64) / 8 & ~1; }
 
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s) {
   k_grid_reset<<<blocks_for(ngu > 0 ? ngu : 1, 128), 128, 0, s>>>(gs, ngu, st);
@@ -221,12 +264,15 @@ void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                      cudaStream_t s) {
+                      int head_base, int nhead, cudaStream_t s) {
   if (ntasks == 0) return;
-  const int want = blocks_for(ntasks, kWarps);
-  const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
-  k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank,
-                                            s_in, s_out, unit_iters, st);
+  const int cap = grid_head_capacity();
+  if (nhead > cap) nhead = cap;
+  if (nhead < 0) nhead = 0;
+  const size_t bytes = static_cast<size_t>(nhead) * 8 + kStageBytes + 16;
+  k_grid_iter<<<grid_iter_ctas(), kHeadThreads, bytes, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part,
+                                                            heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
+                                                            head_base, nhead);
 }
 
 }  // namespace lrk
