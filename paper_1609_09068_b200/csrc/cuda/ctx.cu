@@ -367,13 +367,15 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.bk1 = static_cast<int>(blocks.size());
     // the shared-memory head belongs to the level's largest grid unit (its
     // rows are ordered by descending in-unit out-degree)
-    long long best = std::getenv("LR_SPMV_HEAD") && std::string(std::getenv("LR_SPMV_HEAD")) == "0" ? (1ll << 62) : -1;
+    long long head_cap = grid_head_capacity();
+    if (const char* e = std::getenv("LR_SPMV_HEAD")) head_cap = std::min<long long>(head_cap, std::atoll(e));
+    long long best = -1;
     for (int gi = T.gu0; gi < T.gu1; ++gi)
       if (ctx->gu_nnz[static_cast<size_t>(gi)] > best) {
         best = ctx->gu_nnz[static_cast<size_t>(gi)];
         const int u = gstate[static_cast<size_t>(gi)].unit;
         T.head_base = L->unit_row_begin[u];
-        T.nhead = static_cast<int>(std::min<long long>(grid_head_capacity(), ctx->gu_rows[static_cast<size_t>(gi)]));
+        T.nhead = static_cast<int>(std::min<long long>(head_cap, ctx->gu_rows[static_cast<size_t>(gi)]));
       }
   }
   // warp tasks first, then CTA tasks, in one array
