@@ -66,7 +66,6 @@ struct LevelTasks {
   int sl0 = 0, sl1 = 0;  // depth slices of large CACs (one launch each)
   int gu0 = 0, gu1 = 0;
   int bk0 = 0, bk1 = 0;
-  int head_base = 0, nhead = 0;  // rows of s staged in shared memory by K4b
 };
 
 // One depth slice of a large CAC: rows [r0, r1), heavy-row tasks [h0, h1).
@@ -365,18 +364,6 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.lc1 = static_cast<int>(lcta.size());
     T.gu1 = static_cast<int>(gstate.size());
     T.bk1 = static_cast<int>(blocks.size());
-    // the shared-memory head belongs to the level's largest grid unit (its
-    // rows are ordered by descending in-unit out-degree)
-    long long head_cap = grid_head_capacity();
-    if (const char* e = std::getenv("LR_SPMV_HEAD")) head_cap = std::min<long long>(head_cap, std::atoll(e));
-    long long best = -1;
-    for (int gi = T.gu0; gi < T.gu1; ++gi)
-      if (ctx->gu_nnz[static_cast<size_t>(gi)] > best) {
-        best = ctx->gu_nnz[static_cast<size_t>(gi)];
-        const int u = gstate[static_cast<size_t>(gi)].unit;
-        T.head_base = L->unit_row_begin[u];
-        T.nhead = static_cast<int>(std::min<long long>(head_cap, ctx->gu_rows[static_cast<size_t>(gi)]));
-      }
   }
   // warp tasks first, then CTA tasks, in one array
   const int nw = static_cast<int>(cac_w.size());
@@ -513,7 +500,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 2)], s));
           launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
-                           ctx->status.p, T.head_base, T.nhead, s);
+                           ctx->status.p, s);
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 1)], s));
           ++launches;
           ++spmv_launches;

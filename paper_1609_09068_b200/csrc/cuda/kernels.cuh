@@ -135,11 +135,10 @@ void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, i
                       const double* pf, double* rank, long long* unit_iters, DevStatus* st, cudaStream_t s);
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s);
 int grid_iter_ctas();
-int grid_head_capacity();  // doubles of s one CTA can stage in shared memory
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
-                      DevStatus* st, int head_base, int nhead, cudaStream_t s);
+                      DevStatus* st, cudaStream_t s);
 void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
                    cudaStream_t s);
 void launch_normalize(const double* r3, double* r1, int n, const double* partial, int nparts, double* total,

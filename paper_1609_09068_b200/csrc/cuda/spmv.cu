@@ -8,18 +8,24 @@
 //   long row  one row with kTileNnz < in-degree <= kSegNnz
 //   segment   kSegNnz in-edges of a heavier row; partials combined in segment
 //             order by whichever segment finishes last
-// One persistent CTA per SM of kHeadWarps warps.  Random 8-byte gathers cost
-// one L1 wavefront per distinct 128-byte line, which bounds this kernel; the
-// layout orders a unit's rows by in-unit out-degree, so the most-gathered
-// pushed values sit at the head of the unit, and each CTA stages that head
-// (up to ~19.6k doubles) in shared memory once per launch: gathers that land
-// there cost a bank access instead of a line.  Every warp walks its own
-// strided slice of the task list and never waits on another warp: a tile
-// issues its 8 index loads per lane, its row offsets and epilogue operands,
-// then the 8 gathers, stages them in a warp-private buffer and reduces rows.
+// Persistent CTAs; every warp walks its own strided slice of the task list and
+// never waits on another warp.  The kernel is bound by random 8-byte gathers
+// (one L1 wavefront and one L2 sector per distinct line), so it keeps as many
+// of them in flight as it can and keeps the gathered vector resident in L2:
+//   * a tile issues its 8 index loads per lane, its row offsets and epilogue
+//     operands, then all 8 gathers back to back (clamped addresses instead of
+//     branches, so nothing serialises them), then stages them in a
+//     warp-private shared buffer and reduces rows;
+//   * streamed data (indices, row pointers, rank, pf) is loaded with an L2
+//     evict-first policy and without L1 allocation, the gathered pushed vector
+//     s with evict-last, and the next pushed vector s' is stored evict-last --
+//     the row order (descending in-unit out-degree) packs the most-gathered
+//     entries together, so they stay in L2 across iterations.
 // Rows up to kLongRow in-edges are summed by one lane in the reference's own
 // order (bit-exact with the CPU push scatter); longer rows use a butterfly.
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 #include "devutil.cuh"
 #include "kernels.cuh"
@@ -29,11 +35,45 @@ namespace {
 
 using namespace dev;
 
-constexpr int kHeadWarps = 32;                  // warps per persistent CTA
-constexpr int kHeadThreads = kHeadWarps * 32;
+constexpr int kWarps = kSpmvThreads / 32;
 constexpr int kPerLane = kTileNnz / 32;
 constexpr int kLongRow = 32;
-constexpr int kStageBytes = kHeadWarps * (kTileNnz * 8 + (kTileRows + 1) * 4 + 12);
+
+__device__ __forceinline__ std::uint64_t policy_evict_first() {
+  std::uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ std::uint64_t policy_evict_last() {
+  std::uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// streamed, read-only: no L1 allocation, first out of L2
+__device__ __forceinline__ int ld_stream(const int* p, std::uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ long long ld_stream(const long long* p, std::uint64_t pol) {
+  long long v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p, std::uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// the gathered pushed vector: cached in L1, kept in L2
+__device__ __forceinline__ double ld_keep(const double* p, std::uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, std::uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 
 __global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,52 +118,25 @@ __device__ void finish_iteration(GridUnitState* gs, int gu0, int ngu, const Solv
   st->ctas_done = 0;
 }
 
-__device__ __forceinline__ void epilogue(int row, double y, double rk, double pfr, double* rank, double* s_out,
-                                         double& lmax) {
-  rank[row] = rk + y;
-  s_out[row] = pfr * y;
-  lmax = fmax(lmax, y);
-}
-
-// s_in[i] through the shared head when i lies in [head_base, head_base + nhead).
-__device__ __forceinline__ double gather(const double* __restrict__ s_in, const double* head, int head_base,
-                                         int nhead, int i) {
-  const unsigned h = static_cast<unsigned>(i - head_base);
-  return h < static_cast<unsigned>(nhead) ? head[h] : __ldg(s_in + i);
-}
-
-__global__ void __launch_bounds__(kHeadThreads, 1)
+__global__ void __launch_bounds__(kSpmvThreads)
     k_grid_iter(DeviceLayout L, const SpmvBlock* __restrict__ tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
-                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-                int head_base, int nhead) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* head = reinterpret_cast<double*>(smem);
-  double* vals = head + nhead;                                          // [kHeadWarps][kTileNnz]
-  int* rp = reinterpret_cast<int*>(vals + kHeadWarps * kTileNnz);       // [kHeadWarps][kTileRows + 1]
-  int* wunit = rp + kHeadWarps * (kTileRows + 1);
-  double* wmax = reinterpret_cast<double*>(wunit + kHeadWarps + (kHeadWarps & 1));
+                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st) {
+  __shared__ double vals[kWarps][kTileNnz];
+  __shared__ int rp[kWarps][kTileRows + 1];
+  __shared__ int wunit[kWarps];
+  __shared__ double wmax[kWarps];
   __shared__ int last_cta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* v = vals + warp * kTileNnz;
-  int* wr = rp + warp * (kTileRows + 1);
-
-  // stage the hot head of the pushed vector (read-only during this launch)
-  if (nhead > 0) {
-    const double2* src = reinterpret_cast<const double2*>(s_in + head_base);
-    double2* dst = reinterpret_cast<double2*>(head);
-    const bool aligned = (head_base & 1) == 0;
-    for (int i = threadIdx.x; i < (nhead >> 1); i += blockDim.x)
-      dst[i] = aligned ? __ldg(src + i) : make_double2(__ldg(s_in + head_base + 2 * i), __ldg(s_in + head_base + 2 * i + 1));
-    if ((nhead & 1) && threadIdx.x == 0) head[nhead - 1] = __ldg(s_in + head_base + nhead - 1);
-    __syncthreads();
-  }
-
+  double* v = vals[warp];
+  int* wr = rp[warp];
+  const std::uint64_t stream = policy_evict_first();
+  const std::uint64_t keep = policy_evict_last();
   int cur_unit = -1;
   double lmax = 0.0;
-  const int stride = gridDim.x * kHeadWarps;
-  for (int t = blockIdx.x * kHeadWarps + warp; t < ntasks; t += stride) {
+  const int stride = gridDim.x * kWarps;
+  for (int t = blockIdx.x * kWarps + warp; t < ntasks; t += stride) {
     const SpmvBlock b = tasks[t];
     if (b.gunit != cur_unit) {
       if (cur_unit >= 0) {
@@ -134,25 +147,30 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       lmax = 0.0;
     }
     if (gs[b.gunit].done) continue;
+    const int* isrc = L.isrc + b.nnz_begin;
     if (b.heavy < 0 && b.nnz <= kTileNnz) {
       int idx[kPerLane];
 #pragma unroll
       for (int k = 0; k < kPerLane; ++k) {
         const int e = lane + 32 * k;
-        idx[k] = e < b.nnz ? __ldg(L.isrc + b.nnz_begin + e) : -1;
+        idx[k] = ld_stream(isrc + (e < b.nnz ? e : 0), stream);
       }
       const int nr = b.row_end - b.row_begin;
-      for (int i = lane; i <= nr; i += 32) wr[i] = static_cast<int>(__ldg(L.iptr + b.row_begin + i) - b.nnz_begin);
+      for (int i = lane; i <= nr; i += 32)
+        wr[i] = static_cast<int>(ld_stream(L.iptr + b.row_begin + i, stream) - b.nnz_begin);
       double rk[kTileRows / 32], pfr[kTileRows / 32];
 #pragma unroll
       for (int j = 0; j < kTileRows / 32; ++j) {
-        const int r = lane + 32 * j;
-        rk[j] = r < nr ? rank[b.row_begin + r] : 0.0;
-        pfr[j] = r < nr ? __ldg(pf + b.row_begin + r) : 0.0;
+        const int r = b.row_begin + (lane + 32 * j < nr ? lane + 32 * j : 0);
+        rk[j] = ld_stream(rank + r, stream);
+        pfr[j] = ld_stream(pf + r, stream);
       }
+      double g[kPerLane];
+#pragma unroll
+      for (int k = 0; k < kPerLane; ++k) g[k] = ld_keep(s_in + idx[k], keep);
 #pragma unroll
       for (int k = 0; k < kPerLane; ++k)
-        if (idx[k] >= 0) v[lane + 32 * k] = gather(s_in, head, head_base, nhead, idx[k]);
+        if (lane + 32 * k < b.nnz) v[lane + 32 * k] = g[k];
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < kTileRows / 32; ++j) {
@@ -162,7 +180,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         if (hi - lo > kLongRow) continue;
         double y = 0.0;
         for (int k = lo; k < hi; ++k) y += v[k];
-        epilogue(b.row_begin + r, y, rk[j], pfr[j], rank, s_out, lmax);
+        const int row = b.row_begin + r;
+        rank[row] = rk[j] + y;
+        st_keep(s_out + row, pfr[j] * y, keep);
+        lmax = fmax(lmax, y);
       }
       for (int r = 0; r < nr; ++r) {
         const int lo = wr[r], hi = wr[r + 1];
@@ -171,7 +192,11 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         for (int k = lo + lane; k < hi; k += 32) y += v[k];
         y = warp_sum(y);
         const int row = b.row_begin + r;
-        if (lane == 0) epilogue(row, y, rank[row], pf[row], rank, s_out, lmax);
+        if (lane == 0) {
+          rank[row] += y;
+          st_keep(s_out + row, pf[row] * y, keep);
+          lmax = fmax(lmax, y);
+        }
       }
       __syncwarp();
     } else {
@@ -181,26 +206,36 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
 #pragma unroll
         for (int k = 0; k < kPerLane; ++k) {
           const int e = base + lane + 32 * k;
-          idx[k] = e < b.nnz ? __ldg(L.isrc + b.nnz_begin + e) : -1;
+          idx[k] = ld_stream(isrc + (e < b.nnz ? e : 0), stream);
         }
+        double g[kPerLane];
+#pragma unroll
+        for (int k = 0; k < kPerLane; ++k) g[k] = ld_keep(s_in + idx[k], keep);
 #pragma unroll
         for (int k = 0; k < kPerLane; ++k)
-          if (idx[k] >= 0) part += gather(s_in, head, head_base, nhead, idx[k]);
+          if (base + lane + 32 * k < b.nnz) part += g[k];
       }
       part = warp_sum(part);
+      int row = -1;
+      double y = part;
       if (b.heavy < 0) {
-        if (lane == 0) epilogue(b.row_begin, part, rank[b.row_begin], pf[b.row_begin], rank, s_out, lmax);
+        row = b.row_begin;
       } else if (lane == 0) {
         const HeavyRow h = heavy[b.heavy];
         heavy_part[h.part_begin + b.seg] = part;
         __threadfence();
         if (atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1) {
           __threadfence();
-          double y = 0.0;
+          y = 0.0;
           for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
           heavy_cnt[b.heavy] = 0;
-          epilogue(h.row, y, rank[h.row], pf[h.row], rank, s_out, lmax);
+          row = h.row;
         }
+      }
+      if (lane == 0 && row >= 0) {
+        rank[row] += y;
+        st_keep(s_out + row, pf[row] * y, keep);
+        lmax = fmax(lmax, y);
       }
     }
   }
@@ -211,10 +246,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 0; w < kHeadWarps; ++w) {
+    for (int w = 0; w < kWarps; ++w) {
       if (wunit[w] < 0 || !(wmax[w] > 0.0)) continue;
       double mm = wmax[w];
-      while (w + 1 < kHeadWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
+      while (w + 1 < kWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
       atomicMax(&gs[wunit[w]].max_bits, dbits(mm));
     }
     __threadfence();
@@ -229,33 +264,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
 
 int blocks_for(long long n, int threads) { return static_cast<int>((n + threads - 1) / threads); }
 
-int optin_smem() {
-  static int v = 0;
-  if (v == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes a{};
-    cudaFuncGetAttributes(&a, k_grid_iter);
-    v -= static_cast<int>(a.sharedSizeBytes);
-    cudaFuncSetAttribute(k_grid_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
-  }
-  return v;
-}
-
 }  // namespace
 
 int grid_iter_ctas() {
   static int ctas = 0;
   if (ctas == 0) {
-    int dev = 0;
+    int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads, 0);
+    ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
   return ctas;
 }
-
-int grid_head_capacity() { return (optin_smem() - kStageBytes - 64) / 8 & ~1; }
 
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s) {
   k_grid_reset<<<blocks_for(ngu > 0 ? ngu : 1, 128), 128, 0, s>>>(gs, ngu, st);
@@ -264,15 +285,12 @@ void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                      int head_base, int nhead, cudaStream_t s) {
+                      cudaStream_t s) {
   if (ntasks == 0) return;
-  const int cap = grid_head_capacity();
-  if (nhead > cap) nhead = cap;
-  if (nhead < 0) nhead = 0;
-  const size_t bytes = static_cast<size_t>(nhead) * 8 + kStageBytes + 16;
-  k_grid_iter<<<grid_iter_ctas(), kHeadThreads, bytes, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part,
-                                                            heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
-                                                            head_base, nhead);
+  const int want = blocks_for(ntasks, kWarps);
+  const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
+  k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank,
+                                            s_in, s_out, unit_iters, st);
 }
 
 }  // namespace lrk
