@@ -66,6 +66,10 @@ struct LevelTasks {
   int sl0 = 0, sl1 = 0;  // depth slices of large CACs (one launch each)
   int gu0 = 0, gu1 = 0;
   int bk0 = 0, bk1 = 0;
+  // L2 residency of the largest grid unit's pushed vectors: rows
+  // [hot_begin, hot_begin + hot_rows) evict-last, the rest of the unit evict-first
+  int hot_begin = 0;
+  long long hot_rows = 0, unit_rows = 0;
 };
 
 // One depth slice of a large CAC: rows [r0, r1), heavy-row tasks [h0, h1).
@@ -364,6 +368,25 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.lc1 = static_cast<int>(lcta.size());
     T.gu1 = static_cast<int>(gstate.size());
     T.bk1 = static_cast<int>(blocks.size());
+    // Hot head of the level's largest grid unit: its rows are ordered by
+    // descending in-unit out-degree, so the first rows are the most gathered.
+    // The head of s_in (read) and of s_out (written, read next iteration)
+    // share a fraction of L2 (LR_L2_HOT_FRAC, default 0.7).
+    {
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+      double frac = 0.7;
+      if (const char* e = std::getenv("LR_L2_HOT_FRAC")) frac = std::atof(e);
+      long long best = -1;
+      for (int gi = T.gu0; gi < T.gu1; ++gi) {
+        if (ctx->gu_nnz[static_cast<size_t>(gi)] <= best) continue;
+        best = ctx->gu_nnz[static_cast<size_t>(gi)];
+        const int u = gstate[static_cast<size_t>(gi)].unit;
+        T.hot_begin = L->unit_row_begin[u];
+        T.unit_rows = ctx->gu_rows[static_cast<size_t>(gi)];
+        T.hot_rows = std::min<long long>(T.unit_rows, static_cast<long long>(frac * l2 / 16.0));
+      }
+    }
   }
   // warp tasks first, then CTA tasks, in one array
   const int nw = static_cast<int>(cac_w.size());
@@ -500,7 +523,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 2)], s));
           launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
-                           ctx->status.p, s);
+                           ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, s);
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 1)], s));
           ++launches;
           ++spmv_launches;

@@ -138,7 +138,7 @@ int grid_iter_ctas();
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
-                      DevStatus* st, cudaStream_t s);
+                      DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s);
 void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
                    cudaStream_t s);
 void launch_normalize(const double* r3, double* r1, int n, const double* partial, int nparts, double* total,

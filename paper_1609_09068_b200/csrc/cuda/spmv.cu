@@ -44,9 +44,13 @@ __device__ __forceinline__ std::uint64_t policy_evict_first() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ std::uint64_t policy_evict_last() {
+// evict-last for the hot head [base, base + primary) of a pushed vector,
+// evict-first for the rest of the unit [base + primary, base + total)
+__device__ __forceinline__ std::uint64_t policy_hot_head(const double* base, unsigned primary, unsigned total) {
   std::uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+      : "=l"(p)
+      : "l"(base), "r"(primary), "r"(total));
   return p;
 }
 // streamed, read-only: no L1 allocation, first out of L2
@@ -122,7 +126,8 @@ __global__ void __launch_bounds__(kSpmvThreads)
     k_grid_iter(DeviceLayout L, const SpmvBlock* __restrict__ tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
-                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st) {
+                const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
+                int hot_begin, unsigned hot_bytes, unsigned unit_bytes) {
   __shared__ double vals[kWarps][kTileNnz];
   __shared__ int rp[kWarps][kTileRows + 1];
   __shared__ int wunit[kWarps];
@@ -132,7 +137,8 @@ __global__ void __launch_bounds__(kSpmvThreads)
   double* v = vals[warp];
   int* wr = rp[warp];
   const std::uint64_t stream = policy_evict_first();
-  const std::uint64_t keep = policy_evict_last();
+  const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
+  const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
   int cur_unit = -1;
   double lmax = 0.0;
   const int stride = gridDim.x * kWarps;
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
         for (int k = lo; k < hi; ++k) y += v[k];
         const int row = b.row_begin + r;
         rank[row] = rk[j] + y;
-        st_keep(s_out + row, pfr[j] * y, keep);
+        st_keep(s_out + row, pfr[j] * y, keep_out);
         lmax = fmax(lmax, y);
       }
       for (int r = 0; r < nr; ++r) {
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
         const int row = b.row_begin + r;
         if (lane == 0) {
           rank[row] += y;
-          st_keep(s_out + row, pf[row] * y, keep);
+          st_keep(s_out + row, pf[row] * y, keep_out);
           lmax = fmax(lmax, y);
         }
       }
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
       }
       if (lane == 0 && row >= 0) {
         rank[row] += y;
-        st_keep(s_out + row, pf[row] * y, keep);
+        st_keep(s_out + row, pf[row] * y, keep_out);
         lmax = fmax(lmax, y);
       }
     }
@@ -285,12 +291,13 @@ void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                      cudaStream_t s) {
+                      int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
   if (ntasks == 0) return;
   const int want = blocks_for(ntasks, kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
   k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank,
-                                            s_in, s_out, unit_iters, st);
+                                            s_in, s_out, unit_iters, st, hot_begin,
+                                            static_cast<unsigned>(hot_rows * 8), static_cast<unsigned>(unit_rows * 8));
 }
 
 }  // namespace lrk
