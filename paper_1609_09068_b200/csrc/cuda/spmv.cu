@@ -129,21 +129,45 @@ __global__ void __launch_bounds__(kSpmvThreads)
                 const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
                 int hot_begin, unsigned hot_bytes, unsigned unit_bytes) {
   __shared__ double vals[kWarps][kTileNnz];
-  __shared__ int rp[kWarps][kTileRows + 1];
   __shared__ int wunit[kWarps];
   __shared__ double wmax[kWarps];
   __shared__ int last_cta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* v = vals[warp];
-  int* wr = rp[warp];
   const std::uint64_t stream = policy_evict_first();
   const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
   const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
   int cur_unit = -1;
   double lmax = 0.0;
   const int stride = gridDim.x * kWarps;
-  for (int t = blockIdx.x * kWarps + warp; t < ntasks; t += stride) {
-    const SpmvBlock b = tasks[t];
+
+  // Software pipeline over 256-edge chunks (a tile is one chunk, long rows and
+  // segments up to four): the index loads of chunk i+1 are issued together
+  // with the gathers and row operands of chunk i, so each chunk costs one
+  // memory round trip instead of two.
+  auto seek = [&](int& tt, SpmvBlock& bb) {  // first task at or after tt whose unit still iterates
+    while (tt < ntasks) {
+      bb = tasks[tt];
+      if (!gs[bb.gunit].done) return;
+      tt += stride;
+    }
+  };
+  auto load_idx = [&](const SpmvBlock& bb, int cc, int* out) {
+    const int* src = L.isrc + bb.nnz_begin + static_cast<long long>(cc) * kTileNnz;
+    const int left = bb.nnz - cc * kTileNnz;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int e = lane + 32 * k;
+      out[k] = ld_stream(src + (e < left ? e : 0), stream);
+    }
+  };
+  int t = blockIdx.x * kWarps + warp, c = 0;
+  SpmvBlock b{};
+  seek(t, b);
+  int idx[kPerLane];
+  if (t < ntasks) load_idx(b, 0, idx);
+  double part = 0.0;  // running sum of a multi-chunk task
+  while (t < ntasks) {
     if (b.gunit != cur_unit) {
       if (cur_unit >= 0) {
         const double m = warp_max(lmax);
@@ -152,98 +176,117 @@ __global__ void __launch_bounds__(kSpmvThreads)
       cur_unit = b.gunit;
       lmax = 0.0;
     }
-    if (gs[b.gunit].done) continue;
-    const int* isrc = L.isrc + b.nnz_begin;
-    if (b.heavy < 0 && b.nnz <= kTileNnz) {
-      int idx[kPerLane];
+    const bool tile = b.heavy < 0 && b.nnz <= kTileNnz;
+    const int left = b.nnz - c * kTileNnz;
+    // 1. this chunk's gathers
+    double g[kPerLane];
 #pragma unroll
-      for (int k = 0; k < kPerLane; ++k) {
-        const int e = lane + 32 * k;
-        idx[k] = ld_stream(isrc + (e < b.nnz ? e : 0), stream);
-      }
-      const int nr = b.row_end - b.row_begin;
-      for (int i = lane; i <= nr; i += 32)
-        wr[i] = static_cast<int>(ld_stream(L.iptr + b.row_begin + i, stream) - b.nnz_begin);
-      double rk[kTileRows / 32], pfr[kTileRows / 32];
-#pragma unroll
-      for (int j = 0; j < kTileRows / 32; ++j) {
-        const int r = b.row_begin + (lane + 32 * j < nr ? lane + 32 * j : 0);
-        rk[j] = ld_stream(rank + r, stream);
-        pfr[j] = ld_stream(pf + r, stream);
-      }
-      double g[kPerLane];
-#pragma unroll
-      for (int k = 0; k < kPerLane; ++k) g[k] = ld_keep(s_in + idx[k], keep);
+    for (int k = 0; k < kPerLane; ++k) g[k] = ld_keep(s_in + idx[k], keep);
+    // 2. this tile's row operands, in flight with the gathers
+    const int nr = tile ? b.row_end - b.row_begin : 0;
+    int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+    double rk0 = 0.0, rk1 = 0.0, pf0 = 0.0, pf1 = 0.0;
+    if (tile) {
+      const long long* ip = L.iptr + b.row_begin;
+      const int r0 = lane < nr ? lane : nr - 1, r1 = lane + 32 < nr ? lane + 32 : nr - 1;
+      lo0 = static_cast<int>(ld_stream(ip + r0, stream) - b.nnz_begin);
+      hi0 = static_cast<int>(ld_stream(ip + r0 + 1, stream) - b.nnz_begin);
+      lo1 = static_cast<int>(ld_stream(ip + r1, stream) - b.nnz_begin);
+      hi1 = static_cast<int>(ld_stream(ip + r1 + 1, stream) - b.nnz_begin);
+      rk0 = ld_stream(rank + b.row_begin + r0, stream);
+      pf0 = ld_stream(pf + b.row_begin + r0, stream);
+      rk1 = ld_stream(rank + b.row_begin + r1, stream);
+      pf1 = ld_stream(pf + b.row_begin + r1, stream);
+    }
+    // 3. the next chunk's indices
+    int tn = t, cn = c + 1;
+    SpmvBlock bn = b;
+    if (cn * kTileNnz >= b.nnz) {
+      tn = t + stride;
+      cn = 0;
+      seek(tn, bn);
+    }
+    int idx_n[kPerLane];
+    if (tn < ntasks) load_idx(bn, cn, idx_n);
+    // 4. consume this chunk
+    if (tile) {
 #pragma unroll
       for (int k = 0; k < kPerLane; ++k)
         if (lane + 32 * k < b.nnz) v[lane + 32 * k] = g[k];
       __syncwarp();
-#pragma unroll
-      for (int j = 0; j < kTileRows / 32; ++j) {
-        const int r = lane + 32 * j;
-        if (r >= nr) continue;
-        const int lo = wr[r], hi = wr[r + 1];
-        if (hi - lo > kLongRow) continue;
+      const bool live0 = lane < nr, live1 = lane + 32 < nr;
+      if (live0 && hi0 - lo0 <= kLongRow) {
         double y = 0.0;
-        for (int k = lo; k < hi; ++k) y += v[k];
-        const int row = b.row_begin + r;
-        rank[row] = rk[j] + y;
-        st_keep(s_out + row, pfr[j] * y, keep_out);
+        for (int k = lo0; k < hi0; ++k) y += v[k];
+        rank[b.row_begin + lane] = rk0 + y;
+        st_keep(s_out + b.row_begin + lane, pf0 * y, keep_out);
         lmax = fmax(lmax, y);
       }
-      for (int r = 0; r < nr; ++r) {
-        const int lo = wr[r], hi = wr[r + 1];
-        if (hi - lo <= kLongRow) continue;
+      if (live1 && hi1 - lo1 <= kLongRow) {
         double y = 0.0;
-        for (int k = lo + lane; k < hi; k += 32) y += v[k];
-        y = warp_sum(y);
-        const int row = b.row_begin + r;
-        if (lane == 0) {
+        for (int k = lo1; k < hi1; ++k) y += v[k];
+        rank[b.row_begin + lane + 32] = rk1 + y;
+        st_keep(s_out + b.row_begin + lane + 32, pf1 * y, keep_out);
+        lmax = fmax(lmax, y);
+      }
+      // rows longer than kLongRow: one warp butterfly each
+      for (int half = 0; half < 2; ++half) {
+        const bool is_long = half == 0 ? (live0 && hi0 - lo0 > kLongRow) : (live1 && hi1 - lo1 > kLongRow);
+        unsigned mask = __ballot_sync(0xffffffffu, is_long);
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int lo = __shfl_sync(0xffffffffu, half == 0 ? lo0 : lo1, src);
+          const int hi = __shfl_sync(0xffffffffu, half == 0 ? hi0 : hi1, src);
+          const double rk = __shfl_sync(0xffffffffu, half == 0 ? rk0 : rk1, src);
+          const double pr = __shfl_sync(0xffffffffu, half == 0 ? pf0 : pf1, src);
+          double y = 0.0;
+          for (int k = lo + lane; k < hi; k += 32) y += v[k];
+          y = warp_sum(y);
+          if (lane == 0) {
+            const int row = b.row_begin + src + 32 * half;
+            rank[row] = rk + y;
+            st_keep(s_out + row, pr * y, keep_out);
+            lmax = fmax(lmax, y);
+          }
+        }
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPerLane; ++k)
+        if (lane + 32 * k < left) part += g[k];
+      if (left <= kTileNnz) {  // last chunk of a long row or segment
+        const double sum = warp_sum(part);
+        part = 0.0;
+        int row = -1;
+        double y = sum;
+        if (b.heavy < 0) {
+          row = b.row_begin;
+        } else if (lane == 0) {
+          const HeavyRow h = heavy[b.heavy];
+          heavy_part[h.part_begin + b.seg] = sum;
+          __threadfence();
+          if (atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1) {
+            __threadfence();
+            y = 0.0;
+            for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
+            heavy_cnt[b.heavy] = 0;
+            row = h.row;
+          }
+        }
+        if (lane == 0 && row >= 0) {
           rank[row] += y;
           st_keep(s_out + row, pf[row] * y, keep_out);
           lmax = fmax(lmax, y);
         }
       }
-      __syncwarp();
-    } else {
-      double part = 0.0;
-      for (int base = 0; base < b.nnz; base += kTileNnz) {
-        int idx[kPerLane];
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) {
-          const int e = base + lane + 32 * k;
-          idx[k] = ld_stream(isrc + (e < b.nnz ? e : 0), stream);
-        }
-        double g[kPerLane];
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) g[k] = ld_keep(s_in + idx[k], keep);
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k)
-          if (base + lane + 32 * k < b.nnz) part += g[k];
-      }
-      part = warp_sum(part);
-      int row = -1;
-      double y = part;
-      if (b.heavy < 0) {
-        row = b.row_begin;
-      } else if (lane == 0) {
-        const HeavyRow h = heavy[b.heavy];
-        heavy_part[h.part_begin + b.seg] = part;
-        __threadfence();
-        if (atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1) {
-          __threadfence();
-          y = 0.0;
-          for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
-          heavy_cnt[b.heavy] = 0;
-          row = h.row;
-        }
-      }
-      if (lane == 0 && row >= 0) {
-        rank[row] += y;
-        st_keep(s_out + row, pf[row] * y, keep_out);
-        lmax = fmax(lmax, y);
-      }
     }
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) idx[k] = idx_n[k];
+    t = tn;
+    c = cn;
+    b = bn;
   }
   const double m = warp_max(lmax);
   if (lane == 0) {
