@@ -33,7 +33,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "liblevelrank_b200.so")
+_SO = os.environ.get("LR_LIB") or os.path.join(_HERE, "liblevelrank_b200.so")  # LR_LIB: A/B builds only
 
 I32P = C.POINTER(C.c_int32)
 I64P = C.POINTER(C.c_int64)

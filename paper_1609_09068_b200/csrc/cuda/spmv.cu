@@ -40,6 +40,7 @@ using namespace dev;
 constexpr int kWarps = kSpmvThreads / 32;
 constexpr int kPerLane = kTileNnz / 32;
 constexpr int kLongRow = 32;
+constexpr int kL1HotRows = 16384;  // columns allowed to allocate in L1 (see ld_gather)
 
 __device__ __forceinline__ std::uint64_t policy_evict_first() {
   std::uint64_t p;
@@ -71,11 +72,28 @@ __device__ __forceinline__ double ld_stream(const double* p, std::uint64_t pol) 
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
-// the gathered pushed vector: cached in L1, kept in L2
+// The gathered pushed vector.  Only its hottest columns (the first rows of
+// the degree-ordered unit) may allocate in L1, so that cold gathers -- the
+// great majority, each touching a different line -- do not evict them: a
+// predicated allocating load and a predicated non-allocating load are both
+// issued and selected afterwards (no branch, all gathers stay in flight).
 __device__ __forceinline__ double ld_keep(const double* p, std::uint64_t pol) {
   double v;
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
+}
+__device__ __forceinline__ double ld_gather(const double* p, std::uint64_t pol, unsigned hot) {
+  double a = 0.0, b = 0.0;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+      : "+d"(a)
+      : "l"(p), "r"(hot), "l"(pol));
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], "
+      "%3;\n\t}"
+      : "+d"(b)
+      : "l"(p), "r"(hot), "l"(pol));
+  return hot ? a : b;
 }
 __device__ __forceinline__ void st_keep(double* p, double v, std::uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
@@ -129,7 +147,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
                 const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-                int hot_begin, unsigned hot_bytes, unsigned unit_bytes) {
+                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int l1_hot) {
   __shared__ double vals[kWarps][kTileNnz];
   __shared__ int wunit[kWarps];
   __shared__ double wmax[kWarps];
@@ -183,7 +201,8 @@ __global__ void __launch_bounds__(kSpmvThreads)
     // 1. this chunk's gathers
     double g[kPerLane];
 #pragma unroll
-    for (int k = 0; k < kPerLane; ++k) g[k] = ld_keep(s_in + idx[k], keep);
+    for (int k = 0; k < kPerLane; ++k)
+      g[k] = ld_gather(s_in + idx[k], keep, static_cast<unsigned>(idx[k] - hot_begin) < static_cast<unsigned>(l1_hot));
     // 2. this tile's row operands, in flight with the gathers
     const int nr = tile ? b.row_end - b.row_begin : 0;
     int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
@@ -313,215 +332,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
   }
 }
 
-// ---------------------------------------------------------------------------
-// K4b-head: the same iteration for very large units, one 1024-thread CTA per SM
-// holding the first `nhead` entries of s_in (the most-gathered columns, by the
-// layout's degree order) in shared memory.  At config 5 the kernel above moves
-// ~38 GB of L2 sectors per iteration -- one 32-byte sector per gather -- which
-// is the L2 throughput bound; every gather served from shared memory removes a
-// sector.  Gathers are branch-free: a predicated global load and a predicated
-// shared load are both issued and selected afterwards, so all eight stay in
-// flight together.
-constexpr int kHeadWarps = 32;
-constexpr int kHeadThreads = kHeadWarps * 32;
-constexpr int kHeadStage = kHeadWarps * (kTileNnz * 8 + (kTileRows + 1) * 4) + kHeadWarps * 12 + 64;
-
-__device__ __forceinline__ double ld_keep_if(const double* p, std::uint64_t pol, unsigned on) {
-  double v = 0.0;
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
-      : "+d"(v)
-      : "l"(p), "r"(on), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double lds_if(unsigned saddr, unsigned on) {
-  double v = 0.0;
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
-               : "+d"(v)
-               : "r"(saddr), "r"(on));
-  return v;
-}
-
-__global__ void __launch_bounds__(kHeadThreads, 1)
-    k_grid_iter_head(DeviceLayout L, const SpmvBlock* __restrict__ tasks, int ntasks, int gu0, int ngu,
-                     GridUnitState* gs, const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
-                     const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
-                     const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters,
-                     DevStatus* st, int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* head = reinterpret_cast<double*>(smem);
-  double* vals = head + nhead;
-  int* rp = reinterpret_cast<int*>(vals + kHeadWarps * kTileNnz);
-  int* wunit = rp + kHeadWarps * (kTileRows + 1);
-  double* wmax = reinterpret_cast<double*>(wunit + kHeadWarps);
-  __shared__ int last_cta;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* v = vals + warp * kTileNnz;
-  int* wr = rp + warp * (kTileRows + 1);
-  const std::uint64_t stream = policy_evict_first();
-  const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
-  const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
-  const unsigned head_s = static_cast<unsigned>(__cvta_generic_to_shared(head));
-  {
-    const double* src = s_in + hot_begin;
-    for (int i = threadIdx.x; i < nhead; i += kHeadThreads) head[i] = ld_keep(src + i, keep);
-    __syncthreads();
-  }
-  auto gather = [&](int i) -> double {
-    const unsigned h = static_cast<unsigned>(i - hot_begin);
-    const unsigned in = h < static_cast<unsigned>(nhead);
-    const double a = ld_keep_if(s_in + i, keep, in ^ 1u);
-    const double b = lds_if(head_s + (in ? h : 0u) * 8u, in);
-    return in ? b : a;
-  };
-  int cur_unit = -1;
-  double lmax = 0.0;
-  const int stride = gridDim.x * kHeadWarps;
-  for (int t = blockIdx.x * kHeadWarps + warp; t < ntasks; t += stride) {
-    const SpmvBlock b = tasks[t];
-    if (b.gunit != cur_unit) {
-      if (cur_unit >= 0) {
-        const double m = warp_max(lmax);
-        if (lane == 0 && m > 0.0) atomicMax(&gs[cur_unit].max_bits, dbits(m));
-      }
-      cur_unit = b.gunit;
-      lmax = 0.0;
-    }
-    if (gs[b.gunit].done) continue;
-    const int* isrc = L.isrc + b.nnz_begin;
-    if (b.heavy < 0 && b.nnz <= kTileNnz) {
-      int idx[kPerLane];
-#pragma unroll
-      for (int k = 0; k < kPerLane; ++k) {
-        const int e = lane + 32 * k;
-        idx[k] = ld_stream(isrc + (e < b.nnz ? e : 0), stream);
-      }
-      const int nr = b.row_end - b.row_begin;
-      for (int i = lane; i <= nr; i += 32)
-        wr[i] = static_cast<int>(ld_stream(L.iptr + b.row_begin + i, stream) - b.nnz_begin);
-      double rk[kTileRows / 32], pfr[kTileRows / 32];
-#pragma unroll
-      for (int j = 0; j < kTileRows / 32; ++j) {
-        const int r = b.row_begin + (lane + 32 * j < nr ? lane + 32 * j : 0);
-        rk[j] = ld_stream(rank + r, stream);
-        pfr[j] = ld_stream(pf + r, stream);
-      }
-      double g[kPerLane];
-#pragma unroll
-      for (int k = 0; k < kPerLane; ++k) g[k] = gather(idx[k]);
-#pragma unroll
-      for (int k = 0; k < kPerLane; ++k)
-        if (lane + 32 * k < b.nnz) v[lane + 32 * k] = g[k];
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < kTileRows / 32; ++j) {
-        const int r = lane + 32 * j;
-        if (r >= nr) continue;
-        const int lo = wr[r], hi = wr[r + 1];
-        if (hi - lo > kLongRow) continue;
-        double y = 0.0;
-        for (int k = lo; k < hi; ++k) y += v[k];
-        const int row = b.row_begin + r;
-        rank[row] = rk[j] + y;
-        st_keep(s_out + row, pfr[j] * y, keep_out);
-        lmax = fmax(lmax, y);
-      }
-      for (int r = 0; r < nr; ++r) {
-        const int lo = wr[r], hi = wr[r + 1];
-        if (hi - lo <= kLongRow) continue;
-        double y = 0.0;
-        for (int k = lo + lane; k < hi; k += 32) y += v[k];
-        y = warp_sum(y);
-        const int row = b.row_begin + r;
-        if (lane == 0) {
-          rank[row] += y;
-          st_keep(s_out + row, pf[row] * y, keep_out);
-          lmax = fmax(lmax, y);
-        }
-      }
-      __syncwarp();
-    } else {
-      double part = 0.0;
-      for (int base = 0; base < b.nnz; base += kTileNnz) {
-        int idx[kPerLane];
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) {
-          const int e = base + lane + 32 * k;
-          idx[k] = ld_stream(isrc + (e < b.nnz ? e : 0), stream);
-        }
-        double g[kPerLane];
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) g[k] = gather(idx[k]);
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k)
-          if (base + lane + 32 * k < b.nnz) part += g[k];
-      }
-      part = warp_sum(part);
-      int row = -1;
-      double y = part;
-      if (b.heavy < 0) {
-        row = b.row_begin;
-      } else if (lane == 0) {
-        const HeavyRow h = heavy[b.heavy];
-        heavy_part[h.part_begin + b.seg] = part;
-        __threadfence();
-        if (atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1) {
-          __threadfence();
-          y = 0.0;
-          for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
-          heavy_cnt[b.heavy] = 0;
-          row = h.row;
-        }
-      }
-      if (lane == 0 && row >= 0) {
-        rank[row] += y;
-        st_keep(s_out + row, pf[row] * y, keep_out);
-        lmax = fmax(lmax, y);
-      }
-    }
-  }
-  const double m = warp_max(lmax);
-  if (lane == 0) {
-    wunit[warp] = cur_unit;
-    wmax[warp] = m;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < kHeadWarps; ++w) {
-      if (wunit[w] < 0 || !(wmax[w] > 0.0)) continue;
-      double mm = wmax[w];
-      while (w + 1 < kHeadWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
-      atomicMax(&gs[wunit[w]].max_bits, dbits(mm));
-    }
-    __threadfence();
-    last_cta = atomicAdd(&st->ctas_done, 1) == static_cast<int>(gridDim.x) - 1;
-  }
-  __syncthreads();
-  if (last_cta && threadIdx.x == 0) {
-    __threadfence();
-    finish_iteration(gs, gu0, ngu, p, unit_iters, st);
-  }
-}
-
 int blocks_for(long long n, int threads) { return static_cast<int>((n + threads - 1) / threads); }
-
-// doubles of s one CTA of k_grid_iter_head can hold next to its staging buffers
-int head_capacity() {
-  static int cap = -1;
-  if (cap < 0) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes a{};
-    cudaFuncGetAttributes(&a, k_grid_iter_head);
-    const int dyn = optin - static_cast<int>(a.sharedSizeBytes);
-    cudaFuncSetAttribute(k_grid_iter_head, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    cap = ((dyn - kHeadStage) / 8) & ~1;
-    if (const char* e = std::getenv("LR_SPMV_HEAD")) cap = std::min(cap, std::atoi(e));
-    if (cap < 0) cap = 0;
-  }
-  return cap;
-}
 
 }  // namespace
 
@@ -547,22 +358,14 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks,
                       int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
   if (ntasks == 0) return;
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
-  // very large units (the giant SCC of R-MAT graphs): shared-memory head
-  const int cap = head_capacity();
-  if (cap > 0 && unit_rows >= 64LL * cap) {
-    int sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t bytes = static_cast<size_t>(cap) * 8 + kHeadStage;
-    k_grid_iter_head<<<sms, kHeadThreads, bytes, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p,
-                                                      pf, rank, s_in, s_out, unit_iters, st, hot_begin, hot_bytes,
-                                                      unit_bytes, cap);
-    return;
-  }
   const int want = blocks_for(ntasks, kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
+  static const int l1_hot = [] {
+    const char* e = std::getenv("LR_L1_HOT");
+    return e ? std::atoi(e) : kL1HotRows;
+  }();
   k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank,
-                                            s_in, s_out, unit_iters, st, hot_begin, hot_bytes, unit_bytes);
+                                            s_in, s_out, unit_iters, st, hot_begin, hot_bytes, unit_bytes, l1_hot);
 }
 
 }  // namespace lrk
