@@ -193,7 +193,13 @@ def run_ours(args):
 
     g, gen_ms = build_graph(lr, args.config, args.shrink)
     log(f"[rank {rank}] graph n={g.n} m={g.m} built in {gen_ms / 1e3:.1f}s")
-    eng = lr.Engine(g, 100, device=local)
+    if world > 1:
+        # the giant SCC is row-sharded over the ranks; NCCL id from rank 0
+        obj = [lr.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng = lr.Engine(g, 100, device=local, rank=rank, world=world, nccl_id=obj[0])
+    else:
+        eng = lr.Engine(g, 100, device=local)
     log(f"[rank {rank}] plan {eng.plan_ms / 1e3:.1f}s upload {eng.upload_ms / 1e3:.1f}s "
         f"device bytes {eng.device_bytes() / 1e9:.2f} GB")
     n = g.n
@@ -243,7 +249,7 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * work / (ms / 1e3) / 1e9
+    value = work / (ms / 1e3) / 1e9  # one job split over the ranks (strong scaling)
 
     # e2e through lr_solve with pinned host buffers
     w_h = torch.full((n,), 1.0 / n, dtype=torch.float64).pin_memory()
@@ -271,7 +277,7 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = world * work / (e2e_ms / 1e3) / 1e9
+    e2e_value = work / (e2e_ms / 1e3) / 1e9
     # parity spot check of the timed path vs the host-API result
     assert torch.equal(r3_h, torch.from_numpy(r3h)), "device-resident and host-API solves differ"
 
@@ -305,14 +311,15 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config, args.shrink), "c": C_DAMP, "tol": TOL,
                        "vertices": n, "edges": g.m, "edge_updates_per_step": work,
                        "iterative_edge_work": int(info0["iterative_edge_work"]),
                        "large_scc_iterations": int(iters[large].max()) if large.any() else 0,
                        "levels": int(layout["n_levels"]), "units": int(layout["n_units"]),
                        "l2": "flushed (512 MB write) before every timed step",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"giant-SCC rows sharded over {world} GPUs (NCCL exchange per iteration), "
+                                       "other units replicated") if world > 1 else "1 GPU",
                        "setup_s": {"generate": gen_ms / 1e3, "plan": eng.plan_ms / 1e3,
                                    "upload": eng.upload_ms / 1e3}},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 8 * n,

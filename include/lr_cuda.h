@@ -161,6 +161,21 @@ lr_status lr_solve(lr_ctx* ctx, const double* w, double c, double tol, double* r
  * unit_iters stays a host pointer.  Stream-ordered on lr_ctx_stream(). */
 lr_status lr_solve_device(lr_ctx* ctx, const double* w_dev, double c, double tol, double* r3_dev,
                           double* r1_dev, lr_solve_info* info, int64_t* unit_iters);
+/* ------------------------------------------------------------ multi-GPU */
+/* The grid-wide SccLarge units (the giant SCC) can be row-sharded over the
+ * GPUs of one node (the reference is single-process,
+ * SPEC.md:383).  Every rank builds the same plan and calls lr_ctx_set_comm
+ * before lr_ctx_upload; each rank then iterates only its nnz-balanced row
+ * shard, and after every iteration the shards of s' are exchanged in place
+ * over NCCL (grouped broadcasts) together with an all-reduce(max) of the shard
+ * maxima, so every rank takes the same stop decision.  All other units are
+ * solved redundantly on every rank; results are identical on all ranks. */
+lr_status lr_nccl_unique_id(char* out128);
+lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* unique_id128);
+/* The nnz-balanced split used for the shards: bounds[world + 1] over rows
+ * [row_begin, row_end) of a pull CSR with row pointers iptr. */
+lr_status lr_shard_rows(const int64_t* iptr, int32_t row_begin, int32_t row_end, int32_t world, int32_t* bounds);
+
 /* cudaStream_t the context launches on. */
 void* lr_ctx_stream(lr_ctx* ctx);
 /* Device bytes held by the context. */

@@ -144,6 +144,9 @@ EXPORTS = {
     "lr_ctx_upload": (C.c_int, [VP, C.POINTER(_Layout)]),
     "lr_solve": (C.c_int, [VP, F64P, C.c_double, C.c_double, F64P, F64P, C.POINTER(_SolveInfo), I64P]),
     "lr_solve_device": (C.c_int, [VP, VP, C.c_double, C.c_double, VP, VP, C.POINTER(_SolveInfo), I64P]),
+    "lr_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "lr_ctx_set_comm": (C.c_int, [VP, C.c_int, C.c_int, C.c_char_p]),
+    "lr_shard_rows": (C.c_int, [I64P, C.c_int32, C.c_int32, C.c_int32, I32P]),
     "lr_ctx_stream": (VP, [VP]),
     "lr_ctx_device_bytes": (C.c_int64, [VP]),
     "lr_ctx_free": (None, [VP]),
@@ -425,6 +428,21 @@ def propagate_weights(src, dst, src_out_degree, ranks, c, weights, device=0):
     return w
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL id (rank 0 creates it and broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().lr_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(iptr, row_begin: int, row_end: int, world: int) -> np.ndarray:
+    """The nnz-balanced row split the multi-GPU solve uses (lr_shard_rows)."""
+    ip = np.ascontiguousarray(iptr, np.int64)
+    out = np.zeros(world + 1, np.int32)
+    _check(lib().lr_shard_rows(_p(ip, I64P), int(row_begin), int(row_end), int(world), _p(out, I32P)))
+    return out
+
+
 @dataclass
 class EngineResult:
     ranks: np.ndarray          # R3 (non-normalised PageRank), vertex order
@@ -437,7 +455,10 @@ class EngineResult:
 class Engine:
     """Plan once, upload once, then solve any number of weight vectors on one GPU."""
 
-    def __init__(self, g: Graph, small_threshold: int = 100, device: int = 0):
+    def __init__(self, g: Graph, small_threshold: int = 100, device: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None):
+        """rank/world/nccl_id: row-shard the giant SCC units over `world` GPUs
+        (one process per GPU, every rank passes the same graph and id)."""
         import time
         t0 = time.perf_counter()
         self.plan = Plan(g, small_threshold)
@@ -447,6 +468,8 @@ class Engine:
         h = VP()
         _check(lib().lr_ctx_create(int(device), C.byref(h)))
         self._h = h
+        if world > 1 or nccl_id is not None:
+            _check(lib().lr_ctx_set_comm(h, int(rank), int(world), nccl_id))
         self._layout = _Layout()
         _check(lib().lr_plan_layout(self.plan._h, C.byref(self._layout)))
         t1 = time.perf_counter()

@@ -13,6 +13,9 @@
 #include "kernels.cuh"
 #include "lr_cuda.h"
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only; the library is resolved at run time (see nccl())
+
 namespace lrerr {
 void set(const std::string& msg);
 }
@@ -77,6 +80,64 @@ struct CacSlice {
   int r0, r1, h0, h1;
 };
 
+// NCCL, resolved with dlopen so the library loads (and every single-GPU path
+// works) where NCCL is absent; in a torch process this binds to the libnccl.so.2
+// torch already loaded.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(h, "ncclBroadcast"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.broadcast && a.all_reduce && a.group_start &&
+           a.group_end && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+#define LR_NCCL_TRY(expr)                                                                          \
+  do {                                                                                             \
+    const ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess) {                                                                       \
+      lrerr::set(std::string("NCCL error: ") + nccl().error_string(r_) + " at " #expr);            \
+      return LR_ENCCL;                                                                             \
+    }                                                                                              \
+  } while (0)
+
+// nnz-balanced contiguous split of rows [rb, re) over `world` parts (iptr is
+// the row-pointer array of the whole layout).
+std::vector<int> shard_bounds(const int64_t* iptr, int rb, int re, int world) {
+  std::vector<int> b(static_cast<size_t>(world) + 1, rb);
+  const long long e0 = iptr[rb], total = iptr[re] - e0;
+  for (int r = 1; r < world; ++r) {
+    const long long target = e0 + total * r / world;
+    b[static_cast<size_t>(r)] = static_cast<int>(std::lower_bound(iptr + rb, iptr + re, target) - iptr);
+  }
+  b[static_cast<size_t>(world)] = re;
+  for (int r = 1; r <= world; ++r) b[static_cast<size_t>(r)] = std::max(b[static_cast<size_t>(r)], b[static_cast<size_t>(r) - 1]);
+  return b;
+}
+
 }  // namespace
 
 struct lr_ctx {
@@ -118,6 +179,11 @@ struct lr_ctx {
   std::vector<cudaEvent_t> lev;              // per-launch event pairs (grid SpMV)
   int64_t launches = 0;
   int64_t spmv_launches = 0;
+  // multi-GPU: grid SccLarge units row-sharded over `world` ranks of `comm`
+  int shard = 0, nshards = 1;  // this process's rank / world size
+  ncclComm_t comm = nullptr;
+  std::vector<std::vector<int>> gu_bounds;  // per grid unit: world + 1 row bounds
+  DevBuf<double> maxbuf;                     // per grid unit: shard max, all-reduced
 
   DeviceLayout dl() const {
     DeviceLayout L;
@@ -142,6 +208,7 @@ struct lr_ctx {
     if (stream) cudaStreamDestroy(stream);
     if (h_params) cudaFreeHost(h_params);
     if (h_status) cudaFreeHost(h_status);
+    if (comm) nccl().comm_destroy(comm);
   }
 };
 
@@ -241,6 +308,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   ctx->lt.assign(static_cast<size_t>(L->n_levels), LevelTasks{});
   ctx->gu_rows.clear();
   ctx->gu_nnz.clear();
+  ctx->gu_bounds.clear();
   ctx->cac_slices.clear();
   int max_small = 0;
   bool small_needs_scratch = false;
@@ -316,8 +384,12 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           rk = kLargeGrid;
           const int gu = static_cast<int>(gstate.size());
           const size_t first_block = blocks.size();
-          int r = rb;
-          while (r < re) {
+          // multi-GPU: this rank owns rows [own0, own1) of the unit (nnz-balanced)
+          ctx->gu_bounds.push_back(shard_bounds(L->iptr, rb, re, ctx->nshards));
+          const int own0 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard)];
+          const int own1 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard) + 1];
+          int r = own0;
+          while (r < own1) {
             const long long len = L->iptr[r + 1] - L->iptr[r];
             if (len > kTileNnz) {
               if (len <= kSegNnz) {
@@ -338,7 +410,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             }
             const int start = r;
             long long acc = 0;
-            while (r < re && r - start < kTileRows) {
+            while (r < own1 && r - start < kTileRows) {
               const long long l2 = L->iptr[r + 1] - L->iptr[r];
               if (l2 > kTileNnz || acc + l2 > kTileNnz) break;
               acc += l2;
@@ -346,8 +418,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             }
             blocks.push_back(SpmvBlock{L->iptr[start], static_cast<int>(acc), start, r, gu, -1, 0});
           }
-          ctx->gu_rows.push_back(m);
-          ctx->gu_nnz.push_back(L->iptr[re] - L->iptr[rb]);
+          ctx->gu_rows.push_back(own1 - own0);  // roofline bookkeeping: this rank's share
+          ctx->gu_nnz.push_back(L->iptr[own1] - L->iptr[own0]);
           GridUnitState g{};
           g.unit = u;
           g.nblocks = static_cast<int>(blocks.size() - first_block);
@@ -383,7 +455,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         best = ctx->gu_nnz[static_cast<size_t>(gi)];
         const int u = gstate[static_cast<size_t>(gi)].unit;
         T.hot_begin = L->unit_row_begin[u];
-        T.unit_rows = ctx->gu_rows[static_cast<size_t>(gi)];
+        T.unit_rows = L->unit_row_begin[u + 1] - L->unit_row_begin[u];
         T.hot_rows = std::min<long long>(T.unit_rows, static_cast<long long>(frac * l2 / 16.0));
       }
     }
@@ -433,12 +505,35 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   const bool any_grid = !gstate.empty();
   LR_CUDA_TRY(ctx->s0.alloc(any_grid ? nn : 0));
   LR_CUDA_TRY(ctx->s1.alloc(any_grid ? nn : 0));
+  LR_CUDA_TRY(ctx->maxbuf.alloc(gstate.size()));
   ctx->nparts = static_cast<int>((nn + kOutBlock - 1) / kOutBlock);
   LR_CUDA_TRY(ctx->partial.alloc(static_cast<size_t>(std::max(ctx->nparts, 1))));
   LR_CUDA_TRY(ctx->total.alloc(1));
   LR_CUDA_TRY(ctx->unit_iters.alloc(static_cast<size_t>(L->n_units)));
   LR_CUDA_TRY(cudaStreamSynchronize(s));
   ctx->loaded = true;
+  return LR_OK;
+}
+
+// Multi-GPU exchange for the grid units of one level: each rank's row shard of
+// `buf` is broadcast in place to all ranks (grouped broadcasts = an all-gather
+// with uneven shards); with_max also all-reduces the shard maxima in maxbuf.
+static lr_status exchange_shards(lr_ctx* ctx, const LevelTasks& T, double* buf, bool with_max) {
+  const NcclApi& nc = nccl();
+  LR_NCCL_TRY(nc.group_start());
+  for (int gi = T.gu0; gi < T.gu1; ++gi) {
+    const std::vector<int>& b = ctx->gu_bounds[static_cast<size_t>(gi)];
+    for (int r = 0; r < ctx->nshards; ++r) {
+      const size_t cnt = static_cast<size_t>(b[static_cast<size_t>(r) + 1] - b[static_cast<size_t>(r)]);
+      if (cnt == 0) continue;
+      double* p = buf + b[static_cast<size_t>(r)];
+      LR_NCCL_TRY(nc.broadcast(p, p, cnt, ncclDouble, r, ctx->comm, ctx->stream));
+    }
+  }
+  if (with_max)
+    LR_NCCL_TRY(nc.all_reduce(ctx->maxbuf.p + T.gu0, ctx->maxbuf.p + T.gu0, static_cast<size_t>(T.gu1 - T.gu0),
+                              ncclDouble, ncclMax, ctx->comm, ctx->stream));
+  LR_NCCL_TRY(nc.group_end());
   return LR_OK;
 }
 
@@ -521,12 +616,22 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
             ctx->lev.push_back(e);
           }
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 2)], s));
+          const bool sharded = ctx->comm != nullptr;
           launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
-                           ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, s);
+                           ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, sharded ? ctx->maxbuf.p : nullptr, s);
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 1)], s));
           ++launches;
           ++spmv_launches;
+          if (sharded) {
+            // exchange step: every rank's s' shard to every rank (grouped
+            // broadcasts = an in-place all-gather with uneven shards), and the
+            // max of the shard maxima; then the same stop decision everywhere
+            if (const lr_status xs = exchange_shards(ctx, T, sout, true); xs != LR_OK) return xs;
+            launch_grid_finish(ctx->gstate.p, T.gu0, T.gu1 - T.gu0, ctx->params.p, ctx->unit_iters.p, ctx->status.p,
+                               ctx->maxbuf.p, s);
+            ++launches;
+          }
         }
         LR_CUDA_TRY(cudaMemcpyAsync(&ctx->h_status->active, &ctx->status.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
         LR_CUDA_TRY(cudaStreamSynchronize(s));
@@ -555,6 +660,9 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
         active_ms += lm;
       }
       active_launches += std::min(kmax, k);
+      // lower levels read these units' final ranks: replicate them on every rank
+      if (ctx->comm)
+        if (const lr_status xs = exchange_shards(ctx, T, ctx->rank.p, false); xs != LR_OK) return xs;
     }
   }
   launch_output(L, ctx->rank.p, r3_dev, ctx->partial.p, ctx->nparts, s);
@@ -622,6 +730,54 @@ lr_status lr_solve(lr_ctx* ctx, const double* w, double c, double tol, double* r
     LR_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   }
   return st;
+}
+
+lr_status lr_nccl_unique_id(char* out128) {
+  const NcclApi& nc = nccl();
+  if (!nc.ok) {
+    lrerr::set("libnccl.so.2 not loadable");
+    return LR_ENCCL;
+  }
+  ncclUniqueId id;
+  LR_NCCL_TRY(nc.get_unique_id(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof id);
+  return LR_OK;
+}
+
+lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* id128) {
+  if (!ctx || world < 1 || rank < 0 || rank >= world) {
+    lrerr::set("bad rank / world");
+    return LR_EINVAL;
+  }
+  if (ctx->comm) {
+    nccl().comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ctx->shard = rank;
+  ctx->nshards = world;
+  ctx->loaded = false;  // the next upload shards the grid units
+  if (world == 1 && !id128) return LR_OK;
+  const NcclApi& nc = nccl();
+  if (!nc.ok) {
+    lrerr::set("libnccl.so.2 not loadable");
+    return LR_ENCCL;
+  }
+  LR_CUDA_TRY(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  LR_NCCL_TRY(nc.comm_init_rank(&ctx->comm, world, id, rank));
+  return LR_OK;
+}
+
+lr_status lr_shard_rows(const int64_t* iptr, int32_t row_begin, int32_t row_end, int32_t world, int32_t* bounds) {
+  if (!iptr || !bounds || world < 1 || row_end < row_begin) {
+    lrerr::set("bad shard request");
+    return LR_EINVAL;
+  }
+  const std::vector<int> b = shard_bounds(iptr, row_begin, row_end, world);
+  std::copy(b.begin(), b.end(), bounds);
+  return LR_OK;
 }
 
 lr_status lr_propagate_weights(int device, const int32_t* src, const int32_t* dst, const int32_t* deg, int64_t m,

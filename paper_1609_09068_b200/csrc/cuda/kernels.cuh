@@ -138,7 +138,12 @@ int grid_iter_ctas();
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
-                      DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s);
+                      DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, double* maxbuf,
+                      cudaStream_t s);
+// multi-GPU: close an iteration from the all-reduced shard maxima in maxbuf
+void launch_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
+                        DevStatus* st, const double* maxbuf, cudaStream_t s);
+void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s);
 void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
                    cudaStream_t s);
 void launch_normalize(const double* r3, double* r1, int n, const double* partial, int nparts, double* total,

@@ -114,12 +114,14 @@ __global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
 
 // Run by the last CTA of a launch: closes the iteration of every unit of the
 // level -- stop when max|inc| < tol (solvers.cpp:160), fail past the cap (:159).
+// `maxbuf` (multi-GPU): the all-reduced maxima of the row shards, else this
+// launch's own max.
 __device__ void finish_iteration(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
-                                 DevStatus* st) {
+                                 DevStatus* st, const double* maxbuf = nullptr) {
   for (int i = gu0; i < gu0 + ngu; ++i) {
     GridUnitState* u = gs + i;
     if (u->done) continue;
-    const double mx = bitsd(atomicAdd(&u->max_bits, 0ull));
+    const double mx = maxbuf ? maxbuf[i] : bitsd(atomicAdd(&u->max_bits, 0ull));
     const int it = u->iterations + 1;
     u->iterations = it;
     u->max_bits = 0ull;
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
                 const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int l1_hot) {
+                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int l1_hot, double* maxbuf) {
   __shared__ double vals[kWarps][kTileNnz];
   __shared__ int wunit[kWarps];
   __shared__ double wmax[kWarps];
@@ -328,8 +330,26 @@ __global__ void __launch_bounds__(kSpmvThreads)
   __syncthreads();
   if (last_cta && threadIdx.x == 0) {
     __threadfence();
-    finish_iteration(gs, gu0, ngu, p, unit_iters, st);
+    if (maxbuf) {  // row-sharded: publish the shard max, decide after the all-reduce
+      for (int i = gu0; i < gu0 + ngu; ++i) {
+        maxbuf[i] = bitsd(atomicAdd(&gs[i].max_bits, 0ull));
+        gs[i].max_bits = 0ull;
+      }
+      st->ctas_done = 0;
+    } else {
+      finish_iteration(gs, gu0, ngu, p, unit_iters, st);
+    }
   }
+}
+
+__global__ void k_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
+                              DevStatus* st, const double* maxbuf) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) finish_iteration(gs, gu0, ngu, p, unit_iters, st, maxbuf);
+}
+
+__global__ void k_grid_zero_max(double* maxbuf, int gu0, int ngu) {
+  const int i = threadIdx.x;
+  if (i < ngu) maxbuf[gu0 + i] = 0.0;
 }
 
 int blocks_for(long long n, int threads) { return static_cast<int>((n + threads - 1) / threads); }
@@ -355,8 +375,11 @@ void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                      int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
-  if (ntasks == 0) return;
+                      int hot_begin, long long hot_rows, long long unit_rows, double* maxbuf, cudaStream_t s) {
+  if (ntasks == 0) {  // this rank owns no rows of the level's units: still publish a zero max
+    if (maxbuf) launch_grid_zero_max(maxbuf, gu0, ngu, s);
+    return;
+  }
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
   const int want = blocks_for(ntasks, kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
@@ -365,7 +388,17 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks,
     return e ? std::atoi(e) : kL1HotRows;
   }();
   k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank,
-                                            s_in, s_out, unit_iters, st, hot_begin, hot_bytes, unit_bytes, l1_hot);
+                                            s_in, s_out, unit_iters, st, hot_begin, hot_bytes, unit_bytes, l1_hot,
+                                            maxbuf);
+}
+
+void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s) {
+  k_grid_zero_max<<<1, 1024, 0, s>>>(maxbuf, gu0, ngu);
+}
+
+void launch_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
+                        DevStatus* st, const double* maxbuf, cudaStream_t s) {
+  k_grid_finish<<<1, 32, 0, s>>>(gs, gu0, ngu, p, unit_iters, st, maxbuf);
 }
 
 }  // namespace lrk

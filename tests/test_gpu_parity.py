@@ -58,6 +58,18 @@ def test_config_recipes(lr, oracle, cfg, shrink):
     assert res.report["total_edge_work"] == ref.report["total_edge_work"]
 
 
+def test_sharded_path_single_rank(lr):
+    """The multi-GPU code path (row shards + NCCL exchange + deferred stop
+    decision) on a one-rank communicator reproduces the unsharded solve."""
+    g = lr.config_graph(2, 6)
+    w = np.full(g.n, 1.0 / g.n)
+    r3a, r1a, _, ita = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
+    eng = lr.Engine(g, rank=0, world=1, nccl_id=lr.nccl_unique_id())
+    r3b, r1b, _, itb = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(ita, itb)
+    assert np.array_equal(r3a, r3b) and np.array_equal(r1a, r1b)
+
+
 def test_engine_reuse_and_zero_weights(lr):
     g = lr.config_graph(2, 8)
     eng = lr.Engine(g)
