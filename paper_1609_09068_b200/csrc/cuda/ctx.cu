@@ -65,7 +65,10 @@ struct LevelTasks {
   int cac_b0 = 0, cac_b1 = 0;  // CTA-per-CAC tasks
   int sm0 = 0, sm1 = 0, sm_max = 0;
   int lc0 = 0, lc1 = 0, lc_max = 0;
-  int xh0 = 0, xh1 = 0;  // heavy cross-row tasks
+  int xh0 = 0, xh1 = 0;  // split cross rows (more than kCrossSplit in-edges)
+  int sb0 = 0, sb1 = 0, sb_max = 0;  // SccSmall units beyond shared memory
+  int lt0 = 0, lt1 = 0;  // CTA tasks of the fused level kernel
+  size_t smem = 0;       // its dynamic shared memory
   int sl0 = 0, sl1 = 0;  // depth slices of large CACs (one launch each)
   int gu0 = 0, gu1 = 0;
   int bk0 = 0, bk1 = 0;
@@ -155,7 +158,8 @@ struct lr_ctx {
   DevBuf<long long> xptr, iptr;
   // tasks
   DevBuf<CacTask> cac;
-  DevBuf<SccTask> small, lcta;
+  DevBuf<SccTask> small, small_big, lcta;
+  DevBuf<LevelTask> ltasks;
   DevBuf<GridUnitState> gstate;
   DevBuf<SpmvBlock> blocks;
   DevBuf<HeavyRow> heavy;
@@ -242,6 +246,10 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
     lrerr::set(std::string("levelrank-b200 is built for sm_100a; found ") + prop.name);
     return fail(LR_ECUDA);
   }
+  if (const cudaError_t e = configure_level_kernel(); e != cudaSuccess) {
+    lrerr::set(std::string("level kernel setup failed: ") + cudaGetErrorString(e));
+    return fail(LR_ECUDA);
+  }
   if (const cudaError_t e = configure_kernels(); e != cudaSuccess) {
     lrerr::set(std::string("kernel setup failed: ") + cudaGetErrorString(e));
     return fail(LR_ECUDA);
@@ -302,6 +310,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   std::vector<SpmvBlock> blocks;
   std::vector<HeavyRow> heavy;
   std::vector<CrossTask> xheavy;
+  std::vector<SccTask> small_big;
+  std::vector<std::vector<std::pair<int, int>>> rowranges(static_cast<size_t>(L->n_levels));  // row tasks per level
   long long xparts = 0;
   int n_xslots = 0;
   long long heavy_parts = 0;
@@ -321,7 +331,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.xh0 = static_cast<int>(xheavy.size());
     for (int r = T.rb; r < T.re; ++r) {
       const long long xd = L->xptr[r + 1] - L->xptr[r];
-      if (xd <= kCrossLight) continue;
+      if (xd <= kCrossSplit) continue;
       const int nseg = static_cast<int>((xd + kCrossSeg - 1) / kCrossSeg);
       const int slot = n_xslots++;
       for (int sg = 0; sg < nseg; ++sg) {
@@ -333,6 +343,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     }
     T.xh1 = static_cast<int>(xheavy.size());
     T.sm0 = static_cast<int>(small.size());
+    T.sb0 = static_cast<int>(small_big.size());
     T.lc0 = static_cast<int>(lcta.size());
     T.gu0 = static_cast<int>(gstate.size());
     T.bk0 = static_cast<int>(blocks.size());
@@ -346,8 +357,10 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         const long long db = L->cac_depth_begin[u];
         int nd = 0;
         while (L->depth_ptr[db + nd] < re) ++nd;  // depth_ptr[db+nd] == re ends the unit
-        if (m > kCacWarpMaxRows) {
-          // large CAC: one grid-wide launch per depth slice
+        if (m > kCacBlockMaxRows) {
+          // very large CAC: start weights by row tasks, then one grid-wide
+          // launch per depth slice
+          rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
           for (int d = 0; d < nd; ++d) {
             const int r0 = L->depth_ptr[db + d], r1 = L->depth_ptr[db + d + 1];
             const int h0 = static_cast<int>(xheavy.size());
@@ -366,22 +379,31 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             ctx->cac_slices.push_back(CacSlice{r0, r1, h0, static_cast<int>(xheavy.size())});
           }
         } else {
-          lw.push_back(CacTask{rb, re, db, nd, 0});
+          (m > kCacWarpMaxRows ? lb : lw).push_back(CacTask{rb, re, db, nd, 0});
         }
       } else if (kind == 2) {
         rk = kSmall;
-        small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
-        T.sm_max = std::max(T.sm_max, m);
-        max_small = std::max(max_small, m);
-        if (m > kSmallSmemMaxM) small_needs_scratch = true;
+        if (m <= kSmallSmemMaxM) {
+          small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+          T.sm_max = std::max(T.sm_max, m);
+        } else {  // beyond shared memory: global-scratch kernel after the level kernel
+          small_big.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+          rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
+          T.sb_max = std::max(T.sb_max, m);
+          max_small = std::max(max_small, m);
+          small_needs_scratch = true;
+        }
       } else if (kind == 3) {
         const long long nnz = L->iptr[re] - L->iptr[rb];
         if (m <= kCtaLargeMaxRows && nnz <= kCtaLargeMaxNnz) {
           rk = kLargeCta;
-          lcta.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+          int has_heavy = 0;
+          for (int r = rb; r < re && !has_heavy; ++r) has_heavy = L->iptr[r + 1] - L->iptr[r] > kCrossLight;
+          lcta.push_back(SccTask{rb, re, u, has_heavy, L->unit_edges[u]});
           T.lc_max = std::max(T.lc_max, m);
         } else {
           rk = kLargeGrid;
+          rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
           const int gu = static_cast<int>(gstate.size());
           const size_t first_block = blocks.size();
           // multi-GPU: this rank owns rows [own0, own1) of the unit (nnz-balanced)
@@ -427,6 +449,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           gstate.push_back(g);
         }
       }
+      if (kind == 0) rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
       for (int r = rb; r < re; ++r) rowkind[static_cast<size_t>(r)] = rk;
     }
     T.cac_w0 = static_cast<int>(cac_w.size());
@@ -437,6 +460,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.cac_b1 = static_cast<int>(cac_b.size());
     T.sl1 = static_cast<int>(ctx->cac_slices.size());
     T.sm1 = static_cast<int>(small.size());
+    T.sb1 = static_cast<int>(small_big.size());
     T.lc1 = static_cast<int>(lcta.size());
     T.gu1 = static_cast<int>(gstate.size());
     T.bk1 = static_cast<int>(blocks.size());
@@ -468,6 +492,23 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   }
   cac_w.insert(cac_w.end(), cac_b.begin(), cac_b.end());
 
+  // CTA tasks of the fused per-level kernel, level by level
+  std::vector<LevelTask> ltasks;
+  for (int li = 0; li < L->n_levels; ++li) {
+    LevelTasks& T = ctx->lt[static_cast<size_t>(li)];
+    T.lt0 = static_cast<int>(ltasks.size());
+    for (const auto& [a, b] : rowranges[static_cast<size_t>(li)])
+      for (int r = a; r < b; r += 256) ltasks.push_back(LevelTask{kTaskRows, r, std::min(b, r + 256), 0});
+    for (int i = T.cac_w0; i < T.cac_w1; i += 8) ltasks.push_back(LevelTask{kTaskCacWarps, i, std::min(T.cac_w1, i + 8), 0});
+    for (int i = T.cac_b0; i < T.cac_b1; ++i) ltasks.push_back(LevelTask{kTaskCacBlock, i, i + 1, 0});
+    for (int i = T.sm0; i < T.sm1; ++i) ltasks.push_back(LevelTask{kTaskSmall, i, i + 1, 0});
+    for (int i = T.lc0; i < T.lc1; ++i) ltasks.push_back(LevelTask{kTaskLcta, i, i + 1, 0});
+    T.lt1 = static_cast<int>(ltasks.size());
+    const size_t ld = static_cast<size_t>(T.sm_max) + 1;
+    T.smem = std::max(T.sm_max > 0 ? ld * (ld + 1) * sizeof(double) : 0,
+                      static_cast<size_t>(3) * static_cast<size_t>(T.lc_max) * sizeof(double));
+  }
+
   LR_CUDA_TRY(ctx->vertex_of.upload(L->vertex_of, nn, s));
   LR_CUDA_TRY(ctx->row_of.upload(L->row_of, nn, s));
   LR_CUDA_TRY(ctx->deg.upload(L->deg, nn, s));
@@ -480,6 +521,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->depth_ptr.upload(L->depth_ptr, static_cast<size_t>(L->depth_ptr_len), s));
   LR_CUDA_TRY(ctx->cac.upload(cac_w.data(), cac_w.size(), s));
   LR_CUDA_TRY(ctx->small.upload(small.data(), small.size(), s));
+  LR_CUDA_TRY(ctx->small_big.upload(small_big.data(), small_big.size(), s));
+  LR_CUDA_TRY(ctx->ltasks.upload(ltasks.data(), ltasks.size(), s));
   LR_CUDA_TRY(ctx->lcta.upload(lcta.data(), lcta.size(), s));
   LR_CUDA_TRY(ctx->gstate.upload(gstate.data(), gstate.size(), s));
   LR_CUDA_TRY(ctx->blocks.upload(blocks.data(), blocks.size(), s));
@@ -562,11 +605,22 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   launch_prep(L, w_dev, ctx->params.p, ctx->pf.p, ctx->status.p, s);
   ++launches;
   for (const LevelTasks& T : ctx->lt) {
-    launch_cross(L, T.rb, T.re, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, s);
-    ++launches;
+    // K1 for rows with more than kCrossSplit cross in-edges (split over warps)
     if (T.xh1 > T.xh0) {
       launch_cross_heavy(L, ctx->xheavy.p + T.xh0, T.xh1 - T.xh0, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p,
                          ctx->s0.p, ctx->xparts.p, ctx->xcnts.p, s);
+      ++launches;
+    }
+    // everything that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
+    if (T.lt1 > T.lt0) {
+      launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
+                   T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
+                   ctx->unit_iters.p, ctx->status.p, s);
+      ++launches;
+    }
+    if (T.sb1 > T.sb0) {
+      launch_small(L, ctx->small_big.p + T.sb0, T.sb1 - T.sb0, ctx->small_scratch_ld - 1, ctx->pf.p, ctx->rank.p,
+                   ctx->small_scratch.p, ctx->status.p, s);
       ++launches;
     }
     for (int i = T.sl0; i < T.sl1; ++i) {
@@ -578,25 +632,6 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
                          ctx->xcnts.p, s);
         ++launches;
       }
-    }
-    if (T.cac_w1 > T.cac_w0) {
-      launch_cac(L, ctx->cac.p + T.cac_w0, T.cac_w1 - T.cac_w0, false, ctx->depth_ptr.p, ctx->params.p, ctx->rank.p, s);
-      ++launches;
-    }
-    if (T.cac_b1 > T.cac_b0) {
-      launch_cac(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, true, ctx->depth_ptr.p, ctx->params.p, ctx->rank.p, s);
-      ++launches;
-    }
-    if (T.sm1 > T.sm0) {
-      launch_small(L, ctx->small.p + T.sm0, T.sm1 - T.sm0, T.sm_max > kSmallSmemMaxM ? ctx->small_scratch_ld - 1 : T.sm_max,
-                   ctx->pf.p, ctx->rank.p, T.sm_max > kSmallSmemMaxM ? ctx->small_scratch.p : nullptr,
-                   ctx->status.p, s);
-      ++launches;
-    }
-    if (T.lc1 > T.lc0) {
-      launch_large_cta(L, ctx->lcta.p + T.lc0, T.lc1 - T.lc0, T.lc_max, ctx->params.p, ctx->pf.p, ctx->rank.p,
-                       ctx->unit_iters.p, ctx->status.p, s);
-      ++launches;
     }
     if (T.gu1 > T.gu0) {
       launch_grid_reset(ctx->gstate.p + T.gu0, T.gu1 - T.gu0, ctx->status.p, s);

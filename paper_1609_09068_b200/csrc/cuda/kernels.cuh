@@ -100,8 +100,19 @@ struct CrossTask {
   int pad;
 };
 
-constexpr int kCrossLight = 32;    // rows up to this many cross in-edges: one thread, reference order
-constexpr int kCrossSeg = 2048;    // cross in-edges per warp task of a heavy row
+constexpr int kCrossLight = 32;    // rows up to this many in-edges: one thread, reference order
+constexpr int kCrossSplit = 4096;  // cross rows above this: split over warps by k_pull_heavy
+constexpr int kCrossSeg = 2048;    // cross in-edges per warp task of a split row
+
+// One CTA of the fused per-level kernel (level.cu).
+enum LevelTaskType : int { kTaskRows = 0, kTaskCacWarps = 1, kTaskCacBlock = 2, kTaskSmall = 3, kTaskLcta = 4 };
+struct LevelTask {
+  int type;
+  int a;  // rows: first row; CAC warps: first CacTask; others: task index
+  int b;  // rows: end row; CAC warps: end CacTask
+  int pad;
+};
+constexpr int kCacBlockMaxRows = 32768;  // larger CACs: one grid-wide launch per depth slice
 constexpr int kSpmvThreads = 256;
 constexpr int kTileNnz = 256;      // in-edges of one warp tile
 constexpr int kTileRows = 64;      // max rows of one warp tile
@@ -114,6 +125,13 @@ constexpr int kSmallScratchBlocks = 296; // grid of the global-scratch small-SCC
 constexpr int kCacWarpMaxRows = 2048;    // larger CACs get a whole CTA
 
 cudaError_t configure_kernels();
+cudaError_t configure_level_kernel();
+
+// fused per-level kernel (level.cu)
+void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
+                  const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
+                  const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
+                  long long* unit_iters, DevStatus* st, cudaStream_t s);
 
 // launch wrappers (stream-ordered)
 void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,

@@ -1,0 +1,368 @@
+// The fused per-level kernel: one launch solves every unit of a level that
+// fits a CTA.  Deep DAGs (config 4: 1000 levels of
+// ~16k vertices, a few hundred small components each) are bound by per-level
+// latency, not bandwidth, so everything a level needs -- the cross-level
+// gather of its start weights (K1), singleton rows, CACs (K3), small SCCs
+// (K5) and CTA-sized large SCCs (K4a) -- runs as heterogeneous CTAs of a
+// single launch.  Each unit task gathers its own rows' cross in-edges first,
+// so no grid-wide barrier is needed between K1 and the unit solves.
+//
+// Accumulation orders are the reference's wherever one thread sums a row
+// (cross in-edges in propagate_weights order, CAC parents in Kahn order, SCC
+// in-edges in source order); rows with more than kCrossLight in-edges are
+// summed by a warp butterfly, and rows with more than kCrossSplit cross
+// in-edges by the separate segment kernel (k_pull_heavy) launched before.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "devutil.cuh"
+#include "kernels.cuh"
+
+namespace lrk {
+namespace {
+
+using namespace dev;
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPer = kThreads / 32;
+
+// ------------------------------------------------------------- K1 pieces
+// w + sum over cross in-edges of (c * r_src) / deg_src, reference order.
+__device__ __forceinline__ double cross_serial(const DeviceLayout& L, int row, const double* __restrict__ w, double c,
+                                               const double* rank, long long e0, long long e1) {
+  double acc = w[L.vertex_of[row]];
+  for (long long e = e0; e < e1; ++e) {
+    const int s = __ldg(L.xsrc + e);
+    acc += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double cross_warp_sum(const DeviceLayout& L, const double* rank, double c, long long e0,
+                                                 long long e1, int lane) {
+  double y = 0.0;
+  for (long long e = e0 + lane; e < e1; e += 32) {
+    const int s = __ldg(L.xsrc + e);
+    y += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
+  }
+  return warp_sum(y);
+}
+
+// start weight finishes: singletons are solved (solvers.cpp:23-35), grid
+// SccLarge rows get their first pushed value s0 = pf * w
+__device__ __forceinline__ void row_finish(const DeviceLayout& L, int row, double acc, double c,
+                                           const double* __restrict__ pf, double* rank, double* s0) {
+  const std::uint8_t k = L.rowkind[row];
+  if (k == kSingle && L.loop[row]) acc /= 1.0 - c / static_cast<double>(L.deg[row]);
+  rank[row] = acc;
+  if (k == kLargeGrid) s0[row] = pf[row] * acc;
+}
+
+// Start weights of rows [r0, r1) by `width` threads at offset `tid` (a whole
+// CTA or one warp; warp-level cooperation for heavy rows happens inside each
+// warp of the group).  Rows above kCrossSplit were done by k_pull_heavy.
+__device__ void cross_rows(const DeviceLayout& L, int r0, int r1, const double* __restrict__ w, double c,
+                           const double* __restrict__ pf, double* rank, double* s0, int tid, int width) {
+  for (int r = r0 + tid; r < r1; r += width) {
+    const long long e0 = L.xptr[r], e1 = L.xptr[r + 1];
+    if (e1 - e0 > kCrossLight) continue;
+    row_finish(L, r, cross_serial(L, r, w, c, rank, e0, e1), c, pf, rank, s0);
+  }
+  // heavy rows: one warp each
+  const int lane = threadIdx.x & 31;
+  const int wid = tid >> 5, nw = width >> 5;
+  for (int base = r0 + wid * 32; base < r1; base += nw * 32) {
+    const int r = base + lane;
+    long long d = 0;
+    if (r < r1) d = L.xptr[r + 1] - L.xptr[r];
+    unsigned mask = __ballot_sync(0xffffffffu, d > kCrossLight && d <= kCrossSplit);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int row = base + src;
+      const double y = cross_warp_sum(L, rank, c, L.xptr[row], L.xptr[row + 1], lane);
+      if (lane == 0) row_finish(L, row, w[L.vertex_of[row]] + y, c, pf, rank, s0);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3
+// One depth-slice row of a CAC: parents in Kahn order, then the kept-loop
+// factor (solvers.cpp:61-83).
+__device__ __forceinline__ double cac_row(const DeviceLayout& L, int r, double c, const double* rank, long long e0,
+                                          long long e1, double acc) {
+  for (long long e = e0; e < e1; ++e) {
+    const int s = L.isrc[e];
+    acc += rank[s] * c / static_cast<double>(L.deg[s]);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double loop_factor(const DeviceLayout& L, int r, double c, double acc) {
+  return L.loop[r] ? acc / (1.0 - c / static_cast<double>(L.deg[r])) : acc;
+}
+
+// depth sweep of one CAC by a warp (kBlock = false) or a CTA (true)
+template <bool kBlock>
+__device__ void cac_sweep(const DeviceLayout& L, const CacTask& t, const int* __restrict__ depth_ptr, double c,
+                          double* rank, int tid, int width) {
+  const int lane = threadIdx.x & 31;
+  const int wid = tid >> 5, nw = width >> 5;
+  const int* dp = depth_ptr + t.depth_begin;
+  for (int d = 0; d < t.ndepth; ++d) {
+    if (d > 0) {
+      if (kBlock) {
+        __syncthreads();
+      } else {
+        __threadfence_block();
+        __syncwarp();
+      }
+    }
+    const int s0 = dp[d], s1 = dp[d + 1];
+    for (int r = s0 + tid; r < s1; r += width) {
+      const long long e0 = L.iptr[r], e1 = L.iptr[r + 1];
+      if (e1 - e0 > kCrossLight) continue;
+      rank[r] = loop_factor(L, r, c, cac_row(L, r, c, rank, e0, e1, rank[r]));
+    }
+    for (int base = s0 + wid * 32; base < s1; base += nw * 32) {
+      const int r = base + lane;
+      long long deg_in = 0;
+      if (r < s1) deg_in = L.iptr[r + 1] - L.iptr[r];
+      unsigned mask = __ballot_sync(0xffffffffu, deg_in > kCrossLight);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int row = base + src;
+        double y = 0.0;
+        for (long long e = L.iptr[row] + lane; e < L.iptr[row + 1]; e += 32) {
+          const int s = L.isrc[e];
+          y += rank[s] * c / static_cast<double>(L.deg[s]);
+        }
+        y = warp_sum(y);
+        if (lane == 0) rank[row] = loop_factor(L, row, c, rank[row] + y);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5
+// Dense (I - cA^T) r = w per SccSmall unit in shared memory
+// (solve_dense_system, solvers.cpp:92-108).  The matrix is strictly
+// diagonally dominant by columns (column sums of cA^T <= c < 1), so partial
+// pivoting never swaps and plain elimination equals the reference's LU.
+// One barrier per elimination step; back substitution by one warp.
+__device__ void small_solve(const DeviceLayout& L, const SccTask& t, int ld, const double* __restrict__ pf,
+                            double* rank, double* sm, double* red, DevStatus* st) {
+  double* M = sm;
+  double* rhs = M + static_cast<size_t>(ld) * ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  for (int i = tid; i < m * ld; i += kThreads) M[i] = 0.0;
+  __syncthreads();
+  for (int b = tid; b < m; b += kThreads) {
+    M[b * ld + b] = 1.0;
+    rhs[b] = rank[rb + b];
+  }
+  __syncthreads();
+  for (int b = tid; b < m; b += kThreads) {
+    const long long e1 = L.iptr[rb + b + 1];
+    for (long long e = L.iptr[rb + b]; e < e1; ++e) {
+      const int s = L.isrc[e];
+      M[b * ld + (s - rb)] -= pf[s];
+    }
+  }
+  for (int k = 0; k < m; ++k) {
+    __syncthreads();
+    const double piv = M[k * ld + k];
+    const double rk = rhs[k];
+    for (int i = k + 1 + warp; i < m; i += kWarpsPer) {
+      const double f = M[i * ld + k] / piv;
+      for (int j = k + 1 + lane; j < m; j += 32) M[i * ld + j] -= f * M[k * ld + j];
+      if (lane == 0) rhs[i] -= f * rk;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int i = m - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int j = i + 1 + lane; j < m; j += 32) s += M[i * ld + j] * rhs[j];
+      s = warp_sum(s);
+      if (lane == 0) rhs[i] = (rhs[i] - s) / M[i * ld + i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // residual check of solvers.cpp:103-106
+  double res = 0.0, wm = 0.0, xm = 0.0;
+  for (int b = tid; b < m; b += kThreads) {
+    const double wb = rank[rb + b];
+    double acc = rhs[b];
+    const long long e1 = L.iptr[rb + b + 1];
+    for (long long e = L.iptr[rb + b]; e < e1; ++e) {
+      const int s = L.isrc[e];
+      acc -= pf[s] * rhs[s - rb];
+    }
+    res = fmax(res, fabs(acc - wb));
+    wm = fmax(wm, fabs(wb));
+    xm = fmax(xm, fabs(rhs[b]));
+  }
+  res = block_max(res, red);
+  __syncthreads();
+  wm = block_max(wm, red);
+  __syncthreads();
+  xm = block_max(xm, red);
+  if (tid == 0 && !(res <= 1e-8 * (1.0 + wm + xm))) atomicOr(&st->err, kErrDegen);
+  for (int b = tid; b < m; b += kThreads) rank[rb + b] = rhs[b];
+}
+
+// ------------------------------------------------------------------ K4a
+// The whole power series of one SccLarge unit in one CTA (solve_large_scc,
+// solvers.cpp:128-162): pushed vectors in shared memory, one thread per row in
+// the reference's order (bit-exact), a warp for rows above kCrossLight.
+__device__ void lcta_solve(const DeviceLayout& L, const SccTask& t, int maxrows, const SolveParams* __restrict__ p,
+                           const double* __restrict__ pf, double* rank, long long* unit_iters, DevStatus* st,
+                           double* sm, double (*red)[32]) {
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sc = sm;
+  double* sn = sm + maxrows;
+  double* pl = sm + 2 * maxrows;
+  const double tol = p->tol;
+  const long long cap = p->cap;
+  for (int i = threadIdx.x; i < m; i += kThreads) {
+    pl[i] = pf[rb + i];
+    sc[i] = pl[i] * rank[rb + i];
+  }
+  __syncthreads();
+  long long it = 0;
+  bool fail = false;
+  for (;;) {
+    double lmax = 0.0;
+    for (int i = threadIdx.x; i < m; i += kThreads) {
+      const int row = rb + i;
+      const long long e0 = L.iptr[row], e1 = L.iptr[row + 1];
+      if (e1 - e0 > kCrossLight) continue;
+      double y = 0.0;
+      for (long long e = e0; e < e1; ++e) y += sc[__ldg(L.isrc + e) - rb];
+      rank[row] += y;
+      sn[i] = pl[i] * y;
+      lmax = fmax(lmax, y);
+    }
+    if (t.pad) {  // the unit has rows above kCrossLight
+      for (int base = warp * 32; base < m; base += kWarpsPer * 32) {
+        const int i = base + lane;
+        long long d = 0;
+        if (i < m) d = L.iptr[rb + i + 1] - L.iptr[rb + i];
+        unsigned mask = __ballot_sync(0xffffffffu, d > kCrossLight);
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int row = rb + base + src;
+          double y = 0.0;
+          for (long long e = L.iptr[row] + lane; e < L.iptr[row + 1]; e += 32) y += sc[__ldg(L.isrc + e) - rb];
+          y = warp_sum(y);
+          if (lane == 0) {
+            rank[row] += y;
+            sn[base + src] = pl[base + src] * y;
+            lmax = fmax(lmax, y);
+          }
+        }
+      }
+    }
+    const double mx = block_max(lmax, red[it & 1]);
+    double* tmp = sc;
+    sc = sn;
+    sn = tmp;
+    ++it;
+    if (it > cap) {
+      fail = true;
+      break;
+    }
+    if (!(mx >= tol)) break;
+  }
+  if (threadIdx.x == 0) {
+    unit_iters[t.unit] = it;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->iterative_edge_work),
+              static_cast<unsigned long long>(it * t.edges));
+    if (fail) atomicOr(&st->err, kErrNoConv);
+  }
+}
+
+// ------------------------------------------------------------- dispatcher
+__global__ void __launch_bounds__(kThreads)
+    k_level(DeviceLayout L, const LevelTask* __restrict__ tasks, const CacTask* __restrict__ cacs,
+            const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
+            int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
+            const double* __restrict__ pf, double* rank, double* s0, long long* unit_iters, DevStatus* st) {
+  extern __shared__ double sm[];
+  __shared__ double red[2][32];
+  const LevelTask t = tasks[blockIdx.x];
+  const double c = p->c;
+  switch (t.type) {
+    case kTaskRows:
+      cross_rows(L, t.a, t.b, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      break;
+    case kTaskCacWarps: {
+      const int ci = t.a + static_cast<int>(threadIdx.x >> 5);
+      if (ci >= t.b) break;
+      const CacTask ct = cacs[ci];
+      const int lane = threadIdx.x & 31;
+      cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, lane, 32);
+      __threadfence_block();
+      __syncwarp();
+      cac_sweep<false>(L, ct, depth_ptr, c, rank, lane, 32);
+      break;
+    }
+    case kTaskCacBlock: {
+      const CacTask ct = cacs[t.a];
+      cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      __syncthreads();
+      cac_sweep<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kThreads);
+      break;
+    }
+    case kTaskSmall: {
+      const SccTask sct = smalls[t.a];
+      cross_rows(L, sct.row_begin, sct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      __syncthreads();
+      small_solve(L, sct, small_ld, pf, rank, sm, red[0], st);
+      break;
+    }
+    case kTaskLcta: {
+      const SccTask lt = lctas[t.a];
+      cross_rows(L, lt.row_begin, lt.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      __syncthreads();
+      lcta_solve(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+}  // namespace
+
+cudaError_t configure_level_kernel() {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes a{};
+  e = cudaFuncGetAttributes(&a, k_level);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - static_cast<int>(a.sharedSizeBytes));
+}
+
+void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
+                  const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
+                  const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
+                  long long* unit_iters, DevStatus* st, cudaStream_t s) {
+  if (ntasks == 0) return;
+  k_level<<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p, pf, rank,
+                                         s0, unit_iters, st);
+}
+
+}  // namespace lrk
