@@ -125,22 +125,19 @@ def cpu_sample(g, lr, eng, budget_s=20.0, threads=None):
         del src
         prep = rg.prepare(100)
         setup_s = time.perf_counter() - t0
-        # one multiply on the SccLarge units tells the per-iteration cost; cut the
-        # series so the sample stays near budget_s
-        _, work1, it1, ms1 = rg.prep_solve(prep, w, C_DAMP, TOL, large_tol=1e300, threads=threads)
-        full_it = None
-        large_tol = 0.0
-        if it1 > 0:
-            per_it_ms = ms1 / max(it1, 1)
-            k = max(2, int(budget_s * 1e3 / max(per_it_ms, 1e-3)))
-            # increments shrink at least geometrically (factor <= c); cut at the
-            # value the max increment reaches after ~k multiplies
-            large_tol = TOL if k >= 2000 else max(TOL, (1.0 / n) * C_DAMP ** k)
-        ranks, work, iters, ms = rg.prep_solve(prep, w, C_DAMP, TOL, large_tol=large_tol, threads=threads)
+        # A level loop with the SccLarge series stopped after its first multiply
+        # (do-while, solvers.cpp:146-160) times every other unit in full plus one
+        # multiply of each large SCC.  If the full solve fits the budget (at
+        # ~130 multiplies) the sample is the full solve, else this bounded one.
+        ranks, work, iters, ms = rg.prep_solve(prep, w, C_DAMP, TOL, large_tol=1e300, threads=threads)
+        large_tol = 1e300
+        if iters == 0 or ms * 130 <= budget_s * 1e3:
+            large_tol = 0.0
+            ranks, work, iters, ms = rg.prep_solve(prep, w, C_DAMP, TOL, large_tol=0.0, threads=threads)
         rg.free_prep(prep)
         sample = (f"reference level loop (oracle/_ref, Parallel pool of {threads}) over its own schedule; "
-                  f"SccLarge series {'in full' if large_tol <= TOL else f'cut at max|inc| < {large_tol:.3g}'}"
-                  f" ({iters} multiplies); setup {setup_s:.1f}s untimed")
+                  f"SccLarge series {'in full' if large_tol <= TOL else 'stopped after its first multiply'}"
+                  f" ({iters} multiplies, {work / 1e9:.2f} G edge updates); setup {setup_s:.1f}s untimed")
         return {"value": work / (ms / 1e3) / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": sample, "edge_updates": int(work), "ms": ms}
     o = Oracle()
