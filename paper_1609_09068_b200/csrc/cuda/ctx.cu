@@ -146,6 +146,8 @@ std::vector<int> shard_bounds(const int64_t* iptr, int rb, int re, int world) {
 struct lr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // side stream for large CACs (joined every level)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int n = 0;
   int n_levels = 0;
@@ -209,6 +211,9 @@ struct lr_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : lev)
       if (e) cudaEventDestroy(e);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
     if (h_params) cudaFreeHost(h_params);
     if (h_status) cudaFreeHost(h_status);
@@ -254,7 +259,10 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
     lrerr::set(std::string("kernel setup failed: ") + cudaGetErrorString(e));
     return fail(LR_ECUDA);
   }
-  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
     lrerr::set("CUDA stream creation failed");
     return fail(LR_ECUDA);
   }
@@ -500,7 +508,6 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     for (const auto& [a, b] : rowranges[static_cast<size_t>(li)])
       for (int r = a; r < b; r += 256) ltasks.push_back(LevelTask{kTaskRows, r, std::min(b, r + 256), 0});
     for (int i = T.cac_w0; i < T.cac_w1; i += 8) ltasks.push_back(LevelTask{kTaskCacWarps, i, std::min(T.cac_w1, i + 8), 0});
-    for (int i = T.cac_b0; i < T.cac_b1; ++i) ltasks.push_back(LevelTask{kTaskCacBlock, i, i + 1, 0});
     for (int i = T.sm0; i < T.sm1; ++i) ltasks.push_back(LevelTask{kTaskSmall, i, i + 1, 0});
     for (int i = T.lc0; i < T.lc1; ++i) ltasks.push_back(LevelTask{kTaskLcta, i, i + 1, 0});
     T.lt1 = static_cast<int>(ltasks.size());
@@ -611,13 +618,24 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
                          ctx->s0.p, ctx->xparts.p, ctx->xcnts.p, s);
       ++launches;
     }
-    // everything that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
+    // large CACs on the side stream, concurrently with the level kernel
+    const bool fork = T.cac_b1 > T.cac_b0;
+    if (fork) {
+      LR_CUDA_TRY(cudaEventRecord(ctx->fork_ev, s));
+      LR_CUDA_TRY(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
+      launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
+                     ctx->rank.p, ctx->s0.p, ctx->stream2);
+      LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->stream2));
+      ++launches;
+    }
+    // everything else that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
     if (T.lt1 > T.lt0) {
       launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
                    ctx->unit_iters.p, ctx->status.p, s);
       ++launches;
     }
+    if (fork) LR_CUDA_TRY(cudaStreamWaitEvent(s, ctx->join_ev, 0));
     if (T.sb1 > T.sb0) {
       launch_small(L, ctx->small_big.p + T.sb0, T.sb1 - T.sb0, ctx->small_scratch_ld - 1, ctx->pf.p, ctx->rank.p,
                    ctx->small_scratch.p, ctx->status.p, s);

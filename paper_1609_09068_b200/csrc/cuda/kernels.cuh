@@ -127,6 +127,9 @@ constexpr int kCacWarpMaxRows = 2048;    // larger CACs get a whole CTA
 cudaError_t configure_kernels();
 cudaError_t configure_level_kernel();
 
+// large CACs, 1024-thread CTAs, meant for a second stream (level.cu)
+void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
+                    const SolveParams* p, const double* pf, double* rank, double* s0, cudaStream_t s);
 // fused per-level kernel (level.cu)
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,

@@ -341,7 +341,30 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Large CACs (kCacWarpMaxRows < rows <= kCacBlockMaxRows): one 1024-thread CTA
+// each, on a second stream concurrently with k_level (the two touch disjoint
+// rows and read only finished levels).  Their depth sweep is the per-level
+// critical path of deep DAGs, so it gets 4x the threads of a k_level CTA.
+constexpr int kBigThreads = 1024;
+
+__global__ void __launch_bounds__(kBigThreads)
+    k_cac_big(DeviceLayout L, const CacTask* __restrict__ cacs, const int* __restrict__ depth_ptr,
+              const double* __restrict__ w, const SolveParams* __restrict__ p, const double* __restrict__ pf,
+              double* rank, double* s0) {
+  const CacTask ct = cacs[blockIdx.x];
+  const double c = p->c;
+  cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, threadIdx.x, kBigThreads);
+  __syncthreads();
+  cac_sweep<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kBigThreads);
+}
+
 }  // namespace
+
+void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
+                    const SolveParams* p, const double* pf, double* rank, double* s0, cudaStream_t s) {
+  if (n == 0) return;
+  k_cac_big<<<n, kBigThreads, 0, s>>>(L, cacs, depth_ptr, w, p, pf, rank, s0);
+}
 
 cudaError_t configure_level_kernel() {
   int dev = 0, optin = 0;
