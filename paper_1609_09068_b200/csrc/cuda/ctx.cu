@@ -62,7 +62,8 @@ struct DevBuf {
 struct LevelTasks {
   int rb = 0, re = 0;
   int cac_w0 = 0, cac_w1 = 0;  // warp-per-CAC tasks
-  int cac_b0 = 0, cac_b1 = 0;  // CTA-per-CAC tasks
+  int cac_m0 = 0, cac_m1 = 0;  // 256-thread CTA per CAC (k_level)
+  int cac_b0 = 0, cac_b1 = 0;  // 1024-thread CTA per CAC (side stream)
   int sm0 = 0, sm1 = 0, sm_max = 0;
   int lc0 = 0, lc1 = 0, lc_max = 0;
   int xh0 = 0, xh1 = 0;  // split cross rows (more than kCrossSplit in-edges)
@@ -334,7 +335,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     LevelTasks& T = ctx->lt[static_cast<size_t>(li)];
     T.rb = L->level_row_begin[li];
     T.re = L->level_row_begin[li + 1];
-    std::vector<CacTask> lw, lb;
+    std::vector<CacTask> lw, lm, lb;
     T.sl0 = static_cast<int>(ctx->cac_slices.size());
     T.xh0 = static_cast<int>(xheavy.size());
     for (int r = T.rb; r < T.re; ++r) {
@@ -387,7 +388,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             ctx->cac_slices.push_back(CacSlice{r0, r1, h0, static_cast<int>(xheavy.size())});
           }
         } else {
-          (m > kCacWarpMaxRows ? lb : lw).push_back(CacTask{rb, re, db, nd, 0});
+          (m > kCacMidMaxRows ? lb : m > kCacWarpMaxRows ? lm : lw).push_back(CacTask{rb, re, db, nd, 0});
         }
       } else if (kind == 2) {
         rk = kSmall;
@@ -463,6 +464,9 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.cac_w0 = static_cast<int>(cac_w.size());
     cac_w.insert(cac_w.end(), lw.begin(), lw.end());
     T.cac_w1 = static_cast<int>(cac_w.size());
+    T.cac_m0 = static_cast<int>(cac_w.size());
+    cac_w.insert(cac_w.end(), lm.begin(), lm.end());
+    T.cac_m1 = static_cast<int>(cac_w.size());
     T.cac_b0 = static_cast<int>(cac_b.size());
     cac_b.insert(cac_b.end(), lb.begin(), lb.end());
     T.cac_b1 = static_cast<int>(cac_b.size());
@@ -508,6 +512,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     for (const auto& [a, b] : rowranges[static_cast<size_t>(li)])
       for (int r = a; r < b; r += 256) ltasks.push_back(LevelTask{kTaskRows, r, std::min(b, r + 256), 0});
     for (int i = T.cac_w0; i < T.cac_w1; i += 8) ltasks.push_back(LevelTask{kTaskCacWarps, i, std::min(T.cac_w1, i + 8), 0});
+    for (int i = T.cac_m0; i < T.cac_m1; ++i) ltasks.push_back(LevelTask{kTaskCacBlock, i, i + 1, 0});
     for (int i = T.sm0; i < T.sm1; ++i) ltasks.push_back(LevelTask{kTaskSmall, i, i + 1, 0});
     for (int i = T.lc0; i < T.lc1; ++i) ltasks.push_back(LevelTask{kTaskLcta, i, i + 1, 0});
     T.lt1 = static_cast<int>(ltasks.size());

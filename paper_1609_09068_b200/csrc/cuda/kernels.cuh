@@ -122,7 +122,8 @@ constexpr long long kCtaLargeMaxNnz = 1 << 16;
 constexpr int kMaxDynSmem = 227 * 1024;
 constexpr int kSmallSmemMaxM = 160;      // ld*(ld+2)*8 <= 227 KB
 constexpr int kSmallScratchBlocks = 296; // grid of the global-scratch small-SCC path
-constexpr int kCacWarpMaxRows = 2048;    // larger CACs get a whole CTA
+constexpr int kCacWarpMaxRows = 64;      // CACs up to this: one warp of a k_level CTA
+constexpr int kCacMidMaxRows = 1024;     // up to this: a 256-thread k_level CTA; above: a 1024-thread CTA
 
 cudaError_t configure_kernels();
 cudaError_t configure_level_kernel();

@@ -32,6 +32,7 @@ constexpr int kWarpsPer = kThreads / 32;
 __device__ __forceinline__ double cross_serial(const DeviceLayout& L, int row, const double* __restrict__ w, double c,
                                                const double* rank, long long e0, long long e1) {
   double acc = w[L.vertex_of[row]];
+#pragma unroll 4
   for (long long e = e0; e < e1; ++e) {
     const int s = __ldg(L.xsrc + e);
     acc += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
@@ -92,6 +93,7 @@ __device__ void cross_rows(const DeviceLayout& L, int r0, int r1, const double* 
 // factor (solvers.cpp:61-83).
 __device__ __forceinline__ double cac_row(const DeviceLayout& L, int r, double c, const double* rank, long long e0,
                                           long long e1, double acc) {
+#pragma unroll 4
   for (long long e = e0; e < e1; ++e) {
     const int s = L.isrc[e];
     acc += rank[s] * c / static_cast<double>(L.deg[s]);
