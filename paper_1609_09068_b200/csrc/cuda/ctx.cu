@@ -389,6 +389,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           }
         } else {
           (m > kCacMidMaxRows ? lb : m > kCacWarpMaxRows ? lm : lw).push_back(CacTask{rb, re, db, nd, 0});
+          if (m > kCacMidMaxRows) rowranges[static_cast<size_t>(li)].emplace_back(rb, re);  // start weights
         }
       } else if (kind == 2) {
         rk = kSmall;
@@ -623,24 +624,19 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
                          ctx->s0.p, ctx->xparts.p, ctx->xcnts.p, s);
       ++launches;
     }
-    // large CACs on the side stream, concurrently with the level kernel
-    const bool fork = T.cac_b1 > T.cac_b0;
-    if (fork) {
-      LR_CUDA_TRY(cudaEventRecord(ctx->fork_ev, s));
-      LR_CUDA_TRY(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
-      launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
-                     ctx->rank.p, ctx->s0.p, ctx->stream2);
-      LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->stream2));
-      ++launches;
-    }
-    // everything else that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
+    // everything that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
     if (T.lt1 > T.lt0) {
       launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
                    ctx->unit_iters.p, ctx->status.p, s);
       ++launches;
     }
-    if (fork) LR_CUDA_TRY(cudaStreamWaitEvent(s, ctx->join_ev, 0));
+    // large CACs: depth sweep in 1024-thread CTAs (start weights came from k_level)
+    if (T.cac_b1 > T.cac_b0) {
+      launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
+                     ctx->rank.p, ctx->s0.p, s);
+      ++launches;
+    }
     if (T.sb1 > T.sb0) {
       launch_small(L, ctx->small_big.p + T.sb0, T.sb1 - T.sb0, ctx->small_scratch_ld - 1, ctx->pf.p, ctx->rank.p,
                    ctx->small_scratch.p, ctx->status.p, s);

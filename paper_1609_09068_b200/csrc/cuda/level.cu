@@ -174,26 +174,39 @@ __device__ void small_solve(const DeviceLayout& L, const SccTask& t, int ld, con
       M[b * ld + (s - rb)] -= pf[s];
     }
   }
+  // Gauss-Jordan: one barrier per pivot, no back substitution.  Each warp
+  // owns rows i = warp (mod 8) and takes them 8 at a time, so the 8 row
+  // factors are loaded together and the column updates of 8 rows overlap.
   for (int k = 0; k < m; ++k) {
     __syncthreads();
-    const double piv = M[k * ld + k];
+    const double inv = 1.0 / M[k * ld + k];
     const double rk = rhs[k];
-    for (int i = k + 1 + warp; i < m; i += kWarpsPer) {
-      const double f = M[i * ld + k] / piv;
-      for (int j = k + 1 + lane; j < m; j += 32) M[i * ld + j] -= f * M[k * ld + j];
-      if (lane == 0) rhs[i] -= f * rk;
+    for (int i0 = warp; i0 < m; i0 += 8 * kWarpsPer) {
+      double f[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kWarpsPer;
+        f[u] = (i < m && i != k) ? M[i * ld + k] * inv : 0.0;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * kWarpsPer;
+          if (i < m && i != k) rhs[i] -= f[u] * rk;
+        }
+      }
+      for (int j = k + 1 + lane; j < m; j += 32) {
+        const double pkj = M[k * ld + j];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * kWarpsPer;
+          if (i < m && i != k) M[i * ld + j] -= f[u] * pkj;
+        }
+      }
     }
   }
   __syncthreads();
-  if (warp == 0) {
-    for (int i = m - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int j = i + 1 + lane; j < m; j += 32) s += M[i * ld + j] * rhs[j];
-      s = warp_sum(s);
-      if (lane == 0) rhs[i] = (rhs[i] - s) / M[i * ld + i];
-      __syncwarp();
-    }
-  }
+  for (int b = tid; b < m; b += kThreads) rhs[b] /= M[b * ld + b];
   __syncthreads();
   // residual check of solvers.cpp:103-106
   double res = 0.0, wm = 0.0, xm = 0.0;
@@ -343,10 +356,10 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Large CACs (kCacWarpMaxRows < rows <= kCacBlockMaxRows): one 1024-thread CTA
-// each, on a second stream concurrently with k_level (the two touch disjoint
-// rows and read only finished levels).  Their depth sweep is the per-level
-// critical path of deep DAGs, so it gets 4x the threads of a k_level CTA.
+// Large CACs (kCacMidMaxRows < rows <= kCacBlockMaxRows): their start weights
+// come from k_level's row tasks (spread over many CTAs); this kernel, launched
+// right after, runs the depth sweep with one 1024-thread CTA per CAC -- the
+// per-level critical path of deep DAGs.
 constexpr int kBigThreads = 1024;
 
 __global__ void __launch_bounds__(kBigThreads)
@@ -354,10 +367,7 @@ __global__ void __launch_bounds__(kBigThreads)
               const double* __restrict__ w, const SolveParams* __restrict__ p, const double* __restrict__ pf,
               double* rank, double* s0) {
   const CacTask ct = cacs[blockIdx.x];
-  const double c = p->c;
-  cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, threadIdx.x, kBigThreads);
-  __syncthreads();
-  cac_sweep<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kBigThreads);
+  cac_sweep<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads);
 }
 
 }  // namespace
