@@ -70,6 +70,7 @@ struct LevelTasks {
   int sb0 = 0, sb1 = 0, sb_max = 0;  // SccSmall units beyond shared memory
   int lt0 = 0, lt1 = 0;  // CTA tasks of the fused level kernel
   size_t smem = 0;       // its dynamic shared memory
+  size_t big_smem = 0;   // dynamic shared memory of the k_cac_big launch
   int sl0 = 0, sl1 = 0;  // depth slices of large CACs (one launch each)
   int gu0 = 0, gu1 = 0;
   int bk0 = 0, bk1 = 0;
@@ -520,6 +521,27 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     const size_t ld = static_cast<size_t>(T.sm_max) + 1;
     T.smem = std::max(T.sm_max > 0 ? ld * (ld + 1) * sizeof(double) : 0,
                       static_cast<size_t>(3) * static_cast<size_t>(T.lc_max) * sizeof(double));
+    // CAC depth sweeps run from shared memory when the CAC's ranks and
+    // in-edges fit (k_level budget kLevelStageBytes so that the level's other
+    // CTAs keep their occupancy; k_cac_big up to kStageMaxBytes).
+    auto need = [&](const CacTask& t) {
+      return (cac_stage_need(t.row_end - t.row_begin, L->iptr[t.row_end] - L->iptr[t.row_begin]) + 15) & ~size_t{15};
+    };
+    size_t warp_need = 0, mid_need = 0;
+    for (int i = T.cac_w0; i < T.cac_w1; ++i) {
+      const size_t b = need(cac_w[static_cast<size_t>(i)]);
+      if (8 * b <= kLevelStageBytes) warp_need = std::max(warp_need, 8 * b);
+    }
+    for (int i = T.cac_m0; i < T.cac_m1; ++i) {
+      const size_t b = need(cac_w[static_cast<size_t>(i)]);
+      if (b <= kLevelStageBytes) mid_need = std::max(mid_need, b);
+    }
+    T.smem = std::max({T.smem, warp_need, mid_need});
+    T.big_smem = 0;
+    for (int i = T.cac_b0; i < T.cac_b1; ++i) {
+      const size_t b = need(cac_w[static_cast<size_t>(i)]);
+      if (b <= kStageMaxBytes) T.big_smem = std::max(T.big_smem, b);
+    }
   }
 
   LR_CUDA_TRY(ctx->vertex_of.upload(L->vertex_of, nn, s));
@@ -634,7 +656,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     // large CACs: depth sweep in 1024-thread CTAs (start weights came from k_level)
     if (T.cac_b1 > T.cac_b0) {
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
-                     ctx->rank.p, ctx->s0.p, s);
+                     ctx->rank.p, ctx->s0.p, T.big_smem, s);
       ++launches;
     }
     if (T.sb1 > T.sb0) {

@@ -130,7 +130,11 @@ cudaError_t configure_level_kernel();
 
 // large CACs, 1024-thread CTAs, meant for a second stream (level.cu)
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
-                    const SolveParams* p, const double* pf, double* rank, double* s0, cudaStream_t s);
+                    const SolveParams* p, const double* pf, double* rank, double* s0, size_t smem, cudaStream_t s);
+// shared-memory bytes a CAC of `rows` rows and `edges` in-edges needs to be swept from shared memory
+size_t cac_stage_need(long long rows, long long edges);
+constexpr size_t kStageMaxBytes = 200 * 1024;  // larger CACs sweep from global memory
+constexpr size_t kLevelStageBytes = 64 * 1024; // CAC staging budget of one k_level CTA
 // fused per-level kernel (level.cu)
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,

@@ -148,6 +148,76 @@ __device__ void cac_sweep(const DeviceLayout& L, const CacTask& t, const int* __
   }
 }
 
+// The same sweep with the CAC staged in shared memory: its start weights,
+// row pointers, parents (as offsets into the CAC) and parent degrees are loaded
+// once, all independent loads in flight together; every depth slice then
+// reads only shared memory, so a slice costs a barrier instead of three
+// dependent global round trips.  Same terms, same order (bit-exact).
+template <bool kBlock>
+__device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const int* __restrict__ depth_ptr, double c,
+                                 double* rank, int tid, int width, void* stage) {
+  const int lane = threadIdx.x & 31;
+  const int wid = tid >> 5, nw = width >> 5;
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  const long long eb = L.iptr[rb];
+  const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  double* sr = static_cast<double*>(stage);
+  int* rp = reinterpret_cast<int*>(sr + m);
+  int* es = rp + m + 1;
+  int* ed = es + ne;
+  for (int i = tid; i < m; i += width) {
+    sr[i] = rank[rb + i];
+    rp[i] = static_cast<int>(L.iptr[rb + i] - eb);
+  }
+  if (tid == 0) rp[m] = ne;
+  for (int e = tid; e < ne; e += width) {
+    const int s = L.isrc[eb + e];
+    es[e] = s - rb;
+    ed[e] = L.deg[s];
+  }
+  auto sync = [&] {
+    if (kBlock) {
+      __syncthreads();
+    } else {
+      __syncwarp();
+    }
+  };
+  sync();
+  const int* dp = depth_ptr + t.depth_begin;
+  for (int d = 0; d < t.ndepth; ++d) {
+    if (d > 0) sync();
+    const int s0 = dp[d] - rb, s1 = dp[d + 1] - rb;
+    for (int i = s0 + tid; i < s1; i += width) {
+      const int e0 = rp[i], e1 = rp[i + 1];
+      if (e1 - e0 > kCrossLight) continue;
+      double acc = sr[i];
+      for (int e = e0; e < e1; ++e) acc += sr[es[e]] * c / static_cast<double>(ed[e]);
+      sr[i] = loop_factor(L, rb + i, c, acc);
+    }
+    for (int base = s0 + wid * 32; base < s1; base += nw * 32) {
+      const int i = base + lane;
+      const int deg_in = i < s1 ? rp[i + 1] - rp[i] : 0;
+      unsigned mask = __ballot_sync(0xffffffffu, deg_in > kCrossLight);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int row = base + src;
+        double y = 0.0;
+        for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) y += sr[es[e]] * c / static_cast<double>(ed[e]);
+        y = warp_sum(y);
+        if (lane == 0) sr[row] = loop_factor(L, rb + row, c, sr[row] + y);
+      }
+    }
+  }
+  sync();
+  for (int i = tid; i < m; i += width) rank[rb + i] = sr[i];
+}
+
+// bytes cac_sweep_staged needs for a CAC of m rows and ne in-edges
+__host__ __device__ constexpr size_t cac_stage_bytes(long long m, long long ne) {
+  return static_cast<size_t>(m) * 8 + static_cast<size_t>(m + 1) * 4 + static_cast<size_t>(ne) * 8 + 16;
+}
+
 // ------------------------------------------------------------------ K5
 // Dense (I - cA^T) r = w per SccSmall unit in shared memory
 // (solve_dense_system, solvers.cpp:92-108).  The matrix is strictly
@@ -310,7 +380,8 @@ __global__ void __launch_bounds__(kThreads)
     k_level(DeviceLayout L, const LevelTask* __restrict__ tasks, const CacTask* __restrict__ cacs,
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
             int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
-            const double* __restrict__ pf, double* rank, double* s0, long long* unit_iters, DevStatus* st) {
+            const double* __restrict__ pf, double* rank, double* s0, long long* unit_iters, DevStatus* st,
+            size_t smem_bytes) {
   extern __shared__ double sm[];
   __shared__ double red[2][32];
   const LevelTask t = tasks[blockIdx.x];
@@ -327,14 +398,22 @@ __global__ void __launch_bounds__(kThreads)
       cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, lane, 32);
       __threadfence_block();
       __syncwarp();
-      cac_sweep<false>(L, ct, depth_ptr, c, rank, lane, 32);
+      const size_t per_warp = (smem_bytes / kWarpsPer) & ~static_cast<size_t>(15);
+      if (cac_stage_bytes(ct.row_end - ct.row_begin, L.iptr[ct.row_end] - L.iptr[ct.row_begin]) <= per_warp)
+        cac_sweep_staged<false>(L, ct, depth_ptr, c, rank, lane, 32,
+                                reinterpret_cast<unsigned char*>(sm) + per_warp * (threadIdx.x >> 5));
+      else
+        cac_sweep<false>(L, ct, depth_ptr, c, rank, lane, 32);
       break;
     }
     case kTaskCacBlock: {
       const CacTask ct = cacs[t.a];
       cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
       __syncthreads();
-      cac_sweep<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kThreads);
+      if (cac_stage_bytes(ct.row_end - ct.row_begin, L.iptr[ct.row_end] - L.iptr[ct.row_begin]) <= smem_bytes)
+        cac_sweep_staged<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kThreads, sm);
+      else
+        cac_sweep<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kThreads);
       break;
     }
     case kTaskSmall: {
@@ -365,18 +444,24 @@ constexpr int kBigThreads = 1024;
 __global__ void __launch_bounds__(kBigThreads)
     k_cac_big(DeviceLayout L, const CacTask* __restrict__ cacs, const int* __restrict__ depth_ptr,
               const double* __restrict__ w, const SolveParams* __restrict__ p, const double* __restrict__ pf,
-              double* rank, double* s0) {
+              double* rank, double* s0, size_t smem_bytes) {
+  extern __shared__ double sm[];
   const CacTask ct = cacs[blockIdx.x];
-  cac_sweep<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads);
+  if (cac_stage_bytes(ct.row_end - ct.row_begin, L.iptr[ct.row_end] - L.iptr[ct.row_begin]) <= smem_bytes)
+    cac_sweep_staged<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads, sm);
+  else
+    cac_sweep<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads);
 }
 
 }  // namespace
 
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
-                    const SolveParams* p, const double* pf, double* rank, double* s0, cudaStream_t s) {
+                    const SolveParams* p, const double* pf, double* rank, double* s0, size_t smem, cudaStream_t s) {
   if (n == 0) return;
-  k_cac_big<<<n, kBigThreads, 0, s>>>(L, cacs, depth_ptr, w, p, pf, rank, s0);
+  k_cac_big<<<n, kBigThreads, smem, s>>>(L, cacs, depth_ptr, w, p, pf, rank, s0, smem);
 }
+
+size_t cac_stage_need(long long rows, long long edges) { return cac_stage_bytes(rows, edges); }
 
 cudaError_t configure_level_kernel() {
   int dev = 0, optin = 0;
@@ -387,7 +472,12 @@ cudaError_t configure_level_kernel() {
   cudaFuncAttributes a{};
   e = cudaFuncGetAttributes(&a, k_level);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           optin - static_cast<int>(a.sharedSizeBytes));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncGetAttributes(&a, k_cac_big);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_cac_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               optin - static_cast<int>(a.sharedSizeBytes));
 }
 
@@ -397,7 +487,7 @@ void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, con
                   long long* unit_iters, DevStatus* st, cudaStream_t s) {
   if (ntasks == 0) return;
   k_level<<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p, pf, rank,
-                                         s0, unit_iters, st);
+                                         s0, unit_iters, st, smem);
 }
 
 }  // namespace lrk
