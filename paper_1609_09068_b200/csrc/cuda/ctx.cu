@@ -71,6 +71,7 @@ struct LevelTasks {
   int lt0 = 0, lt1 = 0;  // CTA tasks of the fused level kernel
   size_t smem = 0;       // its dynamic shared memory
   size_t big_smem = 0;   // dynamic shared memory of the k_cac_big launch
+  size_t sm_tile = 0;    // largest small_solve_tile footprint of the level
   int sl0 = 0, sl1 = 0;  // depth slices of large CACs (one launch each)
   int gu0 = 0, gu1 = 0;
   int bk0 = 0, bk1 = 0;
@@ -396,6 +397,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         rk = kSmall;
         if (m <= kSmallSmemMaxM) {
           small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+          // the tile solve, or the normalised one where small_tile_ok(m, c) fails
+          if (m <= kSmallTileMaxM) T.sm_tile = std::max(T.sm_tile, small_tile_bytes(m, L->iptr[re] - L->iptr[rb]));
           T.sm_max = std::max(T.sm_max, m);
         } else {  // beyond shared memory: global-scratch kernel after the level kernel
           small_big.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
@@ -536,7 +539,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
       const size_t b = need(cac_w[static_cast<size_t>(i)]);
       if (b <= kLevelStageBytes) mid_need = std::max(mid_need, b);
     }
-    T.smem = std::max({T.smem, warp_need, mid_need});
+    T.smem = std::max({T.smem, T.sm_tile, warp_need, mid_need});
     T.big_smem = 0;
     for (int i = T.cac_b0; i < T.cac_b1; ++i) {
       const size_t b = need(cac_w[static_cast<size_t>(i)]);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cmath>
 #include <cstdint>
 
 namespace lrk {
@@ -122,6 +123,18 @@ constexpr long long kCtaLargeMaxNnz = 1 << 16;
 constexpr int kMaxDynSmem = 227 * 1024;
 constexpr int kSmallSmemMaxM = 160;      // ld*(ld+2)*8 <= 227 KB
 constexpr int kSmallScratchBlocks = 296; // grid of the global-scratch small-SCC path
+constexpr int kSmallTileMaxM = 128;     // small SCCs up to this: tile Gauss-Jordan (level.cu)
+// the fraction-free tile solve keeps minors of size down to (1-c)^m: use it
+// while that stays far from underflow, else the normalised solve (level.cu)
+__host__ __device__ inline bool small_tile_ok(int m, double c) {
+  return m <= kSmallTileMaxM && static_cast<double>(m) * log1p(-c) > -640.0;
+}
+// shared memory of the tile solve: m x ((m+1)|1) matrix, m solution values,
+// the unit's ne in-edges (value + column)
+__host__ __device__ constexpr size_t small_tile_bytes(int m, long long ne) {
+  return (static_cast<size_t>(m) * static_cast<size_t>((m + 1) | 1) + static_cast<size_t>(m)) * sizeof(double) +
+         static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
+}
 constexpr int kCacWarpMaxRows = 64;      // CACs up to this: one warp of a k_level CTA
 constexpr int kCacMidMaxRows = 1024;     // up to this: a 256-thread k_level CTA; above: a 1024-thread CTA
 

@@ -301,6 +301,162 @@ __device__ void small_solve(const DeviceLayout& L, const SccTask& t, int ld, con
   for (int b = tid; b < m; b += kThreads) rank[rb + b] = rhs[b];
 }
 
+// Gauss-Jordan for m <= kSmallTileMaxM, shaped for the per-step latency
+// (measured on B200: FP64 multiply/add 23 cycles, shared load 29, barrier 38,
+// IEEE double division 90 -- the chain of dependent operations per
+// elimination step is what the solve time is made of).
+//  * The system [I - cA^T | w] is an m x (m+1) tile with an odd row stride;
+//    thread (warp, lane) always owns rows lane + 32a and columns warp + 8b.
+//  * Fraction-free (Bareiss) Gauss-Jordan: step k replaces every row i != k by
+//    (p_k * row_i - M[i][k] * row_k) / p_{k-1} on the columns j > k.  The
+//    entries stay minors of the matrix, within [(1-c)^m, (1+c)^m], and the
+//    reciprocal of p_{k-1} is computed during step k-1 after its stores, so
+//    a step's chain is shared load -> two multiplies -> multiply pair ->
+//    subtract -> store, without a division.  The step reads column k and
+//    row k and writes neither: one barrier per step.  Finished rows keep
+//    their diagonal in step with the others (the owner of M[i][i] applies
+//    p_k / p_{k-1}), so x_i = M[i][m] / M[i][i] at the end.
+//  * The in-edges are stashed in shared memory during assembly so the
+//    residual check of solvers.cpp:103-106 needs no second global gather.
+template <int A>
+__device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const double* __restrict__ pf,
+                                 double* rank, double* sm, unsigned long long* red, DevStatus* st) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  const int ld = (m + 1) | 1;
+  const long long eb = L.iptr[rb];
+  const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  double* M = sm;
+  double* x = M + static_cast<size_t>(m) * ld;
+  double* ev = x + m;
+  int* es = reinterpret_cast<int*>(ev + ne);
+  // this thread's row (m <= kThreads): start weight and in-edge range, loaded
+  // before the tile is cleared so the global latency overlaps it
+  const bool mine = tid < m;
+  double wb = 0.0;
+  int e0 = 0, e1 = 0;
+  if (mine) {
+    wb = rank[rb + tid];
+    e0 = static_cast<int>(L.iptr[rb + tid] - eb);
+    e1 = static_cast<int>(L.iptr[rb + tid + 1] - eb);
+  }
+  for (int i = tid; i < m * ld; i += kThreads) M[i] = 0.0;
+  __syncthreads();
+  if (mine) {
+    double* Mr = M + static_cast<size_t>(tid) * ld;
+    Mr[tid] = 1.0;
+    Mr[m] = wb;
+    for (int e = e0; e < e1; ++e) {
+      const int s = L.isrc[eb + e];
+      const double v = pf[s];
+      es[e] = s - rb;
+      ev[e] = v;
+      Mr[s - rb] -= v;
+    }
+  }
+  double* row[A];
+  bool valid[A], diag[A];
+#pragma unroll
+  for (int a = 0; a < A; ++a) {
+    const int i = lane + 32 * a;
+    valid[a] = i < m;
+    diag[a] = valid[a] && (i & 7) == warp;  // this thread owns M[i][i]
+    row[a] = M + static_cast<size_t>(valid[a] ? i : 0) * ld;
+  }
+  double rprev = 1.0;  // 1 / p_{k-1}
+  for (int k = 0; k < m; ++k) {
+    __syncthreads();
+    const double* pr = M + static_cast<size_t>(k) * ld;
+    const double p = pr[k];
+    const double pp = p * rprev;
+    double f[A];
+    bool ok[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int i = lane + 32 * a;
+      f[a] = row[a][k] * rprev;
+      ok[a] = valid[a] && i != k;
+      if (diag[a] && i < k) row[a][i] *= pp;  // finished rows: diagonal follows the row scale
+    }
+    // first owned column above k, then four owned columns per chunk: all
+    // loads first (addresses clamped into the tile), updates, predicated stores
+    for (int j = warp + ((k + 8 - warp) & ~7); j <= m; j += 32) {
+      double pk[4], v[4][A];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int jc = min(j + 8 * q, m);
+        pk[q] = pr[jc];
+#pragma unroll
+        for (int a = 0; a < A; ++a) v[q][a] = row[a][jc];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int a = 0; a < A; ++a) v[q][a] = pp * v[q][a] - f[a] * pk[q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j + 8 * q <= m) {
+#pragma unroll
+          for (int a = 0; a < A; ++a)
+            if (ok[a]) row[a][j + 8 * q] = v[q][a];
+        }
+    }
+    rprev = 1.0 / p;  // for step k+1; overlaps the barrier wait
+  }
+  __syncthreads();
+  double xb = 0.0;
+  if (mine) {
+    xb = M[static_cast<size_t>(tid) * ld + m] / M[static_cast<size_t>(tid) * ld + tid];
+    x[tid] = xb;
+  }
+  __syncthreads();
+  // residual check of solvers.cpp:103-106 on the stashed in-edges; maxima of
+  // non-negative doubles as integer maxima of their bit patterns
+  unsigned long long res = 0, wm = 0, xm = 0;
+  if (mine) {
+    double acc = xb;
+    for (int e = e0; e < e1; ++e) acc -= ev[e] * x[es[e]];
+    res = dbits(fabs(acc - wb));
+    wm = dbits(fabs(wb));
+    xm = dbits(fabs(xb));
+    rank[rb + tid] = xb;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    res = max(res, __shfl_xor_sync(0xffffffffu, res, o));
+    wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    xm = max(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+  }
+  if (lane == 0) {
+    red[warp] = res;
+    red[8 + warp] = wm;
+    red[16 + warp] = xm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < kWarpsPer; ++i) {
+      res = max(res, red[i]);
+      wm = max(wm, red[8 + i]);
+      xm = max(xm, red[16 + i]);
+    }
+    if (!(bitsd(res) <= 1e-8 * (1.0 + bitsd(wm) + bitsd(xm)))) atomicOr(&st->err, kErrDegen);
+  }
+}
+
+__device__ void small_dispatch(const DeviceLayout& L, const SccTask& t, int ld, double c,
+                               const double* __restrict__ pf, double* rank, double* sm, double* red, DevStatus* st) {
+  const int m = t.row_end - t.row_begin;
+  auto* r = reinterpret_cast<unsigned long long*>(red);
+  if (!small_tile_ok(m, c))
+    small_solve(L, t, ld, pf, rank, sm, red, st);
+  else if (m <= 32)
+    small_solve_tile<1>(L, t, pf, rank, sm, r, st);
+  else if (m <= 64)
+    small_solve_tile<2>(L, t, pf, rank, sm, r, st);
+  else
+    small_solve_tile<4>(L, t, pf, rank, sm, r, st);
+}
+
 // ------------------------------------------------------------------ K4a
 // The whole power series of one SccLarge unit in one CTA (solve_large_scc,
 // solvers.cpp:128-162): pushed vectors in shared memory, one thread per row in
@@ -420,7 +576,7 @@ __global__ void __launch_bounds__(kThreads)
       const SccTask sct = smalls[t.a];
       cross_rows(L, sct.row_begin, sct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
       __syncthreads();
-      small_solve(L, sct, small_ld, pf, rank, sm, red[0], st);
+      small_dispatch(L, sct, small_ld, c, pf, rank, sm, red[0], st);
       break;
     }
     case kTaskLcta: {
