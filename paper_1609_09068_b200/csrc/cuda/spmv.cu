@@ -40,7 +40,7 @@ using namespace dev;
 constexpr int kWarps = kSpmvThreads / 32;
 constexpr int kPerLane = kTileNnz / 32;
 constexpr int kLongRow = 32;
-constexpr int kL1HotRows = 16384;  // columns allowed to allocate in L1 (see ld_gather)
+constexpr int kHeadRows = 8192;  // shared-memory head entries (LR_SPMV_HEAD overrides)
 
 __device__ __forceinline__ std::uint64_t policy_evict_first() {
   std::uint64_t p;
@@ -72,28 +72,29 @@ __device__ __forceinline__ double ld_stream(const double* p, std::uint64_t pol) 
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
-// The gathered pushed vector.  Only its hottest columns (the first rows of
-// the degree-ordered unit) may allocate in L1, so that cold gathers -- the
-// great majority, each touching a different line -- do not evict them: a
-// predicated allocating load and a predicated non-allocating load are both
-// issued and selected afterwards (no branch, all gathers stay in flight).
+// The gathered pushed vector.  Its hottest columns -- the first rows of the
+// degree-ordered unit, the target of most in-edges -- are copied into shared
+// memory at the start of each launch; a gather reads shared memory when its
+// column is in that head and global memory (no L1 allocation) otherwise.  Both
+// loads are issued predicated and selected afterwards (no branch, so all of a
+// chunk's gathers stay in flight together).
 __device__ __forceinline__ double ld_keep(const double* p, std::uint64_t pol) {
   double v;
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ double ld_gather(const double* p, std::uint64_t pol, unsigned hot) {
+__device__ __forceinline__ double ld_gather(const double* gp, unsigned sh, unsigned in_head, std::uint64_t pol) {
   double a = 0.0, b = 0.0;
   asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
       : "+d"(a)
-      : "l"(p), "r"(hot), "l"(pol));
+      : "r"(sh), "r"(in_head));
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], "
       "%3;\n\t}"
       : "+d"(b)
-      : "l"(p), "r"(hot), "l"(pol));
-  return hot ? a : b;
+      : "l"(gp), "r"(in_head), "l"(pol));
+  return in_head ? a : b;
 }
 __device__ __forceinline__ void st_keep(double* p, double v, std::uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
@@ -149,19 +150,24 @@ __global__ void __launch_bounds__(kSpmvThreads)
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
                 const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int l1_hot, double* maxbuf) {
-  __shared__ double vals[kWarps][kTileNnz];
+                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, double* maxbuf) {
+  extern __shared__ double dyn[];  // [kWarps][kTileNnz] staging, then the head
+  double* head = dyn + kWarps * kTileNnz;
   __shared__ int wunit[kWarps];
   __shared__ double wmax[kWarps];
   __shared__ int last_cta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* v = vals[warp];
+  double* v = dyn + warp * kTileNnz;
   const std::uint64_t stream = policy_evict_first();
   const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
   const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
   int cur_unit = -1;
   double lmax = 0.0;
   const int stride = gridDim.x * kWarps;
+  // this launch's copy of the hot head of s_in (read-only for the launch)
+  for (int i = threadIdx.x; i < nhead; i += kSpmvThreads) head[i] = ld_keep(s_in + hot_begin + i, keep);
+  const unsigned head_sh = static_cast<unsigned>(__cvta_generic_to_shared(head));
+  __syncthreads();
 
   // Software pipeline over 256-edge chunks (a tile is one chunk, long rows and
   // segments up to four): the index loads of chunk i+1 are issued together
@@ -204,7 +210,11 @@ __global__ void __launch_bounds__(kSpmvThreads)
     double g[kPerLane];
 #pragma unroll
     for (int k = 0; k < kPerLane; ++k)
-      g[k] = ld_gather(s_in + idx[k], keep, static_cast<unsigned>(idx[k] - hot_begin) < static_cast<unsigned>(l1_hot));
+    {
+      const unsigned off = static_cast<unsigned>(idx[k] - hot_begin);
+      const unsigned in = off < static_cast<unsigned>(nhead);
+      g[k] = ld_gather(s_in + idx[k], head_sh + (in ? off : 0u) * 8u, in, keep);
+    }
     // 2. this tile's row operands, in flight with the gathers
     const int nr = tile ? b.row_end - b.row_begin : 0;
     int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
@@ -356,13 +366,32 @@ int blocks_for(long long n, int threads) { return static_cast<int>((n + threads 
 
 }  // namespace
 
+// Dynamic shared memory of k_grid_iter: as many head entries as fit next to
+// the static staging buffers (LR_SPMV_HEAD caps it; 0 disables the head).
+static int head_capacity() {
+  static int cap = -1;
+  if (cap < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, k_grid_iter);
+    cap = ((optin - static_cast<int>(a.sharedSizeBytes)) / 8 - kWarps * kTileNnz) / 32 * 32;
+    const char* e = std::getenv("LR_SPMV_HEAD");
+    cap = std::min(cap, e ? std::max(0, std::atoi(e)) : kHeadRows);
+    cudaFuncSetAttribute(k_grid_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + kWarps * kTileNnz) * 8);
+  }
+  return cap;
+}
+
 int grid_iter_ctas() {
   static int ctas = 0;
   if (ctas == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads,
+                                                  static_cast<size_t>(head_capacity() + kWarps * kTileNnz) * 8);
     ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
   return ctas;
@@ -383,13 +412,10 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks,
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
   const int want = blocks_for(ntasks, kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
-  static const int l1_hot = [] {
-    const char* e = std::getenv("LR_L1_HOT");
-    return e ? std::atoi(e) : kL1HotRows;
-  }();
-  k_grid_iter<<<grid, kSpmvThreads, 0, s>>>(L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank,
-                                            s_in, s_out, unit_iters, st, hot_begin, hot_bytes, unit_bytes, l1_hot,
-                                            maxbuf);
+  const int nhead = static_cast<int>(std::min<long long>(head_capacity(), unit_rows));
+  k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
+      L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
+      hot_begin, hot_bytes, unit_bytes, nhead, maxbuf);
 }
 
 void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s) {
