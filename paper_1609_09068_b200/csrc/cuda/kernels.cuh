@@ -114,7 +114,7 @@ struct LevelTask {
   int pad;
 };
 constexpr int kCacBlockMaxRows = 32768;  // larger CACs: one grid-wide launch per depth slice
-constexpr int kSpmvThreads = 768;  // one persistent CTA per SM: 24 warps + a shared-memory head
+constexpr int kSpmvThreads = 1024;  // one persistent CTA per SM: 32 warps + a shared-memory head
 constexpr int kTileNnz = 256;      // in-edges of one warp tile
 constexpr int kTileRows = 64;      // max rows of one warp tile
 constexpr int kSegNnz = 1024;      // rows above this are split into segments
