@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -540,6 +541,11 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
       if (b <= kLevelStageBytes) mid_need = std::max(mid_need, b);
     }
     T.smem = std::max({T.smem, T.sm_tile, warp_need, mid_need});
+    for (int i = T.lc0; i < T.lc1; ++i) {  // CTA power series staged in shared memory where it fits
+      const SccTask& lt = lcta[static_cast<size_t>(i)];
+      const size_t b = lcta_stage_bytes(T.lc_max, L->iptr[lt.row_end] - L->iptr[lt.row_begin]);
+      if (b <= kLctaStageMaxBytes) T.smem = std::max(T.smem, b);
+    }
     T.big_smem = 0;
     for (int i = T.cac_b0; i < T.cac_b1; ++i) {
       const size_t b = need(cac_w[static_cast<size_t>(i)]);
@@ -640,6 +646,17 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   LR_CUDA_TRY(cudaMemsetAsync(ctx->status.p, 0, sizeof(DevStatus), s));
   if (ctx->n_units > 0) LR_CUDA_TRY(cudaMemsetAsync(ctx->unit_iters.p, 0, ctx->unit_iters.bytes(), s));
   LR_CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
+  // LR_LEVEL_PROF=1: per-level timing of k_level's CTAs by task type (diagnostic, synchronises every level)
+  const bool prof_on = std::getenv("LR_LEVEL_PROF") != nullptr;
+  DevBuf<long long> prof_buf;
+  double prof_max[5] = {0, 0, 0, 0, 0}, prof_crit[5] = {0, 0, 0, 0, 0}, prof_span = 0;
+  long long prof_cnt[5] = {0, 0, 0, 0, 0};
+  if (prof_on) {
+    int most = 1;
+    for (const LevelTasks& T : ctx->lt) most = std::max(most, T.lt1 - T.lt0);
+    LR_CUDA_TRY(prof_buf.alloc(static_cast<size_t>(3 * most)));
+    LR_CUDA_TRY(set_level_prof(prof_buf.p));
+  }
   launch_prep(L, w_dev, ctx->params.p, ctx->pf.p, ctx->status.p, s);
   ++launches;
   for (const LevelTasks& T : ctx->lt) {
@@ -655,6 +672,28 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
                    ctx->unit_iters.p, ctx->status.p, s);
       ++launches;
+      if (prof_on) {  // LR_LEVEL_PROF: per task type, the longest CTA of this level
+        const int nt = T.lt1 - T.lt0;
+        std::vector<long long> h(static_cast<size_t>(3 * nt));
+        LR_CUDA_TRY(cudaMemcpyAsync(h.data(), prof_buf.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+        LR_CUDA_TRY(cudaStreamSynchronize(s));
+        long long lo = h[1], hi = h[2];
+        double mx[5] = {0, 0, 0, 0, 0};
+        for (int i = 0; i < nt; ++i) {
+          const int ty = static_cast<int>(h[3 * i]);
+          lo = std::min(lo, h[3 * i + 1]);
+          hi = std::max(hi, h[3 * i + 2]);
+          mx[ty] = std::max(mx[ty], (h[3 * i + 2] - h[3 * i + 1]) * 1e-3);
+          prof_cnt[ty] += 1;
+        }
+        prof_span += (hi - lo) * 1e-3;
+        int arg = 0;
+        for (int ty = 0; ty < 5; ++ty) {
+          prof_max[ty] += mx[ty];
+          if (mx[ty] > mx[arg]) arg = ty;
+        }
+        prof_crit[arg] += mx[arg];
+      }
     }
     // large CACs: depth sweep in 1024-thread CTAs (start weights came from k_level)
     if (T.cac_b1 > T.cac_b0) {
@@ -749,6 +788,14 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   launches += 2 + (r1_dev ? 1 : 0);
   LR_CUDA_TRY(cudaGetLastError());
   LR_CUDA_TRY(cudaEventRecord(ctx->ev[1], s));
+  if (prof_on) {
+    LR_CUDA_TRY(set_level_prof(nullptr));
+    static const char* names[5] = {"rows", "cac_warps", "cac_block", "small", "lcta"};
+    std::fprintf(stderr, "[LR_LEVEL_PROF] k_level span sum %.1f us over %zu levels\n", prof_span, ctx->lt.size());
+    for (int ty = 0; ty < 5; ++ty)
+      std::fprintf(stderr, "  %-10s ctas %8lld  sum of per-level max %9.1f us  critical in levels: %9.1f us\n",
+                   names[ty], prof_cnt[ty], prof_max[ty], prof_crit[ty]);
+  }
   LR_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   if (unit_iters && ctx->n_units > 0)
     LR_CUDA_TRY(cudaMemcpyAsync(unit_iters, ctx->unit_iters.p, ctx->unit_iters.bytes(), cudaMemcpyDeviceToHost, s));

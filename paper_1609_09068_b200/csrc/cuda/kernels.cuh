@@ -129,12 +129,20 @@ constexpr int kSmallTileMaxM = 128;     // small SCCs up to this: tile Gauss-Jor
 __host__ __device__ inline bool small_tile_ok(int m, double c) {
   return m <= kSmallTileMaxM && static_cast<double>(m) * log1p(-c) > -640.0;
 }
-// shared memory of the tile solve: m x ((m+1)|1) matrix, m solution values,
+// shared memory of the tile solve: m x small_tile_ld(m) matrix, m solution values,
 // the unit's ne in-edges (value + column)
+__host__ __device__ constexpr int small_tile_ld(int m) { return (m + 32) | 1; }
 __host__ __device__ constexpr size_t small_tile_bytes(int m, long long ne) {
-  return (static_cast<size_t>(m) * static_cast<size_t>((m + 1) | 1) + static_cast<size_t>(m)) * sizeof(double) +
+  return (static_cast<size_t>(m) * static_cast<size_t>(small_tile_ld(m)) + static_cast<size_t>(m)) * sizeof(double) +
          static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
 }
+// shared memory of lcta_solve_staged for a unit of m rows and ne in-edges,
+// with the level's largest unit at maxrows rows
+__host__ __device__ constexpr size_t lcta_stage_bytes(int maxrows, long long ne) {
+  return static_cast<size_t>(maxrows) * 32 + ((static_cast<size_t>(maxrows) + 1) * 4 + 7) / 8 * 8 +
+         static_cast<size_t>(ne) * 2;
+}
+constexpr size_t kLctaStageMaxBytes = 96 * 1024;  // k_level smem budget for staged CTA power series
 constexpr int kCacWarpMaxRows = 64;      // CACs up to this: one warp of a k_level CTA
 constexpr int kCacMidMaxRows = 1024;     // up to this: a 256-thread k_level CTA; above: a 1024-thread CTA
 
@@ -148,6 +156,8 @@ void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int
 size_t cac_stage_need(long long rows, long long edges);
 constexpr size_t kStageMaxBytes = 200 * 1024;  // larger CACs sweep from global memory
 constexpr size_t kLevelStageBytes = 64 * 1024; // CAC staging budget of one k_level CTA
+// k_level per-CTA timing buffer (3 int64 per CTA: type, start ns, end ns), nullptr = off
+cudaError_t set_level_prof(long long* buf);
 // fused per-level kernel (level.cu)
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,

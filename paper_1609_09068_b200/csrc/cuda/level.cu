@@ -308,22 +308,25 @@ __device__ void small_solve(const DeviceLayout& L, const SccTask& t, int ld, con
 //  * The system [I - cA^T | w] is an m x (m+1) tile with an odd row stride;
 //    thread (warp, lane) always owns rows lane + 32a and columns warp + 8b.
 //  * Fraction-free (Bareiss) Gauss-Jordan: step k replaces every row i != k by
-//    (p_k * row_i - M[i][k] * row_k) / p_{k-1} on the columns j > k.  The
-//    entries stay minors of the matrix, within [(1-c)^m, (1+c)^m], and the
-//    reciprocal of p_{k-1} is computed during step k-1 after its stores, so
-//    a step's chain is shared load -> two multiplies -> multiply pair ->
+//    (p_k * row_i - M[i][k] * row_k) * r, r ~ 1/p_{k-1}, on the columns j > k.
+//    The entries stay near minors of the matrix, within [(1-c)^m, (1+c)^m];
+//    r comes from the hardware reciprocal approximation issued in step k-1,
+//    so a step's chain is shared load -> two multiplies -> multiply pair ->
 //    subtract -> store, without a division.  The step reads column k and
 //    row k and writes neither: one barrier per step.  Finished rows keep
 //    their diagonal in step with the others (the owner of M[i][i] applies
 //    p_k / p_{k-1}), so x_i = M[i][m] / M[i][i] at the end.
 //  * The in-edges are stashed in shared memory during assembly so the
 //    residual check of solvers.cpp:103-106 needs no second global gather.
+#ifdef LR_TILE_PROBE
+__device__ long long* g_tile_probe;
+#endif
 template <int A>
 __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const double* __restrict__ pf,
                                  double* rank, double* sm, unsigned long long* red, DevStatus* st) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rb = t.row_begin, m = t.row_end - t.row_begin;
-  const int ld = (m + 1) | 1;
+  const int ld = small_tile_ld(m);  // zero columns past m: a chunk never needs a bound check
   const long long eb = L.iptr[rb];
   const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
   double* M = sm;
@@ -366,6 +369,9 @@ __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const 
   double rprev = 1.0;  // 1 / p_{k-1}
   for (int k = 0; k < m; ++k) {
     __syncthreads();
+#ifdef LR_TILE_PROBE  // tools/small_bench.cu: per-step cycle stamps of warp 0
+    if (threadIdx.x == 0) g_tile_probe[blockIdx.x * 160 + k] = clock64();
+#endif
     const double* pr = M + static_cast<size_t>(k) * ld;
     const double p = pr[k];
     const double pp = p * rprev;
@@ -373,35 +379,39 @@ __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const 
     bool ok[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
-      const int i = lane + 32 * a;
       f[a] = row[a][k] * rprev;
-      ok[a] = valid[a] && i != k;
-      if (diag[a] && i < k) row[a][i] *= pp;  // finished rows: diagonal follows the row scale
+      ok[a] = valid[a] && lane + 32 * a != k;
     }
     // first owned column above k, then four owned columns per chunk: all
-    // loads first (addresses clamped into the tile), updates, predicated stores
+    // loads first, then the updates, then the stores (columns past m are zero
+    // padding and stay zero)
     for (int j = warp + ((k + 8 - warp) & ~7); j <= m; j += 32) {
       double pk[4], v[4][A];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int jc = min(j + 8 * q, m);
-        pk[q] = pr[jc];
+        pk[q] = pr[j + 8 * q];
 #pragma unroll
-        for (int a = 0; a < A; ++a) v[q][a] = row[a][jc];
+        for (int a = 0; a < A; ++a) v[q][a] = row[a][j + 8 * q];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
         for (int a = 0; a < A; ++a) v[q][a] = pp * v[q][a] - f[a] * pk[q];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (j + 8 * q <= m) {
+      for (int a = 0; a < A; ++a)
+        if (ok[a]) {
 #pragma unroll
-          for (int a = 0; a < A; ++a)
-            if (ok[a]) row[a][j + 8 * q] = v[q][a];
+          for (int q = 0; q < 4; ++q) row[a][j + 8 * q] = v[q][a];
         }
     }
-    rprev = 1.0 / p;  // for step k+1; overlaps the barrier wait
+#pragma unroll
+    for (int a = 0; a < A; ++a)  // finished rows: the diagonal follows the row scale
+      if (diag[a] && lane + 32 * a < k) row[a][lane + 32 * a] *= pp;
+    // Row scale for step k+1.  Any nonzero factor is a valid row operation
+    // (the solution does not depend on it); ~1/p_k only keeps the entries
+    // near the minors, so the hardware approximation (one MUFU, no Newton
+    // steps, no branch) is enough.
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rprev) : "d"(p));
   }
   __syncthreads();
   double xb = 0.0;
@@ -458,6 +468,108 @@ __device__ void small_dispatch(const DeviceLayout& L, const SccTask& t, int ld, 
 }
 
 // ------------------------------------------------------------------ K4a
+// Block max of non-negative doubles as the max of their bit patterns: two
+// warp reductions (high word, then low word among the lanes holding the top
+// high word), one barrier, eight integer compares -- no FP64 on the chain.
+__device__ __forceinline__ unsigned long long block_max_bits(unsigned long long v, unsigned long long* red) {
+  const unsigned hi = static_cast<unsigned>(v >> 32);
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? static_cast<unsigned>(v) : 0u);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = (static_cast<unsigned long long>(mh) << 32) | ml;
+  __syncthreads();
+  unsigned long long m = red[0];
+#pragma unroll
+  for (int i = 1; i < kWarpsPer; ++i) m = max(m, red[i]);
+  return m;
+}
+
+// The whole power series of one SccLarge unit in one CTA (solve_large_scc,
+// solvers.cpp:128-162), everything in shared memory: the pushed vectors, the
+// ranks, pf, the row offsets and the in-edges as 16-bit offsets into the unit,
+// so an iteration touches no global memory -- one thread per row in the
+// reference's order (bit-exact), a warp for rows above kCrossLight, and the
+// stop test on integer maxima.
+__device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int maxrows,
+                                  const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
+                                  long long* unit_iters, DevStatus* st, double* sm, double (*red)[32]) {
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sc = sm;
+  double* sn = sm + maxrows;
+  double* pl = sm + 2 * maxrows;
+  double* rk = sm + 3 * maxrows;
+  int* rp = reinterpret_cast<int*>(sm + 4 * maxrows);
+  unsigned short* es = reinterpret_cast<unsigned short*>(sm + 4 * maxrows + (maxrows + 2) / 2);
+  const long long eb = L.iptr[rb];
+  const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  for (int i = threadIdx.x; i < m; i += kThreads) {
+    const double pv = pf[rb + i], r = rank[rb + i];
+    pl[i] = pv;
+    rk[i] = r;
+    sc[i] = pv * r;
+    rp[i] = static_cast<int>(L.iptr[rb + i] - eb);
+  }
+  if (threadIdx.x == 0) rp[m] = ne;
+  for (int e = threadIdx.x; e < ne; e += kThreads) es[e] = static_cast<unsigned short>(L.isrc[eb + e] - rb);
+  __syncthreads();
+  const double tol = p->tol;
+  const long long cap = p->cap;
+  auto* rb2 = reinterpret_cast<unsigned long long(*)[32]>(red);
+  long long it = 0;
+  bool fail = false;
+  for (;;) {
+    unsigned long long lmax = 0ull;
+    for (int i = threadIdx.x; i < m; i += kThreads) {
+      const int e0 = rp[i], e1 = rp[i + 1];
+      if (e1 - e0 > kCrossLight) continue;
+      double y = 0.0;
+      for (int e = e0; e < e1; ++e) y += sc[es[e]];
+      rk[i] += y;
+      sn[i] = pl[i] * y;
+      lmax = max(lmax, dbits(y));
+    }
+    if (t.pad) {  // the unit has rows above kCrossLight
+      for (int base = warp * 32; base < m; base += kWarpsPer * 32) {
+        const int i = base + lane;
+        const int d = i < m ? rp[i + 1] - rp[i] : 0;
+        unsigned mask = __ballot_sync(0xffffffffu, d > kCrossLight);
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int row = base + src;
+          double y = 0.0;
+          for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) y += sc[es[e]];
+          y = warp_sum(y);
+          if (lane == 0) {
+            rk[row] += y;
+            sn[row] = pl[row] * y;
+            lmax = max(lmax, dbits(y));
+          }
+        }
+      }
+    }
+    const double mx = bitsd(block_max_bits(lmax, rb2[it & 1]));
+    double* tmp = sc;
+    sc = sn;
+    sn = tmp;
+    ++it;
+    if (it > cap) {
+      fail = true;
+      break;
+    }
+    if (!(mx >= tol)) break;
+  }
+  for (int i = threadIdx.x; i < m; i += kThreads) rank[rb + i] = rk[i];
+  if (threadIdx.x == 0) {
+    unit_iters[t.unit] = it;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->iterative_edge_work),
+              static_cast<unsigned long long>(it * t.edges));
+    if (fail) atomicOr(&st->err, kErrNoConv);
+  }
+}
+
+// Fallback when the unit does not fit lcta_solve_staged: in-edges read from global memory.
 // The whole power series of one SccLarge unit in one CTA (solve_large_scc,
 // solvers.cpp:128-162): pushed vectors in shared memory, one thread per row in
 // the reference's order (bit-exact), a warp for rows above kCrossLight.
@@ -532,6 +644,15 @@ __device__ void lcta_solve(const DeviceLayout& L, const SccTask& t, int maxrows,
 }
 
 // ------------------------------------------------------------- dispatcher
+// Optional per-CTA timing of k_level (LR_LEVEL_PROF): task type, start, end (ns).
+__device__ long long* g_level_prof = nullptr;
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kThreads)
     k_level(DeviceLayout L, const LevelTask* __restrict__ tasks, const CacTask* __restrict__ cacs,
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
@@ -542,6 +663,8 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ double red[2][32];
   const LevelTask t = tasks[blockIdx.x];
   const double c = p->c;
+  long long* const prof = g_level_prof;
+  const long long t_start = prof ? global_ns() : 0;
   switch (t.type) {
     case kTaskRows:
       cross_rows(L, t.a, t.b, w, c, pf, rank, s0, threadIdx.x, kThreads);
@@ -583,11 +706,22 @@ __global__ void __launch_bounds__(kThreads)
       const SccTask lt = lctas[t.a];
       cross_rows(L, lt.row_begin, lt.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
       __syncthreads();
-      lcta_solve(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
+      if (lcta_stage_bytes(lcta_rows, L.iptr[lt.row_end] - L.iptr[lt.row_begin]) <= smem_bytes)
+        lcta_solve_staged(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
+      else
+        lcta_solve(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
       break;
     }
     default:
       break;
+  }
+  if (prof) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      prof[3 * blockIdx.x] = t.type;
+      prof[3 * blockIdx.x + 1] = t_start;
+      prof[3 * blockIdx.x + 2] = global_ns();
+    }
   }
 }
 
@@ -636,6 +770,8 @@ cudaError_t configure_level_kernel() {
   return cudaFuncSetAttribute(k_cac_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               optin - static_cast<int>(a.sharedSizeBytes));
 }
+
+cudaError_t set_level_prof(long long* buf) { return cudaMemcpyToSymbol(g_level_prof, &buf, sizeof(buf)); }
 
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,

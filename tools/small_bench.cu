@@ -4,6 +4,7 @@
 //   ./small_bench [m] [count]
 // Times the production small_solve against the variants below, one CTA per
 // SCC, and reports cycles per CTA (clock64) and the kernel time.
+#define LR_TILE_PROBE
 #include "../paper_1609_09068_b200/csrc/cuda/level.cu"
 
 #include <algorithm>
@@ -153,6 +154,14 @@ int main(int argc, char** argv) {
                 best * 1e3, sum / K, mx, rel, hs.err, hres);
   };
   run("prod", [&] { k_bench_prod<<<K, kThreads, smem>>>(L, d_tasks, ld, d_pf, d_rank, st, cyc); });
+  long long* probe;
+  CK(cudaMalloc(&probe, static_cast<size_t>(K) * 160 * sizeof(long long)));
+  CK(cudaMemcpyToSymbol(g_tile_probe, &probe, sizeof(probe)));
   run("tile", [&] { k_bench_tile<<<K, kThreads, tsmem>>>(L, d_tasks, ld, d_pf, d_rank, st, cyc); });
+  std::vector<long long> hp(static_cast<size_t>(K) * 160);
+  CK(cudaMemcpy(hp.data(), probe, hp.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  std::printf("  step cycles (CTA 0):");
+  for (int k = 1; k < std::min(m, 24); ++k) std::printf(" %lld", hp[k] - hp[k - 1]);
+  std::printf("\n");
   return 0;
 }
