@@ -1,0 +1,141 @@
+"""GPU parity on the reference's edge cases and on every device code path.
+
+Each graph is shaped to force one path of the CUDA solve (heavy cross rows,
+segmented SpMV rows, CAC slices, the three SccSmall solvers, deep level
+chains) and is checked against the oracle restatement: ranks to 1e-10
+relative, per-unit iteration counts and report counters exactly.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def check(lr, oracle, n, src, dst, w=None, c=0.85, tol=1e-12, th=100, keep=False):
+    src = np.asarray(src, dtype=np.int32)
+    dst = np.asarray(dst, dtype=np.int32)
+    w = np.full(n, 1.0 / max(n, 1)) if w is None else np.asarray(w, dtype=np.float64)
+    g = lr.Graph.from_edges(n, src=src, dst=dst, loop_policy=int(keep))
+    ref = oracle.graph(n, src, dst, keep).compute_pagerank(w, c, tol, th)
+    res = lr.compute_pagerank(g, w, lr.SolverParams(c, tol), small_threshold=th)
+    assert np.array_equal(res.unit_iters, ref.unit_iters)
+    if n:
+        rel = np.abs(res.ranks - ref.ranks) / np.maximum(np.abs(ref.ranks), 1e-300)
+        assert rel.max() <= 1e-10, rel.max()
+    for k in ("total_edge_work", "iterative_edge_work", "components", "level_count", "total_iterations"):
+        assert res.report[k] == ref.report[k], k
+    return res
+
+
+# proj/tests/test_engine.cpp:191-223
+def test_degenerate_inputs(lr):
+    empty = lr.Graph.from_edges(0, src=np.zeros(0, np.int32), dst=np.zeros(0, np.int32))
+    assert len(lr.compute_pagerank(empty, np.zeros(0), lr.SolverParams(0.85, 1e-9)).ranks) == 0
+    from conftest import FIXTURE8
+    g = lr.Graph.from_edges(8, FIXTURE8)
+    z = lr.compute_pagerank(g, np.zeros(8), lr.SolverParams(0.85, 1e-9))
+    assert z.report["all_weights_zero"] == 1 and not z.ranks.any()
+    with pytest.raises(ValueError):
+        lr.compute_pagerank(g, np.ones(7), lr.SolverParams(0.85, 1e-9))
+    w = np.ones(8)
+    w[3] = -0.25
+    with pytest.raises(ValueError):
+        lr.compute_pagerank(g, w, lr.SolverParams(0.85, 1e-9))
+    with pytest.raises(ValueError):
+        lr.compute_pagerank(g, np.ones(8), lr.SolverParams(1.0, 1e-9))
+    iso = lr.Graph.from_edges(5, src=np.zeros(0, np.int32), dst=np.zeros(0, np.int32))
+    w = np.array([1.0, 0.5, 0.0, 2.0, 0.25])
+    assert np.array_equal(lr.compute_pagerank(iso, w, lr.SolverParams(0.85, 1e-9)).ranks, w)
+
+
+# proj/tests/test_solvers.cpp (kept self-loops: closed forms)
+def test_kept_self_loops(lr, oracle):
+    r = check(lr, oracle, 1, [0], [0], w=[1.0], keep=True, tol=1e-9).ranks
+    assert abs(r[0] - 1 / 0.15) < 1e-12
+    r = check(lr, oracle, 2, [0, 0], [0, 1], w=[1.0, 1.0], keep=True, tol=1e-9).ranks
+    assert abs(r[0] - 40 / 23) < 1e-12
+
+
+def test_heavy_cross_rows(lr, oracle):
+    # one sink with 20,000 cross in-edges (> kCrossSplit: split over warps) and
+    # one with 3,000 (> kCrossLight: warp butterfly)
+    n = 20_003
+    src = np.r_[np.arange(3, n), np.arange(3, 3003)]
+    dst = np.r_[np.zeros(n - 3, np.int32), np.ones(3000, np.int32)]
+    check(lr, oracle, n, src, dst)
+
+
+def test_segmented_spmv_rows(lr, oracle):
+    # a 6,000-vertex SCC (grid SpMV) whose vertex 0 has 5,999 intra in-edges
+    # (segments of kSegNnz) and vertex 1 has 600 (long row)
+    m = 6000
+    ring_s = np.arange(m)
+    ring_d = (ring_s + 1) % m
+    src = np.r_[ring_s, np.arange(1, m), np.arange(2, 602)]
+    dst = np.r_[ring_d, np.zeros(m - 1, np.int32), np.ones(600, np.int32)]
+    res = check(lr, oracle, m, src, dst)
+    assert res.report["large_scc_vertices"] == m
+
+
+def test_big_cac_slices_and_depth(lr, oracle):
+    # a 40,000-vertex out-tree (one CAC > kCacBlockMaxRows: grid-wide depth
+    # slices) and a 20,000-vertex path (one CAC, 20,000 depth slices)
+    rng = np.random.default_rng(7)
+    n1 = 40_000
+    parent = np.array([rng.integers(0, v) for v in range(1, n1)], dtype=np.int32)
+    n2 = 20_000
+    src = np.r_[parent, n1 + np.arange(n2 - 1)]
+    dst = np.r_[np.arange(1, n1), n1 + np.arange(1, n2)]
+    check(lr, oracle, n1 + n2, src, dst)
+
+
+def test_cac_heavy_parent_rows(lr, oracle):
+    # DAG: 300 sources all feeding one vertex (a CAC row with > kCrossLight parents), then a chain
+    src = np.r_[np.arange(300), 300 + np.arange(50)]
+    dst = np.r_[np.full(300, 300), 301 + np.arange(50)]
+    check(lr, oracle, 351, src, dst)
+
+
+def _scc(rng, base, m, deg=4):
+    s = np.arange(m)
+    extra_s = rng.integers(0, m, m * deg)
+    extra_d = rng.integers(0, m, m * deg)
+    keep = extra_s != extra_d
+    return base + np.r_[s, extra_s[keep]], base + np.r_[(s + 1) % m, extra_d[keep]]
+
+
+@pytest.mark.parametrize("m,th,c", [
+    (60, 100, 0.85),     # register-tile Bareiss Gauss-Jordan
+    (120, 200, 0.85),    # tile, A = 4
+    (150, 200, 0.85),    # normalised shared-memory Gauss-Jordan (m > kSmallTileMaxM)
+    (220, 300, 0.85),    # global-scratch path (m > kSmallSmemMaxM)
+    (100, 200, 0.9999),  # (1-c)^m would underflow the fraction-free minors: normalised path
+])
+def test_small_scc_paths(lr, oracle, m, th, c):
+    rng = np.random.default_rng(m)
+    s1, d1 = _scc(rng, 0, m)
+    s2, d2 = _scc(rng, m, 7)
+    src = np.r_[s1, s2, [m + 1]]
+    dst = np.r_[d1, d2, [3]]
+    check(lr, oracle, m + 7, src, dst, th=th, c=c)
+
+
+def test_cta_and_grid_power_series(lr, oracle):
+    # SccLarge units on both sides of the CTA limit (kCtaLargeMaxRows rows) in one level
+    rng = np.random.default_rng(11)
+    s1, d1 = _scc(rng, 0, 3000, 3)
+    s2, d2 = _scc(rng, 3000, 5000, 3)
+    res = check(lr, oracle, 8000, np.r_[s1, s2], np.r_[d1, d2], c=0.9)
+    assert (res.unit_iters > 0).sum() == 2
+
+
+def test_ragged_weights(lr, oracle):
+    # zeros, tiny and huge weights on a random graph with every unit kind
+    rng = np.random.default_rng(5)
+    n = 3000
+    src = rng.integers(0, n, 9000)
+    dst = rng.integers(0, n, 9000)
+    w = rng.uniform(0, 1, n) * (rng.random(n) < 0.5)
+    w[:10] = 1e-280
+    w[10:20] = 1e120
+    check(lr, oracle, n, src, dst, w=w, th=50)
