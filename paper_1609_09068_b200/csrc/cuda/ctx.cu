@@ -150,8 +150,6 @@ std::vector<int> shard_bounds(const int64_t* iptr, int rb, int re, int world) {
 struct lr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t stream2 = nullptr;  // side stream for large CACs (joined every level)
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int n = 0;
   int n_levels = 0;
@@ -215,9 +213,6 @@ struct lr_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : lev)
       if (e) cudaEventDestroy(e);
-    if (fork_ev) cudaEventDestroy(fork_ev);
-    if (join_ev) cudaEventDestroy(join_ev);
-    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
     if (h_params) cudaFreeHost(h_params);
     if (h_status) cudaFreeHost(h_status);
@@ -263,10 +258,7 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
     lrerr::set(std::string("kernel setup failed: ") + cudaGetErrorString(e));
     return fail(LR_ECUDA);
   }
-  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     lrerr::set("CUDA stream creation failed");
     return fail(LR_ECUDA);
   }

@@ -75,32 +75,6 @@ __global__ void k_prep(DeviceLayout L, const double* __restrict__ w, const Solve
   if (threadIdx.x == 0 && m > 0.0) atomicMax(&st->wmax_bits, dbits(m));
 }
 
-// ---------------------------------------------------------------- cross
-// K1: start weights of one level = w + pushes from every higher level along
-// cross edges (propagate_weights, engine.cpp:83-87, in pull form; sources are
-// final).  Per row the terms are (c * r_src) / deg_src added in the
-// reference's order (source level desc, source id asc).  Singleton rows are
-// solved here (solve_singletons, solvers.cpp:23-35); SccLarge grid rows also
-// get their first pushed value s0 = pf * w (solvers.cpp:141-150).
-__global__ void k_cross(DeviceLayout L, int row_begin, int row_end, const double* __restrict__ w,
-                        const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
-                        double* __restrict__ s0) {
-  const int row = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= row_end) return;
-  const long long e1 = L.xptr[row + 1];
-  if (e1 - L.xptr[row] > kCrossLight) return;  // heavy rows: k_cross_heavy
-  const double c = p->c;
-  double acc = w[L.vertex_of[row]];
-  for (long long e = L.xptr[row]; e < e1; ++e) {
-    const int s = __ldg(L.xsrc + e);
-    acc += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
-  }
-  const std::uint8_t k = L.rowkind[row];
-  if (k == kSingle && L.loop[row]) acc /= 1.0 - c / static_cast<double>(L.deg[row]);
-  rank[row] = acc;
-  if (k == kLargeGrid) s0[row] = pf[row] * acc;
-}
-
 __device__ __forceinline__ void cross_finish(const DeviceLayout& L, int row, double acc, double c,
                                              const double* __restrict__ pf, double* rank, double* s0) {
   const std::uint8_t k = L.rowkind[row];
@@ -152,50 +126,6 @@ __global__ void k_pull_heavy(DeviceLayout L, const CrossTask* __restrict__ tasks
 }
 
 // ------------------------------------------------------------------ CAC
-// K3: one-pass topological propagation (solve_cac, solvers.cpp:37-88) in pull
-// form, depth slice by depth slice.  A row's parents sit in earlier slices
-// and are summed in the reference's Kahn dequeue order; the kept-loop factor
-// is applied after all parents, as at dequeue time (solvers.cpp:71-74).
-template <bool kBlock>
-__global__ void k_cac(DeviceLayout L, const CacTask* __restrict__ tasks, int ntasks,
-                      const int* __restrict__ depth_ptr, const SolveParams* __restrict__ p, double* rank) {
-  int task, lane, width;
-  if (kBlock) {
-    task = blockIdx.x;
-    lane = threadIdx.x;
-    width = blockDim.x;
-  } else {
-    task = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    lane = threadIdx.x & 31;
-    width = 32;
-  }
-  if (task >= ntasks) return;
-  const CacTask t = tasks[task];
-  const double c = p->c;
-  const int* dp = depth_ptr + t.depth_begin;
-  for (int r = dp[0] + lane; r < dp[1]; r += width)
-    if (L.loop[r]) rank[r] /= 1.0 - c / static_cast<double>(L.deg[r]);
-  for (int d = 1; d < t.ndepth; ++d) {
-    if (kBlock) {
-      __syncthreads();
-    } else {
-      __threadfence_block();
-      __syncwarp();
-    }
-    const int r1 = dp[d + 1];
-    for (int r = dp[d] + lane; r < r1; r += width) {
-      double acc = rank[r];
-      const long long e1 = L.iptr[r + 1];
-      for (long long e = L.iptr[r]; e < e1; ++e) {
-        const int s = L.isrc[e];
-        acc += rank[s] * c / static_cast<double>(L.deg[s]);
-      }
-      if (L.loop[r]) acc /= 1.0 - c / static_cast<double>(L.deg[r]);
-      rank[r] = acc;
-    }
-  }
-}
-
 // One depth slice of a large CAC across the whole grid (the slice's parents
 // are final: earlier slices ran in earlier launches).
 __global__ void k_cac_slice(DeviceLayout L, int row_begin, int row_end, const SolveParams* __restrict__ p,
@@ -293,62 +223,6 @@ __global__ void k_small(DeviceLayout L, const SccTask* __restrict__ tasks, int n
   }
 }
 
-// ---------------------------------------------------------- SccLarge, CTA
-// K4a: the whole accumulated power series of one SccLarge unit inside one CTA
-// (solve_large_scc, solvers.cpp:128-162) when its rows fit in shared memory.
-// Pull form: y_i = sum_{j in in(i)} s_j with s_j = pf_j * inc_j, summed by one
-// thread in ascending source order -> bit-identical to the reference's push
-// scatter; rank += y; stop when max y < tol; cap -> kErrNoConv.
-__global__ void k_large_cta(DeviceLayout L, const SccTask* __restrict__ tasks, int ntasks, int maxrows,
-                            const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
-                            long long* unit_iters, DevStatus* st) {
-  extern __shared__ double sm[];
-  __shared__ double red[2][32];
-  const SccTask t = tasks[blockIdx.x];
-  const int rb = t.row_begin, m = t.row_end - t.row_begin;
-  double* sc = sm;
-  double* sn = sm + maxrows;
-  double* pl = sm + 2 * maxrows;
-  const double tol = p->tol;
-  const long long cap = p->cap;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    pl[i] = pf[rb + i];
-    sc[i] = pl[i] * rank[rb + i];
-  }
-  __syncthreads();
-  long long it = 0;
-  bool fail = false;
-  for (;;) {
-    double lmax = 0.0;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      const int row = rb + i;
-      double y = 0.0;
-      const long long e1 = L.iptr[row + 1];
-      for (long long e = L.iptr[row]; e < e1; ++e) y += sc[__ldg(L.isrc + e) - rb];
-      rank[row] += y;
-      sn[i] = pl[i] * y;
-      lmax = fmax(lmax, y);
-    }
-    const double mx = block_max(lmax, red[it & 1]);
-    double* tmp = sc;
-    sc = sn;
-    sn = tmp;
-    ++it;
-    if (it > cap) {
-      fail = true;
-      break;
-    }
-    if (!(mx >= tol)) break;
-  }
-  if (threadIdx.x == 0) {
-    unit_iters[t.unit] = it;
-    atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&st->iterative_edge_work),
-              static_cast<unsigned long long>(it * t.edges));
-    if (fail) atomicOr(&st->err, kErrNoConv);
-  }
-}
-
 // --------------------------------------------------------------- output
 // R3 back to vertex order and fixed-order partial sums for the R1 total.
 __global__ void k_output(DeviceLayout L, const double* __restrict__ rank, double* __restrict__ r3,
@@ -407,12 +281,6 @@ void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, d
   k_prep<<<grid, 256, 0, s>>>(L, w, p, pf, st);
 }
 
-void launch_cross(const DeviceLayout& L, int row_begin, int row_end, const double* w, const SolveParams* p,
-                  const double* pf, double* rank, double* s0, cudaStream_t s) {
-  if (row_end <= row_begin) return;
-  k_cross<<<blocks_for(row_end - row_begin, 256), 256, 0, s>>>(L, row_begin, row_end, w, p, pf, rank, s0);
-}
-
 void launch_cross_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const double* w,
                         const SolveParams* p, const double* pf, double* rank, double* s0, double* parts, int* cnts,
                         cudaStream_t s) {
@@ -431,15 +299,6 @@ void launch_cac_slice(const DeviceLayout& L, int row_begin, int row_end, const S
                       cudaStream_t s) {
   if (row_end <= row_begin) return;
   k_cac_slice<<<blocks_for(row_end - row_begin, 256), 256, 0, s>>>(L, row_begin, row_end, p, rank);
-}
-
-void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool big, const int* depth_ptr,
-                const SolveParams* p, double* rank, cudaStream_t s) {
-  if (ntasks == 0) return;
-  if (big)
-    k_cac<true><<<ntasks, 512, 0, s>>>(L, tasks, ntasks, depth_ptr, p, rank);
-  else
-    k_cac<false><<<blocks_for(ntasks, 8), 256, 0, s>>>(L, tasks, ntasks, depth_ptr, p, rank);
 }
 
 void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_m, const double* pf,
@@ -470,18 +329,8 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
-  e = allow_dynamic_smem(k_small, optin);
-  if (e != cudaSuccess) return e;
-  return allow_dynamic_smem(k_large_cta, optin);
+  return allow_dynamic_smem(k_small, optin);
 }
-
-void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
-                      const double* pf, double* rank, long long* unit_iters, DevStatus* st, cudaStream_t s) {
-  if (ntasks == 0) return;
-  const size_t bytes = static_cast<size_t>(3) * max_rows * sizeof(double);
-  k_large_cta<<<ntasks, 256, bytes, s>>>(L, tasks, ntasks, max_rows, p, pf, rank, unit_iters, st);
-}
-
 
 void launch_output(const DeviceLayout& L, const double* rank, double* r3, double* partial, int nparts,
                    cudaStream_t s) {

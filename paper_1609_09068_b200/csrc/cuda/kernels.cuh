@@ -167,21 +167,15 @@ void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, con
 // launch wrappers (stream-ordered)
 void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,
                  cudaStream_t s);
-void launch_cross(const DeviceLayout& L, int row_begin, int row_end, const double* w, const SolveParams* p,
-                  const double* pf, double* rank, double* s0, cudaStream_t s);
 void launch_cross_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const double* w,
                         const SolveParams* p, const double* pf, double* rank, double* s0, double* parts, int* cnts,
                         cudaStream_t s);
-void launch_cac(const DeviceLayout& L, const CacTask* tasks, int ntasks, bool big, const int* depth_ptr,
-                const SolveParams* p, double* rank, cudaStream_t s);
 void launch_cac_slice(const DeviceLayout& L, int row_begin, int row_end, const SolveParams* p, double* rank,
                       cudaStream_t s);
 void launch_cac_heavy(const DeviceLayout& L, const CrossTask* tasks, int ntasks, const SolveParams* p, double* rank,
                       double* parts, int* cnts, cudaStream_t s);
 void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_m, const double* pf,
                   double* rank, double* scratch, DevStatus* st, cudaStream_t s);
-void launch_large_cta(const DeviceLayout& L, const SccTask* tasks, int ntasks, int max_rows, const SolveParams* p,
-                      const double* pf, double* rank, long long* unit_iters, DevStatus* st, cudaStream_t s);
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s);
 int grid_iter_ctas();
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,

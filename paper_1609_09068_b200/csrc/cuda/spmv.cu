@@ -40,7 +40,7 @@ using namespace dev;
 constexpr int kWarps = kSpmvThreads / 32;
 constexpr int kPerLane = kTileNnz / 32;
 constexpr int kLongRow = 32;
-constexpr int kHeadRows = 8192;  // shared-memory head entries (LR_SPMV_HEAD overrides)
+constexpr int kHeadRows = 8192;  // shared-memory head entries (see launch_grid_iter)
 
 __device__ __forceinline__ std::uint64_t policy_evict_first() {
   std::uint64_t p;
@@ -366,8 +366,8 @@ int blocks_for(long long n, int threads) { return static_cast<int>((n + threads 
 
 }  // namespace
 
-// Dynamic shared memory of k_grid_iter: as many head entries as fit next to
-// the static staging buffers (LR_SPMV_HEAD caps it; 0 disables the head).
+// Dynamic shared memory of k_grid_iter: at most as many head entries as fit
+// next to the staging buffers.
 static int head_capacity() {
   static int cap = -1;
   if (cap < 0) {
@@ -377,8 +377,6 @@ static int head_capacity() {
     cudaFuncAttributes a{};
     cudaFuncGetAttributes(&a, k_grid_iter);
     cap = ((optin - static_cast<int>(a.sharedSizeBytes)) / 8 - kWarps * kTileNnz) / 32 * 32;
-    const char* e = std::getenv("LR_SPMV_HEAD");
-    cap = std::min(cap, e ? std::max(0, std::atoi(e)) : kHeadRows);
     cudaFuncSetAttribute(k_grid_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + kWarps * kTileNnz) * 8);
   }
   return cap;
@@ -412,7 +410,13 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks,
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
   const int want = blocks_for(ntasks, kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
-  const int nhead = static_cast<int>(std::min<long long>(head_capacity(), unit_rows));
+  // Head size: measured optimum 4-12k entries at configs 2 and 5.  Larger
+  // heads lose: the fill costs microseconds per launch, and the L1 left over
+  // holds the in-flight misses of the cold gathers (at 20k entries config 5
+  // runs 3x slower).  LR_SPMV_HEAD overrides (0 disables the head).
+  int want_head = kHeadRows;
+  if (const char* e = std::getenv("LR_SPMV_HEAD")) want_head = std::max(0, std::atoi(e));
+  const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
   k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
       L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
       hot_begin, hot_bytes, unit_bytes, nhead, maxbuf);

@@ -81,7 +81,8 @@ def full(rep, out, traffic=None):
             return float(vals[i].replace(",", "")) * scale
         json.dump({"kernel": got.get("Kernel Name", "").split("(")[0].strip(), "report": rep.split("/")[-1],
                    "dram_bytes_per_launch": mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
-                   "duration_us": float(got.get("gpu__time_duration.sum", "0").replace(",", ""))},
+                   "duration_us": float(got.get("gpu__time_duration.sum", "0").replace(",", "")) *
+                   {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}[units[h.index("gpu__time_duration.sum")].strip()]},
                   open(traffic, "w"), indent=1)
 
 
