@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "devutil.cuh"
 #include "kernels.cuh"
@@ -517,7 +518,13 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
   auto* rb2 = reinterpret_cast<unsigned long long(*)[32]>(red);
   long long it = 0;
   bool fail = false;
+#ifdef LR_LCTA_PROBE  // tools/build_variant.sh probe: thread 0's cycles in the row phase / the stop test
+  long long cyc_rows = 0, cyc_max = 0, cyc_t0 = 0, cyc_t1 = 0;
+#endif
   for (;;) {
+#ifdef LR_LCTA_PROBE
+    cyc_t0 = clock64();
+#endif
     unsigned long long lmax = 0ull;
     for (int i = threadIdx.x; i < m; i += kThreads) {
       const int e0 = rp[i], e1 = rp[i + 1];
@@ -548,7 +555,14 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
         }
       }
     }
+#ifdef LR_LCTA_PROBE
+    cyc_t1 = clock64();
+    cyc_rows += cyc_t1 - cyc_t0;
+#endif
     const double mx = bitsd(block_max_bits(lmax, rb2[it & 1]));
+#ifdef LR_LCTA_PROBE
+    cyc_max += clock64() - cyc_t1;
+#endif
     double* tmp = sc;
     sc = sn;
     sn = tmp;
@@ -560,6 +574,11 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
     if (!(mx >= tol)) break;
   }
   for (int i = threadIdx.x; i < m; i += kThreads) rank[rb + i] = rk[i];
+#ifdef LR_LCTA_PROBE
+  if (threadIdx.x == 0)
+    printf("lcta unit %d m %d ne %d pad %d it %lld rows %lld max %lld cycles/iter\n", t.unit, m, ne, t.pad, it,
+           cyc_rows / it, cyc_max / it);
+#endif
   if (threadIdx.x == 0) {
     unit_iters[t.unit] = it;
     atomicAdd(reinterpret_cast<unsigned long long*>(&st->total_iterations), static_cast<unsigned long long>(it));
