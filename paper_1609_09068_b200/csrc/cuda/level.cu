@@ -526,14 +526,46 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
     cyc_t0 = clock64();
 #endif
     unsigned long long lmax = 0ull;
-    for (int i = threadIdx.x; i < m; i += kThreads) {
-      const int e0 = rp[i], e1 = rp[i + 1];
-      if (e1 - e0 > kCrossLight) continue;
-      double y = 0.0;
-      for (int e = e0; e < e1; ++e) y += sc[es[e]];
-      rk[i] += y;
-      sn[i] = pl[i] * y;
-      lmax = max(lmax, dbits(y));
+    // Two rows per thread in flight together; each row's in-edges in groups
+    // of four (indices, then values, then the adds in order), so a row costs
+    // two shared-memory round trips per group instead of two per edge.
+    for (int i0 = threadIdx.x; i0 < m; i0 += 2 * kThreads) {
+      const int i1 = i0 + kThreads;
+      const bool has1 = i1 < m;
+      const int a0 = rp[i0], a1 = rp[i0 + 1];
+      const int b0 = has1 ? rp[i1] : 0, b1 = has1 ? rp[i1 + 1] : 0;
+      const bool light0 = a1 - a0 <= kCrossLight, light1 = has1 && b1 - b0 <= kCrossLight;
+      const int na = light0 ? a1 - a0 : 0, nb = light1 ? b1 - b0 : 0;
+      double ya = 0.0, yb = 0.0;
+      for (int g = 0; g < na || g < nb; g += 4) {
+        int ia[4], ib[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ia[q] = g + q < na ? es[a0 + g + q] : 0;
+          ib[q] = g + q < nb ? es[b0 + g + q] : 0;
+        }
+        double va[4], vb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          va[q] = sc[ia[q]];
+          vb[q] = sc[ib[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (g + q < na) ya += va[q];
+          if (g + q < nb) yb += vb[q];
+        }
+      }
+      if (light0) {
+        rk[i0] += ya;
+        sn[i0] = pl[i0] * ya;
+        lmax = max(lmax, dbits(ya));
+      }
+      if (light1) {
+        rk[i1] += yb;
+        sn[i1] = pl[i1] * yb;
+        lmax = max(lmax, dbits(yb));
+      }
     }
     if (t.pad) {  // the unit has rows above kCrossLight
       for (int base = warp * 32; base < m; base += kWarpsPer * 32) {
