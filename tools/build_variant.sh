@@ -8,6 +8,6 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 dst=$root/build_variants/$name
 rm -rf "$dst" && mkdir -p "$dst"
 cp -r "$root/paper_1609_09068_b200/csrc" "$root/paper_1609_09068_b200/Makefile" "$dst/"
-ln -s "$root/include" "$root/build_variants/include" 2>/dev/null || true
+[ -e "$root/build_variants/include" ] || ln -s "$root/include" "$root/build_variants/include"
 make -C "$dst" -j8 NVFLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false -Xcompiler -fPIC $*" >/dev/null
 echo "$dst/liblevelrank_b200.so"
