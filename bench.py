@@ -104,7 +104,7 @@ def workload_name(cfg, shrink):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_sample(g, lr, eng, budget_s=20.0, threads=None, reps=1):
+def cpu_sample(g, lr, eng, budget_s=20.0, threads=None, reps=1, extra_methods=False):
     """Bounded CPU baseline.  Uses the reference compiled from its own sources
     (oracle/_ref) when present, else the plain-C port (oracle/).  Sample: the
     reference level loop (engine.cpp:126-158) over its own schedule with the
@@ -142,6 +142,8 @@ def cpu_sample(g, lr, eng, budget_s=20.0, threads=None, reps=1):
             out.append({"value": work / (ms / 1e3) / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
                         "sample": sample, "edge_updates": int(work), "ms": ms})
         rg.free_prep(prep)
+        if large_tol <= TOL and extra_methods:
+            out[-1]["reference_methods"] = reference_methods(rg, w, threads)
         return out if reps > 1 else out[0]
     o = Oracle()
     go = o.graph_from_csr(n, off, tgt)
@@ -149,6 +151,38 @@ def cpu_sample(g, lr, eng, budget_s=20.0, threads=None, reps=1):
     return {"value": eu / (ms / 1e3) / 1e9 if ms > 0 else None, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": "oracle port: 4 multiplies of the largest SccLarge unit (push COO)", "edge_updates": int(eu),
             "ms": ms}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_methods(rg, w, threads):
+    """SURVEY 8(d) CPU side: the reference's compute_pagerank Sequential and
+    Parallel (its own wall_ms: partition + schedule + solve) and its
+    whole-graph power-iteration baseline, on the same graph and weights."""
+    res = {"threads": threads, "cpu_model": cpu_model()}
+    t0 = time.perf_counter()
+    seq = rg.compute_pagerank(w, C_DAMP, TOL, 100, parallel=False)
+    res["sequential_ms"] = (time.perf_counter() - t0) * 1e3
+    res["sequential_reference_wall_ms"] = seq.report["wall_ms"]
+    t0 = time.perf_counter()
+    par = rg.compute_pagerank(w, C_DAMP, TOL, 100, parallel=True, threads=threads)
+    res["parallel_ms"] = (time.perf_counter() - t0) * 1e3
+    res["parallel_reference_wall_ms"] = par.report["wall_ms"]
+    t0 = time.perf_counter()
+    rg.compute_baseline(w, C_DAMP, TOL)
+    res["whole_graph_baseline_ms"] = (time.perf_counter() - t0) * 1e3
+    res["note"] = ("wall times include the reference's partition + schedule; the headline cpu_baseline value is its "
+                   "level loop only")
+    return res
 
 
 def run_reference(args):
@@ -290,6 +324,7 @@ def run_ours(args):
             traffic = json.load(f).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "frac_vs_nominal_8000": (achieved / 8000.0) if achieved else None,
                 "kernel": "k_grid_iter (SccLarge power-series SpMV)", "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": (inf["spmv_bytes"] / inf["spmv_active_launches"])
                 if inf["spmv_active_launches"] else None,
@@ -300,7 +335,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_sample(g, lr, eng, budget_s=args.ref_budget)
+            cpu = cpu_sample(g, lr, eng, budget_s=args.ref_budget, extra_methods=True)
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
 
