@@ -533,6 +533,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
       if (b <= kLevelStageBytes) mid_need = std::max(mid_need, b);
     }
     T.smem = std::max({T.smem, T.sm_tile, warp_need, mid_need});
+    if (!rowranges[static_cast<size_t>(li)].empty()) T.smem = std::max(T.smem, kRowTaskSmem);  // tiled row gathers
     for (int i = T.lc0; i < T.lc1; ++i) {  // CTA power series staged in shared memory where it fits
       const SccTask& lt = lcta[static_cast<size_t>(i)];
       const size_t b = lcta_stage_bytes(T.lc_max, L->iptr[lt.row_end] - L->iptr[lt.row_begin]);
@@ -640,6 +641,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   LR_CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
   // LR_LEVEL_PROF=1: per-level timing of k_level's CTAs by task type (diagnostic, synchronises every level)
   const bool prof_on = std::getenv("LR_LEVEL_PROF") != nullptr;
+  const bool prof_detail = prof_on && std::atoi(std::getenv("LR_LEVEL_PROF")) > 1;
   DevBuf<long long> prof_buf;
   double prof_max[5] = {0, 0, 0, 0, 0}, prof_crit[5] = {0, 0, 0, 0, 0}, prof_span = 0;
   long long prof_cnt[5] = {0, 0, 0, 0, 0};
@@ -679,6 +681,9 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           prof_cnt[ty] += 1;
         }
         prof_span += (hi - lo) * 1e-3;
+        if (prof_detail)
+          std::fprintf(stderr, "[LR_LEVEL_PROF] level ctas %d span %.1f us  max rows %.1f cacw %.1f cacb %.1f small %.1f lcta %.1f\n",
+                       nt, (hi - lo) * 1e-3, mx[0], mx[1], mx[2], mx[3], mx[4]);
         int arg = 0;
         for (int ty = 0; ty < 5; ++ty) {
           prof_max[ty] += mx[ty];

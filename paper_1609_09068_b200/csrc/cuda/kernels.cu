@@ -83,8 +83,9 @@ __device__ __forceinline__ void cross_finish(const DeviceLayout& L, int row, dou
   if (k == kLargeGrid) s0[row] = pf[row] * acc;
 }
 
-// Pull rows with many in-edges (R-MAT hubs): one warp per kCrossSeg-edge
-// slice; slices of one row combine in slice order in the last one to finish.
+// Pull rows with more than kCrossLight in-edges: one warp per kCrossSeg-edge
+// slice (every gather of a slice in flight together); slices of one row
+// combine in slice order in the last one to finish.
 // kCac = false: cross in-edges of K1 (base = w, finish = cross_finish);
 // kCac = true : intra in-edges of a large-CAC depth slice (base = rank).
 // Same terms as the one-thread paths, tree-summed.
@@ -99,11 +100,22 @@ __global__ void k_pull_heavy(DeviceLayout L, const CrossTask* __restrict__ tasks
   const CrossTask x = tasks[t];
   const double c = p->c;
   const int* src = kCac ? L.isrc : L.xsrc;
-  double sum = 0.0;
-  for (int i = lane; i < x.cnt; i += 32) {
-    const int s = __ldg(src + x.e_begin + i);
-    sum += c * rank[s] / static_cast<double>(__ldg(L.deg + s));
+  // kCrossSeg = 8 x 32 edges: indices, then all gathers, then the terms
+  constexpr int kPer = kCrossSeg / 32;
+  int s[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) s[k] = lane + 32 * k < x.cnt ? __ldg(src + x.e_begin + lane + 32 * k) : -1;
+  double rv[kPer];
+  int dv[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    rv[k] = s[k] >= 0 ? rank[s[k]] : 0.0;
+    dv[k] = s[k] >= 0 ? __ldg(L.deg + s[k]) : 1;
   }
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+    if (s[k] >= 0) sum += c * rv[k] / static_cast<double>(dv[k]);
   sum = dev::warp_sum(sum);
   if (lane != 0) return;
   double y = sum;

@@ -102,8 +102,10 @@ struct CrossTask {
 };
 
 constexpr int kCrossLight = 32;    // rows up to this many in-edges: one thread, reference order
-constexpr int kCrossSplit = 4096;  // cross rows above this: split over warps by k_pull_heavy
-constexpr int kCrossSeg = 2048;    // cross in-edges per warp task of a split row
+constexpr int kCrossSplit = 32;    // cross rows above this: split over warps by k_pull_heavy
+constexpr int kCrossSeg = 256;     // in-edges per warp task of a split row (8 per lane, all in flight)
+constexpr int kTileNnzCross = 256; // cross in-edges per chunk of a row task (level.cu cross_rows_tiled)
+constexpr size_t kRowTaskSmem = 8 * kTileNnzCross * sizeof(double);  // k_level smem a row task needs
 
 // One CTA of the fused per-level kernel (level.cu).
 enum LevelTaskType : int { kTaskRows = 0, kTaskCacWarps = 1, kTaskCacBlock = 2, kTaskSmall = 3, kTaskLcta = 4 };

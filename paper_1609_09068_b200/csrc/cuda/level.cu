@@ -89,6 +89,67 @@ __device__ void cross_rows(const DeviceLayout& L, int r0, int r1, const double* 
   }
 }
 
+// Row tasks, one warp per 32 consecutive rows, edge-parallel: the warp walks
+// its rows' cross in-edges in chunks of 256 (coalesced index loads, all the
+// rank/deg gathers of a chunk in flight together), each lane computes its
+// edges' terms (c * r_src) / deg_src into a warp-private stage, and the lane
+// owning a row adds that row's terms in order, carrying its sum across
+// chunks -- the reference's order, bit-exact, for every row.  Rows above
+// kCrossSplit (= kCrossLight) are done by k_pull_heavy; a warp whose rows carry
+// more than kTiledCrossMax edges takes the per-row path.
+constexpr int kTiledCrossMax = 2048;
+
+__device__ void cross_rows_tiled(const DeviceLayout& L, int r0, int r1, const double* __restrict__ w, double c,
+                                 const double* __restrict__ pf, double* rank, double* s0, double* stage) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rb = r0 + 32 * warp;
+  if (rb >= r1) return;
+  const int re = min(rb + 32, r1);
+  const int row = rb + lane;
+  const bool mine = row < re;
+  long long lo = 0, hi = 0;
+  if (mine) {
+    lo = L.xptr[row];
+    hi = L.xptr[row + 1];
+  }
+  const long long base = __shfl_sync(0xffffffffu, lo, 0);
+  const long long end = L.xptr[re];
+  if (end - base > kTiledCrossMax) {
+    cross_rows(L, rb, re, w, c, pf, rank, s0, lane, 32);
+    return;
+  }
+  const bool light = mine && hi - lo <= kCrossLight;  // heavier rows: k_pull_heavy
+  double acc = light ? w[L.vertex_of[row]] : 0.0;
+  for (long long cb = base; cb < end; cb += kTileNnzCross) {
+    const int n = static_cast<int>(min(static_cast<long long>(kTileNnzCross), end - cb));
+    int src[kTileNnzCross / 32];
+#pragma unroll
+    for (int k = 0; k < kTileNnzCross / 32; ++k) {
+      const int e = lane + 32 * k;
+      src[k] = e < n ? __ldg(L.xsrc + cb + e) : 0;
+    }
+    double rv[kTileNnzCross / 32];
+    int dv[kTileNnzCross / 32];
+#pragma unroll
+    for (int k = 0; k < kTileNnzCross / 32; ++k) {
+      rv[k] = rank[src[k]];
+      dv[k] = __ldg(L.deg + src[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kTileNnzCross / 32; ++k) {
+      const int e = lane + 32 * k;
+      if (e < n) stage[e] = c * rv[k] / static_cast<double>(dv[k]);
+    }
+    __syncwarp();
+    if (light) {
+      const int a = static_cast<int>(max(lo, cb) - cb), b = static_cast<int>(min(hi, cb + n) - cb);
+      for (int e = a; e < b; ++e) acc += stage[e];
+    }
+    __syncwarp();
+  }
+  if (light) row_finish(L, row, acc, c, pf, rank, s0);
+}
+
 // ------------------------------------------------------------------ K3
 // One depth-slice row of a CAC: parents in Kahn order, then the kept-loop
 // factor (solvers.cpp:61-83).
@@ -718,7 +779,10 @@ __global__ void __launch_bounds__(kThreads)
   const long long t_start = prof ? global_ns() : 0;
   switch (t.type) {
     case kTaskRows:
-      cross_rows(L, t.a, t.b, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      if (smem_bytes >= kRowTaskSmem)
+        cross_rows_tiled(L, t.a, t.b, w, c, pf, rank, s0, sm + (threadIdx.x >> 5) * kTileNnzCross);
+      else
+        cross_rows(L, t.a, t.b, w, c, pf, rank, s0, threadIdx.x, kThreads);
       break;
     case kTaskCacWarps: {
       const int ci = t.a + static_cast<int>(threadIdx.x >> 5);
