@@ -748,10 +748,20 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
             ++launches;
           }
         }
-        LR_CUDA_TRY(cudaMemcpyAsync(&ctx->h_status->active, &ctx->status.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LR_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         LR_CUDA_TRY(cudaStreamSynchronize(s));
         if (ctx->h_status->active <= 0 || k > cap + 2) break;
-        batch = std::min(16, batch * 2);
+        // Next batch: the increments shrink geometrically, so the remaining
+        // iterations follow from the last two maxima; enqueue them all (plus
+        // one) so the level usually needs a single further poll.  Launches
+        // past convergence exit at once.
+        const double lm = ctx->h_status->last_max, pm = ctx->h_status->prev_max, tol = ctx->h_params->tol;
+        int next = std::min(16, batch * 2);
+        if (lm > 0.0 && pm > lm && lm >= tol) {
+          const double rem = std::ceil(std::log(tol / lm) / std::log(lm / pm));
+          if (rem >= 0.0 && rem < 4096.0) next = std::max(1, std::min(static_cast<int>(rem) + 1, 512));
+        }
+        batch = next;
       }
       LR_CUDA_TRY(cudaEventRecord(ctx->ev[3], s));
       LR_CUDA_TRY(cudaEventSynchronize(ctx->ev[3]));

@@ -30,6 +30,8 @@ struct DevStatus {
   long long iterative_edge_work;
   int active;              // grid SccLarge units still iterating on the current level
   int ctas_done;           // CTAs finished with the running grid SpMV launch
+  double last_max;         // largest max|inc| over the level's running units, latest closed iteration
+  double prev_max;         // the same one iteration earlier (host predicts the remaining iterations)
 };
 
 // One SccLarge grid unit's iteration state.

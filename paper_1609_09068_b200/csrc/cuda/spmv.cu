@@ -110,6 +110,8 @@ __global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
   if (i == 0) {
     st->active = ngu;
     st->ctas_done = 0;
+    st->last_max = 0.0;
+    st->prev_max = 0.0;
   }
 }
 
@@ -119,10 +121,12 @@ __global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
 // launch's own max.
 __device__ void finish_iteration(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
                                  DevStatus* st, const double* maxbuf = nullptr) {
+  double level_max = 0.0;
   for (int i = gu0; i < gu0 + ngu; ++i) {
     GridUnitState* u = gs + i;
     if (u->done) continue;
     const double mx = maxbuf ? maxbuf[i] : bitsd(atomicAdd(&u->max_bits, 0ull));
+    level_max = fmax(level_max, mx);
     const int it = u->iterations + 1;
     u->iterations = it;
     u->max_bits = 0ull;
@@ -142,6 +146,8 @@ __device__ void finish_iteration(GridUnitState* gs, int gu0, int ngu, const Solv
       atomicSub(&st->active, 1);
     }
   }
+  st->prev_max = st->last_max;
+  st->last_max = level_max;
   st->ctas_done = 0;
 }
 
