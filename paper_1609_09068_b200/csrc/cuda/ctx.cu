@@ -725,17 +725,19 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           ++k;
           const double* sin = (k & 1) ? ctx->s0.p : ctx->s1.p;
           double* sout = (k & 1) ? ctx->s1.p : ctx->s0.p;
-          while (ctx->lev.size() < static_cast<size_t>(2 * k)) {
+          // one event per launch (lev[k] after launch k, lev[0] before the
+          // first): the active launches' time is lev[0] -> lev[last active]
+          while (ctx->lev.size() < static_cast<size_t>(k + 1)) {
             cudaEvent_t e;
             LR_CUDA_TRY(cudaEventCreate(&e));
             ctx->lev.push_back(e);
           }
-          LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 2)], s));
+          if (k == 1) LR_CUDA_TRY(cudaEventRecord(ctx->lev[0], s));
           const bool sharded = ctx->comm != nullptr;
           launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
                            ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, sharded ? ctx->maxbuf.p : nullptr, s);
-          LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(2 * k - 1)], s));
+          LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(k)], s));
           ++launches;
           ++spmv_launches;
           if (sharded) {
@@ -779,9 +781,9 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
         spmv_bytes += it * (12 * ctx->gu_nnz[static_cast<size_t>(T.gu0 + i)] + 32 * ctx->gu_rows[static_cast<size_t>(T.gu0 + i)]);
         spmv_edges += it * ctx->gu_nnz[static_cast<size_t>(T.gu0 + i)];
       }
-      for (long long j = 0; j < std::min(kmax, k); ++j) {
+      if (std::min(kmax, k) > 0) {
         float lm = 0.f;
-        cudaEventElapsedTime(&lm, ctx->lev[static_cast<size_t>(2 * j)], ctx->lev[static_cast<size_t>(2 * j + 1)]);
+        cudaEventElapsedTime(&lm, ctx->lev[0], ctx->lev[static_cast<size_t>(std::min(kmax, k))]);
         active_ms += lm;
       }
       active_launches += std::min(kmax, k);
