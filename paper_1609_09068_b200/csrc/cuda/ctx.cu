@@ -57,6 +57,13 @@ struct DevBuf {
     if (e != cudaSuccess || count == 0) return e;
     return cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s);
   }
+  cudaError_t upload_padded(const T* src, size_t count, size_t pad, cudaStream_t s) {
+    cudaError_t e = alloc(count + pad);
+    n = count;
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(p + count, 0, pad * sizeof(T), s)) != cudaSuccess || count == 0) return e;
+    return cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s);
+  }
   size_t bytes() const { return n * sizeof(T); }
 };
 
@@ -80,6 +87,7 @@ struct LevelTasks {
   // [hot_begin, hot_begin + hot_rows) evict-last, the rest of the unit evict-first
   int hot_begin = 0;
   long long hot_rows = 0, unit_rows = 0;
+  int keep_stream = 0;  // L2 priority of the streamed SpMV operands (spmv.cu policy_stream)
 };
 
 // One depth slice of a large CAC: rows [r0, r1), heavy-row tasks [h0, h1).
@@ -417,20 +425,29 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           ctx->gu_bounds.push_back(shard_bounds(L->iptr, rb, re, ctx->nshards));
           const int own0 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard)];
           const int own1 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard) + 1];
+          // K4c chunks hold <= kChunkNnz in-edges and never put an empty row
+          // inside a multi-row tile (its row-start flag would collide)
+          const int tile_nnz = spmv_seg() ? kChunkNnz : kTileNnz;
+          const int seg_nnz = spmv_seg() ? kChunkSegNnz : kSegNnz;
           int r = own0;
           while (r < own1) {
             const long long len = L->iptr[r + 1] - L->iptr[r];
-            if (len > kTileNnz) {
-              if (len <= kSegNnz) {
+            if (len == 0 && spmv_seg()) {
+              blocks.push_back(SpmvBlock{L->iptr[r], 0, r, r + 1, gu, -1, 0});
+              ++r;
+              continue;
+            }
+            if (len > tile_nnz) {
+              if (len <= seg_nnz) {
                 blocks.push_back(SpmvBlock{L->iptr[r], static_cast<int>(len), r, r + 1, gu, -1, 0});
               } else {
-                const int nseg = static_cast<int>((len + kSegNnz - 1) / kSegNnz);
+                const int nseg = static_cast<int>((len + seg_nnz - 1) / seg_nnz);
                 const int hid = static_cast<int>(heavy.size());
                 heavy.push_back(HeavyRow{r, nseg, heavy_parts});
                 heavy_parts += nseg;
                 for (int sg = 0; sg < nseg; ++sg) {
-                  const long long nb = L->iptr[r] + static_cast<long long>(sg) * kSegNnz;
-                  const int cnt = static_cast<int>(std::min<long long>(kSegNnz, L->iptr[r + 1] - nb));
+                  const long long nb = L->iptr[r] + static_cast<long long>(sg) * seg_nnz;
+                  const int cnt = static_cast<int>(std::min<long long>(seg_nnz, L->iptr[r + 1] - nb));
                   blocks.push_back(SpmvBlock{nb, cnt, r, r + 1, gu, hid, sg});
                 }
               }
@@ -441,7 +458,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             long long acc = 0;
             while (r < own1 && r - start < kTileRows) {
               const long long l2 = L->iptr[r + 1] - L->iptr[r];
-              if (l2 > kTileNnz || acc + l2 > kTileNnz) break;
+              if (l2 > tile_nnz || acc + l2 > tile_nnz || (l2 == 0 && spmv_seg())) break;
               acc += l2;
               ++r;
             }
@@ -492,6 +509,16 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         T.unit_rows = L->unit_row_begin[u + 1] - L->unit_row_begin[u];
         T.hot_rows = std::min<long long>(T.unit_rows, static_cast<long long>(frac * l2 / 16.0));
       }
+      // The whole level's SpMV working set -- in-edge indices and row offsets,
+      // rank, pf and both pushed vectors -- stays L2-resident across iterations
+      // when it fits in a fraction of L2 (config 2: 82 MB); streamed operands
+      // are then kept (evict-last) instead of streamed through (evict-first).
+      double ws = 0.0;
+      for (int gi = T.gu0; gi < T.gu1; ++gi)
+        ws += 4.0 * static_cast<double>(ctx->gu_nnz[static_cast<size_t>(gi)]) +
+              40.0 * static_cast<double>(ctx->gu_rows[static_cast<size_t>(gi)]);
+      T.keep_stream = ws <= 0.75 * l2 ? 2 : 0;
+      if (const char* e = std::getenv("LR_SPMV_KEEP")) T.keep_stream = std::atoi(e);
     }
   }
   // warp tasks first, then CTA tasks, in one array
@@ -554,7 +581,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->xptr.upload(reinterpret_cast<const long long*>(L->xptr), nn + 1, s));
   LR_CUDA_TRY(ctx->xsrc.upload(L->xsrc, static_cast<size_t>(L->nnz_cross), s));
   LR_CUDA_TRY(ctx->iptr.upload(reinterpret_cast<const long long*>(L->iptr), nn + 1, s));
-  LR_CUDA_TRY(ctx->isrc.upload(L->isrc, static_cast<size_t>(L->nnz_intra), s));
+  // padded: K4c's aligned 256-slot index windows may reach past the last in-edge
+  LR_CUDA_TRY(ctx->isrc.upload_padded(L->isrc, static_cast<size_t>(L->nnz_intra), kIdxPad, s));
   LR_CUDA_TRY(ctx->depth_ptr.upload(L->depth_ptr, static_cast<size_t>(L->depth_ptr_len), s));
   LR_CUDA_TRY(ctx->cac.upload(cac_w.data(), cac_w.size(), s));
   LR_CUDA_TRY(ctx->small.upload(small.data(), small.size(), s));
@@ -736,7 +764,8 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           const bool sharded = ctx->comm != nullptr;
           launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
-                           ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, sharded ? ctx->maxbuf.p : nullptr, s);
+                           ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, T.keep_stream,
+                           sharded ? ctx->maxbuf.p : nullptr, s);
           LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(k)], s));
           ++launches;
           ++spmv_launches;

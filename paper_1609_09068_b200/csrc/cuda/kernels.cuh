@@ -122,6 +122,13 @@ constexpr int kSpmvThreads = 1024;  // one persistent CTA per SM: 32 warps + a s
 constexpr int kTileNnz = 256;      // in-edges of one warp tile
 constexpr int kTileRows = 64;      // max rows of one warp tile
 constexpr int kSegNnz = 1024;      // rows above this are split into segments
+// k_spmv_seg (spmv.cu): a chunk of <= kChunkNnz in-edges always lies inside the
+// 32-byte aligned 256-slot window that starts at or below it, so one 256-bit
+// index load per lane covers it; heavy-row segments are four chunks.
+constexpr int kChunkNnz = 248;
+constexpr int kChunkSegNnz = 4 * kChunkNnz;
+constexpr int kIdxPad = 256;       // isrc is allocated this many entries past its end
+constexpr int kMaxSharedUnits = 256;  // grid units whose done flags k_spmv_seg keeps in shared memory
 constexpr int kCtaLargeMaxRows = 4096;
 constexpr long long kCtaLargeMaxNnz = 1 << 16;
 constexpr int kMaxDynSmem = 227 * 1024;
@@ -182,11 +189,12 @@ void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int m
                   double* rank, double* scratch, DevStatus* st, cudaStream_t s);
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s);
 int grid_iter_ctas();
+bool spmv_seg();  // K4c segmented-scan SpMV (default) or K4b staged tiles (LR_SPMV=tile)
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
-                      DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, double* maxbuf,
-                      cudaStream_t s);
+                      DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, int keep_stream,
+                      double* maxbuf, cudaStream_t s);
 // multi-GPU: close an iteration from the all-reduced shard maxima in maxbuf
 void launch_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
                         DevStatus* st, const double* maxbuf, cudaStream_t s);

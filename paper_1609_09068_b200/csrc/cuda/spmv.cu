@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 
 #include "devutil.cuh"
 #include "kernels.cuh"
@@ -40,11 +41,20 @@ using namespace dev;
 constexpr int kWarps = kSpmvThreads / 32;
 constexpr int kPerLane = kTileNnz / 32;
 constexpr int kLongRow = 32;
-constexpr int kHeadRows = 8192;  // shared-memory head entries (see launch_grid_iter)
+constexpr int kHeadRows = 8192;  // shared-memory head entries of K4b (see launch_grid_iter)
+constexpr int kHeadRowsSeg = 16384;  // ... of K4c
 
-__device__ __forceinline__ std::uint64_t policy_evict_first() {
+// L2 priority of the streamed operands (indices, row offsets, rank, pf):
+// evict-first when they cannot stay resident across iterations, evict-last when
+// the whole level's working set fits in L2 (then nothing is re-read from HBM)
+__device__ __forceinline__ std::uint64_t policy_stream(int keep) {
   std::uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  if (keep == 2)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (keep == 1)
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 // evict-last for the hot head [base, base + primary) of a pushed vector,
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
                 const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, double* maxbuf) {
+                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, int keep_stream, double* maxbuf) {
   extern __shared__ double dyn[];  // [kWarps][kTileNnz] staging, then the head
   double* head = dyn + kWarps * kTileNnz;
   __shared__ int wunit[kWarps];
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
   __shared__ int last_cta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* v = dyn + warp * kTileNnz;
-  const std::uint64_t stream = policy_evict_first();
+  const std::uint64_t stream = policy_stream(keep_stream);
   const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
   const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
   int cur_unit = -1;
@@ -358,6 +368,299 @@ __global__ void __launch_bounds__(kSpmvThreads)
   }
 }
 
+// K4c: the same iteration with every lane owning 8 CONSECUTIVE in-edges of a
+// chunk (one 256-bit index load), rows reduced by a segmented warp scan instead
+// of a shared-memory staging buffer -- fewer instructions per edge, no serial
+// per-lane row loops, and the shared memory the staging took goes to the head.
+//   chunk  in-edges [cb, cb + n), n <= kChunkNnz, inside the aligned window
+//          [A, A + 256), A = cb & ~7: lane l owns slots 8l .. 8l + 7
+//   tile   rows [row_begin, row_end) whole (one chunk); row r starts at slot
+//          iptr[r] - A.  Row-start flags (8 bitmap words per warp in shared
+//          memory) give each lane its rows; a lane sums its own complete rows,
+//          rows crossing lanes are combined by an inclusive segmented scan.
+//   long row / heavy-row segment: one row, up to four chunks, warp sum.
+// Summation order differs from the reference's sequential push (rows agree to
+// ~1e-16 relative; the stop test and iteration counts are unaffected).
+__device__ __forceinline__ void ld_idx8(const int* p, std::uint64_t pol, int* o) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ SpmvBlock ld_task(const SpmvBlock* t) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(t));
+  const int4 b = __ldg(reinterpret_cast<const int4*>(t) + 1);
+  SpmvBlock r;
+  r.nnz_begin = static_cast<long long>(static_cast<unsigned>(a.x)) | (static_cast<long long>(a.y) << 32);
+  r.nnz = a.z;
+  r.row_begin = a.w;
+  r.row_end = b.x;
+  r.gunit = b.y;
+  r.heavy = b.z;
+  r.seg = b.w;
+  return r;
+}
+
+__device__ __forceinline__ SpmvBlock from_lanes(int v) {
+  SpmvBlock r;
+  const unsigned lo = static_cast<unsigned>(__shfl_sync(0xffffffffu, v, 0));
+  const int hi = __shfl_sync(0xffffffffu, v, 1);
+  r.nnz_begin = static_cast<long long>(lo) | (static_cast<long long>(hi) << 32);
+  r.nnz = __shfl_sync(0xffffffffu, v, 2);
+  r.row_begin = __shfl_sync(0xffffffffu, v, 3);
+  r.row_end = __shfl_sync(0xffffffffu, v, 4);
+  r.gunit = __shfl_sync(0xffffffffu, v, 5);
+  r.heavy = __shfl_sync(0xffffffffu, v, 6);
+  r.seg = __shfl_sync(0xffffffffu, v, 7);
+  return r;
+}
+
+__global__ void __launch_bounds__(kSpmvThreads, 1)
+    k_spmv_seg(DeviceLayout L, const SpmvBlock* __restrict__ tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
+               const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
+               const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
+               const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
+               int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, int keep_stream, double* maxbuf) {
+  extern __shared__ double dyn[];  // [kWarps][kTileRows] row totals, then the head
+  double* head = dyn + kWarps * kTileRows;
+  __shared__ unsigned flags[kWarps][8];
+  __shared__ int wunit[kWarps];
+  __shared__ double wmax[kWarps];
+  __shared__ unsigned char sdone[kMaxSharedUnits];
+  __shared__ int last_cta;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ysh = dyn + warp * kTileRows;
+  unsigned* fw = flags[warp];
+  const std::uint64_t stream = policy_stream(keep_stream);
+  const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
+  const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
+  for (int i = threadIdx.x; i < nhead; i += kSpmvThreads) head[i] = ld_keep(s_in + hot_begin + i, keep);
+  for (int i = threadIdx.x; i < ngu && i < kMaxSharedUnits; i += kSpmvThreads) sdone[i] = gs[gu0 + i].done ? 1 : 0;
+  const unsigned head_sh = static_cast<unsigned>(__cvta_generic_to_shared(head));
+  __syncthreads();
+  auto unit_done = [&](int gu) {
+    const int i = gu - gu0;
+    return i < kMaxSharedUnits ? sdone[i] != 0 : gs[gu].done != 0;
+  };
+  const int stride = gridDim.x * kWarps;
+  // first task at or after tt whose unit still iterates
+  auto seek = [&](int& tt, SpmvBlock& bb) {
+    while (tt < ntasks) {
+      bb = ld_task(tasks + tt);
+      if (!unit_done(bb.gunit)) return;
+      tt += stride;
+    }
+  };
+  auto load_idx = [&](const SpmvBlock& bb, int cc, int* out) {
+    const long long cb = bb.nnz_begin + static_cast<long long>(cc) * kChunkNnz;
+    ld_idx8(L.isrc + (cb & ~7ll) + 8 * lane, stream, out);
+  };
+  int cur_unit = -1;
+  double lmax = 0.0;
+  int t = blockIdx.x * kWarps + warp, c = 0;
+  SpmvBlock b{};
+  seek(t, b);
+  // the descriptor of the task after b, loaded one task ahead (its unit's done
+  // flag is checked when the warp gets there)
+  int tq = t + stride;
+  int bq = 0;  // lane i < 8 holds int i of the descriptor
+  if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
+  int idx[8];
+  if (t < ntasks) load_idx(b, 0, idx);
+  double part = 0.0;  // running sum of a multi-chunk task
+  while (t < ntasks) {
+    if (b.gunit != cur_unit) {
+      if (cur_unit >= 0) {
+        const double m = warp_max(lmax);
+        if (lane == 0 && m > 0.0) atomicMax(&gs[cur_unit].max_bits, dbits(m));
+      }
+      cur_unit = b.gunit;
+      lmax = 0.0;
+    }
+    const long long cb = b.nnz_begin + static_cast<long long>(c) * kChunkNnz;
+    const int q0 = static_cast<int>(cb & 7ll);
+    const int left = b.nnz - c * kChunkNnz;
+    const int q1 = q0 + (left < kChunkNnz ? left : kChunkNnz);
+    const bool tile = b.heavy < 0 && b.nnz <= kChunkNnz;
+    // 1. this chunk's gathers (slots outside [q0, q1) read nothing and add 0)
+    double g[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int slot = 8 * lane + k;
+      const unsigned off = static_cast<unsigned>(idx[k] - hot_begin);
+      const unsigned valid = slot >= q0 && slot < q1;
+      const unsigned in = valid & (off < static_cast<unsigned>(nhead));
+      const unsigned glob = valid & !in;
+      double a = 0.0, v = 0.0;
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
+                   : "+d"(a)
+                   : "r"(head_sh + (in ? off : 0u) * 8u), "r"(in));
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, "
+          "[%1], %3;\n\t}"
+          : "+d"(v)
+          : "l"(s_in + (glob ? idx[k] : hot_begin)), "r"(glob), "l"(keep));
+      g[k] = in ? a : v;
+    }
+    // 2. the tile's row starts and epilogue operands, in flight with the gathers
+    const int nr = tile ? b.row_end - b.row_begin : 0;
+    int st0 = -1, st1 = -1;
+    double rk0 = 0.0, rk1 = 0.0, pf0 = 0.0, pf1 = 0.0;
+    if (tile) {
+      const long long A = cb & ~7ll;
+      if (lane < nr) {
+        st0 = static_cast<int>(ld_stream(L.iptr + b.row_begin + lane, stream) - A);
+        rk0 = ld_stream(rank + b.row_begin + lane, stream);
+        pf0 = ld_stream(pf + b.row_begin + lane, stream);
+      }
+      if (lane + 32 < nr) {
+        st1 = static_cast<int>(ld_stream(L.iptr + b.row_begin + lane + 32, stream) - A);
+        rk1 = ld_stream(rank + b.row_begin + lane + 32, stream);
+        pf1 = ld_stream(pf + b.row_begin + lane + 32, stream);
+      }
+    }
+    // 3. the next chunk's indices (and the descriptor one task further on)
+    int tn = t, cn = c + 1;
+    SpmvBlock bn = b;
+    if (cn * kChunkNnz >= b.nnz) {
+      tn = tq;
+      cn = 0;
+      bn = from_lanes(bq);
+      if (tn < ntasks && unit_done(bn.gunit)) {
+        tn += stride;
+        seek(tn, bn);
+      }
+    }
+    int idx_n[8];
+    if (tn < ntasks) load_idx(bn, cn, idx_n);
+    if (tn != t) {
+      tq = tn + stride;
+      if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
+    }
+    // 4. consume this chunk
+    if (tile) {
+      if (lane < 8) fw[lane] = 0u;
+      __syncwarp();
+      if (st0 >= 0) atomicOr(fw + (st0 >> 5), 1u << (st0 & 31));
+      if (st1 >= 0) atomicOr(fw + (st1 >> 5), 1u << (st1 & 31));
+      __syncwarp();
+      const unsigned mine = (fw[lane >> 2] >> (8u * static_cast<unsigned>(lane & 3))) & 0xffu;  // my 8 slots
+      int before = __popc(mine);  // rows starting before my first slot: exclusive scan of the counts
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, before, d);
+        if (lane >= d) before += u;
+      }
+      before -= __popc(mine);
+      // my complete rows go straight to ysh; `pre` continues a row begun in an
+      // earlier lane, `run` ends as the part of a row continued by later lanes
+      double pre = 0.0, run = 0.0;
+      int o = before - 1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if ((mine >> k) & 1u) {
+          if (o >= before) ysh[o] = run;
+          else pre = run;
+          ++o;
+          run = 0.0;
+        }
+        run += g[k];
+      }
+      const bool seen = mine != 0u;
+      double v = run;  // segment value: the row part after my last flag, or my whole sum
+      bool f = seen;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double vu = __shfl_up_sync(0xffffffffu, v, d);
+        const bool fu = __shfl_up_sync(0xffffffffu, static_cast<int>(f), d) != 0;
+        if (lane >= d) {
+          if (!f) v += vu;
+          f = f || fu;
+        }
+      }
+      const double prev = __shfl_up_sync(0xffffffffu, v, 1);
+      if (seen && before > 0) ysh[before - 1] = (lane > 0 ? prev : 0.0) + pre;
+      if (q1 > q0 && lane == ((q1 - 1) >> 3)) ysh[nr - 1] = v;
+      if (q1 == q0 && lane == 0) ysh[0] = 0.0;
+      __syncwarp();
+      if (lane < nr) {
+        const double y = ysh[lane];
+        rank[b.row_begin + lane] = rk0 + y;
+        st_keep(s_out + b.row_begin + lane, pf0 * y, keep_out);
+        lmax = fmax(lmax, y);
+      }
+      if (lane + 32 < nr) {
+        const double y = ysh[lane + 32];
+        rank[b.row_begin + lane + 32] = rk1 + y;
+        st_keep(s_out + b.row_begin + lane + 32, pf1 * y, keep_out);
+        lmax = fmax(lmax, y);
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) part += g[k];
+      if (left <= kChunkNnz) {  // last chunk of a long row or segment
+        const double sum = warp_sum(part);
+        part = 0.0;
+        int row = -1;
+        double y = sum;
+        if (b.heavy < 0) {
+          row = b.row_begin;
+        } else if (lane == 0) {
+          const HeavyRow h = heavy[b.heavy];
+          heavy_part[h.part_begin + b.seg] = sum;
+          __threadfence();
+          if (atomicAdd(heavy_cnt + b.heavy, 1) == h.nseg - 1) {
+            __threadfence();
+            y = 0.0;
+            for (int k = 0; k < h.nseg; ++k) y += __ldcg(heavy_part + h.part_begin + k);
+            heavy_cnt[b.heavy] = 0;
+            row = h.row;
+          }
+        }
+        if (lane == 0 && row >= 0) {
+          rank[row] += y;
+          st_keep(s_out + row, pf[row] * y, keep_out);
+          lmax = fmax(lmax, y);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) idx[k] = idx_n[k];
+    t = tn;
+    c = cn;
+    b = bn;
+  }
+  const double m = warp_max(lmax);
+  if (lane == 0) {
+    wunit[warp] = cur_unit;
+    wmax[warp] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kWarps; ++w) {
+      if (wunit[w] < 0 || !(wmax[w] > 0.0)) continue;
+      double mm = wmax[w];
+      while (w + 1 < kWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
+      atomicMax(&gs[wunit[w]].max_bits, dbits(mm));
+    }
+    __threadfence();
+    last_cta = atomicAdd(&st->ctas_done, 1) == static_cast<int>(gridDim.x) - 1;
+  }
+  __syncthreads();
+  if (last_cta && threadIdx.x == 0) {
+    __threadfence();
+    if (maxbuf) {
+      for (int i = gu0; i < gu0 + ngu; ++i) {
+        maxbuf[i] = bitsd(atomicAdd(&gs[i].max_bits, 0ull));
+        gs[i].max_bits = 0ull;
+      }
+      st->ctas_done = 0;
+    } else {
+      finish_iteration(gs, gu0, ngu, p, unit_iters, st);
+    }
+  }
+}
+
 __global__ void k_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
                               DevStatus* st, const double* maxbuf) {
   if (threadIdx.x == 0 && blockIdx.x == 0) finish_iteration(gs, gu0, ngu, p, unit_iters, st, maxbuf);
@@ -372,8 +675,17 @@ int blocks_for(long long n, int threads) { return static_cast<int>((n + threads 
 
 }  // namespace
 
-// Dynamic shared memory of k_grid_iter: at most as many head entries as fit
-// next to the staging buffers.
+// K4c (k_spmv_seg) unless LR_SPMV=tile selects the staged-tile kernel K4b.
+bool spmv_seg() {
+  static const bool seg = [] {
+    const char* e = std::getenv("LR_SPMV");
+    return !(e && std::string(e) == "tile");
+  }();
+  return seg;
+}
+
+// Dynamic shared memory: at most as many head entries as fit next to the
+// per-warp buffers (staging for K4b, row totals for K4c).
 static int head_capacity() {
   static int cap = -1;
   if (cap < 0) {
@@ -381,9 +693,18 @@ static int head_capacity() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes a{};
-    cudaFuncGetAttributes(&a, k_grid_iter);
-    cap = ((optin - static_cast<int>(a.sharedSizeBytes)) / 8 - kWarps * kTileNnz) / 32 * 32;
-    cudaFuncSetAttribute(k_grid_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + kWarps * kTileNnz) * 8);
+    const int per_warp = spmv_seg() ? kWarps * kTileRows : kWarps * kTileNnz;
+    if (spmv_seg()) {
+      cudaFuncGetAttributes(&a, k_spmv_seg);
+    } else {
+      cudaFuncGetAttributes(&a, k_grid_iter);
+    }
+    cap = ((optin - static_cast<int>(a.sharedSizeBytes)) / 8 - per_warp) / 32 * 32;
+    const int bytes = (cap + per_warp) * 8;
+    if (spmv_seg())
+      cudaFuncSetAttribute(k_spmv_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    else
+      cudaFuncSetAttribute(k_grid_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   }
   return cap;
 }
@@ -394,8 +715,12 @@ int grid_iter_ctas() {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads,
-                                                  static_cast<size_t>(head_capacity() + kWarps * kTileNnz) * 8);
+    const int per_warp = spmv_seg() ? kWarps * kTileRows : kWarps * kTileNnz;
+    const size_t bytes = static_cast<size_t>(head_capacity() + per_warp) * 8;
+    if (spmv_seg())
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_seg, kSpmvThreads, bytes);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads, bytes);
     ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
   return ctas;
@@ -408,7 +733,8 @@ void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s
 void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                      int hot_begin, long long hot_rows, long long unit_rows, double* maxbuf, cudaStream_t s) {
+                      int hot_begin, long long hot_rows, long long unit_rows, int keep_stream, double* maxbuf,
+                      cudaStream_t s) {
   if (ntasks == 0) {  // this rank owns no rows of the level's units: still publish a zero max
     if (maxbuf) launch_grid_zero_max(maxbuf, gu0, ngu, s);
     return;
@@ -416,16 +742,22 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks,
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
   const int want = blocks_for(ntasks, kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
-  // Head size: measured optimum 4-12k entries at configs 2 and 5.  Larger
-  // heads lose: the fill costs microseconds per launch, and the L1 left over
-  // holds the in-flight misses of the cold gathers (at 20k entries config 5
-  // runs 3x slower).  LR_SPMV_HEAD overrides (0 disables the head).
-  int want_head = kHeadRows;
+  // Head size: measured optimum 4-12k entries at configs 2 and 5 for K4b.
+  // Larger heads lose: the fill costs microseconds per launch, and the L1 left
+  // over holds the in-flight misses of the cold gathers.  LR_SPMV_HEAD
+  // overrides (0 disables the head).
+  int want_head = spmv_seg() ? kHeadRowsSeg : kHeadRows;
   if (const char* e = std::getenv("LR_SPMV_HEAD")) want_head = std::max(0, std::atoi(e));
   const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
-  k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
-      L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
-      hot_begin, hot_bytes, unit_bytes, nhead, maxbuf);
+  if (spmv_seg()) {
+    k_spmv_seg<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileRows) * 8, s>>>(
+        L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
+        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf);
+  } else {
+    k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
+        L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
+        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf);
+  }
 }
 
 void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s) {
