@@ -174,6 +174,7 @@ struct lr_ctx {
   DevBuf<LevelTask> ltasks;
   DevBuf<GridUnitState> gstate;
   DevBuf<SpmvBlock> blocks;
+  DevBuf<unsigned short> meta;  // k_spmv_seg lane metadata, 32 per task
   DevBuf<HeavyRow> heavy;
   DevBuf<double> heavy_part;
   DevBuf<int> heavy_cnt;
@@ -294,7 +295,7 @@ int64_t lr_ctx_device_bytes(const lr_ctx* c) {
   return static_cast<int64_t>(c->vertex_of.bytes() + c->row_of.bytes() + c->deg.bytes() + c->xsrc.bytes() +
                               c->isrc.bytes() + c->depth_ptr.bytes() + c->loop.bytes() + c->rowkind.bytes() +
                               c->xptr.bytes() + c->iptr.bytes() + c->cac.bytes() + c->small.bytes() +
-                              c->lcta.bytes() + c->gstate.bytes() + c->blocks.bytes() + c->heavy.bytes() +
+                              c->lcta.bytes() + c->gstate.bytes() + c->blocks.bytes() + c->meta.bytes() + c->heavy.bytes() +
                               c->heavy_part.bytes() + c->heavy_cnt.bytes() + c->small_scratch.bytes() +
                               c->w.bytes() + c->rank.bytes() + c->s0.bytes() + c->s1.bytes() + c->pf.bytes() +
                               c->r3.bytes() + c->r1.bytes() + c->partial.bytes() + c->unit_iters.bytes());
@@ -591,6 +592,28 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->lcta.upload(lcta.data(), lcta.size(), s));
   LR_CUDA_TRY(ctx->gstate.upload(gstate.data(), gstate.size(), s));
   LR_CUDA_TRY(ctx->blocks.upload(blocks.data(), blocks.size(), s));
+  // k_spmv_seg tiles: per lane of the aligned 256-slot window, the row-start
+  // flags of its 8 slots and the number of rows starting before them
+  std::vector<unsigned short> meta;
+  if (spmv_seg()) {
+    meta.assign(blocks.size() * 32, 0);
+    for (size_t t = 0; t < blocks.size(); ++t) {
+      const SpmvBlock& b = blocks[t];
+      if (b.heavy >= 0 || b.nnz > kChunkNnz) continue;
+      const long long A = b.nnz_begin & ~7ll;
+      unsigned char fl[32] = {};
+      for (int r = b.row_begin; r < b.row_end; ++r) {
+        const int slot = static_cast<int>(L->iptr[r] - A);
+        fl[slot >> 3] = static_cast<unsigned char>(fl[slot >> 3] | (1u << (slot & 7)));
+      }
+      int before = 0;
+      for (int l = 0; l < 32; ++l) {
+        meta[t * 32 + static_cast<size_t>(l)] = static_cast<unsigned short>(fl[l] | (before << 8));
+        before += __builtin_popcount(fl[l]);
+      }
+    }
+  }
+  LR_CUDA_TRY(ctx->meta.upload(meta.data(), meta.size(), s));
   LR_CUDA_TRY(ctx->heavy.upload(heavy.data(), heavy.size(), s));
   LR_CUDA_TRY(ctx->heavy_part.alloc(static_cast<size_t>(heavy_parts)));
   LR_CUDA_TRY(ctx->heavy_cnt.alloc(heavy.size()));
@@ -762,7 +785,8 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           }
           if (k == 1) LR_CUDA_TRY(cudaEventRecord(ctx->lev[0], s));
           const bool sharded = ctx->comm != nullptr;
-          launch_grid_iter(L, ctx->blocks.p + T.bk0, T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
+          launch_grid_iter(L, ctx->blocks.p + T.bk0, ctx->meta.p ? ctx->meta.p + static_cast<size_t>(T.bk0) * 32 : nullptr,
+                           T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,
                            ctx->status.p, T.hot_begin, T.hot_rows, T.unit_rows, T.keep_stream,
                            sharded ? ctx->maxbuf.p : nullptr, s);

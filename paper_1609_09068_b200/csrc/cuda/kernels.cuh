@@ -32,6 +32,8 @@ struct DevStatus {
   int ctas_done;           // CTAs finished with the running grid SpMV launch
   double last_max;         // largest max|inc| over the level's running units, latest closed iteration
   double prev_max;         // the same one iteration earlier (host predicts the remaining iterations)
+  int next_task;           // k_spmv_seg: next unclaimed task of the running launch (reset by its last CTA)
+  int pad;
 };
 
 // One SccLarge grid unit's iteration state.
@@ -190,7 +192,10 @@ void launch_small(const DeviceLayout& L, const SccTask* tasks, int ntasks, int m
 void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s);
 int grid_iter_ctas();
 bool spmv_seg();  // K4c segmented-scan SpMV (default) or K4b staged tiles (LR_SPMV=tile)
-void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, int nblocks, int gu0, int ngu, GridUnitState* gs,
+// meta: per task 32 lane words (row-start flags of the lane's 8 slots | rows
+// starting before them << 8) for k_spmv_seg tiles (build_chunk_meta)
+void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, const unsigned short* meta, int nblocks, int gu0,
+                      int ngu, GridUnitState* gs,
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
                       DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, int keep_stream,

@@ -122,6 +122,7 @@ __global__ void k_grid_reset(GridUnitState* gs, int ngu, DevStatus* st) {
     st->ctas_done = 0;
     st->last_max = 0.0;
     st->prev_max = 0.0;
+    st->next_task = 0;
   }
 }
 
@@ -414,58 +415,89 @@ __device__ __forceinline__ SpmvBlock from_lanes(int v) {
   return r;
 }
 
+__device__ __forceinline__ unsigned ld_meta(const unsigned short* p, std::uint64_t pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __global__ void __launch_bounds__(kSpmvThreads, 1)
-    k_spmv_seg(DeviceLayout L, const SpmvBlock* __restrict__ tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
-               const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
-               const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
-               const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-               int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, int keep_stream, double* maxbuf) {
+    k_spmv_seg(DeviceLayout L, const SpmvBlock* __restrict__ tasks, const unsigned short* __restrict__ meta,
+               int ntasks, int gu0, int ngu, GridUnitState* gs, const HeavyRow* __restrict__ heavy,
+               double* heavy_part, int* heavy_cnt, const SolveParams* __restrict__ p, const double* __restrict__ pf,
+               double* __restrict__ rank, const double* __restrict__ s_in, double* __restrict__ s_out,
+               long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes, unsigned unit_bytes,
+               int nhead, int keep_stream, double* maxbuf) {
   extern __shared__ double dyn[];  // [kWarps][kTileRows] row totals, then the head
   double* head = dyn + kWarps * kTileRows;
-  __shared__ unsigned flags[kWarps][8];
   __shared__ int wunit[kWarps];
   __shared__ double wmax[kWarps];
   __shared__ unsigned char sdone[kMaxSharedUnits];
   __shared__ int last_cta;
+  __shared__ int cta_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* ysh = dyn + warp * kTileRows;
-  unsigned* fw = flags[warp];
+  if (threadIdx.x == 0) cta_next = 0;
   const std::uint64_t stream = policy_stream(keep_stream);
   const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
   const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
-  for (int i = threadIdx.x; i < nhead; i += kSpmvThreads) head[i] = ld_keep(s_in + hot_begin + i, keep);
-  for (int i = threadIdx.x; i < ngu && i < kMaxSharedUnits; i += kSpmvThreads) sdone[i] = gs[gu0 + i].done ? 1 : 0;
-  const unsigned head_sh = static_cast<unsigned>(__cvta_generic_to_shared(head));
+  int live = 0;
+  for (int i = threadIdx.x; i < ngu; i += kSpmvThreads) {
+    const int d = gs[gu0 + i].done;
+    live |= !d;
+    if (i < kMaxSharedUnits) sdone[i] = d ? 1 : 0;
+  }
+  live = __syncthreads_or(live);  // launches past convergence exit at once
+  if (live)
+    for (int i = threadIdx.x; i < nhead; i += kSpmvThreads) head[i] = ld_keep(s_in + hot_begin + i, keep);
   __syncthreads();
+  // generic addresses of column j: glob_base + 8 j, or (head) head_base + 8 j
+  const long long glob_base = reinterpret_cast<long long>(s_in);
+  const long long head_base = reinterpret_cast<long long>(head) - 8ll * hot_begin;
   auto unit_done = [&](int gu) {
     const int i = gu - gu0;
     return i < kMaxSharedUnits ? sdone[i] != 0 : gs[gu].done != 0;
   };
-  const int stride = gridDim.x * kWarps;
-  // first task at or after tt whose unit still iterates
+  // CTA b owns tasks b, b + grid, b + 2 grid, ... (the whole grid sweeps the
+  // rows in order); its warps claim them one at a time from a shared counter,
+  // one task ahead of the one being processed, so no warp idles at the end of
+  // a launch while another of its CTA still has a static share left.
+  auto grab = [&]() {
+    int v = ntasks;
+    if (lane == 0 && live) {
+      const long long k = atomicAdd(&cta_next, 1);
+      const long long tt = blockIdx.x + k * gridDim.x;
+      v = tt < ntasks ? static_cast<int>(tt) : ntasks;
+    }
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  // first claimed task whose unit still iterates
   auto seek = [&](int& tt, SpmvBlock& bb) {
     while (tt < ntasks) {
       bb = ld_task(tasks + tt);
       if (!unit_done(bb.gunit)) return;
-      tt += stride;
+      tt = grab();
     }
   };
-  auto load_idx = [&](const SpmvBlock& bb, int cc, int* out) {
+  // a chunk's 8 index slots and, for a tile, its lane metadata (row-start
+  // flags of my 8 slots | rows starting before them << 8)
+  auto load_chunk = [&](int tt, const SpmvBlock& bb, int cc, int* out, unsigned& mt) {
     const long long cb = bb.nnz_begin + static_cast<long long>(cc) * kChunkNnz;
     ld_idx8(L.isrc + (cb & ~7ll) + 8 * lane, stream, out);
+    mt = bb.heavy < 0 && bb.nnz <= kChunkNnz ? ld_meta(meta + static_cast<long long>(tt) * 32 + lane, stream) : 0u;
   };
   int cur_unit = -1;
   double lmax = 0.0;
-  int t = blockIdx.x * kWarps + warp, c = 0;
+  int t = grab(), c = 0;
   SpmvBlock b{};
   seek(t, b);
   // the descriptor of the task after b, loaded one task ahead (its unit's done
   // flag is checked when the warp gets there)
-  int tq = t + stride;
+  int tq = t < ntasks ? grab() : ntasks;
   int bq = 0;  // lane i < 8 holds int i of the descriptor
   if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
   int idx[8];
-  if (t < ntasks) load_idx(b, 0, idx);
+  unsigned mt = 0u;
+  if (t < ntasks) load_chunk(t, b, 0, idx, mt);
   double part = 0.0;  // running sum of a multi-chunk task
   while (t < ntasks) {
     if (b.gunit != cur_unit) {
@@ -476,47 +508,41 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
       cur_unit = b.gunit;
       lmax = 0.0;
     }
-    const long long cb = b.nnz_begin + static_cast<long long>(c) * kChunkNnz;
-    const int q0 = static_cast<int>(cb & 7ll);
     const int left = b.nnz - c * kChunkNnz;
-    const int q1 = q0 + (left < kChunkNnz ? left : kChunkNnz);
     const bool tile = b.heavy < 0 && b.nnz <= kChunkNnz;
-    // 1. this chunk's gathers (slots outside [q0, q1) read nothing and add 0)
+    // 1. this chunk's gathers: valid slots [q0, q1) of the window, my bits of it
+    unsigned vm;
+    {
+      const int q0 = static_cast<int>((b.nnz_begin + static_cast<long long>(c) * kChunkNnz) & 7ll);
+      const int q1 = q0 + (left < kChunkNnz ? left : kChunkNnz);
+      const int lo = min(max(q0 - 8 * lane, 0), 8), hi = min(max(q1 - 8 * lane, 0), 8);
+      vm = (0xffu >> (8 - hi)) & (0xffu << lo) & 0xffu;
+    }
     double g[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int slot = 8 * lane + k;
+      // one generic load: the shared-memory head or the global pushed vector,
+      // both addressed as base + 8 * column
       const unsigned off = static_cast<unsigned>(idx[k] - hot_begin);
-      const unsigned valid = slot >= q0 && slot < q1;
-      const unsigned in = valid & (off < static_cast<unsigned>(nhead));
-      const unsigned glob = valid & !in;
-      double a = 0.0, v = 0.0;
-      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
-                   : "+d"(a)
-                   : "r"(head_sh + (in ? off : 0u) * 8u), "r"(in));
+      const long long base = off < static_cast<unsigned>(nhead) ? head_base : glob_base;
+      const double* src = reinterpret_cast<const double*>(base + (static_cast<long long>(idx[k]) << 3));
+      double v = 0.0;
       asm volatile(
-          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, "
-          "[%1], %3;\n\t}"
+          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
           : "+d"(v)
-          : "l"(s_in + (glob ? idx[k] : hot_begin)), "r"(glob), "l"(keep));
-      g[k] = in ? a : v;
+          : "l"(src), "r"(vm & (1u << k)), "l"(keep));
+      g[k] = v;
     }
-    // 2. the tile's row starts and epilogue operands, in flight with the gathers
+    // 2. the tile's epilogue operands (lane j: rows j and j + 32), in flight with the gathers
     const int nr = tile ? b.row_end - b.row_begin : 0;
-    int st0 = -1, st1 = -1;
     double rk0 = 0.0, rk1 = 0.0, pf0 = 0.0, pf1 = 0.0;
-    if (tile) {
-      const long long A = cb & ~7ll;
-      if (lane < nr) {
-        st0 = static_cast<int>(ld_stream(L.iptr + b.row_begin + lane, stream) - A);
-        rk0 = ld_stream(rank + b.row_begin + lane, stream);
-        pf0 = ld_stream(pf + b.row_begin + lane, stream);
-      }
-      if (lane + 32 < nr) {
-        st1 = static_cast<int>(ld_stream(L.iptr + b.row_begin + lane + 32, stream) - A);
-        rk1 = ld_stream(rank + b.row_begin + lane + 32, stream);
-        pf1 = ld_stream(pf + b.row_begin + lane + 32, stream);
-      }
+    if (lane < nr) {
+      rk0 = ld_stream(rank + b.row_begin + lane, stream);
+      pf0 = ld_stream(pf + b.row_begin + lane, stream);
+    }
+    if (lane + 32 < nr) {
+      rk1 = ld_stream(rank + b.row_begin + lane + 32, stream);
+      pf1 = ld_stream(pf + b.row_begin + lane + 32, stream);
     }
     // 3. the next chunk's indices (and the descriptor one task further on)
     int tn = t, cn = c + 1;
@@ -526,31 +552,22 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
       cn = 0;
       bn = from_lanes(bq);
       if (tn < ntasks && unit_done(bn.gunit)) {
-        tn += stride;
+        tn = grab();
         seek(tn, bn);
       }
     }
     int idx_n[8];
-    if (tn < ntasks) load_idx(bn, cn, idx_n);
+    unsigned mt_n = 0u;
+    if (tn < ntasks) load_chunk(tn, bn, cn, idx_n, mt_n);
     if (tn != t) {
-      tq = tn + stride;
+      tq = tn < ntasks ? grab() : ntasks;
       if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
     }
     // 4. consume this chunk
     if (tile) {
-      if (lane < 8) fw[lane] = 0u;
-      __syncwarp();
-      if (st0 >= 0) atomicOr(fw + (st0 >> 5), 1u << (st0 & 31));
-      if (st1 >= 0) atomicOr(fw + (st1 >> 5), 1u << (st1 & 31));
-      __syncwarp();
-      const unsigned mine = (fw[lane >> 2] >> (8u * static_cast<unsigned>(lane & 3))) & 0xffu;  // my 8 slots
-      int before = __popc(mine);  // rows starting before my first slot: exclusive scan of the counts
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, before, d);
-        if (lane >= d) before += u;
-      }
-      before -= __popc(mine);
+      double* ysh = dyn + warp * kTileRows;
+      const unsigned mine = mt & 0xffu;   // row starts among my 8 slots
+      const int before = static_cast<int>(mt >> 8);  // rows starting before my first slot
       // my complete rows go straight to ysh; `pre` continues a row begun in an
       // earlier lane, `run` ends as the part of a row continued by later lanes
       double pre = 0.0, run = 0.0;
@@ -565,22 +582,21 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         }
         run += g[k];
       }
-      const bool seen = mine != 0u;
-      double v = run;  // segment value: the row part after my last flag, or my whole sum
-      bool f = seen;
+      // inclusive segmented scan over lanes; segments start at lanes with a row start
+      const unsigned fl = __ballot_sync(0xffffffffu, mine != 0u);
+      const unsigned upto = fl & (0xffffffffu >> (31 - lane));
+      const int seg0 = upto ? 31 - __clz(upto) : 0;
+      double v = run;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const double vu = __shfl_up_sync(0xffffffffu, v, d);
-        const bool fu = __shfl_up_sync(0xffffffffu, static_cast<int>(f), d) != 0;
-        if (lane >= d) {
-          if (!f) v += vu;
-          f = f || fu;
-        }
+        if (lane - d >= seg0) v += vu;
       }
       const double prev = __shfl_up_sync(0xffffffffu, v, 1);
-      if (seen && before > 0) ysh[before - 1] = (lane > 0 ? prev : 0.0) + pre;
-      if (q1 > q0 && lane == ((q1 - 1) >> 3)) ysh[nr - 1] = v;
-      if (q1 == q0 && lane == 0) ysh[0] = 0.0;
+      if (mine && before > 0) ysh[before - 1] = (lane > 0 ? prev : 0.0) + pre;
+      const int last_lane = (static_cast<int>((b.nnz_begin & 7ll)) + b.nnz - 1) >> 3;
+      if (b.nnz > 0 && lane == last_lane) ysh[nr - 1] = v;
+      if (b.nnz == 0 && lane == 0) ysh[0] = 0.0;
       __syncwarp();
       if (lane < nr) {
         const double y = ysh[lane];
@@ -626,6 +642,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) idx[k] = idx_n[k];
+    mt = mt_n;
     t = tn;
     c = cn;
     b = bn;
@@ -730,8 +747,8 @@ void launch_grid_reset(GridUnitState* gs, int ngu, DevStatus* st, cudaStream_t s
   k_grid_reset<<<blocks_for(ngu > 0 ? ngu : 1, 128), 128, 0, s>>>(gs, ngu, st);
 }
 
-void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks, int gu0, int ngu, GridUnitState* gs,
-                      const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
+void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsigned short* meta, int ntasks, int gu0,
+                      int ngu, GridUnitState* gs, const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
                       int hot_begin, long long hot_rows, long long unit_rows, int keep_stream, double* maxbuf,
                       cudaStream_t s) {
@@ -751,7 +768,7 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, int ntasks,
   const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
   if (spmv_seg()) {
     k_spmv_seg<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileRows) * 8, s>>>(
-        L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
+        L, tasks, meta, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
         hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf);
   } else {
     k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
