@@ -763,7 +763,9 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
   // Larger heads lose: the fill costs microseconds per launch, and the L1 left
   // over holds the in-flight misses of the cold gathers.  LR_SPMV_HEAD
   // overrides (0 disables the head).
-  int want_head = spmv_seg() ? kHeadRowsSeg : kHeadRows;
+  // K4c: 16k entries while the pushed vector is L2-resident (configs 2, 3),
+  // 8k for vectors far beyond L2 (config 5: the cold gathers need the L1)
+  int want_head = spmv_seg() ? (unit_rows * 8 <= (48ll << 20) ? kHeadRowsSeg : kHeadRows) : kHeadRows;
   if (const char* e = std::getenv("LR_SPMV_HEAD")) want_head = std::max(0, std::atoi(e));
   const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
   if (spmv_seg()) {
