@@ -120,7 +120,14 @@ struct LevelTask {
   int pad;
 };
 constexpr int kCacBlockMaxRows = 32768;  // larger CACs: one grid-wide launch per depth slice
-constexpr int kSpmvThreads = 1024;  // one persistent CTA per SM: 32 warps + a shared-memory head
+#ifndef LR_SPMV_THREADS
+#define LR_SPMV_THREADS 1024
+#endif
+constexpr int kSpmvThreads = LR_SPMV_THREADS;  // K4b: one persistent CTA per SM: 32 warps + a shared-memory head
+#ifndef LR_SEG_THREADS
+#define LR_SEG_THREADS 768
+#endif
+constexpr int kSegThreads = LR_SEG_THREADS;    // K4c: 24 warps per SM (78 registers, no spills)
 constexpr int kTileNnz = 256;      // in-edges of one warp tile
 constexpr int kTileRows = 64;      // max rows of one warp tile
 constexpr int kSegNnz = 1024;      // rows above this are split into segments

@@ -387,19 +387,6 @@ __device__ __forceinline__ void ld_idx8(const int* p, std::uint64_t pol, int* o)
                : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7])
                : "l"(p), "l"(pol));
 }
-__device__ __forceinline__ SpmvBlock ld_task(const SpmvBlock* t) {
-  const int4 a = __ldg(reinterpret_cast<const int4*>(t));
-  const int4 b = __ldg(reinterpret_cast<const int4*>(t) + 1);
-  SpmvBlock r;
-  r.nnz_begin = static_cast<long long>(static_cast<unsigned>(a.x)) | (static_cast<long long>(a.y) << 32);
-  r.nnz = a.z;
-  r.row_begin = a.w;
-  r.row_end = b.x;
-  r.gunit = b.y;
-  r.heavy = b.z;
-  r.seg = b.w;
-  return r;
-}
 
 __device__ __forceinline__ SpmvBlock from_lanes(int v) {
   SpmvBlock r;
@@ -421,17 +408,30 @@ __device__ __forceinline__ unsigned ld_meta(const unsigned short* p, std::uint64
   return v;
 }
 
-__global__ void __launch_bounds__(kSpmvThreads, 1)
+// A chunk in flight: its task, its gathers and (tiles) its row operands.
+#ifndef LR_SEG_PIPE
+#define LR_SEG_PIPE 1
+#endif
+struct SegStage {
+  SpmvBlock b;
+  int t, c;
+  unsigned mt;  // tile lane metadata
+  double g[8];
+  double rk0, rk1, pf0, pf1;
+};
+
+__global__ void __launch_bounds__(kSegThreads, 1)
     k_spmv_seg(DeviceLayout L, const SpmvBlock* __restrict__ tasks, const unsigned short* __restrict__ meta,
                int ntasks, int gu0, int ngu, GridUnitState* gs, const HeavyRow* __restrict__ heavy,
                double* heavy_part, int* heavy_cnt, const SolveParams* __restrict__ p, const double* __restrict__ pf,
                double* __restrict__ rank, const double* __restrict__ s_in, double* __restrict__ s_out,
                long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes, unsigned unit_bytes,
                int nhead, int keep_stream, double* maxbuf) {
-  extern __shared__ double dyn[];  // [kWarps][kTileRows] row totals, then the head
-  double* head = dyn + kWarps * kTileRows;
-  __shared__ int wunit[kWarps];
-  __shared__ double wmax[kWarps];
+  constexpr int kW = kSegThreads / 32;
+  extern __shared__ double dyn[];  // [kW][kTileRows] row totals, then the head
+  double* head = dyn + kW * kTileRows;
+  __shared__ int wunit[kW];
+  __shared__ double wmax[kW];
   __shared__ unsigned char sdone[kMaxSharedUnits];
   __shared__ int last_cta;
   __shared__ int cta_next;
@@ -441,14 +441,14 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
   const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
   const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
   int live = 0;
-  for (int i = threadIdx.x; i < ngu; i += kSpmvThreads) {
+  for (int i = threadIdx.x; i < ngu; i += kSegThreads) {
     const int d = gs[gu0 + i].done;
     live |= !d;
     if (i < kMaxSharedUnits) sdone[i] = d ? 1 : 0;
   }
   live = __syncthreads_or(live);  // launches past convergence exit at once
   if (live)
-    for (int i = threadIdx.x; i < nhead; i += kSpmvThreads) head[i] = ld_keep(s_in + hot_begin + i, keep);
+    for (int i = threadIdx.x; i < nhead; i += kSegThreads) head[i] = ld_keep(s_in + hot_begin + i, keep);
   __syncthreads();
   // generic addresses of column j: glob_base + 8 j, or (head) head_base + 8 j
   const long long glob_base = reinterpret_cast<long long>(s_in);
@@ -459,8 +459,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
   };
   // CTA b owns tasks b, b + grid, b + 2 grid, ... (the whole grid sweeps the
   // rows in order); its warps claim them one at a time from a shared counter,
-  // one task ahead of the one being processed, so no warp idles at the end of
-  // a launch while another of its CTA still has a static share left.
+  // so no warp idles at the end of a launch while another of its CTA still
+  // has a static share left.
   auto grab = [&]() {
     int v = ntasks;
     if (lane == 0 && live) {
@@ -470,12 +470,29 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     }
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  // first claimed task whose unit still iterates
-  auto seek = [&](int& tt, SpmvBlock& bb) {
-    while (tt < ntasks) {
-      bb = ld_task(tasks + tt);
+  // The descriptor of the next task to claim is loaded one task ahead (lane
+  // i < 8 holds its int i); its unit's done flag is checked on arrival.
+  int tq = grab();
+  int bq = 0;
+  if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
+  auto next_task = [&](int& tt, SpmvBlock& bb) {
+    for (;;) {
+      tt = tq;
+      if (tt >= ntasks) return;
+      bb = from_lanes(bq);
+      tq = grab();
+      if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
       if (!unit_done(bb.gunit)) return;
-      tt = grab();
+    }
+  };
+  // the chunk after (tt, bb, cc): the next chunk of the same task or the
+  // first chunk of the next task
+  auto advance = [&](int& tt, SpmvBlock& bb, int& cc) {
+    if ((cc + 1) * kChunkNnz < bb.nnz) {
+      ++cc;
+    } else {
+      cc = 0;
+      next_task(tt, bb);
     }
   };
   // a chunk's 8 index slots and, for a tile, its lane metadata (row-start
@@ -485,44 +502,16 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     ld_idx8(L.isrc + (cb & ~7ll) + 8 * lane, stream, out);
     mt = bb.heavy < 0 && bb.nnz <= kChunkNnz ? ld_meta(meta + static_cast<long long>(tt) * 32 + lane, stream) : 0u;
   };
-  int cur_unit = -1;
-  double lmax = 0.0;
-  int t = grab(), c = 0;
-  SpmvBlock b{};
-  seek(t, b);
-  // the descriptor of the task after b, loaded one task ahead (its unit's done
-  // flag is checked when the warp gets there)
-  int tq = t < ntasks ? grab() : ntasks;
-  int bq = 0;  // lane i < 8 holds int i of the descriptor
-  if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
-  int idx[8];
-  unsigned mt = 0u;
-  if (t < ntasks) load_chunk(t, b, 0, idx, mt);
-  double part = 0.0;  // running sum of a multi-chunk task
-  while (t < ntasks) {
-    if (b.gunit != cur_unit) {
-      if (cur_unit >= 0) {
-        const double m = warp_max(lmax);
-        if (lane == 0 && m > 0.0) atomicMax(&gs[cur_unit].max_bits, dbits(m));
-      }
-      cur_unit = b.gunit;
-      lmax = 0.0;
-    }
-    const int left = b.nnz - c * kChunkNnz;
-    const bool tile = b.heavy < 0 && b.nnz <= kChunkNnz;
-    // 1. this chunk's gathers: valid slots [q0, q1) of the window, my bits of it
-    unsigned vm;
-    {
-      const int q0 = static_cast<int>((b.nnz_begin + static_cast<long long>(c) * kChunkNnz) & 7ll);
-      const int q1 = q0 + (left < kChunkNnz ? left : kChunkNnz);
-      const int lo = min(max(q0 - 8 * lane, 0), 8), hi = min(max(q1 - 8 * lane, 0), 8);
-      vm = (0xffu >> (8 - hi)) & (0xffu << lo) & 0xffu;
-    }
-    double g[8];
+  // issue a chunk's gathers (valid slots [q0, q1) of its window) and its tile's row operands
+  auto issue = [&](SegStage& S, const int* idx) {
+    const int left = S.b.nnz - S.c * kChunkNnz;
+    const int q0 = static_cast<int>((S.b.nnz_begin + static_cast<long long>(S.c) * kChunkNnz) & 7ll);
+    const int q1 = q0 + (left < kChunkNnz ? left : kChunkNnz);
+    const int lo = min(max(q0 - 8 * lane, 0), 8), hi = min(max(q1 - 8 * lane, 0), 8);
+    const unsigned vm = (0xffu >> (8 - hi)) & (0xffu << lo) & 0xffu;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      // one generic load: the shared-memory head or the global pushed vector,
-      // both addressed as base + 8 * column
+      // one generic load: the shared-memory head or the global pushed vector
       const unsigned off = static_cast<unsigned>(idx[k] - hot_begin);
       const long long base = off < static_cast<unsigned>(nhead) ? head_base : glob_base;
       const double* src = reinterpret_cast<const double*>(base + (static_cast<long long>(idx[k]) << 3));
@@ -531,43 +520,39 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
           "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
           : "+d"(v)
           : "l"(src), "r"(vm & (1u << k)), "l"(keep));
-      g[k] = v;
+      S.g[k] = v;
     }
-    // 2. the tile's epilogue operands (lane j: rows j and j + 32), in flight with the gathers
-    const int nr = tile ? b.row_end - b.row_begin : 0;
-    double rk0 = 0.0, rk1 = 0.0, pf0 = 0.0, pf1 = 0.0;
+    const bool tile = S.b.heavy < 0 && S.b.nnz <= kChunkNnz;
+    const int nr = tile ? S.b.row_end - S.b.row_begin : 0;
+    S.rk0 = S.rk1 = S.pf0 = S.pf1 = 0.0;
     if (lane < nr) {
-      rk0 = ld_stream(rank + b.row_begin + lane, stream);
-      pf0 = ld_stream(pf + b.row_begin + lane, stream);
+      S.rk0 = ld_stream(rank + S.b.row_begin + lane, stream);
+      S.pf0 = ld_stream(pf + S.b.row_begin + lane, stream);
     }
     if (lane + 32 < nr) {
-      rk1 = ld_stream(rank + b.row_begin + lane + 32, stream);
-      pf1 = ld_stream(pf + b.row_begin + lane + 32, stream);
+      S.rk1 = ld_stream(rank + S.b.row_begin + lane + 32, stream);
+      S.pf1 = ld_stream(pf + S.b.row_begin + lane + 32, stream);
     }
-    // 3. the next chunk's indices (and the descriptor one task further on)
-    int tn = t, cn = c + 1;
-    SpmvBlock bn = b;
-    if (cn * kChunkNnz >= b.nnz) {
-      tn = tq;
-      cn = 0;
-      bn = from_lanes(bq);
-      if (tn < ntasks && unit_done(bn.gunit)) {
-        tn = grab();
-        seek(tn, bn);
+  };
+  int cur_unit = -1;
+  double lmax = 0.0;
+  double part = 0.0;  // running sum of a multi-chunk task
+  // consume a chunk whose gathers have been issued
+  auto consume = [&](const SegStage& S) {
+    const SpmvBlock& b = S.b;
+    if (b.gunit != cur_unit) {
+      if (cur_unit >= 0) {
+        const double m = warp_max(lmax);
+        if (lane == 0 && m > 0.0) atomicMax(&gs[cur_unit].max_bits, dbits(m));
       }
+      cur_unit = b.gunit;
+      lmax = 0.0;
     }
-    int idx_n[8];
-    unsigned mt_n = 0u;
-    if (tn < ntasks) load_chunk(tn, bn, cn, idx_n, mt_n);
-    if (tn != t) {
-      tq = tn < ntasks ? grab() : ntasks;
-      if (tq < ntasks && lane < 8) bq = __ldg(reinterpret_cast<const int*>(tasks + tq) + lane);
-    }
-    // 4. consume this chunk
-    if (tile) {
+    if (b.heavy < 0 && b.nnz <= kChunkNnz) {
+      const int nr = b.row_end - b.row_begin;
       double* ysh = dyn + warp * kTileRows;
-      const unsigned mine = mt & 0xffu;   // row starts among my 8 slots
-      const int before = static_cast<int>(mt >> 8);  // rows starting before my first slot
+      const unsigned mine = S.mt & 0xffu;             // row starts among my 8 slots
+      const int before = static_cast<int>(S.mt >> 8);  // rows starting before my first slot
       // my complete rows go straight to ysh; `pre` continues a row begun in an
       // earlier lane, `run` ends as the part of a row continued by later lanes
       double pre = 0.0, run = 0.0;
@@ -580,7 +565,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
           ++o;
           run = 0.0;
         }
-        run += g[k];
+        run += S.g[k];
       }
       // inclusive segmented scan over lanes; segments start at lanes with a row start
       const unsigned fl = __ballot_sync(0xffffffffu, mine != 0u);
@@ -600,21 +585,21 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
       __syncwarp();
       if (lane < nr) {
         const double y = ysh[lane];
-        rank[b.row_begin + lane] = rk0 + y;
-        st_keep(s_out + b.row_begin + lane, pf0 * y, keep_out);
+        rank[b.row_begin + lane] = S.rk0 + y;
+        st_keep(s_out + b.row_begin + lane, S.pf0 * y, keep_out);
         lmax = fmax(lmax, y);
       }
       if (lane + 32 < nr) {
         const double y = ysh[lane + 32];
-        rank[b.row_begin + lane + 32] = rk1 + y;
-        st_keep(s_out + b.row_begin + lane + 32, pf1 * y, keep_out);
+        rank[b.row_begin + lane + 32] = S.rk1 + y;
+        st_keep(s_out + b.row_begin + lane + 32, S.pf1 * y, keep_out);
         lmax = fmax(lmax, y);
       }
       __syncwarp();
     } else {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) part += g[k];
-      if (left <= kChunkNnz) {  // last chunk of a long row or segment
+      for (int k = 0; k < 8; ++k) part += S.g[k];
+      if (b.nnz - S.c * kChunkNnz <= kChunkNnz) {  // last chunk of a long row or segment
         const double sum = warp_sum(part);
         part = 0.0;
         int row = -1;
@@ -640,12 +625,42 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) idx[k] = idx_n[k];
-    mt = mt_n;
-    t = tn;
-    c = cn;
-    b = bn;
+  };
+  // Two chunks in flight per warp: while chunk A is reduced, the gathers of
+  // chunk B are outstanding and the indices of the chunk after B are loading.
+  SegStage A, B;
+  int idx[8];
+  A.c = 0;
+  next_task(A.t, A.b);
+  if (A.t < ntasks) {
+    load_chunk(A.t, A.b, 0, idx, A.mt);
+    issue(A, idx);
+    B.t = A.t;
+    B.b = A.b;
+    B.c = A.c;
+    advance(B.t, B.b, B.c);
+    if (B.t < ntasks) load_chunk(B.t, B.b, B.c, idx, B.mt);
+  }
+  while (A.t < ntasks) {
+    int tn = B.t, cn = B.c;
+    SpmvBlock bn = B.b;
+    unsigned mtn = 0u;
+#if LR_SEG_PIPE == 1
+    consume(A);  // one chunk in flight: B's gathers wait for A's reduction
+#endif
+    if (B.t < ntasks) {
+      issue(B, idx);
+      advance(tn, bn, cn);
+      if (tn < ntasks) load_chunk(tn, bn, cn, idx, mtn);
+    }
+#if LR_SEG_PIPE != 1
+    consume(A);
+#endif
+    A = B;
+    B.t = tn;
+    B.b = bn;
+    B.c = cn;
+    B.mt = mtn;
   }
   const double m = warp_max(lmax);
   if (lane == 0) {
@@ -654,10 +669,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < kW; ++w) {
       if (wunit[w] < 0 || !(wmax[w] > 0.0)) continue;
       double mm = wmax[w];
-      while (w + 1 < kWarps && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
+      while (w + 1 < kW && wunit[w + 1] == wunit[w]) mm = fmax(mm, wmax[++w]);
       atomicMax(&gs[wunit[w]].max_bits, dbits(mm));
     }
     __threadfence();
@@ -710,7 +725,7 @@ static int head_capacity() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes a{};
-    const int per_warp = spmv_seg() ? kWarps * kTileRows : kWarps * kTileNnz;
+    const int per_warp = spmv_seg() ? (kSegThreads / 32) * kTileRows : kWarps * kTileNnz;
     if (spmv_seg()) {
       cudaFuncGetAttributes(&a, k_spmv_seg);
     } else {
@@ -732,10 +747,10 @@ int grid_iter_ctas() {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_warp = spmv_seg() ? kWarps * kTileRows : kWarps * kTileNnz;
+    const int per_warp = spmv_seg() ? (kSegThreads / 32) * kTileRows : kWarps * kTileNnz;
     const size_t bytes = static_cast<size_t>(head_capacity() + per_warp) * 8;
     if (spmv_seg())
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_seg, kSpmvThreads, bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_seg, kSegThreads, bytes);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_iter, kSpmvThreads, bytes);
     ctas = sms * (per_sm > 0 ? per_sm : 1);
@@ -757,7 +772,7 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
     return;
   }
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
-  const int want = blocks_for(ntasks, kWarps);
+  const int want = blocks_for(ntasks, spmv_seg() ? kSegThreads / 32 : kWarps);
   const int grid = want < grid_iter_ctas() ? want : grid_iter_ctas();
   // Head size: measured optimum 4-12k entries at configs 2 and 5 for K4b.
   // Larger heads lose: the fill costs microseconds per launch, and the L1 left
@@ -769,7 +784,7 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
   if (const char* e = std::getenv("LR_SPMV_HEAD")) want_head = std::max(0, std::atoi(e));
   const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
   if (spmv_seg()) {
-    k_spmv_seg<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileRows) * 8, s>>>(
+    k_spmv_seg<<<grid, kSegThreads, static_cast<size_t>(nhead + (kSegThreads / 32) * kTileRows) * 8, s>>>(
         L, tasks, meta, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
         hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf);
   } else {
