@@ -325,12 +325,37 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "frac_vs_nominal_8000": (achieved / 8000.0) if achieved else None,
-                "kernel": "k_grid_iter (SccLarge power-series SpMV)", "peak_kind": peak_kind,
+                "kernel": "k_spmv_seg (K4c: SccLarge power-series SpMV)", "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": (inf["spmv_bytes"] / inf["spmv_active_launches"])
                 if inf["spmv_active_launches"] else None,
                 "avg_launch_ms": (inf["spmv_active_ms"] / inf["spmv_active_launches"])
                 if inf["spmv_active_launches"] else None,
                 "spmv_share_of_step": inf["spmv_active_ms"] / ms if ms > 0 else None}
+
+    # ablation on the same GPU: the reference's partition-free whole-graph power
+    # series (compute_baseline, lr_plan_build_baseline) over the same graph
+    gpu_base = None
+    if world == 1 and not args.no_gpu_baseline:
+        try:
+            beng = lr.Engine(g, device=local, baseline=True)
+            binfo0 = beng.solve_ptr(w_dev.data_ptr(), r3_dev.data_ptr(), r1_dev.data_ptr(), host=False, params=params)
+            bt = []
+            for _ in range(args.steps):
+                with torch.cuda.stream(stream):
+                    flush.zero_()
+                torch.cuda.synchronize()
+                bi = beng.solve_ptr(w_dev.data_ptr(), r3_dev.data_ptr(), r1_dev.data_ptr(), host=False,
+                                    params=params)
+                bt.append(bi["device_ms"])
+            bms = float(np.mean(bt))
+            bwork = int(binfo0["iterative_edge_work"])
+            gpu_base = {"what": "whole-graph power series (compute_baseline) on this GPU, same graph and weights",
+                        "value": bwork / (bms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": bms,
+                        "iterations": int(binfo0["total_iterations"]), "edge_updates_per_step": bwork,
+                        "partitioned_speedup": bms / ms, "plan_s": beng.plan_ms / 1e3}
+            del beng
+        except Exception as e:  # reported, never required
+            gpu_base = {"value": None, "error": str(e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -359,6 +384,7 @@ def run_ours(args):
             "gpu_launches": int(inf["kernel_launches"]) * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "gpu_baseline": gpu_base,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -376,6 +402,7 @@ def main():
     ap.add_argument("--shrink", type=int, default=0)
     ap.add_argument("--ref-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

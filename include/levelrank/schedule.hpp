@@ -109,5 +109,14 @@ std::vector<VertexId> schedule_permutation(const Partition& p);
 /// Multi-threaded layout build (std::invalid_argument if small_threshold < 1).
 Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold);
 
+/// The whole graph as ONE power-series unit (kind SccLarge, one level, no
+/// cross edges): the device layout of compute_baseline / solve_baseline
+/// (proj/src/engine.cpp:184-218, proj/src/solvers.cpp:164-198), the
+/// partition-free "basic method".  Rows by descending walk out-degree (ties by
+/// vertex id), vertices without in-edges last; every row's in-edges by source vertex ascending (the
+/// reference's push order); ignored self-loops dropped, kept ones included;
+/// unit_edges = walk_edge_count (proj/src/engine.cpp:20-24).
+Layout build_baseline_layout(const Graph& g);
+
 }  // namespace b200
 }  // namespace levelrank

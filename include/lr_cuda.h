@@ -72,6 +72,11 @@ lr_status lr_find_components(const lr_graph* g, int merge_cacs, int32_t* comp_of
  * The plan borrows g; g must outlive it. */
 typedef struct lr_plan lr_plan;
 lr_status lr_plan_build(const lr_graph* g, int32_t small_threshold, lr_plan** out);
+/* The whole graph as one power-series unit: the layout of compute_baseline
+ * (proj/src/engine.cpp:184-218, solve_baseline proj/src/solvers.cpp:164-198),
+ * no partition and no schedule (those views return LR_EINVAL).  Upload and
+ * solve it like any plan; the unit's iteration count is the baseline's. */
+lr_status lr_plan_build_baseline(const lr_graph* g, lr_plan** out);
 void lr_plan_free(lr_plan* p);
 
 /* The reference Schedule (proj/include/levelrank/schedule.hpp:13-57), flattened
@@ -207,6 +212,12 @@ typedef struct lr_report {
 lr_status lr_compute_pagerank(const lr_graph* g, const double* w, int64_t wn, double c, double tol,
                               int32_t small_threshold, int device, double* ranks, double* r1,
                               lr_report* report, int64_t* unit_iters, int64_t unit_cap);
+
+/* compute_baseline (proj/src/engine.cpp:184-218; engine.hpp:98-99): the
+ * whole-graph power series on the GPU, report as the reference fills it
+ * (total_iterations, iterative_edge_work = iterations * walk edges, ...). */
+lr_status lr_compute_baseline(const lr_graph* g, const double* w, int64_t wn, double c, double tol,
+                              int device, double* ranks, double* r1, lr_report* report);
 
 /* ------------------------------------------------------- solver helpers */
 /* validate_params (proj/src/solvers.cpp:11-15). */

@@ -134,6 +134,7 @@ EXPORTS = {
     "lr_graph_free": (None, [VP]),
     "lr_find_components": (C.c_int, [VP, C.c_int, I32P, I32P, I32P, I32P, I32P, I32P, I64P]),
     "lr_plan_build": (C.c_int, [VP, C.c_int32, C.POINTER(VP)]),
+    "lr_plan_build_baseline": (C.c_int, [VP, C.POINTER(VP)]),
     "lr_plan_free": (None, [VP]),
     "lr_plan_schedule_sizes": (C.c_int, [VP, I64P]),
     "lr_plan_schedule_get": (C.c_int, [VP, I32P, I32P, I64P, I32P, I32P, I32P, I64P, I64P, I32P, I32P, I32P,
@@ -152,6 +153,8 @@ EXPORTS = {
     "lr_ctx_free": (None, [VP]),
     "lr_compute_pagerank": (C.c_int, [VP, F64P, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_int, F64P,
                                       F64P, C.POINTER(_Report), I64P, C.c_int64]),
+    "lr_compute_baseline": (C.c_int, [VP, F64P, C.c_int64, C.c_double, C.c_double, C.c_int, F64P, F64P,
+                                      C.POINTER(_Report)]),
     "lr_validate_params": (C.c_int, [C.c_double, C.c_double]),
     "lr_iteration_cap": (C.c_int64, [C.c_double, C.c_double]),
     "lr_error_bound": (None, [C.c_int64, C.c_int64, C.c_double, C.c_double, F64P]),
@@ -335,12 +338,18 @@ _SCHED_ORDER = ["level_values", "level_unit_begin", "level_cross_begin", "unit_k
 class Plan:
     """find_components + build_schedule + device Layout (lr_plan)."""
 
-    def __init__(self, g: Graph, small_threshold: int = 100):
+    def __init__(self, g: Graph, small_threshold: int = 100, baseline: bool = False):
+        """baseline=True: the whole graph as one power-series unit (compute_baseline's
+        layout, lr_plan_build_baseline) -- no partition, no schedule."""
         self.graph = g  # keeps the borrowed graph alive
         h = VP()
-        _check(lib().lr_plan_build(g._h, int(small_threshold), C.byref(h)))
+        if baseline:
+            _check(lib().lr_plan_build_baseline(g._h, C.byref(h)))
+        else:
+            _check(lib().lr_plan_build(g._h, int(small_threshold), C.byref(h)))
         self._h = h
         self.small_threshold = small_threshold
+        self.baseline = baseline
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -456,12 +465,13 @@ class Engine:
     """Plan once, upload once, then solve any number of weight vectors on one GPU."""
 
     def __init__(self, g: Graph, small_threshold: int = 100, device: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, baseline: bool = False):
         """rank/world/nccl_id: row-shard the giant SCC units over `world` GPUs
-        (one process per GPU, every rank passes the same graph and id)."""
+        (one process per GPU, every rank passes the same graph and id).
+        baseline=True: solve the whole graph as one power series (compute_baseline)."""
         import time
         t0 = time.perf_counter()
-        self.plan = Plan(g, small_threshold)
+        self.plan = Plan(g, small_threshold, baseline=baseline)
         self.plan_ms = (time.perf_counter() - t0) * 1e3
         self.n = g.n
         self.m = g.m
@@ -476,7 +486,7 @@ class Engine:
         _check(lib().lr_ctx_upload(self._h, C.byref(self._layout)))
         self.upload_ms = (time.perf_counter() - t1) * 1e3
         self.n_units = int(self._layout.n_units)
-        self.census = self.plan.census()
+        self.census = {} if baseline else self.plan.census()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -537,6 +547,29 @@ def compute_pagerank(g: Graph, weights, params: SolverParams = SolverParams(), m
     d["largest_component_kind"] = "scc" if d.pop("largest_is_scc") else "cac"
     d["all_weights_zero"] = bool(d["all_weights_zero"])
     return EngineResult(ranks, r1, d, it[: rep.n_units].copy())
+
+
+def compute_baseline(g: Graph, weights, params: SolverParams = SolverParams(), device: int = 0) -> EngineResult:
+    """compute_baseline (engine.cpp:184-218): the whole-graph power series
+    (solve_baseline, solvers.cpp:164-198) on the GPU -- the partition-free
+    "basic method" the level-scheduled solve is measured against."""
+    w = _f64(weights)
+    n = g.n
+    ranks = np.zeros(n)
+    r1 = np.zeros(n)
+    rep = _Report()
+    _check(lib().lr_compute_baseline(g._h, _p(w, F64P), len(w), float(params.c), float(params.tol), int(device),
+                                     _p(ranks, F64P), _p(r1, F64P), C.byref(rep)))
+    d = rep.as_dict()
+    d["method"] = "baseline"
+    d["c"], d["tol"] = params.c, params.tol
+    d["all_weights_zero"] = bool(d["all_weights_zero"])
+    for k in ("components", "scc_components", "cac_components", "singleton_cacs", "largest_component",
+              "largest_is_scc", "level_count", "large_scc_vertices", "eps_tot", "eps_avg", "cross_edge_count",
+              "single_pass_edge_work"):
+        d.pop(k, None)
+    d["max_level"] = -1
+    return EngineResult(ranks, r1, d, np.array([rep.total_iterations], np.int64))
 
 
 # --------------------------------------------------------- synthetic inputs

@@ -433,9 +433,10 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           int r = own0;
           while (r < own1) {
             const long long len = L->iptr[r + 1] - L->iptr[r];
-            if (len == 0 && spmv_seg()) {
-              blocks.push_back(SpmvBlock{L->iptr[r], 0, r, r + 1, gu, -1, 0});
-              ++r;
+            if (len == 0 && spmv_seg()) {  // a run of rows without in-edges: y = 0
+              const int start = r;
+              while (r < own1 && r - start < kTileRows && L->iptr[r + 1] == L->iptr[r]) ++r;
+              blocks.push_back(SpmvBlock{L->iptr[start], 0, start, r, gu, -1, 0});
               continue;
             }
             if (len > tile_nnz) {
@@ -599,7 +600,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     meta.assign(blocks.size() * 32, 0);
     for (size_t t = 0; t < blocks.size(); ++t) {
       const SpmvBlock& b = blocks[t];
-      if (b.heavy >= 0 || b.nnz > kChunkNnz) continue;
+      if (b.heavy >= 0 || b.nnz > kChunkNnz || b.nnz == 0) continue;
       const long long A = b.nnz_begin & ~7ll;
       unsigned char fl[32] = {};
       for (int r = b.row_begin; r < b.row_end; ++r) {

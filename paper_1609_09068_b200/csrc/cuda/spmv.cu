@@ -581,16 +581,15 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       if (mine && before > 0) ysh[before - 1] = (lane > 0 ? prev : 0.0) + pre;
       const int last_lane = (static_cast<int>((b.nnz_begin & 7ll)) + b.nnz - 1) >> 3;
       if (b.nnz > 0 && lane == last_lane) ysh[nr - 1] = v;
-      if (b.nnz == 0 && lane == 0) ysh[0] = 0.0;
       __syncwarp();
       if (lane < nr) {
-        const double y = ysh[lane];
+        const double y = b.nnz > 0 ? ysh[lane] : 0.0;  // nnz = 0: a run of rows without in-edges
         rank[b.row_begin + lane] = S.rk0 + y;
         st_keep(s_out + b.row_begin + lane, S.pf0 * y, keep_out);
         lmax = fmax(lmax, y);
       }
       if (lane + 32 < nr) {
-        const double y = ysh[lane + 32];
+        const double y = b.nnz > 0 ? ysh[lane + 32] : 0.0;
         rank[b.row_begin + lane + 32] = S.rk1 + y;
         st_keep(s_out + b.row_begin + lane + 32, S.pf1 * y, keep_out);
         lmax = fmax(lmax, y);

@@ -43,6 +43,7 @@ struct lr_plan {
   levelrank::Partition p;
   levelrank::Layout L;
   std::int32_t threshold = 100;
+  bool baseline = false;                       // whole graph as one unit (no partition, no schedule)
   std::unique_ptr<levelrank::Schedule> sched;  // built lazily for parity views
   std::vector<std::int32_t> flat_ids_cache;
 };
@@ -192,7 +193,23 @@ lr_status lr_plan_build(const lr_graph* gp, int32_t small_threshold, lr_plan** o
 
 void lr_plan_free(lr_plan* p) { delete p; }
 
+lr_status lr_plan_build_baseline(const lr_graph* gp, lr_plan** out) {
+  *out = nullptr;
+  if (!gp) {
+    lrerr::set("null graph");
+    return LR_EINVAL;
+  }
+  return guarded([&] {
+    auto plan = std::make_unique<lr_plan>();
+    plan->g = &gp->g;
+    plan->baseline = true;
+    plan->L = build_baseline_layout(gp->g);
+    *out = plan.release();
+  });
+}
+
 static const Schedule& plan_schedule(lr_plan* p) {
+  if (p->baseline) throw std::invalid_argument("a baseline plan has no schedule");
   if (!p->sched) p->sched = std::make_unique<Schedule>(build_schedule(*p->g, p->p, p->threshold));
   return *p->sched;
 }
@@ -264,6 +281,7 @@ lr_status lr_plan_schedule_get(const lr_plan* cp, int32_t* level_values, int32_t
 
 lr_status lr_plan_census(const lr_plan* p, lr_census* out) {
   return guarded([&] {
+    if (p->baseline) throw std::invalid_argument("a baseline plan has no partition");
     const PartitionCensus c = census(p->p);
     out->components = c.components;
     out->scc_components = c.scc_components;
@@ -425,6 +443,71 @@ lr_status lr_compute_pagerank(const lr_graph* gp, const double* w, int64_t wn, d
   lr_error_bound(rep->large_scc_vertices, n, c, tol, eb);
   rep->eps_tot = eb[0];
   rep->eps_avg = eb[1];
+  rep->wall_ms = ms_since(t0);
+  return LR_OK;
+}
+
+lr_status lr_compute_baseline(const lr_graph* gp, const double* w, int64_t wn, double c, double tol, int device,
+                              double* ranks, double* r1, lr_report* rep) {
+  if (!gp) {
+    lrerr::set("null graph");
+    return LR_EINVAL;
+  }
+  lr_status st = lr_validate_params(c, tol);
+  if (st != LR_OK) return st;
+  const Graph& g = gp->g;
+  const int64_t n = g.vertex_count();
+  if (wn != n) {
+    lrerr::set("weight vector does not match the vertex count");
+    return LR_EINVAL;
+  }
+  for (int64_t v = 0; v < n; ++v)
+    if (w[v] < 0.0) {
+      lrerr::set("weights must be non-negative");
+      return LR_EINVAL;
+    }
+  const auto t0 = std::chrono::steady_clock::now();
+  lr_report local{};
+  if (!rep) rep = &local;
+  std::memset(rep, 0, sizeof *rep);
+  rep->vertices = n;
+  rep->edges = g.edge_count();
+  rep->max_level = -1;
+  rep->threads = 1;
+  if (n == 0) return LR_OK;
+  double wmax = w[0];
+  for (int64_t v = 1; v < n; ++v) wmax = std::max(wmax, w[v]);
+  rep->all_weights_zero = wmax == 0.0;
+  lr_plan* plan = nullptr;
+  st = lr_plan_build_baseline(gp, &plan);
+  if (st != LR_OK) return st;
+  std::unique_ptr<lr_plan, void (*)(lr_plan*)> plan_guard(plan, lr_plan_free);
+  rep->plan_ms = ms_since(t0);
+  lr_ctx* ctx = nullptr;
+  st = lr_ctx_create(device, &ctx);
+  if (st != LR_OK) return st;
+  std::unique_ptr<lr_ctx, void (*)(lr_ctx*)> ctx_guard(ctx, lr_ctx_free);
+  lr_layout lay{};
+  lr_plan_layout(plan, &lay);
+  const auto t1 = std::chrono::steady_clock::now();
+  st = lr_ctx_upload(ctx, &lay);
+  if (st != LR_OK) return st;
+  rep->upload_ms = ms_since(t1);
+  int64_t iters = 0;
+  lr_solve_info info{};
+  const auto t2 = std::chrono::steady_clock::now();
+  st = lr_solve(ctx, w, c, tol, ranks, r1, &info, &iters);
+  rep->solve_ms = ms_since(t2);
+  rep->device_ms = info.device_ms;
+  if (st != LR_OK) return st;
+  // engine.cpp:210-215
+  const int64_t walk_edges = plan->L.unit_edges[0];
+  rep->n_units = 1;
+  rep->total_iterations = iters;
+  rep->iterative_edge_work = iters * walk_edges;
+  rep->iterative_edges = walk_edges;
+  rep->total_edge_work = rep->iterative_edge_work;
+  rep->mean_iterations_per_edge = static_cast<double>(iters);
   rep->wall_ms = ms_since(t0);
   return LR_OK;
 }

@@ -467,5 +467,101 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   return L;
 }
 
+Layout build_baseline_layout(const Graph& g) {
+  const VertexId n = g.vertex_count();
+  const std::size_t nn = static_cast<std::size_t>(n);
+  const bool keep = g.loop_policy() == LoopPolicy::Keep;
+  Layout L;
+  L.n = n;
+  L.keep_loops = keep;
+  L.level_row_begin.assign(1, 0);
+  L.level_unit_begin.assign(1, 0);
+  L.unit_row_begin.assign(1, 0);
+  L.xptr.assign(1, 0);
+  L.iptr.assign(1, 0);
+  if (n == 0) return L;
+  const EdgeId* off = g.offsets_data();
+  const VertexId* tgt = g.targets_data();
+  const std::uint8_t* lp = g.loop_data();
+  L.max_level = 0;
+  L.level_row_begin = {0, n};
+  L.level_unit_begin = {0, 1};
+  L.unit_row_begin = {0, n};
+  L.unit_kind = {static_cast<std::uint8_t>(UnitKind::SccLarge)};
+  L.unit_level = {0};
+  L.cac_depth_begin = {-1};
+  // walk out-degree and in-degree (ignored self-loops excluded)
+  std::vector<VertexId> wd(nn);
+  std::vector<std::atomic<std::int64_t>> indeg(nn);
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v) indeg[static_cast<std::size_t>(v)].store(0, std::memory_order_relaxed);
+  });
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t uu = b; uu < e; ++uu) {
+      const VertexId u = static_cast<VertexId>(uu);
+      const bool drop = lp[u] && !keep;
+      wd[static_cast<std::size_t>(u)] = static_cast<VertexId>(off[u + 1] - off[u]) - (drop ? 1 : 0);
+      for (EdgeId k = off[u]; k < off[u + 1]; ++k)
+        if (tgt[k] != u || keep) indeg[static_cast<std::size_t>(tgt[k])].fetch_add(1, std::memory_order_relaxed);
+    }
+  });
+  // rows by descending walk out-degree (the most-gathered pushed values
+  // first), vertices without in-edges after all others: their rows never
+  // change after the first iteration and form one run of empty SpMV rows
+  L.vertex_of.resize(nn);
+  for (std::size_t v = 0; v < nn; ++v) L.vertex_of[v] = static_cast<VertexId>(v);
+  std::stable_sort(L.vertex_of.begin(), L.vertex_of.end(), [&](VertexId a, VertexId b) {
+    const bool ea = indeg[static_cast<std::size_t>(a)].load(std::memory_order_relaxed) == 0;
+    const bool eb = indeg[static_cast<std::size_t>(b)].load(std::memory_order_relaxed) == 0;
+    if (ea != eb) return eb;
+    return wd[static_cast<std::size_t>(a)] > wd[static_cast<std::size_t>(b)];
+  });
+  L.row_of.resize(nn);
+  L.deg.resize(nn);
+  L.loop.assign(nn, 0);
+  L.xptr.assign(nn + 1, 0);
+  L.iptr.assign(nn + 1, 0);
+  for (std::size_t r = 0; r < nn; ++r) {
+    const VertexId v = L.vertex_of[r];
+    L.row_of[static_cast<std::size_t>(v)] = static_cast<VertexId>(r);
+    L.deg[r] = wd[static_cast<std::size_t>(v)];
+    L.iptr[r + 1] = L.iptr[r] + indeg[static_cast<std::size_t>(v)].load(std::memory_order_relaxed);
+  }
+  const EdgeId m = L.iptr[nn];
+  L.isrc.resize(static_cast<std::size_t>(m));
+  // scatter (row of the source) into each destination row, then restore the
+  // source-ascending order within every row
+  std::vector<std::atomic<std::int64_t>> cur(nn);
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t r = b; r < e; ++r) cur[static_cast<std::size_t>(r)].store(L.iptr[static_cast<std::size_t>(r)], std::memory_order_relaxed);
+  });
+  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t uu = b; uu < e; ++uu) {
+      const VertexId u = static_cast<VertexId>(uu);
+      const VertexId ru = L.row_of[static_cast<std::size_t>(u)];
+      for (EdgeId k = off[u]; k < off[u + 1]; ++k) {
+        if (tgt[k] == u && !keep) continue;
+        const std::size_t rv = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(tgt[k])]);
+        L.isrc[static_cast<std::size_t>(cur[rv].fetch_add(1, std::memory_order_relaxed))] = ru;
+      }
+    }
+  });
+  detail::parallel_dynamic(n, 4096, [&](std::int64_t b, std::int64_t e) {
+    for (std::int64_t r = b; r < e; ++r)
+      std::sort(L.isrc.begin() + L.iptr[static_cast<std::size_t>(r)], L.isrc.begin() + L.iptr[static_cast<std::size_t>(r) + 1],
+                [&](VertexId x, VertexId y) {
+                  return L.vertex_of[static_cast<std::size_t>(x)] < L.vertex_of[static_cast<std::size_t>(y)];
+                });
+  });
+  L.unit_edges = {m};
+  L.intra_edge_count = m;
+  L.cross_edge_count = 0;
+  EdgeId dropped = 0;
+  if (!keep)
+    for (VertexId v = 0; v < n; ++v) dropped += lp[v] ? 1 : 0;
+  L.dropped_loop_count = dropped;
+  return L;
+}
+
 }  // namespace b200
 }  // namespace levelrank
