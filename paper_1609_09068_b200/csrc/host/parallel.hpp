@@ -86,6 +86,91 @@ T exclusive_scan_inplace(T* v, std::int64_t n) {
   return part[static_cast<std::size_t>(t)];
 }
 
+// Stable bucketed transpose into K CSRs over `nrows` rows, without atomics.
+// emit(u, sink) is called for every source u in [0, n_src) -- twice, with the
+// same calls both times -- and calls sink(k, row, value) for each entry of
+// CSR k.  Sources are split into contiguous ascending chunks, one per thread;
+// entries go to row buckets of 2^14 rows (per-thread cursors, sequential
+// writes), then each bucket is counting-sorted by row.  Every row's values end
+// up in emission order: source ascending, then the order emit produced them.
+template <int K, typename Emit>
+void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, std::vector<std::int64_t>* ptr,
+                std::vector<VertexId>* col) {
+  constexpr int kShift = 14;
+  const std::int64_t nb = (nrows >> kShift) + 1;
+  const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n_src / 4096) + 1));
+  auto at = [&](int k, int th, std::int64_t b) {
+    return (static_cast<std::size_t>(k) * static_cast<std::size_t>(t) + static_cast<std::size_t>(th)) *
+               static_cast<std::size_t>(nb) + static_cast<std::size_t>(b);
+  };
+  std::vector<std::int64_t> cur(static_cast<std::size_t>(K) * static_cast<std::size_t>(t) * static_cast<std::size_t>(nb), 0);
+  auto run = [&](auto&& body) {
+    std::vector<std::thread> pool;
+    for (int i = 0; i < t; ++i) pool.emplace_back(body, i);
+    for (auto& th : pool) th.join();
+  };
+  run([&](int th) {  // 1. per-(thread, bucket) counts
+    const std::int64_t b = n_src * th / t, e = n_src * (th + 1) / t;
+    for (std::int64_t u = b; u < e; ++u)
+      emit(u, [&](int k, std::int64_t row, VertexId) { ++cur[at(k, th, row >> kShift)]; });
+  });
+  std::vector<std::int64_t> bstart(static_cast<std::size_t>(K) * static_cast<std::size_t>(nb + 1), 0);
+  std::vector<std::vector<std::uint64_t>> tmp(K);
+  for (int k = 0; k < K; ++k) {  // bucket-major, then thread: stable
+    std::int64_t run_total = 0;
+    for (std::int64_t b = 0; b < nb; ++b) {
+      bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(b)] = run_total;
+      for (int th = 0; th < t; ++th) {
+        const std::int64_t c = cur[at(k, th, b)];
+        cur[at(k, th, b)] = run_total;
+        run_total += c;
+      }
+    }
+    bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(nb)] = run_total;
+    tmp[static_cast<std::size_t>(k)].resize(static_cast<std::size_t>(run_total));
+    ptr[k].assign(static_cast<std::size_t>(nrows) + 1, 0);
+    col[k].resize(static_cast<std::size_t>(run_total));
+  }
+  run([&](int th) {  // 2. (row, value) pairs into their buckets
+    const std::int64_t b = n_src * th / t, e = n_src * (th + 1) / t;
+    for (std::int64_t u = b; u < e; ++u)
+      emit(u, [&](int k, std::int64_t row, VertexId v) {
+        tmp[static_cast<std::size_t>(k)][static_cast<std::size_t>(cur[at(k, th, row >> kShift)]++)] =
+            (static_cast<std::uint64_t>(row) << 32) | static_cast<std::uint32_t>(v);
+      });
+  });
+  std::atomic<std::int64_t> next{0};
+  run([&](int) {  // 3. counting sort of every bucket by row
+    std::vector<std::int64_t> cnt(static_cast<std::size_t>(1) << kShift);
+    for (;;) {
+      const std::int64_t job = next.fetch_add(1);
+      if (job >= K * nb) return;
+      const int k = static_cast<int>(job / nb);
+      const std::int64_t b = job % nb, r0 = b << kShift, r1 = std::min(nrows, (b + 1) << kShift);
+      const std::int64_t s0 = bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(b)];
+      const std::int64_t s1 = bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(b) + 1];
+      if (r0 >= r1) continue;
+      std::fill(cnt.begin(), cnt.begin() + (r1 - r0), 0);
+      const std::uint64_t* src = tmp[static_cast<std::size_t>(k)].data();
+      for (std::int64_t i = s0; i < s1; ++i) ++cnt[static_cast<std::size_t>((src[i] >> 32) - static_cast<std::uint64_t>(r0))];
+      std::int64_t pos = s0;
+      for (std::int64_t r = r0; r < r1; ++r) {
+        ptr[k][static_cast<std::size_t>(r)] = pos;
+        const std::int64_t c = cnt[static_cast<std::size_t>(r - r0)];
+        cnt[static_cast<std::size_t>(r - r0)] = pos;
+        pos += c;
+      }
+      VertexId* out = col[k].data();
+      for (std::int64_t i = s0; i < s1; ++i) {
+        const std::size_t lr = static_cast<std::size_t>((src[i] >> 32) - static_cast<std::uint64_t>(r0));
+        out[cnt[lr]++] = static_cast<VertexId>(static_cast<std::uint32_t>(src[i]));
+      }
+    }
+  });
+  for (int k = 0; k < K; ++k)
+    ptr[k][static_cast<std::size_t>(nrows)] = bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(nb)];
+}
+
 }  // namespace detail
 }  // namespace b200
 }  // namespace levelrank

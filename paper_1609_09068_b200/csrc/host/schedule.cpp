@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <stdexcept>
 
@@ -12,6 +15,18 @@
 namespace levelrank {
 inline namespace b200 {
 namespace {
+
+// LR_PLAN_PROF=1: per-phase wall times of the layout build on stderr
+struct PhaseClock {
+  bool on = std::getenv("LR_PLAN_PROF") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[plan] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // Stable counting sort, descending key (schedule.cpp:14-28).
 std::vector<VertexId> stable_desc(const std::vector<VertexId>& items, const std::vector<std::int32_t>& key,
@@ -203,6 +218,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   const std::uint8_t* lp = g.loop_data();
   const auto& comp_of = p.comp_of;
 
+  PhaseClock clk;
   const auto comps = ordered_components(p, n);
   std::vector<std::int64_t> mb;
   std::vector<VertexId> mem;
@@ -210,6 +226,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   std::vector<std::vector<VertexId>> singles;
   const auto plan = plan_units(p, comps, small_threshold, L.level_unit_begin, singles, mb, mem);
   const std::size_t nu = plan.size();
+  clk.mark("components + unit plan");
   const std::int32_t nl = p.max_level + 1;
 
   // unit of every vertex, local index (= position in ascending members)
@@ -241,6 +258,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
       }
   }, 1);
 
+  clk.mark("unit_of / local_of");
   // CAC units: Kahn pass of solve_cac (solvers.cpp:43-83) to get each vertex's
   // dequeue position and its depth (longest path from the unit's sources).
   std::vector<std::int32_t> kahn_pos(nn, 0), depth(nn, 0);
@@ -296,6 +314,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   });
 
   if (cycle) throw std::logic_error("cycle inside an acyclic component");
+  clk.mark("CAC Kahn passes");
 
   // rows: units in order; CAC rows by (depth, vertex)
   L.vertex_of.resize(nn);
@@ -350,6 +369,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
       for (std::int64_t r = m0; r < m1; ++r) L.row_of[static_cast<std::size_t>(L.vertex_of[static_cast<std::size_t>(r)])] = static_cast<VertexId>(r);
     }
   });
+  clk.mark("unit out-degrees + row order");
   L.level_row_begin.assign(static_cast<std::size_t>(nl) + 1, 0);
   for (std::int32_t li = 0; li <= nl; ++li)
     L.level_row_begin[static_cast<std::size_t>(li)] = L.unit_row_begin[static_cast<std::size_t>(L.level_unit_begin[static_cast<std::size_t>(li)])];
@@ -365,8 +385,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
     }
   });
 
-  // in-degree counts: intra (pull lists), cross, per-unit reference edge counts
-  std::vector<EdgeId> icnt(nn + 1, 0), xcnt(nn + 1, 0);
+  // per-unit reference edge counts (unit.edges.size()) and totals
   std::vector<EdgeId> uedges(nu, 0);
   std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
   detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
@@ -375,26 +394,16 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
       const VertexId u = static_cast<VertexId>(uu);
       const VertexId cu = comp_of[static_cast<std::size_t>(u)];
       const std::size_t un = static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)]);
-      const bool scc = plan[un].kind == UnitKind::SccSmall || plan[un].kind == UnitKind::SccLarge;
       EdgeId ue = 0;
       for (EdgeId k = off[u]; k < off[u + 1]; ++k) {
         const VertexId v = tgt[k];
         if (v == u) {
-          if (keep) {
-            ++ue;
-            if (scc) std::atomic_ref<EdgeId>(icnt[static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)])]).fetch_add(1, std::memory_order_relaxed);
-          } else {
-            ++ld;
-          }
-          continue;
-        }
-        const std::size_t rv = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
-        if (comp_of[static_cast<std::size_t>(v)] == cu) {
+          if (keep) ++ue;
+          else ++ld;
+        } else if (comp_of[static_cast<std::size_t>(v)] == cu) {
           ++ue;
-          std::atomic_ref<EdgeId>(icnt[rv]).fetch_add(1, std::memory_order_relaxed);
         } else {
           ++lx;
-          std::atomic_ref<EdgeId>(xcnt[rv]).fetch_add(1, std::memory_order_relaxed);
         }
       }
       li += ue;
@@ -408,34 +417,34 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   L.cross_edge_count = n_cross;
   L.dropped_loop_count = n_dropped;
   L.unit_edges = std::move(uedges);
-  const EdgeId ti = detail::exclusive_scan_inplace(icnt.data(), static_cast<std::int64_t>(nn) + 1);
-  const EdgeId tx = detail::exclusive_scan_inplace(xcnt.data(), static_cast<std::int64_t>(nn) + 1);
-  L.isrc.resize(static_cast<std::size_t>(ti));
-  L.xsrc.resize(static_cast<std::size_t>(tx));
-  {
-    std::vector<EdgeId> icur(icnt.begin(), icnt.end() - 1), xcur(xcnt.begin(), xcnt.end() - 1);
-    detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-      for (std::int64_t uu = b; uu < e; ++uu) {
+  clk.mark("deg/loop + edge counts");
+  // pull lists (sources as vertex ids, source ascending): intra = CSR 0
+  // (kept self-loops only in SCC rows), cross = CSR 1
+  std::vector<EdgeId> ptrs[2];
+  std::vector<VertexId> cols[2];
+  detail::bucket_csr<2>(
+      n, n,
+      [&](std::int64_t uu, auto&& sink) {
         const VertexId u = static_cast<VertexId>(uu);
         const VertexId cu = comp_of[static_cast<std::size_t>(u)];
         const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)])].kind;
         const bool scc = k == UnitKind::SccSmall || k == UnitKind::SccLarge;
         for (EdgeId q = off[u]; q < off[u + 1]; ++q) {
           const VertexId v = tgt[q];
-          const std::size_t rv = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
+          const std::int64_t rv = L.row_of[static_cast<std::size_t>(v)];
           if (v == u) {
-            if (keep && scc)
-              L.isrc[static_cast<std::size_t>(std::atomic_ref<EdgeId>(icur[rv]).fetch_add(1, std::memory_order_relaxed))] = u;
-            continue;
+            if (keep && scc) sink(0, rv, u);
+          } else {
+            sink(comp_of[static_cast<std::size_t>(v)] == cu ? 0 : 1, rv, u);
           }
-          if (comp_of[static_cast<std::size_t>(v)] == cu)
-            L.isrc[static_cast<std::size_t>(std::atomic_ref<EdgeId>(icur[rv]).fetch_add(1, std::memory_order_relaxed))] = u;
-          else
-            L.xsrc[static_cast<std::size_t>(std::atomic_ref<EdgeId>(xcur[rv]).fetch_add(1, std::memory_order_relaxed))] = u;
         }
-      }
-    });
-  }
+      },
+      ptrs, cols);
+  std::vector<EdgeId>& icnt = ptrs[0];
+  std::vector<EdgeId>& xcnt = ptrs[1];
+  L.isrc = std::move(cols[0]);
+  L.xsrc = std::move(cols[1]);
+  clk.mark("in-edge transpose");
   // per-row ordering = the reference's accumulation order, then vertex -> row
   std::vector<std::int32_t> level_idx_of(nn);
   detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
@@ -448,10 +457,8 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
       const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(v)])].kind;
       VertexId* a = L.isrc.data() + icnt[static_cast<std::size_t>(r)];
       VertexId* ae = L.isrc.data() + icnt[static_cast<std::size_t>(r) + 1];
-      if (k == UnitKind::Cac)
+      if (k == UnitKind::Cac)  // (SCC rows are source-ascending already)
         std::sort(a, ae, [&](VertexId x, VertexId y) { return kahn_pos[static_cast<std::size_t>(x)] < kahn_pos[static_cast<std::size_t>(y)]; });
-      else
-        std::sort(a, ae);
       for (VertexId* q = a; q < ae; ++q) *q = L.row_of[static_cast<std::size_t>(*q)];
       VertexId* x = L.xsrc.data() + xcnt[static_cast<std::size_t>(r)];
       VertexId* xe = L.xsrc.data() + xcnt[static_cast<std::size_t>(r) + 1];
@@ -462,6 +469,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
       for (VertexId* q = x; q < xe; ++q) *q = L.row_of[static_cast<std::size_t>(*q)];
     }
   });
+  clk.mark("per-row sorts");
   L.iptr = std::move(icnt);
   L.xptr = std::move(xcnt);
   return L;
@@ -527,32 +535,21 @@ Layout build_baseline_layout(const Graph& g) {
     L.deg[r] = wd[static_cast<std::size_t>(v)];
     L.iptr[r + 1] = L.iptr[r] + indeg[static_cast<std::size_t>(v)].load(std::memory_order_relaxed);
   }
+  // in-edges per row, source ascending (the reference's push order)
+  std::vector<EdgeId> ptrs[1];
+  std::vector<VertexId> cols[1];
+  detail::bucket_csr<1>(
+      n, n,
+      [&](std::int64_t uu, auto&& sink) {
+        const VertexId u = static_cast<VertexId>(uu);
+        const VertexId ru = L.row_of[static_cast<std::size_t>(u)];
+        for (EdgeId k = off[u]; k < off[u + 1]; ++k)
+          if (tgt[k] != u || keep) sink(0, L.row_of[static_cast<std::size_t>(tgt[k])], ru);
+      },
+      ptrs, cols);
+  L.isrc = std::move(cols[0]);
   const EdgeId m = L.iptr[nn];
-  L.isrc.resize(static_cast<std::size_t>(m));
-  // scatter (row of the source) into each destination row, then restore the
-  // source-ascending order within every row
-  std::vector<std::atomic<std::int64_t>> cur(nn);
-  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t r = b; r < e; ++r) cur[static_cast<std::size_t>(r)].store(L.iptr[static_cast<std::size_t>(r)], std::memory_order_relaxed);
-  });
-  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t uu = b; uu < e; ++uu) {
-      const VertexId u = static_cast<VertexId>(uu);
-      const VertexId ru = L.row_of[static_cast<std::size_t>(u)];
-      for (EdgeId k = off[u]; k < off[u + 1]; ++k) {
-        if (tgt[k] == u && !keep) continue;
-        const std::size_t rv = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(tgt[k])]);
-        L.isrc[static_cast<std::size_t>(cur[rv].fetch_add(1, std::memory_order_relaxed))] = ru;
-      }
-    }
-  });
-  detail::parallel_dynamic(n, 4096, [&](std::int64_t b, std::int64_t e) {
-    for (std::int64_t r = b; r < e; ++r)
-      std::sort(L.isrc.begin() + L.iptr[static_cast<std::size_t>(r)], L.isrc.begin() + L.iptr[static_cast<std::size_t>(r) + 1],
-                [&](VertexId x, VertexId y) {
-                  return L.vertex_of[static_cast<std::size_t>(x)] < L.vertex_of[static_cast<std::size_t>(y)];
-                });
-  });
+  if (ptrs[0][nn] != m) throw std::logic_error("baseline layout: in-edge count mismatch");
   L.unit_edges = {m};
   L.intra_edge_count = m;
   L.cross_edge_count = 0;
