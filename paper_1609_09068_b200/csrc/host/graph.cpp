@@ -57,23 +57,13 @@ Graph Graph::from_edge_arrays(VertexId n, const VertexId* src, const VertexId* d
   if (bad) throw std::invalid_argument("edge endpoint out of range");
 
   const std::size_t nn = static_cast<std::size_t>(n);
-  std::vector<EdgeId> off(nn + 1, 0);
-  detail::parallel_chunks(m, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t i = b; i < e; ++i)
-      std::atomic_ref<EdgeId>(off[static_cast<std::size_t>(src[i])]).fetch_add(1, std::memory_order_relaxed);
-  });
-  detail::exclusive_scan_inplace(off.data(), static_cast<std::int64_t>(nn) + 1);
-  std::vector<VertexId> tmp(static_cast<std::size_t>(m));
-  {
-    std::vector<EdgeId> cur(off.begin(), off.end() - 1);
-    detail::parallel_chunks(m, [&](int, std::int64_t b, std::int64_t e) {
-      for (std::int64_t i = b; i < e; ++i) {
-        const EdgeId at = std::atomic_ref<EdgeId>(cur[static_cast<std::size_t>(src[i])])
-                              .fetch_add(1, std::memory_order_relaxed);
-        tmp[static_cast<std::size_t>(at)] = dst[i];
-      }
-    });
-  }
+  // rows by source: atomic-free stable bucketed transpose of the edge list
+  std::vector<EdgeId> offs[1];
+  std::vector<VertexId> cols[1];
+  detail::bucket_csr<1>(
+      m, n, [&](std::int64_t i, auto&& sink) { sink(0, src[i], dst[i]); }, offs, cols);
+  std::vector<EdgeId> off = std::move(offs[0]);
+  std::vector<VertexId> tmp = std::move(cols[0]);
   std::vector<EdgeId> deg(nn + 1, 0);
   detail::parallel_dynamic(n, 4096, [&](std::int64_t b, std::int64_t e) {
     for (std::int64_t u = b; u < e; ++u) {
