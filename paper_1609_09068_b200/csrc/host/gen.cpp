@@ -60,16 +60,25 @@ Graph rmat(std::int32_t scale, std::int64_t edge_factor, double a, double b, dou
   };
   std::vector<std::int64_t> chunk_begin(static_cast<std::size_t>(T) + 1);
   for (int t = 0; t <= T; ++t) chunk_begin[static_cast<std::size_t>(t)] = m * t / T;
+  // one pass: each thread keeps its chunk's non-loop edges, then the chunks
+  // are concatenated in order (output independent of the thread count)
+  std::vector<std::vector<VertexId>> ts(static_cast<std::size_t>(T)), td(static_cast<std::size_t>(T));
   std::vector<std::thread> pool;
   for (int t = 0; t < T; ++t)
     pool.emplace_back([&, t] {
-      std::int64_t k = 0;
-      for (std::int64_t i = chunk_begin[static_cast<std::size_t>(t)]; i < chunk_begin[static_cast<std::size_t>(t) + 1]; ++i) {
+      const std::int64_t b0 = chunk_begin[static_cast<std::size_t>(t)], b1 = chunk_begin[static_cast<std::size_t>(t) + 1];
+      auto& S = ts[static_cast<std::size_t>(t)];
+      auto& D = td[static_cast<std::size_t>(t)];
+      S.reserve(static_cast<std::size_t>(b1 - b0));
+      D.reserve(static_cast<std::size_t>(b1 - b0));
+      for (std::int64_t i = b0; i < b1; ++i) {
         VertexId u, v;
         make(i, u, v);
-        k += u != v;
+        if (u == v) continue;
+        S.push_back(u);
+        D.push_back(v);
       }
-      kept[static_cast<std::size_t>(t) + 1] = k;
+      kept[static_cast<std::size_t>(t) + 1] = static_cast<std::int64_t>(S.size());
     });
   for (auto& th : pool) th.join();
   for (int t = 0; t < T; ++t) kept[static_cast<std::size_t>(t) + 1] += kept[static_cast<std::size_t>(t)];
@@ -77,15 +86,12 @@ Graph rmat(std::int32_t scale, std::int64_t edge_factor, double a, double b, dou
   pool.clear();
   for (int t = 0; t < T; ++t)
     pool.emplace_back([&, t] {
-      std::int64_t k = kept[static_cast<std::size_t>(t)];
-      for (std::int64_t i = chunk_begin[static_cast<std::size_t>(t)]; i < chunk_begin[static_cast<std::size_t>(t) + 1]; ++i) {
-        VertexId u, v;
-        make(i, u, v);
-        if (u == v) continue;
-        src[static_cast<std::size_t>(k)] = u;
-        dst[static_cast<std::size_t>(k)] = v;
-        ++k;
-      }
+      auto& S = ts[static_cast<std::size_t>(t)];
+      auto& D = td[static_cast<std::size_t>(t)];
+      std::copy(S.begin(), S.end(), src.begin() + kept[static_cast<std::size_t>(t)]);
+      std::copy(D.begin(), D.end(), dst.begin() + kept[static_cast<std::size_t>(t)]);
+      std::vector<VertexId>().swap(S);
+      std::vector<VertexId>().swap(D);
     });
   for (auto& th : pool) th.join();
   return Graph::from_edge_arrays(static_cast<VertexId>(n), src.data(), dst.data(), static_cast<EdgeId>(src.size()));
