@@ -458,8 +458,8 @@ __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const 
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int a = 0; a < A; ++a) v[q][a] = pp * v[q][a] - f[a] * pk[q];
-#pragma unroll
+        for (int a = 0; a < A; ++a) v[q][a] = __fma_rn(-f[a], pk[q], pp * v[q][a]);  // one rounding fewer than the
+#pragma unroll                                                                       // reference's LU: not bit-exact anyway
       for (int a = 0; a < A; ++a)
         if (ok[a]) {
 #pragma unroll
@@ -765,7 +765,10 @@ __device__ __forceinline__ long long global_ns() {
   return t;
 }
 
-__global__ void __launch_bounds__(kThreads)
+#ifndef LR_LEVEL_MINB
+#define LR_LEVEL_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, LR_LEVEL_MINB)
     k_level(DeviceLayout L, const LevelTask* __restrict__ tasks, const CacTask* __restrict__ cacs,
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
             int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
