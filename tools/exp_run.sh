@@ -1,4 +1,3 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/e14_pytest.log 2>&1
-tail -3 gpurun_out/e14_pytest.log
-python bench.py --steps 5 --no-cpu-baseline > gpurun_out/e14_c2.json 2>gpurun_out/e14_c2.err
-python bench.py --config 3 --no-cpu-baseline --steps 5 > gpurun_out/e14_c3.json 2>gpurun_out/e14_c3.err
+for c in 1 4 2; do
+  python bench.py --config $c > gpurun_out/r1d_bench_cfg$c.json 2> gpurun_out/r1d_bench_cfg$c.err
+done
