@@ -90,13 +90,13 @@ T exclusive_scan_inplace(T* v, std::int64_t n) {
 // emit(u, sink) is called for every source u in [0, n_src) -- twice, with the
 // same calls both times -- and calls sink(k, row, value) for each entry of
 // CSR k.  Sources are split into contiguous ascending chunks, one per thread;
-// entries go to row buckets of 2^14 rows (per-thread cursors, sequential
+// entries go to row buckets of 2^16 rows (per-thread cursors, sequential
 // writes), then each bucket is counting-sorted by row.  Every row's values end
 // up in emission order: source ascending, then the order emit produced them.
 template <int K, typename Emit>
 void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, std::vector<std::int64_t>* ptr,
                 std::vector<VertexId>* col) {
-  constexpr int kShift = 14;
+  constexpr int kShift = 16;
   const std::int64_t nb = (nrows >> kShift) + 1;
   const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n_src / 4096) + 1));
   auto at = [&](int k, int th, std::int64_t b) {

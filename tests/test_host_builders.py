@@ -1,4 +1,4 @@
-"""Host builders at sizes that cross the bucketed transpose's 2^14-row buckets
+"""Host builders at sizes that cross the bucketed transpose's 2^16-row buckets
 (parallel.hpp bucket_csr): Graph::from_edges (proj/src/graph.cpp:14-36
 semantics: sorted, deduplicated rows, loop flags) and the whole-graph baseline
 layout, checked against numpy restatements."""
@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 
-@pytest.mark.parametrize("n,m,seed", [(40000, 250000, 1), (70001, 600000, 2), (16384, 100000, 3)])
+@pytest.mark.parametrize("n,m,seed", [(40000, 250000, 1), (140001, 900000, 2), (65536, 300000, 3)])
 def test_from_edges_csr_matches_numpy(lr, n, m, seed):
     rng = np.random.default_rng(seed)
     src = rng.integers(0, n, m, dtype=np.int64).astype(np.int32)
@@ -23,7 +23,7 @@ def test_from_edges_csr_matches_numpy(lr, n, m, seed):
 @pytest.mark.parametrize("keep", [False, True])
 def test_baseline_layout_large(lr, keep):
     rng = np.random.default_rng(11 + keep)
-    n, m = 50000, 300000
+    n, m = 150000, 600000
     src = rng.integers(0, n, m).astype(np.int32)
     dst = (src + rng.integers(0, 3000, m)).astype(np.int64) % n  # some locality, some self-loops
     g = lr.Graph.from_edges(n, src=src, dst=dst.astype(np.int32), loop_policy=int(keep))
