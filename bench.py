@@ -249,6 +249,18 @@ def run_ours(args):
     edges = layout["unit_edges"]
     large = kinds == 3
     work = int((iters[large] * edges[large]).sum() + edges[~large].sum() + len(layout["xsrc"]))
+    # in-edges of the largest grid unit served by K4c's shared-memory head
+    # (spmv.cu: 16k head rows while the unit's pushed vector is <= 48 MB, else 8k)
+    head_share = None
+    if large.any():
+        u = int(np.argmax(np.where(large, edges, -1)))
+        r0, r1 = int(layout["unit_row_begin"][u]), int(layout["unit_row_begin"][u + 1])
+        nhead = min(16384 if (r1 - r0) * 8 <= (48 << 20) else 8192, r1 - r0)
+        ip = layout["iptr"]
+        cols = layout["isrc"][ip[r0]:ip[r1]]
+        head_share = float(np.count_nonzero(cols < r0 + nhead)) / max(1, len(cols))
+    n_levels, n_units = int(layout["n_levels"]), int(layout["n_units"])
+    del layout
 
     def dev_step():
         return eng.solve_ptr(w_dev.data_ptr(), r3_dev.data_ptr(), r1_dev.data_ptr(), host=False, params=params)
@@ -331,6 +343,14 @@ def run_ours(args):
                 "avg_launch_ms": (inf["spmv_active_ms"] / inf["spmv_active_launches"])
                 if inf["spmv_active_launches"] else None,
                 "spmv_share_of_step": inf["spmv_active_ms"] / ms if ms > 0 else None}
+    # the bound that applies (profiles/r01_gather_ceiling.md): every in-edge not
+    # served by the shared-memory head is one random 8-byte gather = one L2 sector
+    if achieved and head_share is not None and inf["spmv_edges"]:
+        g_per_s = inf["spmv_edges"] * (1.0 - head_share) / (inf["spmv_active_ms"] / 1e3)
+        roofline["gathers"] = {"head_share_of_in_edges": head_share, "global_gathers_per_s": g_per_s,
+                               "ceiling_l2_resident_per_s": 195e9, "ceiling_171MB_uniform_per_s": 86e9,
+                               "frac_of_l2_resident_ceiling": g_per_s / 195e9,
+                               "source": "tools/gather_bench.cu, profiles/r01_gather_ceiling.md"}
 
     # ablation on the same GPU: the reference's partition-free whole-graph power
     # series (compute_baseline, lr_plan_build_baseline) over the same graph
@@ -373,7 +393,7 @@ def run_ours(args):
                        "vertices": n, "edges": g.m, "edge_updates_per_step": work,
                        "iterative_edge_work": int(info0["iterative_edge_work"]),
                        "large_scc_iterations": int(iters[large].max()) if large.any() else 0,
-                       "levels": int(layout["n_levels"]), "units": int(layout["n_units"]),
+                       "levels": n_levels, "units": n_units,
                        "l2": "flushed (512 MB write) before every timed step",
                        "parallelism": (f"giant-SCC rows sharded over {world} GPUs (NCCL exchange per iteration), "
                                        "other units replicated") if world > 1 else "1 GPU",
