@@ -159,6 +159,8 @@ struct lr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t side = nullptr;  // large CACs, concurrent with each level's k_level
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int n = 0;
   int n_levels = 0;
   int64_t n_units = 0;
@@ -222,6 +224,9 @@ struct lr_ctx {
       if (e) cudaEventDestroy(e);
     for (auto& e : lev)
       if (e) cudaEventDestroy(e);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
     if (h_params) cudaFreeHost(h_params);
     if (h_status) cudaFreeHost(h_status);
@@ -276,6 +281,12 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
       lrerr::set("cudaEventCreate failed");
       return fail(LR_ECUDA);
     }
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+    lrerr::set("CUDA side stream creation failed");
+    return fail(LR_ECUDA);
+  }
   if (cudaMallocHost(&ctx->h_params, sizeof(SolveParams)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_status, sizeof(DevStatus)) != cudaSuccess ||
       ctx->params.alloc(1) != cudaSuccess || ctx->status.alloc(1) != cudaSuccess) {
@@ -392,8 +403,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             ctx->cac_slices.push_back(CacSlice{r0, r1, h0, static_cast<int>(xheavy.size())});
           }
         } else {
+          // (large CACs gather their own start weights in k_cac_big)
           (m > kCacMidMaxRows ? lb : m > kCacWarpMaxRows ? lm : lw).push_back(CacTask{rb, re, db, nd, 0});
-          if (m > kCacMidMaxRows) rowranges[static_cast<size_t>(li)].emplace_back(rb, re);  // start weights
         }
       } else if (kind == 2) {
         rk = kSmall;
@@ -712,6 +723,18 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
                          ctx->s0.p, ctx->xparts.p, ctx->xcnts.p, s);
       ++launches;
     }
+    // large CACs (start weights + depth sweep, 1024-thread CTAs) on the side
+    // stream, concurrently with the level's k_level: units of one level are
+    // independent, both only read ranks of the levels above
+    const bool fork = T.cac_b1 > T.cac_b0;
+    if (fork) {
+      LR_CUDA_TRY(cudaEventRecord(ctx->fork_ev, s));
+      LR_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+      launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
+                     ctx->rank.p, ctx->s0.p, T.big_smem, ctx->side);
+      LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));
+      ++launches;
+    }
     // everything that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
     if (T.lt1 > T.lt0) {
       launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
@@ -744,12 +767,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
         prof_crit[arg] += mx[arg];
       }
     }
-    // large CACs: depth sweep in 1024-thread CTAs (start weights came from k_level)
-    if (T.cac_b1 > T.cac_b0) {
-      launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
-                     ctx->rank.p, ctx->s0.p, T.big_smem, s);
-      ++launches;
-    }
+    if (fork) LR_CUDA_TRY(cudaStreamWaitEvent(s, ctx->join_ev, 0));
     if (T.sb1 > T.sb0) {
       launch_small(L, ctx->small_big.p + T.sb0, T.sb1 - T.sb0, ctx->small_scratch_ld - 1, ctx->pf.p, ctx->rank.p,
                    ctx->small_scratch.p, ctx->status.p, s);

@@ -843,10 +843,10 @@ __global__ void __launch_bounds__(kThreads, LR_LEVEL_MINB)
   }
 }
 
-// Large CACs (kCacMidMaxRows < rows <= kCacBlockMaxRows): their start weights
-// come from k_level's row tasks (spread over many CTAs); this kernel, launched
-// right after, runs the depth sweep with one 1024-thread CTA per CAC -- the
-// per-level critical path of deep DAGs.
+// Large CACs (kCacMidMaxRows < rows <= kCacBlockMaxRows): one 1024-thread CTA
+// per CAC gathers its rows' start weights and runs the depth sweep, on a side
+// stream concurrently with the level's k_level (config 4: one such CAC per
+// level, ~20 us, formerly serialised after k_level).
 constexpr int kBigThreads = 1024;
 
 __global__ void __launch_bounds__(kBigThreads)
@@ -855,6 +855,11 @@ __global__ void __launch_bounds__(kBigThreads)
               double* rank, double* s0, size_t smem_bytes) {
   extern __shared__ double sm[];
   const CacTask ct = cacs[blockIdx.x];
+  // the CAC's own start weights (rows above kCrossSplit cross in-edges were
+  // done by k_pull_heavy before the level), so the launch runs concurrently
+  // with the level's k_level on a side stream
+  cross_rows(L, ct.row_begin, ct.row_end, w, p->c, pf, rank, s0, threadIdx.x, kBigThreads);
+  __syncthreads();
   if (cac_stage_bytes(ct.row_end - ct.row_begin, L.iptr[ct.row_end] - L.iptr[ct.row_begin]) <= smem_bytes)
     cac_sweep_staged<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads, sm);
   else
