@@ -159,6 +159,21 @@ struct lr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // runs of levels without grid SpMV units, captured once into CUDA graphs and
+  // replayed every solve (their launches depend on nothing the host decides)
+  struct Segment {
+    int begin, end;          // levels [begin, end)
+    int64_t launches;        // kernel launches inside
+    cudaGraphExec_t exec;
+  };
+  std::vector<Segment> segs;
+  bool segs_built = false;
+  void drop_graphs() {
+    for (auto& g : segs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    segs.clear();
+    segs_built = false;
+  }
   cudaStream_t side = nullptr;  // large CACs, concurrent with each level's k_level
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int n = 0;
@@ -220,6 +235,7 @@ struct lr_ctx {
   }
   ~lr_ctx() {
     if (device >= 0) cudaSetDevice(device);
+    drop_graphs();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : lev)
@@ -281,7 +297,12 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
       lrerr::set("cudaEventCreate failed");
       return fail(LR_ECUDA);
     }
-  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+  // the side stream outranks the main one, so a large CAC's 1024-thread CTA is
+  // placed before the level's many k_level CTAs fill the SMs (otherwise it
+  // waits for them and the level is serialised again)
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
     lrerr::set("CUDA side stream creation failed");
@@ -321,6 +342,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   cudaStream_t s = ctx->stream;
   const int n = L->n;
   ctx->loaded = false;
+  ctx->drop_graphs();
   ctx->n = n;
   ctx->n_levels = L->n_levels;
   ctx->n_units = L->n_units;
@@ -714,14 +736,25 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     LR_CUDA_TRY(prof_buf.alloc(static_cast<size_t>(3 * most)));
     LR_CUDA_TRY(set_level_prof(prof_buf.p));
   }
+  // graph replays read the weights from ctx->w (a fixed address)
+  const bool use_graphs = !prof_on && [] {
+    const char* e = std::getenv("LR_GRAPHS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (use_graphs && w_dev != ctx->w.p && ctx->n > 0) {
+    LR_CUDA_TRY(cudaMemcpyAsync(ctx->w.p, w_dev, static_cast<size_t>(ctx->n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    w_dev = ctx->w.p;
+  }
   launch_prep(L, w_dev, ctx->params.p, ctx->pf.p, ctx->status.p, s);
   ++launches;
-  for (const LevelTasks& T : ctx->lt) {
+  // everything of one level that the host does not steer: enqueued directly, or
+  // captured into a segment graph
+  auto static_level = [&](const LevelTasks& T, int64_t& nl) -> lr_status {
     // K1 for rows with more than kCrossSplit cross in-edges (split over warps)
     if (T.xh1 > T.xh0) {
       launch_cross_heavy(L, ctx->xheavy.p + T.xh0, T.xh1 - T.xh0, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p,
                          ctx->s0.p, ctx->xparts.p, ctx->xcnts.p, s);
-      ++launches;
+      ++nl;
     }
     // large CACs (start weights + depth sweep, 1024-thread CTAs) on the side
     // stream, concurrently with the level's k_level: units of one level are
@@ -733,14 +766,14 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
                      ctx->rank.p, ctx->s0.p, T.big_smem, ctx->side);
       LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));
-      ++launches;
+      ++nl;
     }
     // everything that fits a CTA: K1 + singletons + CACs + small SCCs + CTA-sized large SCCs
     if (T.lt1 > T.lt0) {
       launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
                    ctx->unit_iters.p, ctx->status.p, s);
-      ++launches;
+      ++nl;
       if (prof_on) {  // LR_LEVEL_PROF: per task type, the longest CTA of this level
         const int nt = T.lt1 - T.lt0;
         std::vector<long long> h(static_cast<size_t>(3 * nt));
@@ -771,18 +804,55 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     if (T.sb1 > T.sb0) {
       launch_small(L, ctx->small_big.p + T.sb0, T.sb1 - T.sb0, ctx->small_scratch_ld - 1, ctx->pf.p, ctx->rank.p,
                    ctx->small_scratch.p, ctx->status.p, s);
-      ++launches;
+      ++nl;
     }
     for (int i = T.sl0; i < T.sl1; ++i) {
       const CacSlice& sl = ctx->cac_slices[static_cast<size_t>(i)];
       launch_cac_slice(L, sl.r0, sl.r1, ctx->params.p, ctx->rank.p, s);
-      ++launches;
+      ++nl;
       if (sl.h1 > sl.h0) {
         launch_cac_heavy(L, ctx->xheavy.p + sl.h0, sl.h1 - sl.h0, ctx->params.p, ctx->rank.p, ctx->xparts.p,
                          ctx->xcnts.p, s);
-        ++launches;
+        ++nl;
       }
     }
+    return LR_OK;
+  };
+  if (use_graphs && !ctx->segs_built) {
+    for (size_t li = 0; li < ctx->lt.size();) {
+      if (ctx->lt[li].gu1 > ctx->lt[li].gu0) {
+        ++li;
+        continue;
+      }
+      size_t lj = li;
+      while (lj < ctx->lt.size() && ctx->lt[lj].gu1 == ctx->lt[lj].gu0) ++lj;
+      lr_ctx::Segment seg{static_cast<int>(li), static_cast<int>(lj), 0, nullptr};
+      LR_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      lr_status cst = LR_OK;
+      for (size_t q = li; q < lj && cst == LR_OK; ++q) cst = static_level(ctx->lt[q], seg.launches);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (cst != LR_OK) return cst;
+      LR_CUDA_TRY(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&seg.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      LR_CUDA_TRY(ie);
+      ctx->segs.push_back(seg);
+      li = lj;
+    }
+    ctx->segs_built = true;
+  }
+  size_t next_seg = 0;
+  for (size_t li = 0; li < ctx->lt.size(); ++li) {
+    if (use_graphs && next_seg < ctx->segs.size() && static_cast<size_t>(ctx->segs[next_seg].begin) == li) {
+      const lr_ctx::Segment& seg = ctx->segs[next_seg++];
+      LR_CUDA_TRY(cudaGraphLaunch(seg.exec, s));
+      launches += seg.launches;
+      li = static_cast<size_t>(seg.end) - 1;
+      continue;
+    }
+    const LevelTasks& T = ctx->lt[li];
+    if (const lr_status ls = static_level(T, launches); ls != LR_OK) return ls;
     if (T.gu1 > T.gu0) {
       launch_grid_reset(ctx->gstate.p + T.gu0, T.gu1 - T.gu0, ctx->status.p, s);
       ++launches;
@@ -929,6 +999,7 @@ lr_status lr_solve(lr_ctx* ctx, const double* w, double c, double tol, double* r
   LR_CUDA_TRY(cudaSetDevice(ctx->device));
   const size_t bytes = static_cast<size_t>(ctx->n) * sizeof(double);
   if (bytes) LR_CUDA_TRY(cudaMemcpyAsync(ctx->w.p, w, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (std::getenv("LR_PROBE_SYNC")) LR_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   const lr_status st = solve_on_device(ctx, ctx->w.p, c, tol, ctx->r3.p, ctx->r1.p, info, unit_iters);
   if (st != LR_OK && st != LR_ENOCONV && st != LR_EDEGEN) return st;
   if (bytes) {

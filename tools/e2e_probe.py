@@ -37,6 +37,7 @@ def wall(f, reps=5):
 
 print("device solve (wall)", wall(lambda: eng.solve_ptr(wd.data_ptr(), r3d.data_ptr(), r1d.data_ptr(), False, p)))
 print("host solve r3+r1 (wall)", wall(lambda: eng.solve_ptr(wh.data_ptr(), r3h.data_ptr(), r1h.data_ptr(), True, p)))
+print("host solve device_ms", eng.solve_ptr(wh.data_ptr(), r3h.data_ptr(), r1h.data_ptr(), True, p)["device_ms"])
 print("host solve r3 only (wall)", wall(lambda: eng.solve_ptr(wh.data_ptr(), r3h.data_ptr(), 0, True, p)))
 print("H2D w", wall(lambda: wd.copy_(wh, non_blocking=True)))
 print("D2H r3", wall(lambda: r3h.copy_(r3d, non_blocking=True)))
