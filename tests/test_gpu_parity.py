@@ -82,3 +82,34 @@ def test_engine_reuse_and_zero_weights(lr):
         w = np.ones(g.n)
         w[3] = -1
         eng.solve(w, lr.SolverParams(0.85, 1e-9))
+
+
+def test_graph_replay_with_new_weights_and_params(lr, oracle):
+    """Runs of static levels are CUDA-graph replays (ctx.cu segments): each solve
+    must see its own weights and parameters, through host and device buffers,
+    and agree bit for bit with the directly enqueued level loop (LR_GRAPHS=0)."""
+    import os
+    import torch
+    g = lr.config_graph(4, 6)  # deep DAG: every level static
+    off, tgt, _, _ = g.csr()
+    go = oracle.graph_from_csr(g.n, off, tgt)
+    eng = lr.Engine(g)
+    rng = np.random.default_rng(5)
+    for trial, c in enumerate((0.85, 0.5, 0.85)):
+        w = rng.uniform(0.1, 2.0, g.n)
+        ref = go.compute_pagerank(w, c, 1e-12, 100)
+        r3, r1, _, it = eng.solve(w, lr.SolverParams(c, 1e-12))
+        assert np.array_equal(it, ref.unit_iters), trial
+        assert np.max(np.abs(r3 - ref.ranks) / ref.ranks) <= 1e-10, trial
+        # device buffers (copied into the context's weight buffer for the replay)
+        wd = torch.tensor(w, dtype=torch.float64, device="cuda")
+        r3d = torch.empty_like(wd)
+        r1d = torch.empty_like(wd)
+        eng.solve_ptr(wd.data_ptr(), r3d.data_ptr(), r1d.data_ptr(), host=False, params=lr.SolverParams(c, 1e-12))
+        assert np.array_equal(r3d.cpu().numpy(), r3), trial
+        os.environ["LR_GRAPHS"] = "0"
+        try:
+            r3n, r1n, _, _ = eng.solve(w, lr.SolverParams(c, 1e-12))
+        finally:
+            os.environ.pop("LR_GRAPHS", None)
+        assert np.array_equal(r3n, r3) and np.array_equal(r1n, r1), trial
