@@ -383,6 +383,9 @@ __device__ void small_solve(const DeviceLayout& L, const SccTask& t, int ld, con
 #ifdef LR_TILE_PROBE
 __device__ long long* g_tile_probe;
 #endif
+#ifndef LR_SMALL_PAIR
+#define LR_SMALL_PAIR 1
+#endif
 template <int A>
 __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const double* __restrict__ pf,
                                  double* rank, double* sm, unsigned long long* red, DevStatus* st) {
@@ -429,7 +432,79 @@ __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const 
     row[a] = M + static_cast<size_t>(valid[a] ? i : 0) * ld;
   }
   double rprev = 1.0;  // 1 / p_{k-1}
-  for (int k = 0; k < m; ++k) {
+  int k0 = 0;
+#if LR_SMALL_PAIR
+  // Two pivots per pass (the shared-memory port is the bound: one load and one
+  // store per trailing entry per pass instead of per pivot).  Phase A updates
+  // only row k+1 (columns > k) and column k+1 (rows other than k, k+1) with
+  // pivot k, one entry per thread; phase B applies both pivots to every other
+  // entry right of column k+1 in registers:
+  //   i != k:  (pp1 (pp0 v - f0 T[k][j]) - f1 T'[k+1][j])
+  //   i == k:  pp1 v - f1 T[k][j]... (row k is pivot k's row: only pivot k+1 acts)
+  // with the same fraction-free scaling as the single step below.
+  for (; k0 + 1 < m; k0 += 2) {
+    const int k = k0;
+    __syncthreads();
+    const double* pr0 = M + static_cast<size_t>(k) * ld;
+    double* pr1 = M + static_cast<size_t>(k + 1) * ld;
+    const double p0 = pr0[k];
+    const double pp0 = p0 * rprev;
+    double r1;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r1) : "d"(p0));
+    {  // phase A
+      const int j = k + 1 + tid;
+      if (j <= m) pr1[j] = __fma_rn(-(pr1[k] * rprev), pr0[j], pp0 * pr1[j]);
+      if (tid < m && tid != k && tid != k + 1) {
+        double* Ti = M + static_cast<size_t>(tid) * ld;
+        Ti[k + 1] = __fma_rn(-(Ti[k] * rprev), pr0[k + 1], pp0 * Ti[k + 1]);
+      }
+    }
+    __syncthreads();
+    const double p1 = pr1[k + 1];
+    const double pp1 = p1 * r1;
+    double f0[A], f1[A];
+    bool ok[A], isk[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int i = lane + 32 * a;
+      f0[a] = row[a][k] * rprev;
+      f1[a] = row[a][k + 1] * r1;
+      isk[a] = i == k;
+      ok[a] = valid[a] && i != k + 1;
+    }
+    for (int j = warp + ((k + 9 - warp) & ~7); j <= m; j += 32) {
+      double pa[4], pb[4], v[4][A];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pa[q] = pr0[j + 8 * q];
+        pb[q] = pr1[j + 8 * q];
+#pragma unroll
+        for (int a = 0; a < A; ++a) v[q][a] = row[a][j + 8 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+          const double u = isk[a] ? v[q][a] : __fma_rn(-f0[a], pa[q], pp0 * v[q][a]);
+          v[q][a] = __fma_rn(-f1[a], pb[q], pp1 * u);
+        }
+#pragma unroll
+      for (int a = 0; a < A; ++a)
+        if (ok[a]) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) row[a][j + 8 * q] = v[q][a];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < A; ++a) {  // finished rows: the diagonal follows the row scales
+      const int i = lane + 32 * a;
+      if (diag[a] && i < k) row[a][i] *= pp0 * pp1;
+      if (diag[a] && i == k) row[a][i] *= pp1;
+    }
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rprev) : "d"(p1));
+  }
+#endif
+  for (int k = k0; k < m; ++k) {
     __syncthreads();
 #ifdef LR_TILE_PROBE  // tools/small_bench.cu: per-step cycle stamps of warp 0
     if (threadIdx.x == 0) g_tile_probe[blockIdx.x * 160 + k] = clock64();
@@ -871,7 +946,24 @@ __global__ void __launch_bounds__(kBigThreads)
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
                     const SolveParams* p, const double* pf, double* rank, double* s0, size_t smem, cudaStream_t s) {
   if (n == 0) return;
-  k_cac_big<<<n, kBigThreads, smem, s>>>(L, cacs, depth_ptr, w, p, pf, rank, s0, smem);
+  // highest launch priority (kept by graph capture): its 1024-thread CTAs need a
+  // whole SM and must be placed before the level's k_level CTAs fill them
+  static const int prio = [] {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    return hi;
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(n));
+  cfg.blockDim = dim3(kBigThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = prio;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, smem);
 }
 
 size_t cac_stage_need(long long rows, long long edges) { return cac_stage_bytes(rows, edges); }
