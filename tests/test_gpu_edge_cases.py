@@ -105,7 +105,13 @@ def _scc(rng, base, m, deg=4):
 
 
 @pytest.mark.parametrize("m,th,c", [
+    (2, 100, 0.85),      # one pivot pair
+    (3, 100, 0.85),      # a pair, then a single step
+    (33, 100, 0.5),      # A = 2 tile, odd: pairs then a single step
+    (64, 100, 0.85),     # A = 2 tile, 32 pivot pairs
     (60, 100, 0.85),     # register-tile Bareiss Gauss-Jordan
+    (127, 200, 0.85),    # tile, A = 4, odd
+    (128, 200, 0.99),    # tile, A = 4, largest
     (120, 200, 0.85),    # tile, A = 4
     (150, 200, 0.85),    # normalised shared-memory Gauss-Jordan (m > kSmallTileMaxM)
     (220, 300, 0.85),    # global-scratch path (m > kSmallSmemMaxM)
