@@ -437,8 +437,20 @@ def propagate_weights(src, dst, src_out_degree, ranks, c, weights, device=0):
     return w
 
 
+def _nccl_first():
+    """The library dlopens "libnccl.so.2" on first NCCL use.  In a process that
+    also uses torch, torch's bundled NCCL must be the one loaded under that
+    soname (a system copy loaded first would leave torch's own symbols
+    unresolved), so torch is imported before the library's first NCCL call."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:  # no torch: the library binds the system libnccl
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """A fresh 128-byte NCCL id (rank 0 creates it and broadcasts it)."""
+    _nccl_first()
     buf = C.create_string_buffer(128)
     _check(lib().lr_nccl_unique_id(buf))
     return buf.raw
@@ -479,6 +491,7 @@ class Engine:
         _check(lib().lr_ctx_create(int(device), C.byref(h)))
         self._h = h
         if world > 1 or nccl_id is not None:
+            _nccl_first()
             _check(lib().lr_ctx_set_comm(h, int(rank), int(world), nccl_id))
         self._layout = _Layout()
         _check(lib().lr_plan_layout(self.plan._h, C.byref(self._layout)))

@@ -614,10 +614,12 @@ __device__ __forceinline__ unsigned long long block_max_bits(unsigned long long 
   const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? static_cast<unsigned>(v) : 0u);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = (static_cast<unsigned long long>(mh) << 32) | ml;
   __syncthreads();
-  unsigned long long m = red[0];
-#pragma unroll
-  for (int i = 1; i < kWarpsPer; ++i) m = max(m, red[i]);
-  return m;
+  // every warp reduces the per-warp maxima again: one load and two redux per lane
+  const int lane = threadIdx.x & 31;
+  const unsigned long long w = lane < kWarpsPer ? red[lane] : 0ull;
+  const unsigned h2 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(w >> 32));
+  const unsigned l2 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(w >> 32) == h2 ? static_cast<unsigned>(w) : 0u);
+  return (static_cast<unsigned long long>(h2) << 32) | l2;
 }
 
 // The whole power series of one SccLarge unit in one CTA (solve_large_scc,
