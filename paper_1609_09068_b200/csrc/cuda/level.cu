@@ -659,11 +659,86 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
 #ifdef LR_LCTA_PROBE  // tools/build_variant.sh probe: thread 0's cycles in the row phase / the stop test
   long long cyc_rows = 0, cyc_max = 0, cyc_t0 = 0, cyc_t1 = 0;
 #endif
+  // Units of up to 2 kThreads rows (one pass of the row loop): each thread's
+  // two rows keep their loop invariants in registers across iterations -- edge
+  // range, the first four in-edge offsets, pf and the rank accumulator -- so an
+  // iteration's chain is the gathers of sc, the adds and the stores of sn.
+  const bool reg_rows = m <= 2 * kThreads;
+  const int ri0 = threadIdx.x, ri1 = threadIdx.x + kThreads;
+  int ra0 = 0, rna = 0, rb0 = 0, rnb = 0;
+  int ria[4] = {0, 0, 0, 0}, rib[4] = {0, 0, 0, 0};
+  double rpl0 = 0.0, rpl1 = 0.0, rrk0 = 0.0, rrk1 = 0.0;
+  bool rl0 = false, rl1 = false;
+  if (reg_rows) {
+    if (ri0 < m) {
+      ra0 = rp[ri0];
+      const int d = rp[ri0 + 1] - ra0;
+      rl0 = d <= kCrossLight;
+      rna = rl0 ? d : 0;
+      rpl0 = pl[ri0];
+      rrk0 = rk[ri0];
+    }
+    if (ri1 < m) {
+      rb0 = rp[ri1];
+      const int d = rp[ri1 + 1] - rb0;
+      rl1 = d <= kCrossLight;
+      rnb = rl1 ? d : 0;
+      rpl1 = pl[ri1];
+      rrk1 = rk[ri1];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ria[q] = q < rna ? es[ra0 + q] : 0;
+      rib[q] = q < rnb ? es[rb0 + q] : 0;
+    }
+  }
   for (;;) {
 #ifdef LR_LCTA_PROBE
     cyc_t0 = clock64();
 #endif
     unsigned long long lmax = 0ull;
+    if (reg_rows) {
+      double va[4], vb[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        va[q] = sc[ria[q]];
+        vb[q] = sc[rib[q]];
+      }
+      double ya = 0.0, yb = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q < rna) ya += va[q];
+        if (q < rnb) yb += vb[q];
+      }
+      for (int g = 4; g < rna || g < rnb; g += 4) {  // rows above four in-edges
+        int ia[4], ib[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ia[q] = g + q < rna ? es[ra0 + g + q] : 0;
+          ib[q] = g + q < rnb ? es[rb0 + g + q] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          va[q] = sc[ia[q]];
+          vb[q] = sc[ib[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (g + q < rna) ya += va[q];
+          if (g + q < rnb) yb += vb[q];
+        }
+      }
+      if (rl0) {
+        rrk0 += ya;
+        sn[ri0] = rpl0 * ya;
+        lmax = max(lmax, dbits(ya));
+      }
+      if (rl1) {
+        rrk1 += yb;
+        sn[ri1] = rpl1 * yb;
+        lmax = max(lmax, dbits(yb));
+      }
+    } else
     // Two rows per thread in flight together; each row's in-edges in groups
     // of four (indices, then values, then the adds in order), so a row costs
     // two shared-memory round trips per group instead of two per edge.
@@ -742,6 +817,11 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
       break;
     }
     if (!(mx >= tol)) break;
+  }
+  if (reg_rows) {  // register accumulators of the light rows back to shared memory
+    if (rl0) rk[ri0] = rrk0;
+    if (rl1) rk[ri1] = rrk1;
+    __syncthreads();
   }
   for (int i = threadIdx.x; i < m; i += kThreads) rank[rb + i] = rk[i];
 #ifdef LR_LCTA_PROBE
