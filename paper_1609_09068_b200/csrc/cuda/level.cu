@@ -628,6 +628,7 @@ __device__ __forceinline__ unsigned long long block_max_bits(unsigned long long 
 // so an iteration touches no global memory -- one thread per row in the
 // reference's order (bit-exact), a warp for rows above kCrossLight, and the
 // stop test on integer maxima.
+constexpr int kLctaRegIdx = 8;  // in-edge offsets per row kept in registers by the CTA power series
 __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int maxrows,
                                   const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
                                   long long* unit_iters, DevStatus* st, double* sm, double (*red)[32]) {
@@ -666,7 +667,7 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
   const bool reg_rows = m <= 2 * kThreads;
   const int ri0 = threadIdx.x, ri1 = threadIdx.x + kThreads;
   int ra0 = 0, rna = 0, rb0 = 0, rnb = 0;
-  int ria[4] = {0, 0, 0, 0}, rib[4] = {0, 0, 0, 0};
+  int ria[kLctaRegIdx], rib[kLctaRegIdx];
   double rpl0 = 0.0, rpl1 = 0.0, rrk0 = 0.0, rrk1 = 0.0;
   bool rl0 = false, rl1 = false;
   if (reg_rows) {
@@ -686,11 +687,11 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
       rpl1 = pl[ri1];
       rrk1 = rk[ri1];
     }
+  }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      ria[q] = q < rna ? es[ra0 + q] : 0;
-      rib[q] = q < rnb ? es[rb0 + q] : 0;
-    }
+  for (int q = 0; q < kLctaRegIdx; ++q) {
+    ria[q] = reg_rows && q < rna ? es[ra0 + q] : 0;
+    rib[q] = reg_rows && q < rnb ? es[rb0 + q] : 0;
   }
   for (;;) {
 #ifdef LR_LCTA_PROBE
@@ -698,19 +699,22 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
 #endif
     unsigned long long lmax = 0ull;
     if (reg_rows) {
-      double va[4], vb[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        va[q] = sc[ria[q]];
-        vb[q] = sc[rib[q]];
-      }
       double ya = 0.0, yb = 0.0;
+      {
+        double va[kLctaRegIdx], vb[kLctaRegIdx];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q < rna) ya += va[q];
-        if (q < rnb) yb += vb[q];
+        for (int q = 0; q < kLctaRegIdx; ++q) {  // (predicated: no shared-memory traffic past the row)
+          va[q] = q < rna ? sc[ria[q]] : 0.0;
+          vb[q] = q < rnb ? sc[rib[q]] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kLctaRegIdx; ++q) {
+          if (q < rna) ya += va[q];
+          if (q < rnb) yb += vb[q];
+        }
       }
-      for (int g = 4; g < rna || g < rnb; g += 4) {  // rows above four in-edges
+      double va[4], vb[4];
+      for (int g = kLctaRegIdx; g < rna || g < rnb; g += 4) {  // rows above kLctaRegIdx in-edges
         int ia[4], ib[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
