@@ -772,7 +772,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     if (T.lt1 > T.lt0) {
       launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
-                   ctx->unit_iters.p, ctx->status.p, s);
+                   ctx->unit_iters.p, ctx->status.p, T.sm1 > T.sm0 || T.lc1 > T.lc0, s);
       ++nl;
       if (prof_on) {  // LR_LEVEL_PROF: per task type, the longest CTA of this level
         const int nt = T.lt1 - T.lt0;

@@ -182,7 +182,7 @@ cudaError_t set_level_prof(long long* buf);
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, cudaStream_t s);
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s);
 
 // launch wrappers (stream-ordered)
 void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,

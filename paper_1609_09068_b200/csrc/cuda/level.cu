@@ -929,7 +929,12 @@ __device__ __forceinline__ long long global_ns() {
 #ifndef LR_LEVEL_MINB
 #define LR_LEVEL_MINB 1
 #endif
-__global__ void __launch_bounds__(kThreads, LR_LEVEL_MINB)
+// HEAVY = the level has SccSmall or CTA power-series tasks.  Levels of row
+// gathers and CAC sweeps only (most CTAs of wide levels: config 3's last level
+// has 34k) run the light instantiation: no dense-solve registers, 64 per thread,
+// four CTAs per SM instead of two for these latency-bound tasks.
+template <bool HEAVY>
+__global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : 4)
     k_level(DeviceLayout L, const LevelTask* __restrict__ tasks, const CacTask* __restrict__ cacs,
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
             int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
@@ -975,20 +980,24 @@ __global__ void __launch_bounds__(kThreads, LR_LEVEL_MINB)
       break;
     }
     case kTaskSmall: {
-      const SccTask sct = smalls[t.a];
-      cross_rows(L, sct.row_begin, sct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
-      __syncthreads();
-      small_dispatch(L, sct, small_ld, c, pf, rank, sm, red[0], st);
+      if constexpr (HEAVY) {
+        const SccTask sct = smalls[t.a];
+        cross_rows(L, sct.row_begin, sct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+        __syncthreads();
+        small_dispatch(L, sct, small_ld, c, pf, rank, sm, red[0], st);
+      }
       break;
     }
     case kTaskLcta: {
-      const SccTask lt = lctas[t.a];
-      cross_rows(L, lt.row_begin, lt.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
-      __syncthreads();
-      if (lcta_stage_bytes(lcta_rows, L.iptr[lt.row_end] - L.iptr[lt.row_begin]) <= smem_bytes)
-        lcta_solve_staged(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
-      else
-        lcta_solve(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
+      if constexpr (HEAVY) {
+        const SccTask lt = lctas[t.a];
+        cross_rows(L, lt.row_begin, lt.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+        __syncthreads();
+        if (lcta_stage_bytes(lcta_rows, L.iptr[lt.row_end] - L.iptr[lt.row_begin]) <= smem_bytes)
+          lcta_solve_staged(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
+        else
+          lcta_solve(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
+      }
       break;
     }
     default:
@@ -1061,9 +1070,14 @@ cudaError_t configure_level_kernel() {
   e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
   cudaFuncAttributes a{};
-  e = cudaFuncGetAttributes(&a, k_level);
+  e = cudaFuncGetAttributes(&a, k_level<true>);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           optin - static_cast<int>(a.sharedSizeBytes));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncGetAttributes(&a, k_level<false>);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            optin - static_cast<int>(a.sharedSizeBytes));
   if (e != cudaSuccess) return e;
   e = cudaFuncGetAttributes(&a, k_cac_big);
@@ -1077,10 +1091,14 @@ cudaError_t set_level_prof(long long* buf) { return cudaMemcpyToSymbol(g_level_p
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, cudaStream_t s) {
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s) {
   if (ntasks == 0) return;
-  k_level<<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p, pf, rank,
-                                         s0, unit_iters, st, smem);
+  if (heavy)
+    k_level<true><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
+                                                 pf, rank, s0, unit_iters, st, smem);
+  else
+    k_level<false><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
+                                                  pf, rank, s0, unit_iters, st, smem);
 }
 
 }  // namespace lrk
