@@ -934,7 +934,10 @@ __device__ __forceinline__ long long global_ns() {
 // has 34k) run the light instantiation: no dense-solve registers, 64 per thread,
 // four CTAs per SM instead of two for these latency-bound tasks.
 template <bool HEAVY>
-__global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : 4)
+#ifndef LR_LIGHT_MINB
+#define LR_LIGHT_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MINB)
     k_level(DeviceLayout L, const LevelTask* __restrict__ tasks, const CacTask* __restrict__ cacs,
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
             int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
