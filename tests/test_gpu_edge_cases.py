@@ -145,3 +145,20 @@ def test_ragged_weights(lr, oracle):
     w[:10] = 1e-280
     w[10:20] = 1e120
     check(lr, oracle, n, src, dst, w=w, th=50)
+
+
+def test_grid_units_converging_apart(lr, oracle):
+    """Three grid-sized SccLarge units in one level whose weights differ by
+    orders of magnitude: they stop at different iterations, and K4c's launches
+    skip the finished units' tasks (unit done flags) while the others go on."""
+    rng = np.random.default_rng(17)
+    parts, base = [], 0
+    for m in (6000, 5000, 4500):
+        s, d = _scc(rng, base, m, deg=5)
+        parts.append((s, d))
+        base += m
+    n = base
+    src = np.concatenate([p[0] for p in parts])
+    dst = np.concatenate([p[1] for p in parts])
+    w = np.concatenate([np.full(6000, 1.0), np.full(5000, 1e-4), np.full(4500, 1e-8)])
+    check(lr, oracle, n, src, dst, w=w)
