@@ -218,6 +218,7 @@ struct lr_ctx {
   ncclComm_t comm = nullptr;
   std::vector<std::vector<int>> gu_bounds;  // per grid unit: world + 1 row bounds
   DevBuf<double> maxbuf;                     // per grid unit: shard max, all-reduced
+  DevBuf<double> cacpv;                      // pushed terms of CACs swept by cac_sweep_compact (n, or empty)
 
   DeviceLayout dl() const {
     DeviceLayout L;
@@ -566,6 +567,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
 
   // CTA tasks of the fused per-level kernel, level by level
   std::vector<LevelTask> ltasks;
+  bool any_compact = false;  // some k_cac_big CAC sweeps with structure-only staging
   for (int li = 0; li < L->n_levels; ++li) {
     LevelTasks& T = ctx->lt[static_cast<size_t>(li)];
     T.lt0 = static_cast<int>(ltasks.size());
@@ -595,6 +597,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
       if (b <= kLevelStageBytes) mid_need = std::max(mid_need, b);
     }
     T.smem = std::max({T.smem, T.sm_tile, warp_need, mid_need});
+    // warp-tiled start-weight gathers of the CTA-solved units (cross_rows_cta)
+    if (T.cac_m1 > T.cac_m0 || T.sm1 > T.sm0 || T.lc1 > T.lc0) T.smem = std::max(T.smem, kRowTaskSmem);
     if (!rowranges[static_cast<size_t>(li)].empty()) T.smem = std::max(T.smem, kRowTaskSmem);  // tiled row gathers
     for (int i = T.lc0; i < T.lc1; ++i) {  // CTA power series staged in shared memory where it fits
       const SccTask& lt = lcta[static_cast<size_t>(i)];
@@ -603,9 +607,18 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     }
     T.big_smem = 0;
     for (int i = T.cac_b0; i < T.cac_b1; ++i) {
-      const size_t b = need(cac_w[static_cast<size_t>(i)]);
-      if (b <= kStageMaxBytes) T.big_smem = std::max(T.big_smem, b);
+      const CacTask& t = cac_w[static_cast<size_t>(i)];
+      const size_t b = need(t);
+      const long long m = t.row_end - t.row_begin;
+      const size_t bc = (cac_compact_need(m, L->iptr[t.row_end] - L->iptr[t.row_begin]) + 15) & ~size_t{15};
+      if (b <= kStageMaxBytes) {
+        T.big_smem = std::max(T.big_smem, b);
+      } else if (m < 65536 && bc <= kStageMaxBytes) {
+        T.big_smem = std::max(T.big_smem, bc);
+        any_compact = true;
+      }
     }
+    if (T.cac_b1 > T.cac_b0) T.big_smem = std::max(T.big_smem, kBigCrossSmem);  // warp-tiled start weights
   }
 
   LR_CUDA_TRY(ctx->vertex_of.upload(L->vertex_of, nn, s));
@@ -669,6 +682,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->r1.alloc(nn));
   const bool any_grid = !gstate.empty();
   LR_CUDA_TRY(ctx->s0.alloc(any_grid ? nn : 0));
+  LR_CUDA_TRY(ctx->cacpv.alloc(any_compact ? nn : 0));
   LR_CUDA_TRY(ctx->s1.alloc(any_grid ? nn : 0));
   LR_CUDA_TRY(ctx->maxbuf.alloc(gstate.size()));
   ctx->nparts = static_cast<int>((nn + kOutBlock - 1) / kOutBlock);
@@ -764,7 +778,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       LR_CUDA_TRY(cudaEventRecord(ctx->fork_ev, s));
       LR_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
-                     ctx->rank.p, ctx->s0.p, T.big_smem, ctx->side);
+                     ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side);
       LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));
       ++nl;
     }

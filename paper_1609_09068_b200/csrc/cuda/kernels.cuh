@@ -110,6 +110,7 @@ constexpr int kCrossSplit = 32;    // cross rows above this: split over warps by
 constexpr int kCrossSeg = 256;     // in-edges per warp task of a split row (8 per lane, all in flight)
 constexpr int kTileNnzCross = 256; // cross in-edges per chunk of a row task (level.cu cross_rows_tiled)
 constexpr size_t kRowTaskSmem = 8 * kTileNnzCross * sizeof(double);  // k_level smem a row task needs
+constexpr size_t kBigCrossSmem = 32 * kTileNnzCross * sizeof(double);  // k_cac_big's warp-tiled start weights
 
 // One CTA of the fused per-level kernel (level.cu).
 enum LevelTaskType : int { kTaskRows = 0, kTaskCacWarps = 1, kTaskCacBlock = 2, kTaskSmall = 3, kTaskLcta = 4 };
@@ -171,9 +172,11 @@ cudaError_t configure_level_kernel();
 
 // large CACs, 1024-thread CTAs, meant for a second stream (level.cu)
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
-                    const SolveParams* p, const double* pf, double* rank, double* s0, size_t smem, cudaStream_t s);
+                    const SolveParams* p, const double* pf, double* rank, double* s0, double* pv, size_t smem,
+                    cudaStream_t s);
 // shared-memory bytes a CAC of `rows` rows and `edges` in-edges needs to be swept from shared memory
 size_t cac_stage_need(long long rows, long long edges);
+size_t cac_compact_need(long long rows, long long edges);  // k_cac_big's structure-only staging
 constexpr size_t kStageMaxBytes = 200 * 1024;  // larger CACs sweep from global memory
 constexpr size_t kLevelStageBytes = 64 * 1024; // CAC staging budget of one k_level CTA
 // k_level per-CTA timing buffer (3 int64 per CTA: type, start ns, end ns), nullptr = off

@@ -99,12 +99,10 @@ __device__ void cross_rows(const DeviceLayout& L, int r0, int r1, const double* 
 // more than kTiledCrossMax edges takes the per-row path.
 constexpr int kTiledCrossMax = 2048;
 
-__device__ void cross_rows_tiled(const DeviceLayout& L, int r0, int r1, const double* __restrict__ w, double c,
-                                 const double* __restrict__ pf, double* rank, double* s0, double* stage) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rb = r0 + 32 * warp;
-  if (rb >= r1) return;
-  const int re = min(rb + 32, r1);
+// rows [rb, re), re - rb <= 32, by the calling warp
+__device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const double* __restrict__ w, double c,
+                                const double* __restrict__ pf, double* rank, double* s0, double* stage) {
+  const int lane = threadIdx.x & 31;
   const int row = rb + lane;
   const bool mine = row < re;
   long long lo = 0, hi = 0;
@@ -148,6 +146,31 @@ __device__ void cross_rows_tiled(const DeviceLayout& L, int r0, int r1, const do
     __syncwarp();
   }
   if (light) row_finish(L, row, acc, c, pf, rank, s0);
+}
+
+// a row task: 32 rows per warp of the CTA
+__device__ void cross_rows_tiled(const DeviceLayout& L, int r0, int r1, const double* __restrict__ w, double c,
+                                 const double* __restrict__ pf, double* rank, double* s0, double* stage) {
+  const int rb = r0 + 32 * static_cast<int>(threadIdx.x >> 5);
+  if (rb < r1) cross_warp_rows(L, rb, min(rb + 32, r1), w, c, pf, rank, s0, stage);
+}
+
+// The start weights of a unit's rows [r0, r1) by a whole CTA of `nwarps` warps
+// before it solves the unit: warp-tiled as above (32 rows per warp and round,
+// every gather of a chunk in flight), each warp staging in its own
+// kTileNnzCross doubles of `sm`; per-thread rows when the CTA has less shared
+// memory than that.
+__device__ void cross_rows_cta(const DeviceLayout& L, int r0, int r1, const double* __restrict__ w, double c,
+                               const double* __restrict__ pf, double* rank, double* s0, double* sm,
+                               size_t smem_bytes, int nwarps) {
+  if (smem_bytes < static_cast<size_t>(nwarps) * kTileNnzCross * sizeof(double)) {
+    cross_rows(L, r0, r1, w, c, pf, rank, s0, threadIdx.x, 32 * nwarps);
+    return;
+  }
+  const int warp = threadIdx.x >> 5;
+  double* stage = sm + warp * kTileNnzCross;
+  for (int rb = r0 + 32 * warp; rb < r1; rb += 32 * nwarps)
+    cross_warp_rows(L, rb, min(rb + 32, r1), w, c, pf, rank, s0, stage);
 }
 
 // ------------------------------------------------------------------ K3
@@ -227,15 +250,44 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
   int* rp = reinterpret_cast<int*>(sr + m);
   int* es = rp + m + 1;
   int* ed = es + ne;
-  for (int i = tid; i < m; i += width) {
-    sr[i] = rank[rb + i];
-    rp[i] = static_cast<int>(L.iptr[rb + i] - eb);
+  std::uint8_t* lp = reinterpret_cast<std::uint8_t*>(ed + ne);  // kept self-loop flags
+  // staging: four rows / in-edges per thread in flight
+  for (int i0 = tid; i0 < m; i0 += 4 * width) {
+    double rv[4];
+    long long pv[4];
+    std::uint8_t fv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = min(i0 + q * width, m - 1);
+      rv[q] = rank[rb + i];
+      pv[q] = __ldg(L.iptr + rb + i);
+      fv[q] = __ldg(L.loop + rb + i);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * width;
+      if (i < m) {
+        sr[i] = rv[q];
+        rp[i] = static_cast<int>(pv[q] - eb);
+        lp[i] = fv[q];
+      }
+    }
   }
   if (tid == 0) rp[m] = ne;
-  for (int e = tid; e < ne; e += width) {
-    const int s = L.isrc[eb + e];
-    es[e] = s - rb;
-    ed[e] = L.deg[s];
+  for (int e0 = tid; e0 < ne; e0 += 4 * width) {
+    int sv[4], dv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[q] = __ldg(L.isrc + eb + min(e0 + q * width, ne - 1));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dv[q] = __ldg(L.deg + sv[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q * width;
+      if (e < ne) {
+        es[e] = sv[q] - rb;
+        ed[e] = dv[q];
+      }
+    }
   }
   auto sync = [&] {
     if (kBlock) {
@@ -254,7 +306,7 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       if (e1 - e0 > kCrossLight) continue;
       double acc = sr[i];
       for (int e = e0; e < e1; ++e) acc += sr[es[e]] * c / static_cast<double>(ed[e]);
-      sr[i] = loop_factor(L, rb + i, c, acc);
+      sr[i] = lp[i] ? acc / (1.0 - c / static_cast<double>(L.deg[rb + i])) : acc;
     }
     for (int base = s0 + wid * 32; base < s1; base += nw * 32) {
       const int i = base + lane;
@@ -267,7 +319,10 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
         double y = 0.0;
         for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) y += sr[es[e]] * c / static_cast<double>(ed[e]);
         y = warp_sum(y);
-        if (lane == 0) sr[row] = loop_factor(L, rb + row, c, sr[row] + y);
+        if (lane == 0) {
+          const double a = sr[row] + y;
+          sr[row] = lp[row] ? a / (1.0 - c / static_cast<double>(L.deg[rb + row])) : a;
+        }
       }
     }
   }
@@ -275,9 +330,82 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
   for (int i = tid; i < m; i += width) rank[rb + i] = sr[i];
 }
 
+// CACs too large for cac_sweep_staged (k_cac_big, up to 65535 rows): only the
+// structure is staged -- row offsets and 16-bit parent offsets -- and every
+// finished row publishes its pushed term (r * c) / deg once to `pv` (global,
+// indexed like rank), so a row of the next slice adds those terms in the same
+// order as cac_row (bit-exact) with one global round trip on the chain instead
+// of four.
+__device__ void cac_sweep_compact(const DeviceLayout& L, const CacTask& t, const int* __restrict__ depth_ptr, double c,
+                                  double* rank, double* pv, void* stage) {
+  const int tid = threadIdx.x, width = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = width >> 5;
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  const long long eb = L.iptr[rb];
+  const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  int* rp = static_cast<int*>(stage);
+  unsigned short* es = reinterpret_cast<unsigned short*>(rp + m + 1);
+  for (int i0 = tid; i0 < m; i0 += 4 * width) {
+    long long o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = __ldg(L.iptr + rb + min(i0 + q * width, m - 1));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q * width < m) rp[i0 + q * width] = static_cast<int>(o[q] - eb);
+  }
+  if (tid == 0) rp[m] = ne;
+  for (int e0 = tid; e0 < ne; e0 += 8 * width) {
+    int v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(L.isrc + eb + min(e0 + q * width, ne - 1));
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (e0 + q * width < ne) es[e0 + q * width] = static_cast<unsigned short>(v[q] - rb);
+  }
+  __syncthreads();
+  const double* pvb = pv + rb;
+  auto finish = [&](int i, double acc) {
+    const int r = rb + i;
+    const double dg = static_cast<double>(__ldg(L.deg + r));
+    const double fin = __ldg(L.loop + r) ? acc / (1.0 - c / dg) : acc;
+    rank[r] = fin;
+    pv[r] = fin * c / dg;
+  };
+  const int* dp = depth_ptr + t.depth_begin;
+  for (int d = 0; d < t.ndepth; ++d) {
+    if (d > 0) __syncthreads();
+    const int s0 = dp[d] - rb, s1 = dp[d + 1] - rb;
+    for (int i = s0 + tid; i < s1; i += width) {
+      const int e0 = rp[i], e1 = rp[i + 1];
+      if (e1 - e0 > kCrossLight) continue;
+      double acc = rank[rb + i];
+      for (int e = e0; e < e1; ++e) acc += pvb[es[e]];
+      finish(i, acc);
+    }
+    for (int base = s0 + wid * 32; base < s1; base += nw * 32) {
+      const int i = base + lane;
+      const int deg_in = i < s1 ? rp[i + 1] - rp[i] : 0;
+      unsigned mask = __ballot_sync(0xffffffffu, deg_in > kCrossLight);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int row = base + src;
+        double y = 0.0;
+        for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) y += pvb[es[e]];
+        y = warp_sum(y);
+        if (lane == 0) finish(row, rank[rb + row] + y);
+      }
+    }
+  }
+}
+
+__host__ __device__ constexpr size_t cac_compact_bytes(long long m, long long ne) {
+  return static_cast<size_t>(m + 1) * 4 + static_cast<size_t>(ne) * 2 + 16;
+}
+
 // bytes cac_sweep_staged needs for a CAC of m rows and ne in-edges
 __host__ __device__ constexpr size_t cac_stage_bytes(long long m, long long ne) {
-  return static_cast<size_t>(m) * 8 + static_cast<size_t>(m + 1) * 4 + static_cast<size_t>(ne) * 8 + 16;
+  return static_cast<size_t>(m) * 9 + static_cast<size_t>(m + 1) * 4 + static_cast<size_t>(ne) * 8 + 16;
 }
 
 // ------------------------------------------------------------------ K5
@@ -642,15 +770,36 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
   unsigned short* es = reinterpret_cast<unsigned short*>(sm + 4 * maxrows + (maxrows + 2) / 2);
   const long long eb = L.iptr[rb];
   const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
-  for (int i = threadIdx.x; i < m; i += kThreads) {
-    const double pv = pf[rb + i], r = rank[rb + i];
-    pl[i] = pv;
-    rk[i] = r;
-    sc[i] = pv * r;
-    rp[i] = static_cast<int>(L.iptr[rb + i] - eb);
+  for (int i0 = threadIdx.x; i0 < m; i0 += 2 * kThreads) {  // two rows per thread in flight
+    double pv[2], r[2];
+    long long o[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = min(i0 + q * kThreads, m - 1);
+      pv[q] = pf[rb + i];
+      r[q] = rank[rb + i];
+      o[q] = __ldg(L.iptr + rb + i);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = i0 + q * kThreads;
+      if (i < m) {
+        pl[i] = pv[q];
+        rk[i] = r[q];
+        sc[i] = pv[q] * r[q];
+        rp[i] = static_cast<int>(o[q] - eb);
+      }
+    }
   }
   if (threadIdx.x == 0) rp[m] = ne;
-  for (int e = threadIdx.x; e < ne; e += kThreads) es[e] = static_cast<unsigned short>(L.isrc[eb + e] - rb);
+  for (int e0 = threadIdx.x; e0 < ne; e0 += 8 * kThreads) {  // eight in-edges per thread in flight
+    int v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(L.isrc + eb + min(e0 + q * kThreads, ne - 1));
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (e0 + q * kThreads < ne) es[e0 + q * kThreads] = static_cast<unsigned short>(v[q] - rb);
+  }
   __syncthreads();
   const double tol = p->tol;
   const long long cap = p->cap;
@@ -974,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
     }
     case kTaskCacBlock: {
       const CacTask ct = cacs[t.a];
-      cross_rows(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      cross_rows_cta(L, ct.row_begin, ct.row_end, w, c, pf, rank, s0, sm, smem_bytes, kWarpsPer);
       __syncthreads();
       if (cac_stage_bytes(ct.row_end - ct.row_begin, L.iptr[ct.row_end] - L.iptr[ct.row_begin]) <= smem_bytes)
         cac_sweep_staged<true>(L, ct, depth_ptr, c, rank, threadIdx.x, kThreads, sm);
@@ -985,7 +1134,7 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
     case kTaskSmall: {
       if constexpr (HEAVY) {
         const SccTask sct = smalls[t.a];
-        cross_rows(L, sct.row_begin, sct.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+        cross_rows_cta(L, sct.row_begin, sct.row_end, w, c, pf, rank, s0, sm, smem_bytes, kWarpsPer);
         __syncthreads();
         small_dispatch(L, sct, small_ld, c, pf, rank, sm, red[0], st);
       }
@@ -994,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
     case kTaskLcta: {
       if constexpr (HEAVY) {
         const SccTask lt = lctas[t.a];
-        cross_rows(L, lt.row_begin, lt.row_end, w, c, pf, rank, s0, threadIdx.x, kThreads);
+        cross_rows_cta(L, lt.row_begin, lt.row_end, w, c, pf, rank, s0, sm, smem_bytes, kWarpsPer);
         __syncthreads();
         if (lcta_stage_bytes(lcta_rows, L.iptr[lt.row_end] - L.iptr[lt.row_begin]) <= smem_bytes)
           lcta_solve_staged(L, lt, lcta_rows, p, pf, rank, unit_iters, st, sm, red);
@@ -1025,16 +1174,20 @@ constexpr int kBigThreads = 1024;
 __global__ void __launch_bounds__(kBigThreads)
     k_cac_big(DeviceLayout L, const CacTask* __restrict__ cacs, const int* __restrict__ depth_ptr,
               const double* __restrict__ w, const SolveParams* __restrict__ p, const double* __restrict__ pf,
-              double* rank, double* s0, size_t smem_bytes) {
+              double* rank, double* s0, double* pv, size_t smem_bytes) {
   extern __shared__ double sm[];
   const CacTask ct = cacs[blockIdx.x];
   // the CAC's own start weights (rows above kCrossSplit cross in-edges were
   // done by k_pull_heavy before the level), so the launch runs concurrently
   // with the level's k_level on a side stream
-  cross_rows(L, ct.row_begin, ct.row_end, w, p->c, pf, rank, s0, threadIdx.x, kBigThreads);
+  cross_rows_cta(L, ct.row_begin, ct.row_end, w, p->c, pf, rank, s0, sm, smem_bytes, kBigThreads / 32);
   __syncthreads();
-  if (cac_stage_bytes(ct.row_end - ct.row_begin, L.iptr[ct.row_end] - L.iptr[ct.row_begin]) <= smem_bytes)
+  const int m = ct.row_end - ct.row_begin;
+  const long long ne = L.iptr[ct.row_end] - L.iptr[ct.row_begin];
+  if (cac_stage_bytes(m, ne) <= smem_bytes)
     cac_sweep_staged<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads, sm);
+  else if (pv != nullptr && m < 65536 && cac_compact_bytes(m, ne) <= smem_bytes)
+    cac_sweep_compact(L, ct, depth_ptr, p->c, rank, pv, sm);
   else
     cac_sweep<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads);
 }
@@ -1042,7 +1195,8 @@ __global__ void __launch_bounds__(kBigThreads)
 }  // namespace
 
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
-                    const SolveParams* p, const double* pf, double* rank, double* s0, size_t smem, cudaStream_t s) {
+                    const SolveParams* p, const double* pf, double* rank, double* s0, double* pv, size_t smem,
+                    cudaStream_t s) {
   if (n == 0) return;
   // highest launch priority (kept by graph capture): its 1024-thread CTAs need a
   // whole SM and must be placed before the level's k_level CTAs fill them
@@ -1061,10 +1215,11 @@ void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int
   attr[0].val.priority = prio;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, smem);
+  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, pv, smem);
 }
 
 size_t cac_stage_need(long long rows, long long edges) { return cac_stage_bytes(rows, edges); }
+size_t cac_compact_need(long long rows, long long edges) { return cac_compact_bytes(rows, edges); }
 
 cudaError_t configure_level_kernel() {
   int dev = 0, optin = 0;

@@ -162,3 +162,28 @@ def test_grid_units_converging_apart(lr, oracle):
     dst = np.concatenate([p[1] for p in parts])
     w = np.concatenate([np.full(6000, 1.0), np.full(5000, 1e-4), np.full(4500, 1e-8)])
     check(lr, oracle, n, src, dst, w=w)
+
+
+def test_big_cac_structure_staged(lr, oracle):
+    # a 20,000-row CAC (random out-tree plus forward chords, kept self-loops):
+    # too large to stage whole, so k_cac_big stages only its structure and the
+    # rows publish their pushed terms (cac_sweep_compact); plus a leaf with 100
+    # parents (warp path).  Every row but that leaf is summed in the
+    # reference's order: bit-exact.
+    rng = np.random.default_rng(11)
+    n = 20_000
+    v = np.arange(1, n - 1)
+    parent = (rng.random(n - 2) * v).astype(np.int32)
+    cu = rng.integers(0, n - 2, 3000)
+    cv = rng.integers(0, n - 2, 3000)
+    keep = cu != cv
+    cu, cv = np.minimum(cu, cv)[keep], np.maximum(cu, cv)[keep]
+    loops = np.arange(0, n - 1, 97)
+    heavy = rng.choice(n - 1, 100, replace=False)
+    src = np.r_[parent, cu, loops, heavy]
+    dst = np.r_[v, cv, loops, np.full(100, n - 1)]
+    w = rng.random(n) + 0.5
+    res = check(lr, oracle, n, src, dst, w=w, keep=True)
+    ref = oracle.graph(n, np.asarray(src, np.int32), np.asarray(dst, np.int32), True).compute_pagerank(
+        w, 0.85, 1e-12, 100)
+    assert np.array_equal(res.ranks[: n - 1], ref.ranks[: n - 1])
