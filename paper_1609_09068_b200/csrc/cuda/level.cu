@@ -756,7 +756,23 @@ __device__ __forceinline__ unsigned long long block_max_bits(unsigned long long 
 // so an iteration touches no global memory -- one thread per row in the
 // reference's order (bit-exact), a warp for rows above kCrossLight, and the
 // stop test on integer maxima.
-constexpr int kLctaRegIdx = 8;  // in-edge offsets per row kept in registers by the CTA power series
+#ifndef LR_LCTA_REGIDX
+#define LR_LCTA_REGIDX 12
+#endif
+constexpr int kLctaRegIdx = LR_LCTA_REGIDX;  // in-edge offsets per row kept in registers by the CTA power series
+
+// pairwise sum of N terms (N a multiple of 4): log2 N dependent adds instead of N
+template <int N>
+__device__ __forceinline__ double tree_sum(const double* v) {
+  if constexpr (N == 4) {
+    return (v[0] + v[1]) + (v[2] + v[3]);
+  } else if constexpr ((N & (N - 1)) == 0) {
+    return tree_sum<N / 2>(v) + tree_sum<N / 2>(v + N / 2);
+  } else {
+    constexpr int P = N & -N;  // lowest power-of-two part
+    return tree_sum<N - P>(v) + tree_sum<P>(v + N - P);
+  }
+}
 __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int maxrows,
                                   const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
                                   long long* unit_iters, DevStatus* st, double* sm, double (*red)[32]) {
@@ -856,11 +872,8 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
           va[q] = q < rna ? sc[ria[q]] : 0.0;
           vb[q] = q < rnb ? sc[rib[q]] : 0.0;
         }
-#pragma unroll
-        for (int q = 0; q < kLctaRegIdx; ++q) {
-          if (q < rna) ya += va[q];
-          if (q < rnb) yb += vb[q];
-        }
+        ya = tree_sum<kLctaRegIdx>(va);  // (predicated-off terms are +0.0: exact)
+        yb = tree_sum<kLctaRegIdx>(vb);
       }
       double va[4], vb[4];
       for (int g = kLctaRegIdx; g < rna || g < rnb; g += 4) {  // rows above kLctaRegIdx in-edges
@@ -872,14 +885,11 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          va[q] = sc[ia[q]];
-          vb[q] = sc[ib[q]];
+          va[q] = g + q < rna ? sc[ia[q]] : 0.0;
+          vb[q] = g + q < rnb ? sc[ib[q]] : 0.0;
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (g + q < rna) ya += va[q];
-          if (g + q < rnb) yb += vb[q];
-        }
+        ya += tree_sum<4>(va);
+        yb += tree_sum<4>(vb);
       }
       if (rl0) {
         rrk0 += ya;
