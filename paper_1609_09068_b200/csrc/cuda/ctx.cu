@@ -251,6 +251,60 @@ struct lr_ctx {
   }
 };
 
+// In-edge order of a CTA power-series unit run by lcta_solve_staged's register
+// rows: lane l of a warp loads the q-th in-edge of its row in the warp's q-th
+// gather, one shared-memory load of a double per lane, so a gather costs as many
+// wavefronts as its busiest bank pair (16 doubles span the 32 banks).  Per 16
+// consecutive rows (a half-warp of one row set) and slot q < kLctaRegIdx, rows
+// with the fewest remaining in-edges pick first, each the in-edge whose bank pair
+// is least loaded in that slot; the rest keep their order.  The rows' sums are
+// pairwise (order-insensitive up to rounding), so only the gathers' bank
+// spread changes.  LR_BANK_ORDER=0 keeps the layout's order.
+static bool bank_order_off() {
+  const char* e = std::getenv("LR_BANK_ORDER");
+  return e && std::atoi(e) == 0;
+}
+
+static void bank_balanced_order(const int64_t* iptr, const int* isrc, int rb, int re, std::vector<int>& out) {
+  const int64_t eb = iptr[rb];
+  out.assign(isrc + eb, isrc + iptr[re]);
+  const int m = re - rb;
+  std::vector<int> rem[16];
+  for (int base = 0; base < m; base += 16) {
+    const int nr = std::min(16, m - base);
+    for (int l = 0; l < nr; ++l) {
+      const int r = rb + base + l;
+      const int64_t d = iptr[r + 1] - iptr[r];
+      rem[l].clear();
+      if (d > kCrossLight) continue;  // warp rows: not in registers
+      rem[l].assign(isrc + iptr[r], isrc + iptr[r + 1]);
+    }
+    std::vector<int> pos(static_cast<size_t>(nr), 0), order(static_cast<size_t>(nr));
+    for (int q = 0; q < kLctaRegIdx; ++q) {
+      int load[16] = {};
+      for (int l = 0; l < nr; ++l) order[static_cast<size_t>(l)] = l;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rem[a].size() < rem[b].size(); });
+      for (int l : order) {
+        std::vector<int>& v = rem[l];
+        if (v.empty()) continue;
+        size_t best = 0;
+        for (size_t k = 1; k < v.size() && load[(v[best] - rb) & 15] > 0; ++k)
+          if (load[(v[k] - rb) & 15] < load[(v[best] - rb) & 15]) best = k;
+        ++load[(v[best] - rb) & 15];
+        const int r = rb + base + l;
+        out[static_cast<size_t>(iptr[r] - eb + q)] = v[best];
+        v.erase(v.begin() + static_cast<std::ptrdiff_t>(best));
+        ++pos[static_cast<size_t>(l)];
+      }
+    }
+    for (int l = 0; l < nr; ++l) {  // the tail (rows above kLctaRegIdx in-edges) in the layout's order
+      const int r = rb + base + l;
+      for (size_t k = 0; k < rem[l].size(); ++k)
+        out[static_cast<size_t>(iptr[r] - eb + pos[static_cast<size_t>(l)] + static_cast<int64_t>(k))] = rem[l][k];
+    }
+  }
+}
+
 extern "C" {
 
 lr_status lr_ctx_create(int device, lr_ctx** out) {
@@ -450,7 +504,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           int has_heavy = 0;
           for (int r = rb; r < re && !has_heavy; ++r) has_heavy = L->iptr[r + 1] - L->iptr[r] > kCrossLight;
           lcta.push_back(SccTask{rb, re, u, has_heavy, L->unit_edges[u]});
-          T.lc_max = std::max(T.lc_max, m);
+          T.lc_max = std::max(T.lc_max, (m + 15) & ~15);  // (16 doubles = the 32 banks: same map for both pushed vectors)
         } else {
           rk = kLargeGrid;
           rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
@@ -631,6 +685,15 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->iptr.upload(reinterpret_cast<const long long*>(L->iptr), nn + 1, s));
   // padded: K4c's aligned 256-slot index windows may reach past the last in-edge
   LR_CUDA_TRY(ctx->isrc.upload_padded(L->isrc, static_cast<size_t>(L->nnz_intra), kIdxPad, s));
+  if (!bank_order_off())
+    for (const SccTask& t : lcta) {
+      if (t.row_end - t.row_begin > kLctaRegRows) continue;
+      std::vector<int> es;
+      bank_balanced_order(L->iptr, L->isrc, t.row_begin, t.row_end, es);
+      if (!es.empty())
+        LR_CUDA_TRY(cudaMemcpyAsync(ctx->isrc.p + L->iptr[t.row_begin], es.data(), es.size() * sizeof(int),
+                                    cudaMemcpyHostToDevice, s));
+    }
   LR_CUDA_TRY(ctx->depth_ptr.upload(L->depth_ptr, static_cast<size_t>(L->depth_ptr_len), s));
   LR_CUDA_TRY(ctx->cac.upload(cac_w.data(), cac_w.size(), s));
   LR_CUDA_TRY(ctx->small.upload(small.data(), small.size(), s));

@@ -164,6 +164,11 @@ __host__ __device__ constexpr size_t lcta_stage_bytes(int maxrows, long long ne)
          static_cast<size_t>(ne) * 2;
 }
 constexpr size_t kLctaStageMaxBytes = 96 * 1024;  // k_level smem budget for staged CTA power series
+#ifndef LR_LCTA_REGIDX
+#define LR_LCTA_REGIDX 12
+#endif
+constexpr int kLctaRegIdx = LR_LCTA_REGIDX;  // in-edge offsets per row kept in registers by the CTA power series
+constexpr int kLctaRegRows = 512;            // units up to this many rows: register rows (two per thread)
 constexpr int kCacWarpMaxRows = 64;      // CACs up to this: one warp of a k_level CTA
 constexpr int kCacMidMaxRows = 1024;     // up to this: a 256-thread k_level CTA; above: a 1024-thread CTA
 

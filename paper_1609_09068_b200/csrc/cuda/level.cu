@@ -756,10 +756,6 @@ __device__ __forceinline__ unsigned long long block_max_bits(unsigned long long 
 // so an iteration touches no global memory -- one thread per row in the
 // reference's order (bit-exact), a warp for rows above kCrossLight, and the
 // stop test on integer maxima.
-#ifndef LR_LCTA_REGIDX
-#define LR_LCTA_REGIDX 12
-#endif
-constexpr int kLctaRegIdx = LR_LCTA_REGIDX;  // in-edge offsets per row kept in registers by the CTA power series
 
 // pairwise sum of N terms (N a multiple of 4): log2 N dependent adds instead of N
 template <int N>
@@ -829,7 +825,8 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
   // two rows keep their loop invariants in registers across iterations -- edge
   // range, the first four in-edge offsets, pf and the rank accumulator -- so an
   // iteration's chain is the gathers of sc, the adds and the stores of sn.
-  const bool reg_rows = m <= 2 * kThreads;
+  static_assert(kLctaRegRows == 2 * kThreads, "two register rows per thread");
+  const bool reg_rows = m <= kLctaRegRows;
   const int ri0 = threadIdx.x, ri1 = threadIdx.x + kThreads;
   int ra0 = 0, rna = 0, rb0 = 0, rnb = 0;
   int ria[kLctaRegIdx], rib[kLctaRegIdx];
