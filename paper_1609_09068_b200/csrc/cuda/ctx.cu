@@ -282,6 +282,8 @@ static void bank_balanced_order(const int64_t* iptr, const int* isrc, int rb, in
     std::vector<int> pos(static_cast<size_t>(nr), 0), order(static_cast<size_t>(nr));
     for (int q = 0; q < kLctaRegIdx; ++q) {
       int load[16] = {};
+      for (int l = 0; l < nr; ++l)  // rows without an in-edge for slot q read the zero slot (row m)
+        if (rem[l].empty()) load[m & 15] = 1;
       for (int l = 0; l < nr; ++l) order[static_cast<size_t>(l)] = l;
       std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rem[a].size() < rem[b].size(); });
       for (int l : order) {
@@ -504,7 +506,9 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           int has_heavy = 0;
           for (int r = rb; r < re && !has_heavy; ++r) has_heavy = L->iptr[r + 1] - L->iptr[r] > kCrossLight;
           lcta.push_back(SccTask{rb, re, u, has_heavy, L->unit_edges[u]});
-          T.lc_max = std::max(T.lc_max, (m + 15) & ~15);  // (16 doubles = the 32 banks: same map for both pushed vectors)
+          // a multiple of 16 doubles (the 32 banks) above m: same bank map for
+          // both pushed vectors, and room for the register path's zero slot
+          T.lc_max = std::max(T.lc_max, (m + 2 + 15) & ~15);
         } else {
           rk = kLargeGrid;
           rowranges[static_cast<size_t>(li)].emplace_back(rb, re);

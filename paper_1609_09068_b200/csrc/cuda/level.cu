@@ -17,6 +17,8 @@
 #include <cstdint>
 #include <cstdio>
 
+#include <type_traits>
+
 #include "devutil.cuh"
 #include "kernels.cuh"
 
@@ -750,6 +752,11 @@ __device__ __forceinline__ unsigned long long block_max_bits(unsigned long long 
   return (static_cast<unsigned long long>(h2) << 32) | l2;
 }
 
+// Interleaved pushed vectors of lcta_solve_staged's register path: element i of
+// vector b at double 32 * (i / 16) + 16 * b + i % 16 (same bank pair i % 16 in
+// both, the other vector 128 bytes further).
+__device__ __forceinline__ int lcta_il(int i) { return ((i >> 4) << 5) | (i & 15); }
+
 // The whole power series of one SccLarge unit in one CTA (solve_large_scc,
 // solvers.cpp:128-162), everything in shared memory: the pushed vectors, the
 // ranks, pf, the row offsets and the in-edges as 16-bit offsets into the unit,
@@ -772,6 +779,11 @@ __device__ __forceinline__ double tree_sum(const double* v) {
 __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int maxrows,
                                   const SolveParams* __restrict__ p, const double* __restrict__ pf, double* rank,
                                   long long* unit_iters, DevStatus* st, double* sm, double (*red)[32]) {
+#ifdef LR_LCTA_PROBE
+  constexpr bool kLctaProbe = true;
+#else
+  constexpr bool kLctaProbe = false;
+#endif
   const int rb = t.row_begin, m = t.row_end - t.row_begin;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sc = sm;
@@ -782,6 +794,9 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
   unsigned short* es = reinterpret_cast<unsigned short*>(sm + 4 * maxrows + (maxrows + 2) / 2);
   const long long eb = L.iptr[rb];
   const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  // register rows, no warp rows: the two pushed vectors interleaved in blocks
+  // of 16 (lcta_il), so the vector read in an iteration is an immediate offset
+  const bool fast = m <= kLctaRegRows && !t.pad && !kLctaProbe;
   for (int i0 = threadIdx.x; i0 < m; i0 += 2 * kThreads) {  // two rows per thread in flight
     double pv[2], r[2];
     long long o[2];
@@ -798,12 +813,15 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
       if (i < m) {
         pl[i] = pv[q];
         rk[i] = r[q];
-        sc[i] = pv[q] * r[q];
+        sm[fast ? lcta_il(i) : i] = pv[q] * r[q];
         rp[i] = static_cast<int>(o[q] - eb);
       }
     }
   }
-  if (threadIdx.x == 0) rp[m] = ne;
+  if (threadIdx.x == 0) {
+    rp[m] = ne;
+    if (fast) sm[lcta_il(m)] = sm[lcta_il(m) + 16] = 0.0;  // the zero slot (maxrows > m) of both vectors
+  }
   for (int e0 = threadIdx.x; e0 < ne; e0 += 8 * kThreads) {  // eight in-edges per thread in flight
     int v[8];
 #pragma unroll
@@ -855,6 +873,61 @@ __device__ void lcta_solve_staged(const DeviceLayout& L, const SccTask& t, int m
     ria[q] = reg_rows && q < rna ? es[ra0 + q] : 0;
     rib[q] = reg_rows && q < rnb ? es[rb0 + q] : 0;
   }
+  if (fast) {
+    // byte offsets into buffer 0 of the interleaved vectors; slots past the
+    // row read the zero slot (unpredicated loads: no per-slot predicates)
+    const char* smb = reinterpret_cast<const char*>(sm);
+    int oa[kLctaRegIdx], ob[kLctaRegIdx];
+#pragma unroll
+    for (int q = 0; q < kLctaRegIdx; ++q) {
+      oa[q] = 8 * lcta_il(q < rna ? ria[q] : m);
+      ob[q] = 8 * lcta_il(q < rnb ? rib[q] : m);
+    }
+    const int own0 = 8 * lcta_il(rl0 ? ri0 : m + 1), own1 = 8 * lcta_il(rl1 ? ri1 : m + 1);
+    // one iteration reading vector B (0/1) and writing the other; true = stop
+    auto step = [&](auto bsel) -> bool {
+      constexpr int rd = decltype(bsel)::value * 128, wr = 128 - rd;
+      double va[kLctaRegIdx], vb[kLctaRegIdx];
+#pragma unroll
+      for (int q = 0; q < kLctaRegIdx; ++q) {
+        va[q] = *reinterpret_cast<const double*>(smb + oa[q] + rd);
+        vb[q] = *reinterpret_cast<const double*>(smb + ob[q] + rd);
+      }
+      double ya = tree_sum<kLctaRegIdx>(va), yb = tree_sum<kLctaRegIdx>(vb);
+      for (int g = kLctaRegIdx; g < rna || g < rnb; g += 4) {  // rows above kLctaRegIdx in-edges
+        double wa[4], wb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wa[q] = g + q < rna ? *reinterpret_cast<const double*>(smb + 8 * lcta_il(es[ra0 + g + q]) + rd) : 0.0;
+          wb[q] = g + q < rnb ? *reinterpret_cast<const double*>(smb + 8 * lcta_il(es[rb0 + g + q]) + rd) : 0.0;
+        }
+        ya += tree_sum<4>(wa);
+        yb += tree_sum<4>(wb);
+      }
+      unsigned long long lmax = 0ull;
+      if (rl0) {
+        rrk0 += ya;
+        *reinterpret_cast<double*>(const_cast<char*>(smb) + own0 + wr) = rpl0 * ya;
+        lmax = dbits(ya);
+      }
+      if (rl1) {
+        rrk1 += yb;
+        *reinterpret_cast<double*>(const_cast<char*>(smb) + own1 + wr) = rpl1 * yb;
+        lmax = max(lmax, dbits(yb));
+      }
+      const double mx = bitsd(block_max_bits(lmax, rb2[it & 1]));
+      ++it;
+      if (it > cap) {
+        fail = true;
+        return true;
+      }
+      return !(mx >= tol);
+    };
+    for (;;) {
+      if (step(std::integral_constant<int, 0>{})) break;
+      if (step(std::integral_constant<int, 1>{})) break;
+    }
+  } else
   for (;;) {
 #ifdef LR_LCTA_PROBE
     cyc_t0 = clock64();
