@@ -77,6 +77,7 @@ struct LevelTasks {
   int xh0 = 0, xh1 = 0;  // split cross rows (more than kCrossSplit in-edges)
   int sb0 = 0, sb1 = 0, sb_max = 0;  // SccSmall units beyond shared memory
   int lt0 = 0, lt1 = 0;  // CTA tasks of the fused level kernel
+  int xb0 = 0, xb1 = 0;  // row tasks: start weights of the level's largest k_cac_big CACs (side stream)
   size_t smem = 0;       // its dynamic shared memory
   size_t big_smem = 0;   // dynamic shared memory of the k_cac_big launch
   size_t sm_tile = 0;    // largest small_solve_tile footprint of the level
@@ -250,6 +251,11 @@ struct lr_ctx {
     if (comm) nccl().comm_destroy(comm);
   }
 };
+
+static bool LR_NO_PREGATHER() {  // A/B switch: LR_PREGATHER=0 keeps the start weights inside k_cac_big
+  const char* e = std::getenv("LR_PREGATHER");
+  return e && std::atoi(e) == 0;
+}
 
 // In-edge order of a CTA power-series unit run by lcta_solve_staged's register
 // rows: lane l of a warp loads the q-th in-edge of its row in the warp's q-th
@@ -636,6 +642,17 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     for (int i = T.sm0; i < T.sm1; ++i) ltasks.push_back(LevelTask{kTaskSmall, i, i + 1, 0});
     for (int i = T.lc0; i < T.lc1; ++i) ltasks.push_back(LevelTask{kTaskLcta, i, i + 1, 0});
     T.lt1 = static_cast<int>(ltasks.size());
+    // a CAC of more than kCacPregatherRows rows would gather its start weights
+    // in 32-row rounds of one CTA: row tasks over many CTAs do it first
+    T.xb0 = T.lt1;
+    for (int i = T.cac_b0; i < T.cac_b1; ++i) {
+      CacTask& t = cac_w[static_cast<size_t>(i)];
+      if (t.row_end - t.row_begin <= kCacPregatherRows || LR_NO_PREGATHER()) continue;
+      t.pregathered = 1;
+      for (int r = t.row_begin; r < t.row_end; r += 256)
+        ltasks.push_back(LevelTask{kTaskRows, r, std::min(t.row_end, r + 256), 0});
+    }
+    T.xb1 = static_cast<int>(ltasks.size());
     const size_t ld = static_cast<size_t>(T.sm_max) + 1;
     T.smem = std::max(T.sm_max > 0 ? ld * (ld + 1) * sizeof(double) : 0,
                       static_cast<size_t>(3) * static_cast<size_t>(T.lc_max) * sizeof(double));
@@ -813,7 +830,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   long long prof_cnt[5] = {0, 0, 0, 0, 0};
   if (prof_on) {
     int most = 1;
-    for (const LevelTasks& T : ctx->lt) most = std::max(most, T.lt1 - T.lt0);
+    for (const LevelTasks& T : ctx->lt) most = std::max({most, T.lt1 - T.lt0, T.xb1 - T.xb0});
     LR_CUDA_TRY(prof_buf.alloc(static_cast<size_t>(3 * most)));
     LR_CUDA_TRY(set_level_prof(prof_buf.p));
   }
@@ -844,6 +861,12 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     if (fork) {
       LR_CUDA_TRY(cudaEventRecord(ctx->fork_ev, s));
       LR_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+      if (T.xb1 > T.xb0) {
+        launch_level(L, ctx->ltasks.p + T.xb0, T.xb1 - T.xb0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
+                     0, 0, kRowTaskSmem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, ctx->unit_iters.p,
+                     ctx->status.p, false, ctx->side);
+        ++nl;
+      }
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
                      ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side);
       LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));

@@ -83,7 +83,7 @@ struct CacTask {
   int row_end;
   long long depth_begin;  // into depth_ptr
   int ndepth;
-  int pad;
+  int pregathered;  // start weights gathered by row tasks launched before (k_cac_big skips its own)
 };
 struct SccTask {
   int row_begin;
@@ -111,6 +111,7 @@ constexpr int kCrossSeg = 256;     // in-edges per warp task of a split row (8 p
 constexpr int kTileNnzCross = 256; // cross in-edges per chunk of a row task (level.cu cross_rows_tiled)
 constexpr size_t kRowTaskSmem = 8 * kTileNnzCross * sizeof(double);  // k_level smem a row task needs
 constexpr size_t kBigCrossSmem = 32 * kTileNnzCross * sizeof(double);  // k_cac_big's warp-tiled start weights
+constexpr int kCacPregatherRows = 4096;  // larger k_cac_big CACs: start weights by grid-wide row tasks first
 
 // One CTA of the fused per-level kernel (level.cu).
 enum LevelTaskType : int { kTaskRows = 0, kTaskCacWarps = 1, kTaskCacBlock = 2, kTaskSmall = 3, kTaskLcta = 4 };

@@ -1260,8 +1260,10 @@ __global__ void __launch_bounds__(kBigThreads)
   // the CAC's own start weights (rows above kCrossSplit cross in-edges were
   // done by k_pull_heavy before the level), so the launch runs concurrently
   // with the level's k_level on a side stream
-  cross_rows_cta(L, ct.row_begin, ct.row_end, w, p->c, pf, rank, s0, sm, smem_bytes, kBigThreads / 32);
-  __syncthreads();
+  if (!ct.pregathered) {
+    cross_rows_cta(L, ct.row_begin, ct.row_end, w, p->c, pf, rank, s0, sm, smem_bytes, kBigThreads / 32);
+    __syncthreads();
+  }
   const int m = ct.row_end - ct.row_begin;
   const long long ne = L.iptr[ct.row_end] - L.iptr[ct.row_begin];
   if (cac_stage_bytes(m, ne) <= smem_bytes)
