@@ -154,6 +154,13 @@ __host__ __device__ inline bool small_tile_ok(int m, double c) {
 // shared memory of the tile solve: m x small_tile_ld(m) matrix, m solution values,
 // the unit's ne in-edges (value + column)
 __host__ __device__ constexpr int small_tile_ld(int m) { return (m + 32) | 1; }
+// SccSmall units up to this many rows: block Gauss-Jordan on FP64 tensor cores
+// (level.cu small_solve_mma); its shared memory: the 64 x 72 system, 64
+// solution values, the unit's in-edges
+constexpr int kSmallMmaMaxM = 64;
+__host__ __device__ constexpr size_t small_mma_bytes(long long ne) {
+  return (64 * 72 + 64) * sizeof(double) + static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
+}
 __host__ __device__ constexpr size_t small_tile_bytes(int m, long long ne) {
   return (static_cast<size_t>(m) * static_cast<size_t>(small_tile_ld(m)) + static_cast<size_t>(m)) * sizeof(double) +
          static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));

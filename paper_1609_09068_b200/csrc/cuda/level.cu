@@ -720,11 +720,190 @@ __device__ void small_solve_tile(const DeviceLayout& L, const SccTask& t, const 
   }
 }
 
+// ------------------------------------------------------------------ K5b
+// SccSmall units of up to 64 rows: block Gauss-Jordan on 8 x 8 tiles with the
+// FP64 tensor cores (DMMA m8n8k4).  The system [I - cA^T | w], padded to
+// 64 x 72 (rows and columns past m: identity; the right-hand side in column
+// 64), lives in the accumulators: warp w holds row tile w, nine column tiles
+// of two doubles per lane, for the whole solve.  Block step k: warp k's row
+// block R and every warp's column block C go to shared memory, every warp
+// inverts the 8 x 8 pivot block P (strictly diagonally dominant by columns:
+// no pivoting) in registers, R' = P^-1 R (DMMA), and every other row tile
+// takes the rank-8 update -= C R' (18 DMMA per warp); row tile k becomes R'.
+// Shared-memory traffic per step is the two blocks, not the trailing matrix,
+// so eight steps replace 64 port-bound pivots.  Not bit-exact (the reference's
+// LU differs by rounding): the residual check of solvers.cpp:103-106 follows.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const double* __restrict__ pf,
+                                double* rank, double* sm, unsigned long long* red, DevStatus* st) {
+  constexpr int W = 72;  // columns of the padded system (9 tiles)
+  static_assert(kWarpsPer == 8, "one 8-row tile per warp");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;  // fragment row / column pair
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  const long long eb = L.iptr[rb];
+  const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  double* M = sm;           // 64 x 72 build area, then the step buffers
+  double* x = M + 64 * W;   // solution
+  double* ev = x + 64;      // in-edge values and columns (residual check)
+  int* es = reinterpret_cast<int*>(ev + ne);
+  const bool mine = tid < m;
+  double wb = 0.0;
+  int e0 = 0, e1 = 0;
+  if (mine) {
+    wb = rank[rb + tid];
+    e0 = static_cast<int>(L.iptr[rb + tid] - eb);
+    e1 = static_cast<int>(L.iptr[rb + tid + 1] - eb);
+  }
+  for (int i = tid; i < 64 * W; i += kThreads) M[i] = (i / W == i % W) ? 1.0 : 0.0;
+  __syncthreads();
+  if (mine) {
+    double* Mr = M + tid * W;
+    Mr[64] = wb;
+    for (int e = e0; e < e1; ++e) {
+      const int s = L.isrc[eb + e];
+      const double v = pf[s];
+      es[e] = s - rb;
+      ev[e] = v;
+      Mr[s - rb] -= v;
+    }
+  }
+  __syncthreads();
+  double acc[9][2];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    acc[j][0] = M[(8 * warp + g) * W + 8 * j + 2 * tq];
+    acc[j][1] = M[(8 * warp + g) * W + 8 * j + 2 * tq + 1];
+  }
+  double* Rb = M;            // 8 x 72: pivot row block
+  double* Cb = M + 8 * W;    // 64 x 8: pivot column block
+  double* Rp = Cb + 64 * 8;  // 8 x 72: P^-1 R
+  const int nb = (m + 7) >> 3;
+  for (int kb = 0; kb < nb; ++kb) {
+    __syncthreads();  // the previous step's readers of Rb / Cb / Rp are done
+    if (warp == kb) {
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        Rb[g * W + 8 * j + 2 * tq] = acc[j][0];
+        Rb[g * W + 8 * j + 2 * tq + 1] = acc[j][1];
+      }
+    }
+    {  // column block kb of this row tile (acc[kb], kb warp-uniform)
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j == kb) {
+          c0 = acc[j][0];
+          c1 = acc[j][1];
+        }
+      Cb[(8 * warp + g) * 8 + 2 * tq] = c0;
+      Cb[(8 * warp + g) * 8 + 2 * tq + 1] = c1;
+    }
+    __syncthreads();
+    // P^-1 by Gauss-Jordan on [P | I] in registers: lane holds P[g][2tq..2tq+1]
+    double p0 = Rb[g * W + 8 * kb + 2 * tq], p1 = Rb[g * W + 8 * kb + 2 * tq + 1];
+    double q0 = g == 2 * tq ? 1.0 : 0.0, q1 = g == 2 * tq + 1 ? 1.0 : 0.0;
+#pragma unroll
+    for (int pv = 0; pv < 8; ++pv) {
+      const int src = pv * 4 + tq;  // row pv, my columns
+      const double rp0 = __shfl_sync(0xffffffffu, p0, src), rp1 = __shfl_sync(0xffffffffu, p1, src);
+      const double rq0 = __shfl_sync(0xffffffffu, q0, src), rq1 = __shfl_sync(0xffffffffu, q1, src);
+      const double piv = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, pv * 4 + (pv >> 1));
+      const double f = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, g * 4 + (pv >> 1));  // P[g][pv]
+      const double inv = 1.0 / piv;
+      if (g == pv) {
+        p0 = rp0 * inv;
+        p1 = rp1 * inv;
+        q0 = rq0 * inv;
+        q1 = rq1 * inv;
+      } else {
+        const double r = f * inv;
+        p0 = __fma_rn(-r, rp0, p0);
+        p1 = __fma_rn(-r, rp1, p1);
+        q0 = __fma_rn(-r, rq0, q0);
+        q1 = __fma_rn(-r, rq1, q1);
+      }
+    }
+    // A fragments of P^-1 (row g, columns tq and 4 + tq)
+    const double u0 = __shfl_sync(0xffffffffu, q0, g * 4 + (tq >> 1)), u1 = __shfl_sync(0xffffffffu, q1, g * 4 + (tq >> 1));
+    const double v0 = __shfl_sync(0xffffffffu, q0, g * 4 + 2 + (tq >> 1)),
+                 v1 = __shfl_sync(0xffffffffu, q1, g * 4 + 2 + (tq >> 1));
+    const double ia = (tq & 1) ? u1 : u0, ib = (tq & 1) ? v1 : v0;
+    // R' = P^-1 R: column tile `warp` (and tile 8 by warp 0)
+    for (int j = warp; j < 9; j += kWarpsPer) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma(d0, d1, ia, Rb[tq * W + 8 * j + g]);
+      dmma(d0, d1, ib, Rb[(4 + tq) * W + 8 * j + g]);
+      Rp[g * W + 8 * j + 2 * tq] = d0;
+      Rp[g * W + 8 * j + 2 * tq + 1] = d1;
+    }
+    __syncthreads();
+    if (warp == kb) {
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        acc[j][0] = Rp[g * W + 8 * j + 2 * tq];
+        acc[j][1] = Rp[g * W + 8 * j + 2 * tq + 1];
+      }
+    } else {
+      const double a0 = -Cb[(8 * warp + g) * 8 + tq], a1 = -Cb[(8 * warp + g) * 8 + 4 + tq];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        dmma(acc[j][0], acc[j][1], a0, Rp[tq * W + 8 * j + g]);
+        dmma(acc[j][0], acc[j][1], a1, Rp[(4 + tq) * W + 8 * j + g]);
+      }
+    }
+  }
+  // x = column 64 (the pivot blocks are now I up to rounding)
+  if (tq == 0 && 8 * warp + g < m) x[8 * warp + g] = acc[8][0];
+  __syncthreads();
+  unsigned long long res = 0, wm = 0, xm = 0;
+  if (mine) {
+    const double xb = x[tid];
+    double acc_r = xb;
+    for (int e = e0; e < e1; ++e) acc_r -= ev[e] * x[es[e]];
+    res = dbits(fabs(acc_r - wb));
+    wm = dbits(fabs(wb));
+    xm = dbits(fabs(xb));
+    rank[rb + tid] = xb;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    res = max(res, __shfl_xor_sync(0xffffffffu, res, o));
+    wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    xm = max(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+  }
+  if (lane == 0) {
+    red[warp] = res;
+    red[8 + warp] = wm;
+    red[16 + warp] = xm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < kWarpsPer; ++i) {
+      res = max(res, red[i]);
+      wm = max(wm, red[8 + i]);
+      xm = max(xm, red[16 + i]);
+    }
+    if (!(bitsd(res) <= 1e-8 * (1.0 + bitsd(wm) + bitsd(xm)))) atomicOr(&st->err, kErrDegen);
+  }
+}
+
+#ifndef LR_SMALL_MMA
+#define LR_SMALL_MMA 1
+#endif
+
 __device__ void small_dispatch(const DeviceLayout& L, const SccTask& t, int ld, double c,
                                const double* __restrict__ pf, double* rank, double* sm, double* red, DevStatus* st) {
   const int m = t.row_end - t.row_begin;
   auto* r = reinterpret_cast<unsigned long long*>(red);
-  if (!small_tile_ok(m, c))
+  if (LR_SMALL_MMA && m <= kSmallMmaMaxM)
+    small_solve_mma(L, t, pf, rank, sm, r, st);
+  else if (!small_tile_ok(m, c))
     small_solve(L, t, ld, pf, rank, sm, red, st);
   else if (m <= 32)
     small_solve_tile<1>(L, t, pf, rank, sm, r, st);

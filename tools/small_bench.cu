@@ -114,7 +114,9 @@ int main(int argc, char** argv) {
   const size_t smem = static_cast<size_t>(ld) * (ld + 1) * sizeof(double);
   CK(cudaFuncSetAttribute(k_bench_prod, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(k_bench_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  const size_t tsmem = m <= kSmallTileMaxM ? small_tile_bytes(m, static_cast<long long>(isrc.size() / K) + 64) : smem;
+  const size_t tsmem = m <= kSmallTileMaxM ? std::max(small_tile_bytes(m, static_cast<long long>(isrc.size() / K) + 64),
+                                                      small_mma_bytes(static_cast<long long>(isrc.size() / K) + 64))
+                                           : smem;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
