@@ -760,7 +760,8 @@ __device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const d
     e0 = static_cast<int>(L.iptr[rb + tid] - eb);
     e1 = static_cast<int>(L.iptr[rb + tid + 1] - eb);
   }
-  for (int i = tid; i < 64 * W; i += kThreads) M[i] = (i / W == i % W) ? 1.0 : 0.0;
+  for (int r = warp; r < 64; r += kWarpsPer)  // identity (no integer division per entry)
+    for (int cidx = lane; cidx < W; cidx += 32) M[r * W + cidx] = cidx == r ? 1.0 : 0.0;
   __syncthreads();
   if (mine) {
     double* Mr = M + tid * W;
@@ -815,7 +816,12 @@ __device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const d
       const double rq0 = __shfl_sync(0xffffffffu, q0, src), rq1 = __shfl_sync(0xffffffffu, q1, src);
       const double piv = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, pv * 4 + (pv >> 1));
       const double f = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, g * 4 + (pv >> 1));  // P[g][pv]
-      const double inv = 1.0 / piv;
+      // 1 / piv: hardware reciprocal plus two Newton steps (~1 ulp; a division is
+      // ~90 cycles on this chain)
+      double inv;
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(piv));
+      inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
+      inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
       if (g == pv) {
         p0 = rp0 * inv;
         p1 = rp1 * inv;
