@@ -105,11 +105,12 @@ def _scc(rng, base, m, deg=4):
 
 
 @pytest.mark.parametrize("m,th,c", [
-    (2, 100, 0.85),      # one pivot pair
-    (3, 100, 0.85),      # a pair, then a single step
-    (33, 100, 0.5),      # A = 2 tile, odd: pairs then a single step
-    (64, 100, 0.85),     # A = 2 tile, 32 pivot pairs
-    (60, 100, 0.85),     # register-tile Bareiss Gauss-Jordan
+    (2, 100, 0.85),      # tensor-core block Gauss-Jordan: one partial 8 x 8 block
+    (8, 100, 0.85),      # one full block
+    (9, 100, 0.85),      # a full block, then a one-row block
+    (33, 100, 0.5),      # five blocks, the last partial
+    (64, 100, 0.85),     # eight blocks, the largest tensor-core system
+    (65, 100, 0.85),     # shared-memory tile, A = 4 (above kSmallMmaMaxM), odd: pairs then a single step
     (127, 200, 0.85),    # tile, A = 4, odd
     (128, 200, 0.99),    # tile, A = 4, largest
     (120, 200, 0.85),    # tile, A = 4
@@ -187,3 +188,19 @@ def test_big_cac_structure_staged(lr, oracle):
     ref = oracle.graph(n, np.asarray(src, np.int32), np.asarray(dst, np.int32), True).compute_pagerank(
         w, 0.85, 1e-12, 100)
     assert np.array_equal(res.ranks[: n - 1], ref.ranks[: n - 1])
+
+
+def test_small_sccs_every_size_with_loops(lr, oracle):
+    # one level of SccSmall units of every size 2..64 (the tensor-core path),
+    # kept self-loops on some rows (diagonal entries other than 1), fed by one
+    # upstream vertex
+    rng = np.random.default_rng(5)
+    src, dst, base = [], [], 1
+    for m in range(2, 65):
+        s1, d1 = _scc(rng, base, m, deg=3)
+        loops = base + np.arange(0, m, 5)
+        src += [s1, loops, [0]]
+        dst += [d1, loops, [base]]
+        base += m
+    w = rng.random(base) + 0.1
+    check(lr, oracle, base, np.concatenate(src), np.concatenate(dst), w=w, keep=True)
