@@ -643,8 +643,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     for (int i = T.sm0; i < T.sm1; ++i) ltasks.push_back(LevelTask{kTaskSmall, i, i + 1, 0});
     for (int i = T.lc0; i < T.lc1; ++i) ltasks.push_back(LevelTask{kTaskLcta, i, i + 1, 0});
     T.lt1 = static_cast<int>(ltasks.size());
-    // a CAC of more than kCacPregatherRows rows would gather its start weights
-    // in 32-row rounds of one CTA: row tasks over many CTAs do it first
+    // a k_cac_big CAC would gather its start weights in 32-row rounds of one
+    // CTA: row tasks over many CTAs do it first
     T.xb0 = T.lt1;
     for (int i = T.cac_b0; i < T.cac_b1; ++i) {
       CacTask& t = cac_w[static_cast<size_t>(i)];

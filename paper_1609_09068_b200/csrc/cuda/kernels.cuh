@@ -111,7 +111,8 @@ constexpr int kCrossSeg = 256;     // in-edges per warp task of a split row (8 p
 constexpr int kTileNnzCross = 256; // cross in-edges per chunk of a row task (level.cu cross_rows_tiled)
 constexpr size_t kRowTaskSmem = 8 * kTileNnzCross * sizeof(double);  // k_level smem a row task needs
 constexpr size_t kBigCrossSmem = 32 * kTileNnzCross * sizeof(double);  // k_cac_big's warp-tiled start weights
-constexpr int kCacPregatherRows = 4096;  // larger k_cac_big CACs: start weights by grid-wide row tasks first
+constexpr int kCacPregatherRows = 1024;  // larger CACs (all of k_cac_big's): start weights by row tasks first
+                                         // (config 4: 34.6 ms at 4096, 32.1 ms at 2048 and 1024)
 
 // One CTA of the fused per-level kernel (level.cu).
 enum LevelTaskType : int { kTaskRows = 0, kTaskCacWarps = 1, kTaskCacBlock = 2, kTaskSmall = 3, kTaskLcta = 4 };
