@@ -250,19 +250,21 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
   const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
   double* sr = static_cast<double*>(stage);
   int* rp = reinterpret_cast<int*>(sr + m);
-  int* es = rp + m + 1;
-  int* ed = es + ne;
-  std::uint8_t* lp = reinterpret_cast<std::uint8_t*>(ed + ne);  // kept self-loop flags
-  // staging: four rows / in-edges per thread in flight
+  int* rd = rp + m + 1;  // walk out-degree of every row (parents are rows of the CAC)
+  int* es = rd + m;
+  std::uint8_t* lp = reinterpret_cast<std::uint8_t*>(es + ne);  // kept self-loop flags
+  // staging: four rows / in-edges per thread in flight, no dependent loads
   for (int i0 = tid; i0 < m; i0 += 4 * width) {
     double rv[4];
     long long pv[4];
+    int dv[4];
     std::uint8_t fv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int i = min(i0 + q * width, m - 1);
       rv[q] = rank[rb + i];
       pv[q] = __ldg(L.iptr + rb + i);
+      dv[q] = __ldg(L.deg + rb + i);
       fv[q] = __ldg(L.loop + rb + i);
     }
 #pragma unroll
@@ -271,25 +273,19 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       if (i < m) {
         sr[i] = rv[q];
         rp[i] = static_cast<int>(pv[q] - eb);
+        rd[i] = dv[q];
         lp[i] = fv[q];
       }
     }
   }
   if (tid == 0) rp[m] = ne;
   for (int e0 = tid; e0 < ne; e0 += 4 * width) {
-    int sv[4], dv[4];
+    int sv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) sv[q] = __ldg(L.isrc + eb + min(e0 + q * width, ne - 1));
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dv[q] = __ldg(L.deg + sv[q]);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = e0 + q * width;
-      if (e < ne) {
-        es[e] = sv[q] - rb;
-        ed[e] = dv[q];
-      }
-    }
+    for (int q = 0; q < 4; ++q)
+      if (e0 + q * width < ne) es[e0 + q * width] = sv[q] - rb;
   }
   auto sync = [&] {
     if (kBlock) {
@@ -307,8 +303,11 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       const int e0 = rp[i], e1 = rp[i + 1];
       if (e1 - e0 > kCrossLight) continue;
       double acc = sr[i];
-      for (int e = e0; e < e1; ++e) acc += sr[es[e]] * c / static_cast<double>(ed[e]);
-      sr[i] = lp[i] ? acc / (1.0 - c / static_cast<double>(L.deg[rb + i])) : acc;
+      for (int e = e0; e < e1; ++e) {
+        const int sp = es[e];
+        acc += sr[sp] * c / static_cast<double>(rd[sp]);
+      }
+      sr[i] = lp[i] ? acc / (1.0 - c / static_cast<double>(rd[i])) : acc;
     }
     for (int base = s0 + wid * 32; base < s1; base += nw * 32) {
       const int i = base + lane;
@@ -319,11 +318,14 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
         mask &= mask - 1;
         const int row = base + src;
         double y = 0.0;
-        for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) y += sr[es[e]] * c / static_cast<double>(ed[e]);
+        for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) {
+          const int sp = es[e];
+          y += sr[sp] * c / static_cast<double>(rd[sp]);
+        }
         y = warp_sum(y);
         if (lane == 0) {
           const double a = sr[row] + y;
-          sr[row] = lp[row] ? a / (1.0 - c / static_cast<double>(L.deg[rb + row])) : a;
+          sr[row] = lp[row] ? a / (1.0 - c / static_cast<double>(rd[row])) : a;
         }
       }
     }
@@ -407,7 +409,7 @@ __host__ __device__ constexpr size_t cac_compact_bytes(long long m, long long ne
 
 // bytes cac_sweep_staged needs for a CAC of m rows and ne in-edges
 __host__ __device__ constexpr size_t cac_stage_bytes(long long m, long long ne) {
-  return static_cast<size_t>(m) * 9 + static_cast<size_t>(m + 1) * 4 + static_cast<size_t>(ne) * 8 + 16;
+  return static_cast<size_t>(m) * 13 + static_cast<size_t>(m + 1) * 4 + static_cast<size_t>(ne) * 4 + 16;
 }
 
 // ------------------------------------------------------------------ K5
