@@ -120,6 +120,16 @@ __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const dou
   }
   const bool light = mine && hi - lo <= kCrossLight;  // heavier rows: k_pull_heavy
   double acc = light ? w[L.vertex_of[row]] : 0.0;
+  // the finish's per-row operands, loaded now (off the gather chain)
+  std::uint8_t kind = 0, lp = 0;
+  int dg = 1;
+  double pfr = 0.0;
+  if (light) {
+    kind = L.rowkind[row];
+    lp = L.loop[row];
+    dg = L.deg[row];
+    pfr = pf[row];
+  }
   for (long long cb = base; cb < end; cb += kTileNnzCross) {
     const int n = static_cast<int>(min(static_cast<long long>(kTileNnzCross), end - cb));
     int src[kTileNnzCross / 32];
@@ -147,7 +157,11 @@ __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const dou
     }
     __syncwarp();
   }
-  if (light) row_finish(L, row, acc, c, pf, rank, s0);
+  if (light) {  // row_finish with the prefetched operands
+    if (kind == kSingle && lp) acc /= 1.0 - c / static_cast<double>(dg);
+    rank[row] = acc;
+    if (kind == kLargeGrid) s0[row] = pfr * acc;
+  }
 }
 
 // a row task: 32 rows per warp of the CTA
