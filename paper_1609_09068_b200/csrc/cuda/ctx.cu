@@ -498,6 +498,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           // the tile solve, or the normalised one where small_tile_ok(m, c) fails
           if (m <= kSmallTileMaxM) T.sm_tile = std::max(T.sm_tile, small_tile_bytes(m, L->iptr[re] - L->iptr[rb]));
           if (m <= kSmallMmaMaxM) T.sm_tile = std::max(T.sm_tile, small_mma_bytes(L->iptr[re] - L->iptr[rb]));
+          else if (m <= kSmallMmaSmemMaxM)
+            T.sm_tile = std::max(T.sm_tile, small_mma_smem_bytes(m, L->iptr[re] - L->iptr[rb]));
           T.sm_max = std::max(T.sm_max, m);
         } else {  // beyond shared memory: global-scratch kernel after the level kernel
           small_big.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});

@@ -162,6 +162,16 @@ constexpr int kSmallMmaMaxM = 64;
 __host__ __device__ constexpr size_t small_mma_bytes(long long ne) {
   return (64 * 72 + 64) * sizeof(double) + static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
 }
+// up to this many rows: the block Gauss-Jordan with the system in shared memory
+// (small_solve_mma_smem): mp x (mp + 8) system, mp x 8 column block, 8 x (mp + 8)
+// row block, mp solution values, the in-edges (mp = m rounded up to 8)
+constexpr int kSmallMmaSmemMaxM = 128;
+__host__ __device__ constexpr size_t small_mma_smem_bytes(int m, long long ne) {
+  return (static_cast<size_t>((m + 7) & ~7) * static_cast<size_t>(((m + 7) & ~7) + 16) +
+          static_cast<size_t>((m + 7) & ~7) * 8 + 8 * static_cast<size_t>(((m + 7) & ~7) + 16) +
+          static_cast<size_t>((m + 7) & ~7)) * sizeof(double) +
+         static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
+}
 __host__ __device__ constexpr size_t small_tile_bytes(int m, long long ne) {
   return (static_cast<size_t>(m) * static_cast<size_t>(small_tile_ld(m)) + static_cast<size_t>(m)) * sizeof(double) +
          static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));

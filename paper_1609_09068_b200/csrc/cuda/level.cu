@@ -755,6 +755,45 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// The inverse of an 8 x 8 pivot block by Gauss-Jordan on [P | I] in
+// registers (no pivoting: the blocks are strictly diagonally dominant by
+// columns).  Lane (g, tq) holds P[g][2tq], P[g][2tq+1]; returns its A fragments
+// of P^-1 for DMMA m8n8k4 (row g, columns tq and 4 + tq).
+__device__ __forceinline__ void pivot_block_inverse(double p0, double p1, int g, int tq, double& ia, double& ib) {
+  double q0 = g == 2 * tq ? 1.0 : 0.0, q1 = g == 2 * tq + 1 ? 1.0 : 0.0;
+#pragma unroll
+  for (int pv = 0; pv < 8; ++pv) {
+    const int src = pv * 4 + tq;  // row pv, my columns
+    const double rp0 = __shfl_sync(0xffffffffu, p0, src), rp1 = __shfl_sync(0xffffffffu, p1, src);
+    const double rq0 = __shfl_sync(0xffffffffu, q0, src), rq1 = __shfl_sync(0xffffffffu, q1, src);
+    const double piv = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, pv * 4 + (pv >> 1));
+    const double f = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, g * 4 + (pv >> 1));  // P[g][pv]
+    // 1 / piv: hardware reciprocal plus two Newton steps (~1 ulp; a division is
+    // ~90 cycles on this chain)
+    double inv;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(piv));
+    inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
+    inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
+    if (g == pv) {
+      p0 = rp0 * inv;
+      p1 = rp1 * inv;
+      q0 = rq0 * inv;
+      q1 = rq1 * inv;
+    } else {
+      const double r = f * inv;
+      p0 = __fma_rn(-r, rp0, p0);
+      p1 = __fma_rn(-r, rp1, p1);
+      q0 = __fma_rn(-r, rq0, q0);
+      q1 = __fma_rn(-r, rq1, q1);
+    }
+  }
+  const double u0 = __shfl_sync(0xffffffffu, q0, g * 4 + (tq >> 1)), u1 = __shfl_sync(0xffffffffu, q1, g * 4 + (tq >> 1));
+  const double v0 = __shfl_sync(0xffffffffu, q0, g * 4 + 2 + (tq >> 1)),
+               v1 = __shfl_sync(0xffffffffu, q1, g * 4 + 2 + (tq >> 1));
+  ia = (tq & 1) ? u1 : u0;
+  ib = (tq & 1) ? v1 : v0;
+}
+
 __device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const double* __restrict__ pf,
                                 double* rank, double* sm, unsigned long long* red, DevStatus* st) {
   constexpr int W = 72;  // columns of the padded system (9 tiles)
@@ -822,40 +861,9 @@ __device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const d
       Cb[(8 * warp + g) * 8 + 2 * tq + 1] = c1;
     }
     __syncthreads();
-    // P^-1 by Gauss-Jordan on [P | I] in registers: lane holds P[g][2tq..2tq+1]
-    double p0 = Rb[g * W + 8 * kb + 2 * tq], p1 = Rb[g * W + 8 * kb + 2 * tq + 1];
-    double q0 = g == 2 * tq ? 1.0 : 0.0, q1 = g == 2 * tq + 1 ? 1.0 : 0.0;
-#pragma unroll
-    for (int pv = 0; pv < 8; ++pv) {
-      const int src = pv * 4 + tq;  // row pv, my columns
-      const double rp0 = __shfl_sync(0xffffffffu, p0, src), rp1 = __shfl_sync(0xffffffffu, p1, src);
-      const double rq0 = __shfl_sync(0xffffffffu, q0, src), rq1 = __shfl_sync(0xffffffffu, q1, src);
-      const double piv = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, pv * 4 + (pv >> 1));
-      const double f = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, g * 4 + (pv >> 1));  // P[g][pv]
-      // 1 / piv: hardware reciprocal plus two Newton steps (~1 ulp; a division is
-      // ~90 cycles on this chain)
-      double inv;
-      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(piv));
-      inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
-      inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
-      if (g == pv) {
-        p0 = rp0 * inv;
-        p1 = rp1 * inv;
-        q0 = rq0 * inv;
-        q1 = rq1 * inv;
-      } else {
-        const double r = f * inv;
-        p0 = __fma_rn(-r, rp0, p0);
-        p1 = __fma_rn(-r, rp1, p1);
-        q0 = __fma_rn(-r, rq0, q0);
-        q1 = __fma_rn(-r, rq1, q1);
-      }
-    }
-    // A fragments of P^-1 (row g, columns tq and 4 + tq)
-    const double u0 = __shfl_sync(0xffffffffu, q0, g * 4 + (tq >> 1)), u1 = __shfl_sync(0xffffffffu, q1, g * 4 + (tq >> 1));
-    const double v0 = __shfl_sync(0xffffffffu, q0, g * 4 + 2 + (tq >> 1)),
-                 v1 = __shfl_sync(0xffffffffu, q1, g * 4 + 2 + (tq >> 1));
-    const double ia = (tq & 1) ? u1 : u0, ib = (tq & 1) ? v1 : v0;
+    // P^-1 (A fragments: row g, columns tq and 4 + tq)
+    double ia, ib;
+    pivot_block_inverse(Rb[g * W + 8 * kb + 2 * tq], Rb[g * W + 8 * kb + 2 * tq + 1], g, tq, ia, ib);
     // R' = P^-1 R: column tile `warp` (and tile 8 by warp 0)
     for (int j = warp; j < 9; j += kWarpsPer) {
       double d0 = 0.0, d1 = 0.0;
@@ -915,6 +923,120 @@ __device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const d
   }
 }
 
+// SccSmall units of 65..kSmallMmaSmemMaxM rows: the same block Gauss-Jordan
+// with the system in shared memory (mp x (mp + 8), mp = m rounded up to 8, the
+// right-hand side in column mp): per block step every 8 x 8 tile is read and
+// written once (2 DMMA in between), a quarter of the paired-pivot tile solve's
+// traffic, and ceil(m/8) pivot-block chains instead of m pivots.
+__device__ void small_solve_mma_smem(const DeviceLayout& L, const SccTask& t, const double* __restrict__ pf,
+                                     double* rank, double* sm, unsigned long long* red, DevStatus* st) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int rb = t.row_begin, m = t.row_end - t.row_begin;
+  // row stride = 8 mod 16 doubles: a tile's 16-byte row pieces hit distinct bank quads
+  const int mp = (m + 7) & ~7, W = mp + ((mp & 15) ? 16 : 8), nrt = mp >> 3, nct = W >> 3;
+  const long long eb = L.iptr[rb];
+  const int ne = static_cast<int>(L.iptr[t.row_end] - eb);
+  double* M = sm;                       // mp x W system
+  double* Cb = M + mp * W;              // mp x 8 pivot column block
+  double* Rp = Cb + mp * 8;             // 8 x W: P^-1 R
+  double* x = Rp + 8 * W;               // solution
+  double* ev = x + mp;                  // in-edge values and columns (residual check)
+  int* es = reinterpret_cast<int*>(ev + ne);
+  const bool mine = tid < m;
+  double wb = 0.0;
+  int e0 = 0, e1 = 0;
+  if (mine) {
+    wb = rank[rb + tid];
+    e0 = static_cast<int>(L.iptr[rb + tid] - eb);
+    e1 = static_cast<int>(L.iptr[rb + tid + 1] - eb);
+  }
+  for (int r = warp; r < mp; r += kWarpsPer)
+    for (int cidx = lane; cidx < W; cidx += 32) M[r * W + cidx] = cidx == r ? 1.0 : 0.0;
+  __syncthreads();
+  if (mine) {
+    double* Mr = M + tid * W;
+    Mr[mp] = wb;
+    for (int e = e0; e < e1; ++e) {
+      const int s = L.isrc[eb + e];
+      const double v = pf[s];
+      es[e] = s - rb;
+      ev[e] = v;
+      Mr[s - rb] -= v;
+    }
+  }
+  for (int kb = 0; kb < nrt; ++kb) {
+    __syncthreads();
+    for (int i = tid; i < mp * 8; i += kThreads) Cb[i] = M[(i >> 3) * W + 8 * kb + (i & 7)];
+    __syncthreads();
+    double ia, ib;
+    pivot_block_inverse(M[(8 * kb + g) * W + 8 * kb + 2 * tq], M[(8 * kb + g) * W + 8 * kb + 2 * tq + 1], g, tq, ia, ib);
+    const double* Rb = M + 8 * kb * W;
+    for (int j = warp; j < nct; j += kWarpsPer) {
+      double d0 = 0.0, d1 = 0.0;
+      dmma(d0, d1, ia, Rb[tq * W + 8 * j + g]);
+      dmma(d0, d1, ib, Rb[(4 + tq) * W + 8 * j + g]);
+      Rp[g * W + 8 * j + 2 * tq] = d0;
+      Rp[g * W + 8 * j + 2 * tq + 1] = d1;
+    }
+    __syncthreads();
+    // warp w: row tiles w, w + 8 (<= 16 row tiles), every column tile; two
+    // independent DMMA chains per column tile in flight
+    for (int rt0 = warp; rt0 < nrt; rt0 += 2 * kWarpsPer) {
+      const int rt1 = rt0 + kWarpsPer;
+      const bool has1 = rt1 < nrt;
+      const double a00 = -Cb[(8 * rt0 + g) * 8 + tq], a01 = -Cb[(8 * rt0 + g) * 8 + 4 + tq];
+      const double a10 = has1 ? -Cb[(8 * rt1 + g) * 8 + tq] : 0.0, a11 = has1 ? -Cb[(8 * rt1 + g) * 8 + 4 + tq] : 0.0;
+      for (int ct = 0; ct < nct; ++ct) {
+        const double b0 = Rp[tq * W + 8 * ct + g], b1 = Rp[(4 + tq) * W + 8 * ct + g];
+        const double2 r = *reinterpret_cast<const double2*>(Rp + g * W + 8 * ct + 2 * tq);
+        double2* T0 = reinterpret_cast<double2*>(M + (8 * rt0 + g) * W + 8 * ct + 2 * tq);
+        double2* T1 = reinterpret_cast<double2*>(M + (8 * (has1 ? rt1 : rt0) + g) * W + 8 * ct + 2 * tq);
+        double2 c = *T0, e = *T1;
+        dmma(c.x, c.y, a00, b0);
+        dmma(e.x, e.y, a10, b0);
+        dmma(c.x, c.y, a01, b1);
+        dmma(e.x, e.y, a11, b1);
+        *T0 = rt0 == kb ? r : c;
+        if (has1) *T1 = rt1 == kb ? r : e;
+      }
+    }
+  }
+  __syncthreads();
+  if (mine) x[tid] = M[tid * W + mp];
+  __syncthreads();
+  unsigned long long res = 0, wm = 0, xm = 0;
+  if (mine) {
+    const double xb = x[tid];
+    double acc_r = xb;
+    for (int e = e0; e < e1; ++e) acc_r -= ev[e] * x[es[e]];
+    res = dbits(fabs(acc_r - wb));
+    wm = dbits(fabs(wb));
+    xm = dbits(fabs(xb));
+    rank[rb + tid] = xb;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    res = max(res, __shfl_xor_sync(0xffffffffu, res, o));
+    wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    xm = max(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+  }
+  if (lane == 0) {
+    red[warp] = res;
+    red[8 + warp] = wm;
+    red[16 + warp] = xm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < kWarpsPer; ++i) {
+      res = max(res, red[i]);
+      wm = max(wm, red[8 + i]);
+      xm = max(xm, red[16 + i]);
+    }
+    if (!(bitsd(res) <= 1e-8 * (1.0 + bitsd(wm) + bitsd(xm)))) atomicOr(&st->err, kErrDegen);
+  }
+}
+
 #ifndef LR_SMALL_MMA
 #define LR_SMALL_MMA 1
 #endif
@@ -925,6 +1047,8 @@ __device__ void small_dispatch(const DeviceLayout& L, const SccTask& t, int ld, 
   auto* r = reinterpret_cast<unsigned long long*>(red);
   if (LR_SMALL_MMA && m <= kSmallMmaMaxM)
     small_solve_mma(L, t, pf, rank, sm, r, st);
+  else if (LR_SMALL_MMA && m <= kSmallMmaSmemMaxM)
+    small_solve_mma_smem(L, t, pf, rank, sm, r, st);
   else if (!small_tile_ok(m, c))
     small_solve(L, t, ld, pf, rank, sm, red, st);
   else if (m <= 32)

@@ -115,7 +115,8 @@ int main(int argc, char** argv) {
   CK(cudaFuncSetAttribute(k_bench_prod, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(k_bench_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const size_t tsmem = m <= kSmallTileMaxM ? std::max(small_tile_bytes(m, static_cast<long long>(isrc.size() / K) + 64),
-                                                      small_mma_bytes(static_cast<long long>(isrc.size() / K) + 64))
+                                                      std::max(small_mma_bytes(static_cast<long long>(isrc.size() / K) + 64),
+                                                               small_mma_smem_bytes(m, static_cast<long long>(isrc.size() / K) + 64)))
                                            : smem;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
