@@ -110,13 +110,13 @@ def _scc(rng, base, m, deg=4):
     (9, 100, 0.85),      # a full block, then a one-row block
     (33, 100, 0.5),      # five blocks, the last partial
     (64, 100, 0.85),     # eight blocks, the largest tensor-core system
-    (65, 100, 0.85),     # shared-memory tile, A = 4 (above kSmallMmaMaxM), odd: pairs then a single step
-    (127, 200, 0.85),    # tile, A = 4, odd
-    (128, 200, 0.99),    # tile, A = 4, largest
-    (120, 200, 0.85),    # tile, A = 4
+    (65, 100, 0.85),     # tensor cores, system in shared memory (above kSmallMmaMaxM), one-row last block
+    (127, 200, 0.85),    # tensor cores, shared memory, partial last block
+    (128, 200, 0.99),    # tensor cores, shared memory, largest (kSmallMmaSmemMaxM)
+    (120, 200, 0.85),    # tensor cores, shared memory, row stride 8 mod 16 with a 16-row pad
     (150, 200, 0.85),    # normalised shared-memory Gauss-Jordan (m > kSmallTileMaxM)
     (220, 300, 0.85),    # global-scratch path (m > kSmallSmemMaxM)
-    (100, 200, 0.9999),  # (1-c)^m would underflow the fraction-free minors: normalised path
+    (100, 200, 0.9999),  # c near 1 (the fraction-free tile would underflow): tensor cores, shared memory
 ])
 def test_small_scc_paths(lr, oracle, m, th, c):
     rng = np.random.default_rng(m)
