@@ -1,3 +1,2 @@
-for c in 1 4 2; do
-  python bench.py --config $c > gpurun_out/r1d_bench_cfg$c.json 2> gpurun_out/r1d_bench_cfg$c.err
-done
+# scratch driver for gpurun experiments (tools/build_variant.sh builds A/B libraries)
+timeout 900 python -m pytest tests -m gpu -x -q
