@@ -755,6 +755,28 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// One row of a small system: its in-edges' columns and pf values stashed for
+// the residual check and subtracted from the row (each column once), four
+// in-edges' index and pf loads in flight at a time.
+__device__ __forceinline__ void stage_row_edges(const DeviceLayout& L, const double* __restrict__ pf, int rb,
+                                                long long eb, int e0, int e1, int* es, double* ev, double* Mr) {
+  for (int e = e0; e < e1; e += 4) {
+    int sv[4];
+    double pv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[q] = __ldg(L.isrc + eb + min(e + q, e1 - 1));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) pv[q] = pf[sv[q]];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (e + q < e1) {
+        es[e + q] = sv[q] - rb;
+        ev[e + q] = pv[q];
+        Mr[sv[q] - rb] -= pv[q];
+      }
+  }
+}
+
 // The inverse of an 8 x 8 pivot block by Gauss-Jordan on [P | I] in
 // registers (no pivoting: the blocks are strictly diagonally dominant by
 // columns).  Lane (g, tq) holds P[g][2tq], P[g][2tq+1]; returns its A fragments
@@ -821,13 +843,7 @@ __device__ void small_solve_mma(const DeviceLayout& L, const SccTask& t, const d
   if (mine) {
     double* Mr = M + tid * W;
     Mr[64] = wb;
-    for (int e = e0; e < e1; ++e) {
-      const int s = L.isrc[eb + e];
-      const double v = pf[s];
-      es[e] = s - rb;
-      ev[e] = v;
-      Mr[s - rb] -= v;
-    }
+    stage_row_edges(L, pf, rb, eb, e0, e1, es, ev, Mr);
   }
   __syncthreads();
   double acc[9][2];
@@ -957,13 +973,7 @@ __device__ void small_solve_mma_smem(const DeviceLayout& L, const SccTask& t, co
   if (mine) {
     double* Mr = M + tid * W;
     Mr[mp] = wb;
-    for (int e = e0; e < e1; ++e) {
-      const int s = L.isrc[eb + e];
-      const double v = pf[s];
-      es[e] = s - rb;
-      ev[e] = v;
-      Mr[s - rb] -= v;
-    }
+    stage_row_edges(L, pf, rb, eb, e0, e1, es, ev, Mr);
   }
   for (int kb = 0; kb < nrt; ++kb) {
     __syncthreads();
