@@ -87,7 +87,11 @@ class Graph {
 /// graph.cpp:54-99: "src<TAB>dst" lines, '#' comments, LF/CRLF; dense ids or
 /// compaction in sorted order.  ParseError on malformed or empty input.
 Graph parse_edge_list(std::istream& in, bool dense_ids, LoopPolicy policy = LoopPolicy::Ignore);
-/// graph.cpp:101-105; IoError if the file cannot be opened.
+/// The same format from a byte buffer (the reader behind both entry points:
+/// chunked over the host threads, errors name the first bad line).
+Graph parse_edge_buffer(const char* data, std::size_t len, bool dense_ids,
+                        LoopPolicy policy = LoopPolicy::Ignore);
+/// graph.cpp:101-105 (the file is mmap'ed); IoError if it cannot be opened.
 Graph load_edge_list(const std::string& path, bool dense_ids, LoopPolicy policy = LoopPolicy::Ignore);
 
 /// Worker threads used by the host builders (LR_THREADS env var, else

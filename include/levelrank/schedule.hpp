@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <stdexcept>
 #include <iosfwd>
 #include <utility>
 #include <vector>
@@ -21,6 +22,13 @@ namespace levelrank {
 inline namespace b200 {
 
 enum class UnitKind : std::uint8_t { SingletonGroup, Cac, SccSmall, SccLarge };
+
+/// solvers.cpp:84-85 throws std::logic_error when a CAC never drains; this
+/// subtype lets the C-ABI tell it apart from other logic errors.
+class CycleError : public std::logic_error {
+ public:
+  using std::logic_error::logic_error;
+};
 
 struct SolveUnit {
   UnitKind kind = UnitKind::SingletonGroup;

@@ -48,8 +48,13 @@ lr_status lr_graph_from_edges(int32_t n, const int32_t* src, const int32_t* dst,
 /* Adopt a CSR with sorted, duplicate-free rows (checked). */
 lr_status lr_graph_from_csr(int32_t n, const int64_t* offsets, const int32_t* targets,
                             int keep_loops, lr_graph** out);
-/* load_edge_list (proj/src/graph.cpp:101-105 -> parse_edge_list :54-99). */
+/* load_edge_list (proj/src/graph.cpp:101-105 -> parse_edge_list :54-99):
+ * the file is mmap'ed and parsed by all host threads; LR_EIO with
+ * "line N: ..." for the first malformed line, as the reference reports it. */
 lr_status lr_graph_load_edge_list(const char* path, int dense_ids, int keep_loops, lr_graph** out);
+/* parse_edge_list (proj/src/graph.cpp:54-99) over an in-memory byte buffer. */
+lr_status lr_graph_parse_edge_buffer(const char* data, int64_t len, int dense_ids, int keep_loops,
+                                     lr_graph** out);
 int32_t lr_graph_vertex_count(const lr_graph* g);
 int64_t lr_graph_edge_count(const lr_graph* g);
 /* CSR export; any pointer may be NULL.  walk_deg = Graph::walk_out_degree. */

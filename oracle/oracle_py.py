@@ -295,6 +295,10 @@ class Ref(_Lib):
         lib.lrref_graph_new.argtypes = [C.c_int32, I32P, I32P, C.c_int64, C.c_int]
         lib.lrref_graph_new.restype = C.c_void_p
         lib.lrref_graph_free.argtypes = [C.c_void_p]
+        lib.lrref_graph_parse.argtypes = [C.c_char_p, C.c_int64, C.c_int]
+        lib.lrref_graph_parse.restype = C.c_void_p
+        lib.lrref_graph_vertex_count.argtypes = [C.c_void_p]
+        lib.lrref_graph_vertex_count.restype = C.c_int32
         lib.lrref_graph_edge_count.argtypes = [C.c_void_p]
         lib.lrref_graph_edge_count.restype = C.c_int64
         lib.lrref_graph_csr.argtypes = [C.c_void_p, I64P, I32P, U8P, I32P]
@@ -333,6 +337,13 @@ class Ref(_Lib):
         if not h:
             raise ValueError(self._err())
         return RefGraph(self, h, n)
+
+    def parse(self, data: bytes, dense_ids=True):
+        """parse_edge_list; returns RefGraph, or raises ValueError(message)."""
+        h = self.lib.lrref_graph_parse(data, len(data), int(dense_ids))
+        if not h:
+            raise ValueError(self._err())
+        return RefGraph(self, h, int(self.lib.lrref_graph_vertex_count(h)))
 
     def iteration_cap(self, c, tol):
         return self.lib.lrref_iteration_cap(c, tol)

@@ -5,6 +5,7 @@
 // oracle/Makefile into oracle/_ref/).  It lets the Python tests and the
 // bench's reference arm call the reference's own public API:
 //   Graph::from_edges            proj/src/graph.cpp:14-36
+//   parse_edge_list              proj/src/graph.cpp:54-99
 //   find_components / _scc_only  proj/src/partition.cpp:246-250
 //   build_schedule               proj/src/schedule.cpp:32-137
 //   compute_pagerank             proj/src/engine.cpp:89-182
@@ -18,6 +19,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <mutex>
 #include <stdexcept>
@@ -107,6 +109,17 @@ void* lrref_graph_new(int32_t n, const int32_t* src, const int32_t* dst, int64_t
     std::vector<std::pair<VertexId, VertexId>> e(static_cast<std::size_t>(m));
     for (int64_t i = 0; i < m; ++i) e[static_cast<std::size_t>(i)] = {src[i], dst[i]};
     return new Graph(Graph::from_edges(n, std::move(e), keep ? LoopPolicy::Keep : LoopPolicy::Ignore));
+  } catch (...) {
+    fail_from_current();
+    return nullptr;
+  }
+}
+// parse_edge_list (proj/src/graph.cpp:54-99) on a byte buffer; NULL and the
+// exception message in lrref_last_error() on failure.
+void* lrref_graph_parse(const char* data, int64_t len, int dense_ids) {
+  try {
+    std::istringstream in(std::string(data, static_cast<std::size_t>(len)));
+    return new Graph(parse_edge_list(in, dense_ids != 0));
   } catch (...) {
     fail_from_current();
     return nullptr;

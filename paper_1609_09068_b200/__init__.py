@@ -128,6 +128,7 @@ EXPORTS = {
     "lr_graph_from_edges": (C.c_int, [C.c_int32, I32P, I32P, C.c_int64, C.c_int, C.POINTER(VP)]),
     "lr_graph_from_csr": (C.c_int, [C.c_int32, I64P, I32P, C.c_int, C.POINTER(VP)]),
     "lr_graph_load_edge_list": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(VP)]),
+    "lr_graph_parse_edge_buffer": (C.c_int, [C.c_char_p, C.c_int64, C.c_int, C.c_int, C.POINTER(VP)]),
     "lr_graph_vertex_count": (C.c_int32, [VP]),
     "lr_graph_edge_count": (C.c_int64, [VP]),
     "lr_graph_csr": (C.c_int, [VP, I64P, I32P, U8P, I32P]),
@@ -249,6 +250,14 @@ class Graph:
     def load_edge_list(cls, path, dense_ids=True, loop_policy=LoopPolicy.Ignore):
         h = VP()
         _check(lib().lr_graph_load_edge_list(os.fsencode(path), int(dense_ids), int(loop_policy), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def parse_edge_list(cls, text, dense_ids=True, loop_policy=LoopPolicy.Ignore):
+        """parse_edge_list (graph.cpp:54-99) over a str/bytes buffer."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        h = VP()
+        _check(lib().lr_graph_parse_edge_buffer(data, len(data), int(dense_ids), int(loop_policy), C.byref(h)))
         return cls(h)
 
     @property

@@ -64,9 +64,15 @@ lr_status from_exception() {
   } catch (const std::invalid_argument& e) {
     lrerr::set(e.what());
     return LR_EINVAL;
-  } catch (const std::logic_error& e) {
+  } catch (const CycleError& e) {
     lrerr::set(e.what());
     return LR_ECYCLE;
+  } catch (const std::length_error& e) {
+    lrerr::set(std::string("out of host memory: ") + e.what());
+    return LR_ENOMEM;
+  } catch (const std::logic_error& e) {  // out_of_range, domain_error, internal consistency checks
+    lrerr::set(e.what());
+    return LR_EINVAL;
   } catch (const std::bad_alloc&) {
     lrerr::set("out of host memory");
     return LR_ENOMEM;
@@ -126,6 +132,16 @@ lr_status lr_graph_load_edge_list(const char* path, int dense_ids, int keep_loop
   *out = nullptr;
   return guarded([&] {
     wrap_graph(load_edge_list(path, dense_ids != 0, keep_loops ? LoopPolicy::Keep : LoopPolicy::Ignore), out);
+  });
+}
+
+lr_status lr_graph_parse_edge_buffer(const char* data, int64_t len, int dense_ids, int keep_loops, lr_graph** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (len < 0 || (len > 0 && !data)) throw std::invalid_argument("bad buffer");
+    wrap_graph(parse_edge_buffer(data, static_cast<std::size_t>(len), dense_ids != 0,
+                                 keep_loops ? LoopPolicy::Keep : LoopPolicy::Ignore),
+               out);
   });
 }
 

@@ -1,16 +1,12 @@
 // Graph core: multi-threaded CSR build with Graph::from_edges semantics
-// (proj/src/graph.cpp:14-36: range check, dedup, sorted rows, loop flags) and
-// the edge-list reader (proj/src/graph.cpp:54-105).
+// (proj/src/graph.cpp:14-36: range check, dedup, sorted rows, loop flags).
+// The edge-list reader is in ingest.cpp.
 #include "levelrank/graph.hpp"
 
 #include <algorithm>
 #include <atomic>
-#include <charconv>
 #include <cstdlib>
-#include <fstream>
-#include <istream>
 #include <stdexcept>
-#include <string>
 #include <thread>
 
 #include "parallel.hpp"
@@ -133,58 +129,6 @@ Graph Graph::from_csr(VertexId n, std::vector<EdgeId> offsets, std::vector<Verte
   });
   if (bad) throw std::invalid_argument("CSR rows must be sorted, unique and in range");
   return g;
-}
-
-namespace {
-[[noreturn]] void fail_line(long long line_no, const std::string& what) {
-  throw ParseError("line " + std::to_string(line_no) + ": " + what);
-}
-}  // namespace
-
-Graph parse_edge_list(std::istream& in, bool dense_ids, LoopPolicy policy) {
-  std::vector<VertexId> src, dst;
-  std::string line;
-  long long line_no = 0, max_id = -1;
-  while (std::getline(in, line)) {
-    ++line_no;
-    if (!line.empty() && line.back() == '\r') line.pop_back();
-    if (line.empty() || line.front() == '#') continue;
-    const char* p = line.data();
-    const char* end = p + line.size();
-    long long a = 0, b = 0;
-    const auto r1 = std::from_chars(p, end, a);
-    if (r1.ec != std::errc{} || r1.ptr == end || *r1.ptr != '\t') fail_line(line_no, "expected \"src<TAB>dst\"");
-    const auto r2 = std::from_chars(r1.ptr + 1, end, b);
-    if (r2.ec != std::errc{} || r2.ptr != end) fail_line(line_no, "expected \"src<TAB>dst\"");
-    if (a < 0 || b < 0 || a > kMaxVertexId || b > kMaxVertexId) fail_line(line_no, "vertex id out of range");
-    src.push_back(static_cast<VertexId>(a));
-    dst.push_back(static_cast<VertexId>(b));
-    max_id = std::max({max_id, a, b});
-  }
-  if (src.empty()) throw ParseError("empty input: no edges");
-  if (!dense_ids) {
-    std::vector<VertexId> ids(src);
-    ids.insert(ids.end(), dst.begin(), dst.end());
-    std::sort(ids.begin(), ids.end());
-    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
-    auto compact = [&](VertexId raw) {
-      return static_cast<VertexId>(std::lower_bound(ids.begin(), ids.end(), raw) - ids.begin());
-    };
-    for (std::size_t i = 0; i < src.size(); ++i) {
-      src[i] = compact(src[i]);
-      dst[i] = compact(dst[i]);
-    }
-    return Graph::from_edge_arrays(static_cast<VertexId>(ids.size()), src.data(), dst.data(),
-                                   static_cast<EdgeId>(src.size()), policy);
-  }
-  return Graph::from_edge_arrays(static_cast<VertexId>(max_id + 1), src.data(), dst.data(),
-                                 static_cast<EdgeId>(src.size()), policy);
-}
-
-Graph load_edge_list(const std::string& path, bool dense_ids, LoopPolicy policy) {
-  std::ifstream in(path);
-  if (!in) throw IoError("cannot open " + path);
-  return parse_edge_list(in, dense_ids, policy);
 }
 
 }  // namespace b200

@@ -313,7 +313,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
     }
   });
 
-  if (cycle) throw std::logic_error("cycle inside an acyclic component");
+  if (cycle) throw CycleError("cycle inside an acyclic component");
   clk.mark("CAC Kahn passes");
 
   // rows: units in order; CAC rows by (depth, vertex)
