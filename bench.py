@@ -10,6 +10,8 @@ R3+R1 D2H inside the timed region).
 
   python bench.py [--config 5] [--steps K] [--warmup W] [--gpus N] [--impl ours|reference]
 
+Default workload: config 5 (R-MAT scale 26, the north-star graph).
+
 N>1 runs under torchrun; see DESIGN.md "Multi-GPU" for what is sharded.
 """
 from __future__ import annotations
@@ -98,61 +100,29 @@ def build_graph(lr, cfg, shrink):
     return g, (time.perf_counter() - t0) * 1e3
 
 
+# BASELINE.json configs (same recipes as paper_1609_09068_b200.config_graph and
+# oracle/lr_gen.c; kept here so the reference arm never imports the product)
+WORKLOADS = {
+    1: "planted 100k: 200 SCCs U[16,1024] rescaled to 50k vertices, out-trees, 50k inter edges, 10% dangling",
+    2: "R-MAT scale 20, edge factor 16, (0.57,0.19,0.19,0.05), loops+dups removed",
+    3: "R-MAT scale 23, edge factor 8, then 30% of vertices lose their out-edges",
+    4: "deep DAG: 1000 levels x 16k vertices, SCCs U[2,64] (deg 6) + trees (branch U[1,4]), reach 1..8",
+    5: "R-MAT scale 26, edge factor 16, (0.57,0.19,0.19,0.05), dedup",
+}
+
+
 def workload_name(cfg, shrink):
-    from paper_1609_09068_b200 import CONFIGS
-    return f"config{cfg}" + (f"-shrink{shrink}" if shrink else "") + ": " + CONFIGS[cfg]
+    return f"config{cfg}" + (f"-shrink{shrink}" if shrink else "") + ": " + WORKLOADS[cfg]
+
+
+def config_dict(cfg, shrink, n, m):
+    """The workload, identical in both arms (the driver compares them)."""
+    return {"workload": workload_name(cfg, shrink), "c": C_DAMP, "tol": TOL, "weights": "uniform 1/|V|",
+            "vertices": int(n), "edges": int(m), "small_threshold": 100,
+            "l2": "GPU arm: L2 flushed (512 MB write) before every timed step"}
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_sample(g, lr, eng, budget_s=20.0, threads=None, reps=1, extra_methods=False):
-    """Bounded CPU baseline.  Uses the reference compiled from its own sources
-    (oracle/_ref) when present, else the plain-C port (oracle/).  Sample: the
-    reference level loop (engine.cpp:126-158) over its own schedule with the
-    SccLarge power series cut to a tolerance that stops it after a bounded
-    number of multiplies (all other units solved in full)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle_py import Oracle, Ref
-    n = g.n
-    w = np.full(n, 1.0 / n)
-    off, tgt, _, _ = g.csr()
-    threads = threads or (os.cpu_count() or 1)
-    if Ref.available():
-        r = Ref()
-        t0 = time.perf_counter()
-        # the reference builds its own Graph (from_edges sort) and schedule
-        src = np.repeat(np.arange(n, dtype=np.int32), np.diff(off))
-        rg = r.graph(n, src, tgt)
-        del src
-        prep = rg.prepare(100)
-        setup_s = time.perf_counter() - t0
-        # A level loop with the SccLarge series stopped after its first multiply
-        # (do-while, solvers.cpp:146-160) times every other unit in full plus one
-        # multiply of each large SCC.  If the full solve fits the budget (at
-        # ~130 multiplies) the sample is the full solve, else this bounded one.
-        ranks, work, iters, ms = rg.prep_solve(prep, w, C_DAMP, TOL, large_tol=1e300, threads=threads)
-        large_tol = 1e300
-        if iters == 0 or ms * 130 <= budget_s * 1e3:
-            large_tol = 0.0
-        out = []
-        for _ in range(reps):  # the schedule is prepared once; each rep is one timed level loop
-            ranks, work, iters, ms = rg.prep_solve(prep, w, C_DAMP, TOL, large_tol=large_tol, threads=threads)
-            sample = (f"reference level loop (oracle/_ref, Parallel pool of {threads}) over its own schedule; "
-                      f"SccLarge series {'in full' if large_tol <= TOL else 'stopped after its first multiply'}"
-                      f" ({iters} multiplies, {work / 1e9:.2f} G edge updates); setup {setup_s:.1f}s untimed")
-            out.append({"value": work / (ms / 1e3) / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
-                        "sample": sample, "edge_updates": int(work), "ms": ms})
-        rg.free_prep(prep)
-        if large_tol <= TOL and extra_methods:
-            out[-1]["reference_methods"] = reference_methods(rg, w, threads)
-        return out if reps > 1 else out[0]
-    o = Oracle()
-    go = o.graph_from_csr(n, off, tgt)
-    eu, ms = go.sample_large_scc(w, C_DAMP, 4)
-    return {"value": eu / (ms / 1e3) / 1e9 if ms > 0 else None, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": "oracle port: 4 multiplies of the largest SccLarge unit (push COO)", "edge_updates": int(eu),
-            "ms": ms}
-
-
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -164,25 +134,107 @@ def cpu_model():
     return "unknown"
 
 
-def reference_methods(rg, w, threads):
-    """SURVEY 8(d) CPU side: the reference's compute_pagerank Sequential and
-    Parallel (its own wall_ms: partition + schedule + solve) and its
-    whole-graph power-iteration baseline, on the same graph and weights."""
-    res = {"threads": threads, "cpu_model": cpu_model()}
-    t0 = time.perf_counter()
-    seq = rg.compute_pagerank(w, C_DAMP, TOL, 100, parallel=False)
-    res["sequential_ms"] = (time.perf_counter() - t0) * 1e3
-    res["sequential_reference_wall_ms"] = seq.report["wall_ms"]
-    t0 = time.perf_counter()
-    par = rg.compute_pagerank(w, C_DAMP, TOL, 100, parallel=True, threads=threads)
-    res["parallel_ms"] = (time.perf_counter() - t0) * 1e3
-    res["parallel_reference_wall_ms"] = par.report["wall_ms"]
-    t0 = time.perf_counter()
-    rg.compute_baseline(w, C_DAMP, TOL)
-    res["whole_graph_baseline_ms"] = (time.perf_counter() - t0) * 1e3
-    res["note"] = ("wall times include the reference's partition + schedule; the headline cpu_baseline value is its "
-                   "level loop only")
-    return res
+class RefLeg:
+    """The reference's CPU path on the same workload: the levelrank sources
+    compiled unmodified (oracle/_ref) when present, else the plain-C port
+    (oracle/).  The graph comes from oracle/lr_gen.c (same edges as the
+    product generator) and is built by the reference's own Graph::from_edges;
+    partition + schedule run once (timed: the drop-in comparison), then each
+    timed step is the reference's level loop (engine.cpp:126-158, unit
+    solvers + propagate_weights) over that schedule with a pool of all host
+    threads.  Bounded sample: when the full solve would not fit the budget,
+    the SccLarge power series stops after its first multiply (every other
+    unit is solved in full)."""
+
+    def __init__(self, cfg, shrink, threads=None, budget_s=20.0):
+        self.cfg, self.shrink, self.budget_s = cfg, shrink, budget_s
+        self.threads = int(threads or os.cpu_count() or 1)
+        self.err = None
+
+    def setup(self):
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            from oracle_py import Oracle, Ref
+            t0 = time.perf_counter()
+            n, src, dst = Oracle().gen_config(self.cfg, self.shrink, threads=self.threads)
+            self.gen_ms = (time.perf_counter() - t0) * 1e3
+            self.n = n
+            self.w = np.full(n, 1.0 / n)
+            self.kind = "reference" if Ref.available() else "port"
+            t0 = time.perf_counter()
+            if self.kind == "reference":
+                self.g = Ref().graph(n, src, dst)
+                del src, dst
+                self.graph_ms = (time.perf_counter() - t0) * 1e3
+                t0 = time.perf_counter()
+                self.prep = self.g.prepare(100)  # find_components + build_schedule
+                self.prep_ms = (time.perf_counter() - t0) * 1e3
+                # the SccLarge series stopped after one multiply (do-while,
+                # solvers.cpp:146-160): every other unit in full plus one multiply
+                _, _, iters, ms = self.g.prep_solve(self.prep, self.w, C_DAMP, TOL, large_tol=1e300,
+                                                    threads=self.threads)
+                self.large_tol = 0.0 if (iters == 0 or ms * 130 <= self.budget_s * 1e3) else 1e300
+            else:
+                self.g = Oracle().graph(n, src, dst)
+                del src, dst
+                self.graph_ms = (time.perf_counter() - t0) * 1e3
+                self.prep_ms = None
+            self.m = self.g.m
+        except Exception as e:  # reported, never required
+            self.err = e
+
+    def steps(self, reps):
+        if self.err:
+            raise self.err
+        out = []
+        for _ in range(reps):
+            if self.kind == "reference":
+                _, work, iters, ms = self.g.prep_solve(self.prep, self.w, C_DAMP, TOL, large_tol=self.large_tol,
+                                                       threads=self.threads)
+                full = self.large_tol <= TOL
+                sample = (f"reference level loop (oracle/_ref, -O3 -DNDEBUG, Parallel pool of {self.threads} on "
+                          f"{cpu_model()}) over its own schedule; SccLarge series "
+                          f"{'in full' if full else 'stopped after its first multiply'} ({iters} multiplies, "
+                          f"{work / 1e9:.2f} G edge updates); graph + partition + schedule built once, untimed")
+                cores = self.threads
+            else:
+                work, ms = self.g.sample_large_scc(self.w, C_DAMP, 4)
+                sample = "oracle port: 4 multiplies of the largest SccLarge unit (push COO)"
+                cores = 1
+            out.append({"value": work / (ms / 1e3) / 1e9 if ms > 0 else None, "unit": UNIT, "cores": cores,
+                        "kind": self.kind, "sample": sample, "edge_updates": int(work), "ms": ms})
+        return out
+
+    def methods(self):
+        """SURVEY 8(d) CPU side on the same graph and weights: the reference's
+        Sequential and Parallel level loops and its whole-graph power series
+        (compute_baseline, solvers.cpp:164-198).  Each runs in full when the
+        full solve fits the budget, else as the same bounded sample (the
+        baseline: one whole-graph multiply, tol = inf)."""
+        if self.err or self.kind != "reference":
+            return None
+        full = self.large_tol <= TOL
+        res = {"threads": self.threads, "cpu_model": cpu_model(), "full_solves": full}
+        for name, th in (("sequential", 1), ("parallel", self.threads)):
+            _, work, iters, ms = self.g.prep_solve(self.prep, self.w, C_DAMP, TOL, large_tol=self.large_tol,
+                                                   threads=th)
+            res[name] = {"ms": ms, "edge_updates": int(work), "ge_s": work / ms / 1e6}
+        t0 = time.perf_counter()
+        _, rep = self.g.compute_baseline(self.w, C_DAMP, TOL if full else 1e300)
+        ms = (time.perf_counter() - t0) * 1e3
+        work = int(rep["iterative_edge_work"])
+        res["whole_graph_baseline"] = {"ms": ms, "iterations": int(rep["total_iterations"]), "edge_updates": work,
+                                       "ge_s": work / ms / 1e6}
+        return res
+
+    def drop_in(self, rate):
+        """The reference's compute_pagerank wall (engine.cpp:99-180) =
+        partition + schedule (measured) + solve (measured in full when the
+        sample is the full solve, else extrapolated from the sample's rate)."""
+        if self.err or self.kind != "reference":
+            return None
+        return {"partition_schedule_ms": self.prep_ms, "from_edges_ms": self.graph_ms,
+                "solve_measured": self.large_tol <= TOL, "edge_update_rate_ge_s": rate}
 
 
 def run_reference(args):
@@ -190,20 +242,31 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_1609_09068_b200 as lr  # only for the synthetic input generator
-    g, gen_ms = build_graph(lr, args.config, args.shrink)
-    steps = cpu_sample(g, lr, None, budget_s=args.ref_budget, reps=args.warmup + args.steps)
-    steps = steps[args.warmup:] if isinstance(steps, list) else [steps]
+    leg = RefLeg(args.config, args.shrink, budget_s=args.ref_budget)
+    leg.setup()
+    steps = leg.steps(args.warmup + args.steps)[args.warmup:]
     res = steps[-1]
     value = float(np.mean([s["value"] for s in steps]))
     ms = float(np.mean([s["ms"] for s in steps]))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(args.config, args.shrink), "c": C_DAMP, "tol": TOL},
+            "config": config_dict(args.config, args.shrink, leg.n, leg.m),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": {"generate": leg.gen_ms / 1e3, "from_edges": leg.graph_ms / 1e3,
+                        "partition_schedule": (leg.prep_ms or 0) / 1e3},
+            "product_library_mapped": product_mapped()}
     print(json.dumps(line), flush=True)
+
+
+def product_mapped():
+    """True if this process mapped the product's liblevelrank_b200.so."""
+    try:
+        with open("/proc/self/maps") as f:
+            return any("liblevelrank_b200" in ln for ln in f)
+    except OSError:
+        return None
 
 
 # ------------------------------------------------------------------ GPU leg
@@ -234,6 +297,13 @@ def run_ours(args):
     log(f"[rank {rank}] plan {eng.plan_ms / 1e3:.1f}s upload {eng.upload_ms / 1e3:.1f}s "
         f"device bytes {eng.device_bytes() / 1e9:.2f} GB")
     n = g.n
+    # the reference CPU leg builds its graph and schedule on a host thread
+    # (ctypes calls release the GIL) while the GPU is measured
+    leg = setup_thread = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        leg = RefLeg(args.config, args.shrink, budget_s=args.ref_budget)
+        setup_thread = threading.Thread(target=leg.setup, daemon=True)
+        setup_thread.start()
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
     w_dev = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
     r3_dev = torch.empty(n, dtype=torch.float64, device=dev)
@@ -379,33 +449,55 @@ def run_ours(args):
             gpu_base = {"value": None, "error": str(e)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    methods = None
+    ref_drop = None
+    if leg is not None:
+        setup_thread.join()
         try:
-            cpu = cpu_sample(g, lr, eng, budget_s=args.ref_budget, extra_methods=True)
+            cpu = leg.steps(1)[0]
+            methods = leg.methods()
+            cpu["reference_methods"] = methods
+            ref_drop = leg.drop_in(cpu["value"])
         except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    # the drop-in call a user makes (lr_compute_pagerank: partition + layout on
+    # the host, upload, one solve with host buffers) against the reference's
+    # compute_pagerank wall (partition + schedule + solve)
+    drop_in = {"ours_ms": {"plan": eng.plan_ms, "upload": eng.upload_ms, "solve_host_buffers": e2e_ms,
+                           "total": eng.plan_ms + eng.upload_ms + e2e_ms}}
+    if ref_drop:
+        solve_ms = None
+        if methods and methods.get("full_solves"):
+            solve_ms = methods["parallel"]["ms"]
+        elif ref_drop.get("edge_update_rate_ge_s"):
+            solve_ms = work / ref_drop["edge_update_rate_ge_s"] / 1e6
+        ref_drop["solve_ms"] = solve_ms
+        ref_drop["solve_ms_kind"] = "measured (Parallel pool)" if ref_drop["solve_measured"] else \
+            "extrapolated: this workload's edge updates at the sampled rate"
+        ref_drop["total_ms"] = ref_drop["partition_schedule_ms"] + (solve_ms or 0.0)
+        drop_in["reference_ms"] = ref_drop
+        drop_in["speedup"] = ref_drop["total_ms"] / drop_in["ours_ms"]["total"]
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, args.shrink), "c": C_DAMP, "tol": TOL,
-                       "vertices": n, "edges": g.m, "edge_updates_per_step": work,
-                       "iterative_edge_work": int(info0["iterative_edge_work"]),
-                       "large_scc_iterations": int(iters[large].max()) if large.any() else 0,
-                       "levels": n_levels, "units": n_units,
-                       "l2": "flushed (512 MB write) before every timed step",
-                       "parallelism": (f"giant-SCC rows sharded over {world} GPUs (NCCL exchange per iteration), "
-                                       "other units replicated") if world > 1 else "1 GPU",
-                       "setup_s": {"generate": gen_ms / 1e3, "plan": eng.plan_ms / 1e3,
-                                   "upload": eng.upload_ms / 1e3}},
+            "config": config_dict(args.config, args.shrink, n, g.m),
+            "parallelism": (f"giant-SCC rows sharded over {world} GPUs (NCCL exchange per iteration), "
+                            "other units replicated") if world > 1 else "1 GPU",
+            "workload_stats": {"edge_updates_per_step": work, "iterative_edge_work": int(info0["iterative_edge_work"]),
+                               "large_scc_iterations": int(iters[large].max()) if large.any() else 0,
+                               "levels": n_levels, "units": n_units},
+            "setup_s": {"generate": gen_ms / 1e3, "plan": eng.plan_ms / 1e3, "upload": eng.upload_ms / 1e3},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "returns": "R3 (the reference's EngineResult.ranks); R1 computed on "
                     "the device, not copied back"},
             "gpu_launches": int(inf["kernel_launches"]) * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "drop_in": drop_in,
             "gpu_baseline": gpu_base,
             "clocks": clk.summary(),
         }
@@ -420,7 +512,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=int(os.environ.get("LR_BENCH_CONFIG", "2")))
+    ap.add_argument("--config", type=int, default=int(os.environ.get("LR_BENCH_CONFIG", "5")))
     ap.add_argument("--shrink", type=int, default=0)
     ap.add_argument("--ref-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

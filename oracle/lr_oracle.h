@@ -89,6 +89,21 @@ int lro_normalize_r1(const double* r3, int64_t n, double* r1);
 int lro_sample_large_scc(const lro_graph* g, const lro_schedule* s, const double* w, double c,
                          int64_t iters, int64_t* edge_updates, double* ms);
 
+/* lr_gen.c: the BASELINE.json generators (same graphs as the product's
+ * csrc/host/gen.cpp, asserted by tests/test_oracle_gen.py).  Edge lists are
+ * malloc'ed; release them with lro_gen_free.  dangle_p > 0 applies config 3's
+ * "each vertex loses all out-edges with probability p" (stream 2 of
+ * dangle_seed) to the R-MAT edges. */
+int lro_gen_rmat(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed, double dangle_p,
+                 uint64_t dangle_seed, int threads, int32_t** src, int32_t** dst, int64_t* m);
+int lro_gen_planted(int32_t n, int32_t n_scc, int32_t smin, int32_t smax, int64_t budget, double out_degree,
+                    int64_t inter_edges, double dangling_fraction, uint64_t seed, int32_t** src, int32_t** dst,
+                    int64_t* m);
+int lro_gen_deep_dag(int32_t levels, int32_t width, int32_t smin, int32_t smax, double scc_out_degree, int32_t bmin,
+                     int32_t bmax, double inter_out_degree, int32_t reach, uint64_t seed, int threads, int32_t** src,
+                     int32_t** dst, int64_t* m);
+void lro_gen_free(int32_t* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -163,8 +163,49 @@ class Oracle(_Lib):
         lib.lro_normalize_r1.argtypes = [F64P, C.c_int64, F64P]
         lib.lro_sample_large_scc.argtypes = [C.c_void_p, C.c_void_p, F64P, C.c_double, C.c_int64, I64P, F64P]
 
+        pp = C.POINTER(I32P)
+        lib.lro_gen_rmat.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                     C.c_double, C.c_uint64, C.c_int, pp, pp, I64P]
+        lib.lro_gen_planted.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_double,
+                                        C.c_int64, C.c_double, C.c_uint64, pp, pp, I64P]
+        lib.lro_gen_deep_dag.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                                         C.c_int32, C.c_double, C.c_int32, C.c_uint64, C.c_int, pp, pp, I64P]
+        lib.lro_gen_free.argtypes = [I32P]
+
     def __getitem__(self, k):
         return getattr(self.lib, k)
+
+    # -- synthetic inputs (oracle/lr_gen.c; same recipes as paper_1609_09068_b200.config_graph)
+    def gen_config(self, cfg, shrink=0, threads=None):
+        """Edge list (n, src, dst) of BASELINE.json config `cfg` (duplicates
+        and, outside R-MAT, self-loops included; Graph::from_edges removes them)."""
+        threads = int(threads or os.cpu_count() or 1)
+        s, d, m = I32P(), I32P(), C.c_int64()
+        f = 2 ** shrink
+        if cfg in (2, 3, 5):
+            scale, ef = {2: (20, 16), 3: (23, 8), 5: (26, 16)}[cfg]
+            scale -= shrink
+            n = 1 << scale
+            self._check(self.lib.lro_gen_rmat(scale, ef, 0.57, 0.19, 0.19, 1, 0.3 if cfg == 3 else 0.0, 2, threads,
+                                              C.byref(s), C.byref(d), C.byref(m)))
+        elif cfg == 1:
+            n = 100_000 // f
+            self._check(self.lib.lro_gen_planted(n, max(200 // f, 2), 16, 1024, 50_000 // f, 4.0, 50_000 // f, 0.10,
+                                                 1, C.byref(s), C.byref(d), C.byref(m)))
+        elif cfg == 4:
+            levels, width = max(1000 // f, 8), max(16_000 // f, 256)
+            n = levels * width
+            self._check(self.lib.lro_gen_deep_dag(levels, width, 2, 64, 6.0, 1, 4, 4.5, 8, 1, threads,
+                                                  C.byref(s), C.byref(d), C.byref(m)))
+        else:
+            raise ValueError(f"unknown config {cfg}")
+        try:
+            src = np.ctypeslib.as_array(s, (m.value,)).copy() if m.value else np.zeros(0, np.int32)
+            dst = np.ctypeslib.as_array(d, (m.value,)).copy() if m.value else np.zeros(0, np.int32)
+        finally:
+            self.lib.lro_gen_free(s)
+            self.lib.lro_gen_free(d)
+        return n, src, dst
 
     # -- graph
     def graph(self, n, src, dst, keep=False):

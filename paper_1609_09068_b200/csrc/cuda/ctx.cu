@@ -493,13 +493,13 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         }
       } else if (kind == 2) {
         rk = kSmall;
-        if (m <= kSmallSmemMaxM) {
+        const long long ne = L->iptr[re] - L->iptr[rb];
+        // dense units (in-edge stash) can outgrow k_level's shared memory at any
+        // m: those go to the global-scratch kernel like the large ones
+        if (m <= kSmallSmemMaxM && small_unit_smem_bytes(m, ne) <= kSmallSmemCap &&
+            static_cast<size_t>(m + 1) * static_cast<size_t>(m + 2) * sizeof(double) <= kSmallSmemCap) {
           small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
-          // the tile solve, or the normalised one where small_tile_ok(m, c) fails
-          if (m <= kSmallTileMaxM) T.sm_tile = std::max(T.sm_tile, small_tile_bytes(m, L->iptr[re] - L->iptr[rb]));
-          if (m <= kSmallMmaMaxM) T.sm_tile = std::max(T.sm_tile, small_mma_bytes(L->iptr[re] - L->iptr[rb]));
-          else if (m <= kSmallMmaSmemMaxM)
-            T.sm_tile = std::max(T.sm_tile, small_mma_smem_bytes(m, L->iptr[re] - L->iptr[rb]));
+          T.sm_tile = std::max(T.sm_tile, small_unit_smem_bytes(m, ne));
           T.sm_max = std::max(T.sm_max, m);
         } else {  // beyond shared memory: global-scratch kernel after the level kernel
           small_big.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
@@ -867,7 +867,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       if (T.xb1 > T.xb0) {
         launch_level(L, ctx->ltasks.p + T.xb0, T.xb1 - T.xb0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                      0, 0, kRowTaskSmem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, ctx->unit_iters.p,
-                     ctx->status.p, false, ctx->side);
+                     ctx->status.p, false, ctx->side, /*profile=*/false);
         ++nl;
       }
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
@@ -1135,23 +1135,28 @@ lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* id128) {
     lrerr::set("bad rank / world");
     return LR_EINVAL;
   }
-  if (ctx->comm) {
-    nccl().comm_destroy(ctx->comm);
-    ctx->comm = nullptr;
+  if (world > 1 && !id128) {
+    lrerr::set("world > 1 needs the NCCL unique id of rank 0");
+    return LR_EINVAL;
   }
+  ncclComm_t comm = nullptr;
+  if (world > 1 || id128) {
+    const NcclApi& nc = nccl();
+    if (!nc.ok) {
+      lrerr::set("libnccl.so.2 not loadable");
+      return LR_ENCCL;
+    }
+    LR_CUDA_TRY(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    LR_NCCL_TRY(nc.comm_init_rank(&comm, world, id, rank));
+  }
+  // commit only once the new communicator exists
+  if (ctx->comm) nccl().comm_destroy(ctx->comm);
+  ctx->comm = comm;
   ctx->shard = rank;
   ctx->nshards = world;
   ctx->loaded = false;  // the next upload shards the grid units
-  if (world == 1 && !id128) return LR_OK;
-  const NcclApi& nc = nccl();
-  if (!nc.ok) {
-    lrerr::set("libnccl.so.2 not loadable");
-    return LR_ENCCL;
-  }
-  LR_CUDA_TRY(cudaSetDevice(ctx->device));
-  ncclUniqueId id;
-  std::memcpy(&id, id128, sizeof id);
-  LR_NCCL_TRY(nc.comm_init_rank(&ctx->comm, world, id, rank));
   return LR_OK;
 }
 

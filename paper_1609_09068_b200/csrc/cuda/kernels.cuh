@@ -172,9 +172,21 @@ __host__ __device__ constexpr size_t small_mma_smem_bytes(int m, long long ne) {
           static_cast<size_t>((m + 7) & ~7)) * sizeof(double) +
          static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
 }
+// shared memory of the small-SCC solve k_level picks for a unit
+// (level.cu small_dispatch): block GJ in registers (m <= 64), block GJ with the
+// system in shared memory (m <= 128), else the normalised GJ (no edge stash)
+__host__ __device__ constexpr size_t small_unit_smem_bytes(int m, long long ne);
+// k_level's dynamic shared memory ceiling (227 KB opt-in less its static
+// shared memory, with margin); units above it run in the global-scratch k_small
+constexpr size_t kSmallSmemCap = 232448 - 1024;
 __host__ __device__ constexpr size_t small_tile_bytes(int m, long long ne) {
   return (static_cast<size_t>(m) * static_cast<size_t>(small_tile_ld(m)) + static_cast<size_t>(m)) * sizeof(double) +
          static_cast<size_t>(ne) * (sizeof(double) + sizeof(int));
+}
+__host__ __device__ constexpr size_t small_unit_smem_bytes(int m, long long ne) {
+  return m <= kSmallMmaMaxM        ? small_mma_bytes(ne)
+         : m <= kSmallMmaSmemMaxM ? small_mma_smem_bytes(m, ne)
+                                   : static_cast<size_t>(m + 1) * static_cast<size_t>(m + 2) * sizeof(double);
 }
 // shared memory of lcta_solve_staged for a unit of m rows and ne in-edges,
 // with the level's largest unit at maxrows rows
@@ -209,7 +221,7 @@ cudaError_t set_level_prof(long long* buf);
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s);
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile = true);
 
 // launch wrappers (stream-ordered)
 void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,

@@ -1095,9 +1095,13 @@ __device__ __forceinline__ int lcta_il(int i) { return ((i >> 4) << 5) | (i & 15
 // The whole power series of one SccLarge unit in one CTA (solve_large_scc,
 // solvers.cpp:128-162), everything in shared memory: the pushed vectors, the
 // ranks, pf, the row offsets and the in-edges as 16-bit offsets into the unit,
-// so an iteration touches no global memory -- one thread per row in the
-// reference's order (bit-exact), a warp for rows above kCrossLight, and the
-// stop test on integer maxima.
+// so an iteration touches no global memory -- one thread per row, a warp for
+// rows above kCrossLight, and the stop test on integer maxima.  Summation
+// order is NOT the reference's source-ordered push: the register path sums a
+// row's first twelve terms pairwise and the host reorders each row's in-edges
+// to spread the gathers over the shared-memory banks (LR_BANK_ORDER=0 keeps
+// source order), so rows agree to ~1e-16 relative; per-unit iteration counts
+// equal the reference's in every parity test (run with both orders).
 
 // pairwise sum of N terms (N a multiple of 4): log2 N dependent adds instead of N
 template <int N>
@@ -1482,7 +1486,7 @@ __device__ void lcta_solve(const DeviceLayout& L, const SccTask& t, int maxrows,
 
 // ------------------------------------------------------------- dispatcher
 // Optional per-CTA timing of k_level (LR_LEVEL_PROF): task type, start, end (ns).
-__device__ long long* g_level_prof = nullptr;
+long long* g_level_prof = nullptr;  // host copy of the per-CTA timing buffer (LR_LEVEL_PROF)
 
 __device__ __forceinline__ long long global_ns() {
   long long t;
@@ -1506,12 +1510,11 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
             int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
             const double* __restrict__ pf, double* rank, double* s0, long long* unit_iters, DevStatus* st,
-            size_t smem_bytes) {
+            size_t smem_bytes, long long* prof) {
   extern __shared__ double sm[];
   __shared__ double red[2][32];
   const LevelTask t = tasks[blockIdx.x];
   const double c = p->c;
-  long long* const prof = g_level_prof;
   const long long t_start = prof ? global_ns() : 0;
   switch (t.type) {
     case kTaskRows:
@@ -1661,19 +1664,23 @@ cudaError_t configure_level_kernel() {
                               optin - static_cast<int>(a.sharedSizeBytes));
 }
 
-cudaError_t set_level_prof(long long* buf) { return cudaMemcpyToSymbol(g_level_prof, &buf, sizeof(buf)); }
+cudaError_t set_level_prof(long long* buf) {
+  g_level_prof = buf;
+  return cudaSuccess;
+}
 
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s) {
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile) {
   if (ntasks == 0) return;
+  long long* prof = profile ? g_level_prof : nullptr;  // one launch per level owns the buffer
   if (heavy)
     k_level<true><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
-                                                 pf, rank, s0, unit_iters, st, smem);
+                                                 pf, rank, s0, unit_iters, st, smem, prof);
   else
     k_level<false><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
-                                                  pf, rank, s0, unit_iters, st, smem);
+                                                  pf, rank, s0, unit_iters, st, smem, prof);
 }
 
 }  // namespace lrk

@@ -23,3 +23,5 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["product_library_mapped"] is False  # the reference arm never loads the product
+    assert line["config"]["vertices"] == 1 << 19 and line["config"]["workload"].startswith("config5")

@@ -204,3 +204,20 @@ def test_small_sccs_every_size_with_loops(lr, oracle):
         base += m
     w = rng.random(base) + 0.1
     check(lr, oracle, base, np.concatenate(src), np.concatenate(dst), w=w, keep=True)
+
+
+@pytest.mark.parametrize("m,th,keep", [(99, 100, True), (128, 200, False), (150, 200, True), (64, 100, True)])
+def test_dense_small_scc_shared_memory_cap(lr, oracle, m, th, keep):
+    """Complete SCCs below small_threshold whose in-edge stash outgrows
+    k_level's 227 KB of shared memory (99 rows with kept loops: 232 KB) run
+    in the global-scratch solve instead of failing the launch."""
+    s, d = np.meshgrid(np.arange(m), np.arange(m), indexing="ij")
+    s, d = s.ravel(), d.ravel()
+    if not keep:
+        s, d = s[s != d], d[s != d]
+    # a second, sparse SCC on the same level keeps the k_level path busy too
+    ring = np.arange(m, m + 40)
+    s = np.concatenate([s, ring, [0]])
+    d = np.concatenate([d, np.roll(ring, -1), [m]])
+    w = np.random.default_rng(m).uniform(0.1, 2.0, m + 40)
+    check(lr, oracle, m + 40, s, d, w=w, th=th, keep=keep)

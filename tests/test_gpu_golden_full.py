@@ -88,10 +88,50 @@ def test_config5_fixed_point_shrunk(lr):
     assert res.report["total_iterations"] > 0
 
 
-@pytest.mark.skipif(os.environ.get("LR_TEST_FULL5") != "1", reason="full north-star size: set LR_TEST_FULL5=1")
-def test_config5_fixed_point_full(lr):
+def _digest(a, dt):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=dt).tobytes()).hexdigest()
+
+
+def test_config5_reference_golden(lr):
+    """The north-star graph at full size (R-MAT scale 26, 1.06 G edges) against
+    the reference's own compute_pagerank run on it (tests/golden/config5.npz,
+    made by make_golden_cfg5.py with oracle/_ref): partition bit-exact per
+    vertex (comp ids, levels, kinds), every unit's iteration count, the
+    report counters, and R3 / R1 within 1e-10 relative on a seeded 2^20-vertex
+    sample plus the giant SCC's 16k highest-out-degree and 16k highest-in-degree
+    rows."""
+    import hashlib
+    from golden.make_golden_cfg5 import edge_checksum, sample_indices
+    d = np.load(os.path.join(GOLDEN, "config5.npz"))
     g = lr.config_graph(5)
-    assert g.n == 67_108_864 and g.m == 1_060_386_603
-    res = _fixed_point_properties(lr, g)
-    print("config5 full:", {k: res.report[k] for k in ("components", "level_count", "large_scc_vertices",
-                                                       "total_iterations", "total_edge_work")})
+    assert (g.n, g.m) == (int(d["n"]), int(d["m"]))
+    _, tgt, _, _ = g.csr()
+    assert edge_checksum(tgt) == int(d["edge_checksum"])
+    del tgt
+    part = lr.find_components(g)
+    assert hashlib.sha256(part.comp_of.astype(np.int32).tobytes()).hexdigest() == str(d["digest_comp_of"])
+    assert _digest(part.levels[part.comp_of], np.int32) == str(d["digest_levels"])
+    assert _digest(part.kinds[part.comp_of], np.uint8) == str(d["digest_kinds"])
+    assert tuple(part.stats) == tuple(int(x) for x in d["partition_stats"])
+    assert part.max_level == int(d["max_level"])
+    del part
+    n = g.n
+    res = lr.compute_pagerank(g, np.full(n, 1.0 / n), lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(res.unit_iters, d["unit_iters"])
+    for k in ("total_edge_work", "iterative_edge_work", "iterative_edges", "single_pass_edge_work", "components",
+              "scc_components", "cac_components", "singleton_cacs", "largest_component", "level_count", "max_level",
+              "large_scc_vertices", "cross_edge_count", "total_iterations"):
+        assert res.report[k] == int(d["report_" + k]), k
+    for k in ("eps_tot", "eps_avg", "mean_iterations_per_edge"):
+        assert res.report[k] == float(d["report_" + k]), k
+    idx = sample_indices(n)
+    worst = 0.0
+    for ix, ref in ((idx, d["sample_r3"]), (d["head_out"], d["head_out_r3"]), (d["head_in"], d["head_in_r3"])):
+        rel = np.abs(res.ranks[ix] - ref) / ref
+        worst = max(worst, float(rel.max()))
+        r1_ref = ref / float(d["r3_sum"])
+        assert (np.abs(res.r1[ix] - r1_ref) / r1_ref).max() <= 1e-10
+    assert worst <= 1e-10, worst
+    print(f"config5 vs reference: units={len(res.unit_iters)} giant iterations={int(res.unit_iters.max())} "
+          f"max rel err {worst:.2e}")
