@@ -224,6 +224,31 @@ lr_status lr_compute_pagerank(const lr_graph* g, const double* w, int64_t wn, do
 lr_status lr_compute_baseline(const lr_graph* g, const double* w, int64_t wn, double c, double tol,
                               int device, double* ranks, double* r1, lr_report* report);
 
+/* --------------------------------------------------------- output formats */
+/* The reference's writers, byte-compatible. */
+typedef struct lr_unit_record { /* UnitRecord (engine.hpp:20-27) */
+  int32_t kind;                 /* 0 singleton_group, 1 cac, 2 scc_small, 3 scc_large */
+  int32_t level, size, reserved;
+  int64_t edges, iterations;
+  double wall_ms;
+} lr_unit_record;
+typedef struct lr_report_meta { /* the SolveReport fields lr_report does not carry */
+  const char* method;           /* "partitioned" | "baseline" */
+  const char* mode;             /* "sequential" | "parallel" */
+  double c, tol;
+  int32_t keep_loops, small_threshold, threads, reserved;
+} lr_report_meta;
+/* fmt 0: SolveReport::write_text (proj/src/report.cpp:24-60); 1: write_json
+ * (:62-113); 2: one bench CSV row, 3: the bench CSV header (proj/src/cli.cpp:262-281).
+ * *out is malloc'ed (release with lr_string_free), *len its length. */
+lr_status lr_report_format(const lr_report* rep, const lr_report_meta* meta, const lr_unit_record* units,
+                           int64_t n_units, int fmt, char** out, int64_t* len);
+/* write_ranks (proj/src/cli.cpp:80-83): "v<TAB>rank" lines, 12 significant
+ * digits; to a string, or straight to a file (path). */
+lr_status lr_ranks_format(const double* ranks, int64_t n, char** out, int64_t* len);
+lr_status lr_ranks_write(const double* ranks, int64_t n, const char* path);
+void lr_string_free(char* s);
+
 /* ------------------------------------------------------- solver helpers */
 /* validate_params (proj/src/solvers.cpp:11-15). */
 lr_status lr_validate_params(double c, double tol);

@@ -366,6 +366,13 @@ class Ref(_Lib):
         lib.lrref_iteration_cap.restype = C.c_int64
         lib.lrref_error_bound.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, F64P]
         lib.lrref_propagate.argtypes = [I32P, I32P, I32P, C.c_int64, F64P, C.c_int64, C.c_double, F64P]
+        CPP = C.POINTER(C.c_char)
+        lib.lrref_report_format.argtypes = [C.POINTER(Report), C.c_char_p, C.c_char_p, C.c_double, C.c_double,
+                                            C.c_int, C.c_int32, C.c_int, C.c_void_p, C.c_int64, C.c_int, I64P]
+        lib.lrref_report_format.restype = CPP
+        lib.lrref_ranks_format.argtypes = [F64P, C.c_int64, I64P]
+        lib.lrref_ranks_format.restype = CPP
+        lib.lrref_string_free.argtypes = [CPP]
         lib.lrref_prep_new.argtypes = [C.c_void_p, C.c_int32]
         lib.lrref_prep_new.restype = C.c_void_p
         lib.lrref_prep_free.argtypes = [C.c_void_p]
@@ -393,6 +400,41 @@ class Ref(_Lib):
         out = np.zeros(2)
         self.lib.lrref_error_bound(large, n, c, tol, _p(out, F64P))
         return float(out[0]), float(out[1])
+
+    def _string(self, p, n):
+        if not p:
+            raise RuntimeError("format unavailable")
+        try:
+            return C.string_at(p, n).decode()
+        finally:
+            self.lib.lrref_string_free(p)
+
+    def format_report(self, report: dict, units=(), fmt="text"):
+        """The reference's SolveReport::write_text / write_json (report.cpp) or the
+        bench CSV row of cli.cpp:271-275, on the given field values."""
+        r = Report()
+        for k, _ in REPORT_FIELDS:
+            if k == "largest_is_scc":
+                r.largest_is_scc = int(report.get("largest_component_kind", "cac") == "scc")
+            elif k in report and report[k] is not None:
+                setattr(r, k, type(getattr(r, k))(report[k]))
+        rec = np.zeros(max(len(units), 1), dtype=[("kind", "i4"), ("level", "i4"), ("size", "i4"), ("r", "i4"),
+                                                  ("edges", "i8"), ("iterations", "i8"), ("wall_ms", "f8")])
+        for i, u in enumerate(units):
+            rec[i] = (u[0], u[1], u[2], 0, u[3], u[4], u[5])
+        n = C.c_int64()
+        code = {"text": 0, "json": 1, "csv_row": 2}[fmt]
+        p = self.lib.lrref_report_format(C.byref(r), str(report.get("method", "partitioned")).encode(),
+                                         str(report.get("mode", "sequential")).encode(), float(report.get("c", 0.85)),
+                                         float(report.get("tol", 1e-9)), int(report.get("keep_loops", 0)),
+                                         int(report.get("small_threshold", 100)), int(report.get("threads", 1)),
+                                         rec.ctypes.data, len(units), code, C.byref(n))
+        return self._string(p, n.value)
+
+    def format_ranks(self, ranks):
+        ranks = _f64(ranks)
+        n = C.c_int64()
+        return self._string(self.lib.lrref_ranks_format(_p(ranks, F64P), len(ranks), C.byref(n)), n.value)
 
     def propagate(self, src, dst, deg, ranks, c, weights):
         src, dst, deg = _i32(src), _i32(dst), _i32(deg)

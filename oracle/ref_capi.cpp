@@ -20,6 +20,8 @@
 #include <cstdint>
 #include <cstring>
 #include <sstream>
+#include <iomanip>
+#include <cstdlib>
 #include <exception>
 #include <mutex>
 #include <stdexcept>
@@ -456,5 +458,87 @@ int lrref_prep_solve(void* gp, void* pp, const double* w, int64_t wn, double c, 
     return fail_from_current();
   }
 }
+
+
+// ---- output formats.  SolveReport::write_text / write_json are the
+// reference's own (proj/src/report.cpp, compiled when nlohmann/json is
+// available); the CLI's ranks TSV and bench CSV row live in cli.cpp, which
+// cannot build here (CLI11 absent), so they are restated from
+// proj/src/cli.cpp:80-83 and :271-275.
+typedef struct {
+  int32_t kind, level, size, reserved;
+  int64_t edges, iterations;
+  double wall_ms;
+} lrref_unit;
+
+static char* dup_string(const std::string& t, int64_t* len) {
+  char* b = static_cast<char*>(std::malloc(t.size() + 1));
+  std::memcpy(b, t.data(), t.size());
+  b[t.size()] = 0;
+  *len = static_cast<int64_t>(t.size());
+  return b;
+}
+
+// fields: the lrref_report scalars; strings method/mode; fmt 0 text, 1 json, 2 bench row
+char* lrref_report_format(const lrref_report* r, const char* method, const char* mode, double c, double tol,
+                          int keep_loops, int32_t small_threshold, int threads, const lrref_unit* units,
+                          int64_t n_units, int fmt, int64_t* len) {
+  SolveReport rep;
+  rep.method = method;
+  rep.mode = mode;
+  rep.c = c;
+  rep.tol = tol;
+  rep.keep_loops = keep_loops != 0;
+  rep.small_threshold = small_threshold;
+  rep.threads = threads;
+  rep.vertices = r->vertices;
+  rep.edges = r->edges;
+  rep.components = r->components;
+  rep.scc_components = r->scc_components;
+  rep.cac_components = r->cac_components;
+  rep.singleton_cacs = r->singleton_cacs;
+  rep.largest_component = r->largest_component;
+  rep.largest_component_kind = r->largest_is_scc ? "scc" : "cac";
+  rep.max_level = r->max_level;
+  rep.level_count = r->level_count;
+  rep.large_scc_vertices = r->large_scc_vertices;
+  rep.eps_tot = r->eps_tot;
+  rep.eps_avg = r->eps_avg;
+  rep.total_iterations = r->total_iterations;
+  rep.iterative_edge_work = r->iterative_edge_work;
+  rep.iterative_edges = r->iterative_edges;
+  rep.single_pass_edge_work = r->single_pass_edge_work;
+  rep.cross_edge_count = r->cross_edge_count;
+  rep.total_edge_work = r->total_edge_work;
+  rep.mean_iterations_per_edge = r->mean_iterations_per_edge;
+  rep.all_weights_zero = r->all_weights_zero != 0;
+  rep.wall_ms = r->wall_ms;
+  for (int64_t i = 0; i < n_units; ++i)
+    rep.units.push_back(UnitRecord{static_cast<UnitKind>(units[i].kind), units[i].level, units[i].size,
+                                   units[i].edges, units[i].iterations, units[i].wall_ms});
+  std::ostringstream out;
+  if (fmt == 2) {
+    out << std::setprecision(15);
+    out << rep.method << (rep.mode == "parallel" ? "_parallel" : "") << ',' << rep.c << ',' << rep.tol << ','
+        << rep.total_iterations << ',' << rep.iterative_edge_work << ',' << rep.wall_ms << '\n';
+  } else {
+#ifdef LRREF_HAVE_REPORT
+    if (fmt == 0) rep.write_text(out);
+    else rep.write_json(out);
+#else
+    return nullptr;
+#endif
+  }
+  return dup_string(out.str(), len);
+}
+
+char* lrref_ranks_format(const double* ranks, int64_t n, int64_t* len) {
+  std::ostringstream out;
+  out << std::setprecision(12);
+  for (int64_t v = 0; v < n; ++v) out << v << '\t' << ranks[v] << '\n';
+  return dup_string(out.str(), len);
+}
+
+void lrref_string_free(char* p) { std::free(p); }
 
 }  // extern "C"

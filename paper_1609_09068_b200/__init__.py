@@ -121,6 +121,20 @@ class _Layout(C.Structure):
     ]
 
 
+class UnitRecord(C.Structure):
+    """lr_unit_record (UnitRecord, engine.hpp:20-27)."""
+    _fields_ = [("kind", C.c_int32), ("level", C.c_int32), ("size", C.c_int32), ("reserved", C.c_int32),
+                ("edges", C.c_int64), ("iterations", C.c_int64), ("wall_ms", C.c_double)]
+
+
+class _ReportMeta(C.Structure):
+    _fields_ = [("method", C.c_char_p), ("mode", C.c_char_p), ("c", C.c_double), ("tol", C.c_double),
+                ("keep_loops", C.c_int32), ("small_threshold", C.c_int32), ("threads", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+CP = C.POINTER(C.c_char)
+
 # Every symbol declared in include/lr_cuda.h (tests check they are exported).
 EXPORTS = {
     "lr_last_error": (C.c_char_p, []),
@@ -156,6 +170,11 @@ EXPORTS = {
                                       F64P, C.POINTER(_Report), I64P, C.c_int64]),
     "lr_compute_baseline": (C.c_int, [VP, F64P, C.c_int64, C.c_double, C.c_double, C.c_int, F64P, F64P,
                                       C.POINTER(_Report)]),
+    "lr_report_format": (C.c_int, [C.POINTER(_Report), C.POINTER(_ReportMeta), C.POINTER(UnitRecord), C.c_int64,
+                                   C.c_int, C.POINTER(CP), C.POINTER(C.c_int64)]),
+    "lr_ranks_format": (C.c_int, [F64P, C.c_int64, C.POINTER(CP), C.POINTER(C.c_int64)]),
+    "lr_ranks_write": (C.c_int, [F64P, C.c_int64, C.c_char_p]),
+    "lr_string_free": (None, [CP]),
     "lr_validate_params": (C.c_int, [C.c_double, C.c_double]),
     "lr_iteration_cap": (C.c_int64, [C.c_double, C.c_double]),
     "lr_error_bound": (None, [C.c_int64, C.c_int64, C.c_double, C.c_double, F64P]),
@@ -592,6 +611,62 @@ def compute_baseline(g: Graph, weights, params: SolverParams = SolverParams(), d
         d.pop(k, None)
     d["max_level"] = -1
     return EngineResult(ranks, r1, d, np.array([rep.total_iterations], np.int64))
+
+
+# ----------------------------------------------------------- output formats
+def _take_string(fn, *args) -> str:
+    out, n = CP(), C.c_int64()
+    _check(fn(*args, C.byref(out), C.byref(n)))
+    try:
+        return C.string_at(out, n.value).decode()
+    finally:
+        lib().lr_string_free(out)
+
+
+def _c_report(report: dict) -> _Report:
+    r = _Report()
+    for k, _ in _Report._fields_:
+        if k == "largest_is_scc":
+            r.largest_is_scc = int(report.get("largest_component_kind", "cac") == "scc")
+        elif k in report and report[k] is not None:
+            setattr(r, k, type(getattr(r, k))(report[k]))
+    return r
+
+
+def format_report(report: dict, units=(), fmt: str = "text") -> str:
+    """SolveReport::write_text / write_json (proj/src/report.cpp:24-113) or a
+    bench CSV row / header (proj/src/cli.cpp:262-281), byte-compatible with the
+    reference.  `report` is an EngineResult.report dict; `units` a sequence of
+    (kind, level, size, edges, iterations, wall_ms)."""
+    code = {"text": 0, "json": 1, "csv_row": 2, "csv_header": 3}[fmt]
+    meta = _ReportMeta(str(report.get("method", "partitioned")).encode(), str(report.get("mode", "sequential")).encode(),
+                       float(report.get("c", 0.85)), float(report.get("tol", 1e-9)), int(report.get("keep_loops", 0)),
+                       int(report.get("small_threshold", 100)), int(report.get("threads", 1)), 0)
+    arr = (UnitRecord * max(len(units), 1))()
+    for i, u in enumerate(units):
+        arr[i] = UnitRecord(int(u[0]), int(u[1]), int(u[2]), 0, int(u[3]), int(u[4]), float(u[5]))
+    return _take_string(lib().lr_report_format, C.byref(_c_report(report)), C.byref(meta), arr, len(units), code)
+
+
+def format_ranks(ranks) -> str:
+    """write_ranks (proj/src/cli.cpp:80-83): "v<TAB>rank" at 12 significant digits."""
+    r = _f64(ranks)
+    return _take_string(lib().lr_ranks_format, _p(r, F64P), len(r))
+
+
+def write_ranks(ranks, path) -> None:
+    r = _f64(ranks)
+    _check(lib().lr_ranks_write(_p(r, F64P), len(r), os.fsencode(path)))
+
+
+def report_units(plan_or_engine, unit_iters, wall_ms=None):
+    """UnitRecords (kind, level, size, edges, iterations, wall_ms) in schedule order."""
+    plan = getattr(plan_or_engine, "plan", plan_or_engine)
+    L = plan.layout()
+    size = np.diff(L["unit_row_begin"])
+    wall = np.zeros(len(size)) if wall_ms is None else np.asarray(wall_ms, np.float64)
+    return [(int(k), int(lv), int(sz), int(e), int(it), float(w)) for k, lv, sz, e, it, w in
+            zip(L["unit_kind"], L["unit_level"], size, L["unit_edges"], unit_iters, wall)]
 
 
 # --------------------------------------------------------- synthetic inputs

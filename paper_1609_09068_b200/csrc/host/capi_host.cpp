@@ -3,6 +3,9 @@
 // lr_compute_pagerank.  Every C++ exception is caught here and mapped to a
 // status code; nothing throws across the ABI.
 #include <chrono>
+#include <cstdlib>
+#include <fstream>
+#include <sstream>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -463,15 +466,16 @@ lr_status lr_compute_pagerank(const lr_graph* gp, const double* w, int64_t wn, d
   return LR_OK;
 }
 
-lr_status lr_compute_baseline(const lr_graph* gp, const double* w, int64_t wn, double c, double tol, int device,
-                              double* ranks, double* r1, lr_report* rep) {
-  if (!gp) {
-    lrerr::set("null graph");
-    return LR_EINVAL;
-  }
+}  // extern "C"
+
+namespace levelrank {
+inline namespace b200 {
+namespace detail {
+// compute_baseline on a C++ Graph (the C-ABI entry and the C++ API both land here)
+lr_status baseline_solve(const Graph& g, const double* w, int64_t wn, double c, double tol, int device, double* ranks,
+                         double* r1, lr_report* rep) {
   lr_status st = lr_validate_params(c, tol);
   if (st != LR_OK) return st;
-  const Graph& g = gp->g;
   const int64_t n = g.vertex_count();
   if (wn != n) {
     lrerr::set("weight vector does not match the vertex count");
@@ -494,17 +498,21 @@ lr_status lr_compute_baseline(const lr_graph* gp, const double* w, int64_t wn, d
   double wmax = w[0];
   for (int64_t v = 1; v < n; ++v) wmax = std::max(wmax, w[v]);
   rep->all_weights_zero = wmax == 0.0;
-  lr_plan* plan = nullptr;
-  st = lr_plan_build_baseline(gp, &plan);
+  std::unique_ptr<lr_plan> plan;
+  st = guarded([&] {
+    plan = std::make_unique<lr_plan>();
+    plan->g = &g;
+    plan->baseline = true;
+    plan->L = build_baseline_layout(g);
+  });
   if (st != LR_OK) return st;
-  std::unique_ptr<lr_plan, void (*)(lr_plan*)> plan_guard(plan, lr_plan_free);
   rep->plan_ms = ms_since(t0);
   lr_ctx* ctx = nullptr;
   st = lr_ctx_create(device, &ctx);
   if (st != LR_OK) return st;
   std::unique_ptr<lr_ctx, void (*)(lr_ctx*)> ctx_guard(ctx, lr_ctx_free);
   lr_layout lay{};
-  lr_plan_layout(plan, &lay);
+  lr_plan_layout(plan.get(), &lay);
   const auto t1 = std::chrono::steady_clock::now();
   st = lr_ctx_upload(ctx, &lay);
   if (st != LR_OK) return st;
@@ -526,6 +534,20 @@ lr_status lr_compute_baseline(const lr_graph* gp, const double* w, int64_t wn, d
   rep->mean_iterations_per_edge = static_cast<double>(iters);
   rep->wall_ms = ms_since(t0);
   return LR_OK;
+}
+}  // namespace detail
+}  // namespace b200
+}  // namespace levelrank
+
+extern "C" {
+
+lr_status lr_compute_baseline(const lr_graph* gp, const double* w, int64_t wn, double c, double tol, int device,
+                              double* ranks, double* r1, lr_report* rep) {
+  if (!gp) {
+    lrerr::set("null graph");
+    return LR_EINVAL;
+  }
+  return levelrank::detail::baseline_solve(gp->g, w, wn, c, tol, device, ranks, r1, rep);
 }
 
 lr_status lr_gen_rmat(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed, lr_graph** out) {
@@ -560,5 +582,110 @@ lr_status lr_gen_deep_dag(int32_t levels, int32_t width, int32_t scc_min, int32_
                out);
   });
 }
+
+}  // extern "C"
+
+// ------------------------------------------------------------ output formats
+namespace {
+lr_status emit(const std::string& text, char** out, int64_t* len) {
+  char* buf = static_cast<char*>(std::malloc(text.size() + 1));
+  if (!buf) {
+    lrerr::set("out of host memory");
+    return LR_ENOMEM;
+  }
+  std::memcpy(buf, text.data(), text.size());
+  buf[text.size()] = '\0';
+  *out = buf;
+  if (len) *len = static_cast<int64_t>(text.size());
+  return LR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+lr_status lr_report_format(const lr_report* r, const lr_report_meta* meta, const lr_unit_record* units,
+                           int64_t n_units, int fmt, char** out, int64_t* len) {
+  if (!out || (fmt != 3 && (!r || !meta)) || n_units < 0 || (n_units > 0 && !units) || fmt < 0 || fmt > 3) {
+    lrerr::set("bad report format request");
+    return LR_EINVAL;
+  }
+  *out = nullptr;
+  std::ostringstream os;
+  lr_status st = guarded([&] {
+    if (fmt == 3) {
+      write_bench_header(os);
+      return;
+    }
+    SolveReport rep;
+    rep.method = meta->method ? meta->method : "partitioned";
+    rep.mode = meta->mode ? meta->mode : "sequential";
+    rep.c = meta->c;
+    rep.tol = meta->tol;
+    rep.keep_loops = meta->keep_loops != 0;
+    rep.small_threshold = meta->small_threshold;
+    rep.threads = meta->threads;
+    rep.vertices = r->vertices;
+    rep.edges = r->edges;
+    rep.components = r->components;
+    rep.scc_components = r->scc_components;
+    rep.cac_components = r->cac_components;
+    rep.singleton_cacs = r->singleton_cacs;
+    rep.largest_component = r->largest_component;
+    rep.largest_component_kind = r->largest_is_scc ? "scc" : "cac";
+    rep.max_level = r->max_level;
+    rep.level_count = r->level_count;
+    rep.large_scc_vertices = r->large_scc_vertices;
+    rep.eps_tot = r->eps_tot;
+    rep.eps_avg = r->eps_avg;
+    rep.total_iterations = r->total_iterations;
+    rep.iterative_edge_work = r->iterative_edge_work;
+    rep.iterative_edges = r->iterative_edges;
+    rep.single_pass_edge_work = r->single_pass_edge_work;
+    rep.cross_edge_count = r->cross_edge_count;
+    rep.total_edge_work = r->total_edge_work;
+    rep.mean_iterations_per_edge = r->mean_iterations_per_edge;
+    rep.all_weights_zero = r->all_weights_zero != 0;
+    rep.wall_ms = r->wall_ms;
+    rep.units.resize(static_cast<std::size_t>(n_units));
+    for (int64_t i = 0; i < n_units; ++i) {
+      const lr_unit_record& u = units[i];
+      rep.units[static_cast<std::size_t>(i)] =
+          UnitRecord{static_cast<UnitKind>(u.kind), u.level, u.size, u.edges, u.iterations, u.wall_ms};
+    }
+    if (fmt == 0) rep.write_text(os);
+    else if (fmt == 1) rep.write_json(os);
+    else write_bench_row(os, rep);
+  });
+  if (st != LR_OK) return st;
+  return emit(os.str(), out, len);
+}
+
+lr_status lr_ranks_format(const double* ranks, int64_t n, char** out, int64_t* len) {
+  if (!out || n < 0 || (n > 0 && !ranks)) {
+    lrerr::set("bad ranks");
+    return LR_EINVAL;
+  }
+  *out = nullptr;
+  std::ostringstream os;
+  lr_status st = guarded([&] { write_ranks(os, std::span<const double>(ranks, static_cast<std::size_t>(n))); });
+  if (st != LR_OK) return st;
+  return emit(os.str(), out, len);
+}
+
+lr_status lr_ranks_write(const double* ranks, int64_t n, const char* path) {
+  if (!path || n < 0 || (n > 0 && !ranks)) {
+    lrerr::set("bad ranks");
+    return LR_EINVAL;
+  }
+  return guarded([&] {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw IoError(std::string("cannot open ") + path + " for writing");
+    write_ranks(f, std::span<const double>(ranks, static_cast<std::size_t>(n)));
+    f.flush();
+    if (!f) throw IoError(std::string("write to ") + path + " failed");
+  });
+}
+
+void lr_string_free(char* s) { std::free(s); }
 
 }  // extern "C"

@@ -11,6 +11,10 @@
 
 namespace levelrank {
 inline namespace b200 {
+namespace detail {
+lr_status baseline_solve(const Graph& g, const double* w, int64_t wn, double c, double tol, int device, double* ranks,
+                         double* r1, lr_report* rep);
+}
 namespace {
 
 [[noreturn]] void raise(lr_status st) {
@@ -209,6 +213,41 @@ EngineResult compute_pagerank(const Graph& g, std::span<const double> weights, c
   }
   PageRankEngine eng(g, small_threshold, device);
   return eng.solve(weights, params, mode, threads);
+}
+
+EngineResult compute_baseline(const Graph& g, std::span<const double> weights, const SolverParams& params,
+                              int device) {
+  validate_params(params);
+  const VertexId n = g.vertex_count();
+  if (static_cast<std::int64_t>(weights.size()) != n)
+    throw std::invalid_argument("weight vector does not match the vertex count");
+  EngineResult res;
+  res.ranks.assign(static_cast<std::size_t>(n), 0.0);
+  res.r1.assign(static_cast<std::size_t>(n), 0.0);
+  lr_report r{};
+  check(detail::baseline_solve(g, weights.data(), static_cast<std::int64_t>(weights.size()), params.c, params.tol,
+                               device, res.ranks.data(), res.r1.data(), &r));
+  SolveReport& rep = res.report;  // engine.cpp:194-216
+  rep.method = "baseline";
+  rep.c = params.c;
+  rep.tol = params.tol;
+  rep.keep_loops = g.loop_policy() == LoopPolicy::Keep;
+  rep.vertices = n;
+  rep.edges = g.edge_count();
+  rep.all_weights_zero = r.all_weights_zero != 0;
+  rep.total_iterations = r.total_iterations;
+  rep.iterative_edge_work = r.iterative_edge_work;
+  rep.iterative_edges = r.iterative_edges;
+  rep.total_edge_work = r.total_edge_work;
+  rep.mean_iterations_per_edge = r.mean_iterations_per_edge;
+  rep.wall_ms = r.wall_ms;
+  rep.plan_ms = r.plan_ms;
+  rep.upload_ms = r.upload_ms;
+  rep.solve_ms = r.solve_ms;
+  rep.device_ms = r.device_ms;
+  rep.device = device;
+  if (rep.all_weights_zero || n == 0) res.r1.clear();
+  return res;
 }
 
 }  // namespace b200
