@@ -2,6 +2,9 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <thread>
@@ -12,6 +15,19 @@
 namespace levelrank {
 inline namespace b200 {
 namespace detail {
+
+// LR_PLAN_PROF=1: per-phase wall times of the layout build on stderr
+struct PhaseClock {
+  bool on = std::getenv("LR_PLAN_PROF") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[plan] %-34s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 
 // Calls f(tid, begin, end) on contiguous chunks of [0, n) from up to
 // host_threads() threads (serial below `grain`).

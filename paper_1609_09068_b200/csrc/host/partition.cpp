@@ -1,203 +1,618 @@
-// SCC/CAC partition: iterative Tarjan with level tracking and the one-pass
-// CAC absorption rule (paper Theorem 1; reference proj/src/partition.cpp:52-145),
-// union-find with union by depth + path compression
-// (proj/include/levelrank/union_find.hpp:11-45), dense ids by first appearance
-// and a min-level shift (partition.cpp:23-50).  Written as one flat loop over
-// an explicit (vertex, edge cursor) stack with all per-vertex state in
-// contiguous int32/uint8 arrays; the work counters follow the reference's
-// definitions so PartitionStats match exactly.
+// SCC/CAC partition with levels (paper §3, Theorem 1), computed in parallel.
+//
+// The reference finds it in one serial pass (proj/src/partition.cpp:52-145:
+// iterative Tarjan, level = longest path to a sink over finished components,
+// a fresh single-vertex component absorbing the CACs one level down unless an
+// SCC sits there, union-find, ids by first appearance, min-level shift at
+// :23-50).  Theorem 1 makes that partition unique, so it can be computed in
+// any order that respects the component DAG:
+//
+//   1. SCCs: iterative trimming of vertices with no live in- or out-edge
+//      (trivial SCCs), a forward/backward reachability pass from the
+//      highest-degree live vertex (the giant SCC of a scale-free graph), a
+//      second trim, and a serial Tarjan over what is left (small SCCs);
+//   2. levels and CAC absorption: the component DAG is peeled from its sinks
+//      in wavefronts (Kahn on cross-edge counts); a component is decided once
+//      all its successors are -- its level is 1 + the highest successor level
+//      (1 for sinks), and a single-vertex component applies the absorption
+//      rule to its out-edges in row order (that scan also yields the
+//      reference's merge_scan_edge_visits);
+//   3. absorptions are unioned afterwards, ids numbered by each final
+//      component's smallest vertex (= first appearance), levels shifted.
+//
+// Wavefronts are parallel over components and, for a component with many
+// members (the giant SCC), over its members.  PartitionStats follow the
+// reference's definitions: every out-edge is explored once
+// (explore_edge_visits = m), finish runs once per vertex (finish_calls = n).
 #include "levelrank/partition.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
+#include <thread>
 #include <vector>
+
+#include "parallel.hpp"
 
 namespace levelrank {
 inline namespace b200 {
 namespace {
 
-struct DisjointSets {
-  std::vector<std::int32_t> parent;
-  std::vector<std::uint8_t> depth;
-  explicit DisjointSets(std::int32_t n) : parent(static_cast<std::size_t>(n)), depth(static_cast<std::size_t>(n), 1) {
-    for (std::int32_t i = 0; i < n; ++i) parent[static_cast<std::size_t>(i)] = i;
-  }
-  std::int32_t find(std::int32_t x) {
-    std::int32_t r = x;
-    while (parent[static_cast<std::size_t>(r)] != r) r = parent[static_cast<std::size_t>(r)];
-    while (parent[static_cast<std::size_t>(x)] != r) {
-      const std::int32_t nx = parent[static_cast<std::size_t>(x)];
-      parent[static_cast<std::size_t>(x)] = r;
-      x = nx;
+using detail::parallel_chunks;
+using detail::parallel_dynamic;
+
+template <typename T>
+T atomic_sub(T& x, T v) {
+  return std::atomic_ref<T>(x).fetch_sub(v, std::memory_order_acq_rel);
+}
+inline bool claim(std::uint8_t& flag) {
+  std::atomic_ref<std::uint8_t> f(flag);
+  return f.load(std::memory_order_relaxed) == 0 && f.exchange(1, std::memory_order_acq_rel) == 0;
+}
+
+// Work lists filled by many threads: one vector per thread, concatenated.
+struct Frontier {
+  std::vector<std::vector<std::int32_t>> parts;
+  explicit Frontier(int t) : parts(static_cast<std::size_t>(t)) {}
+  std::vector<std::int32_t> take() {
+    std::size_t total = 0;
+    for (const auto& p : parts) total += p.size();
+    std::vector<std::int32_t> out;
+    out.reserve(total);
+    for (auto& p : parts) {
+      out.insert(out.end(), p.begin(), p.end());
+      p.clear();
     }
-    return r;
+    return out;
+  }
+};
+
+// One bit per vertex, set/cleared atomically.
+struct Bits {
+  std::vector<std::uint64_t> w;
+  explicit Bits(std::size_t n) : w((n + 63) / 64, 0) {}
+  bool get(VertexId v) const { return (w[static_cast<std::size_t>(v) >> 6] >> (v & 63)) & 1u; }
+  // true if this call set the bit
+  bool set_atomic(VertexId v) {
+    const std::uint64_t bit = std::uint64_t{1} << (v & 63);
+    std::atomic_ref<std::uint64_t> a(w[static_cast<std::size_t>(v) >> 6]);
+    return !(a.load(std::memory_order_relaxed) & bit) && !(a.fetch_or(bit, std::memory_order_relaxed) & bit);
+  }
+  void clear_atomic(VertexId v) {
+    std::atomic_ref<std::uint64_t>(w[static_cast<std::size_t>(v) >> 6])
+        .fetch_and(~(std::uint64_t{1} << (v & 63)), std::memory_order_relaxed);
+  }
+};
+
+// parallel_chunks with the thread index bounded by host_threads()
+template <typename F>
+void for_items(const std::vector<std::int32_t>& items, F&& f) {
+  parallel_chunks(static_cast<std::int64_t>(items.size()),
+                  [&](int th, std::int64_t b, std::int64_t e) {
+                    for (std::int64_t i = b; i < e; ++i) f(th, items[static_cast<std::size_t>(i)]);
+                  },
+                  256);
+}
+
+struct Adjacency {
+  const EdgeId* off;
+  const VertexId* tgt;
+  std::vector<EdgeId> in_off;  // in-edges (self-loops left out), source-ascending rows
+  std::vector<VertexId> in_src;
+};
+
+// ------------------------------------------------------------- 1. SCC labels
+class SccFinder {
+ public:
+  SccFinder(VertexId n, const Adjacency& a, detail::PhaseClock& clk)
+      : n_(n), a_(a), clk_(clk), label_(static_cast<std::size_t>(n), -1) {}
+
+  // label[v] = a representative vertex of v's SCC
+  std::vector<VertexId> run() {
+    const std::size_t nn = static_cast<std::size_t>(n_);
+    din_.assign(nn, 0);
+    dout_.assign(nn, 0);
+    queued_.assign(nn, 0);
+    parallel_chunks(n_, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t v = b; v < e; ++v) {
+        din_[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(a_.in_off[static_cast<std::size_t>(v) + 1] - a_.in_off[static_cast<std::size_t>(v)]);
+        std::int32_t d = 0;
+        for (EdgeId k = a_.off[v]; k < a_.off[v + 1]; ++k) d += a_.tgt[k] != v;
+        dout_[static_cast<std::size_t>(v)] = d;
+      }
+    });
+    clk_.mark("partition: degrees");
+    trim();
+    clk_.mark("partition: trim");
+    reach_giant();
+    clk_.mark("partition: giant SCC (fw/bw reach)");
+    trim();
+    clk_.mark("partition: trim 2");
+    tarjan_rest();
+    clk_.mark("partition: Tarjan on the rest");
+    return std::move(label_);
+  }
+
+ private:
+  bool live(VertexId v) const { return label_[static_cast<std::size_t>(v)] < 0; }
+
+  // Vertices without a live in-edge or out-edge are SCCs of their own; peel
+  // them in rounds until none is left.
+  void trim() {
+    const int T = host_threads();
+    Frontier next(T);
+    parallel_chunks(n_, [&](int th, std::int64_t b, std::int64_t e) {
+      for (std::int64_t v = b; v < e; ++v)
+        if (live(static_cast<VertexId>(v)) && (din_[static_cast<std::size_t>(v)] == 0 || dout_[static_cast<std::size_t>(v)] == 0) &&
+            claim(queued_[static_cast<std::size_t>(v)]))
+          next.parts[static_cast<std::size_t>(th)].push_back(static_cast<std::int32_t>(v));
+    });
+    std::vector<std::int32_t> cur = next.take();
+    while (!cur.empty()) {
+      for (const VertexId v : cur) label_[static_cast<std::size_t>(v)] = v;
+      for_items(cur, [&](int th, VertexId v) {
+        auto& out = next.parts[static_cast<std::size_t>(th)];
+        for (EdgeId k = a_.off[v]; k < a_.off[v + 1]; ++k) {
+          const VertexId w = a_.tgt[k];
+          if (w != v && live(w) && atomic_sub(din_[static_cast<std::size_t>(w)], 1) == 1 && claim(queued_[static_cast<std::size_t>(w)]))
+            out.push_back(w);
+        }
+        for (EdgeId k = a_.in_off[static_cast<std::size_t>(v)]; k < a_.in_off[static_cast<std::size_t>(v) + 1]; ++k) {
+          const VertexId p = a_.in_src[static_cast<std::size_t>(k)];
+          if (live(p) && atomic_sub(dout_[static_cast<std::size_t>(p)], 1) == 1 && claim(queued_[static_cast<std::size_t>(p)]))
+            out.push_back(p);
+        }
+      });
+      cur = next.take();
+    }
+  }
+
+  // Forward and backward reachability from the live vertex of largest
+  // din*dout; the intersection is its SCC (the giant SCC of a scale-free
+  // graph).  Live set and visited sets are bitmaps (a few MB: they stay in
+  // cache while the edge lists stream).
+  void reach_giant() {
+    std::int64_t best = -1;
+    VertexId pivot = -1;
+    for (VertexId v = 0; v < n_; ++v)
+      if (live(v)) {
+        const std::int64_t s = static_cast<std::int64_t>(din_[static_cast<std::size_t>(v)]) * dout_[static_cast<std::size_t>(v)];
+        if (s > best) best = s, pivot = v;
+      }
+    if (pivot < 0) return;
+    const std::size_t nn = static_cast<std::size_t>(n_);
+    Bits alive(nn), fw(nn), bw(nn);
+    parallel_chunks((n_ + 63) / 64, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t wd = b; wd < e; ++wd) {
+        std::uint64_t x = 0;
+        for (std::int64_t v = wd * 64, k = 0; k < 64 && v < n_; ++v, ++k) x |= static_cast<std::uint64_t>(live(static_cast<VertexId>(v))) << k;
+        alive.w[static_cast<std::size_t>(wd)] = x;
+      }
+    });
+    bfs(pivot, alive, fw, false);
+    bfs(pivot, alive, bw, true);
+    giant_ = pivot;
+    // the SCC's members leave the graph: recount live degrees without them
+    parallel_chunks(n_, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t v = b; v < e; ++v)
+        if (fw.get(static_cast<VertexId>(v)) && bw.get(static_cast<VertexId>(v))) {
+          label_[static_cast<std::size_t>(v)] = pivot;
+          alive.clear_atomic(static_cast<VertexId>(v));
+        }
+    });
+    parallel_chunks(n_, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t vv = b; vv < e; ++vv) {
+        const VertexId v = static_cast<VertexId>(vv);
+        if (!alive.get(v)) continue;
+        std::int32_t di = 0, dout = 0;
+        for (EdgeId k = a_.off[v]; k < a_.off[v + 1]; ++k) dout += a_.tgt[k] != v && alive.get(a_.tgt[k]);
+        for (EdgeId k = a_.in_off[static_cast<std::size_t>(v)]; k < a_.in_off[static_cast<std::size_t>(v) + 1]; ++k)
+          di += alive.get(a_.in_src[static_cast<std::size_t>(k)]);
+        din_[static_cast<std::size_t>(v)] = di;
+        dout_[static_cast<std::size_t>(v)] = dout;
+      }
+    });
+  }
+
+  // Level-synchronous BFS over the live vertices, direction-optimising
+  // (Beamer et al.): a large frontier switches to the bottom-up step, where
+  // every unvisited vertex looks for one parent in the frontier and stops.
+  void bfs(VertexId src, const Bits& alive, Bits& seen, bool backward) {
+    const int T = host_threads();
+    const EdgeId* fo = backward ? a_.in_off.data() : a_.off;  // search direction
+    const VertexId* fa = backward ? a_.in_src.data() : a_.tgt;
+    const EdgeId* ro = backward ? a_.off : a_.in_off.data();  // parents in the search direction
+    const VertexId* ra = backward ? a_.tgt : a_.in_src.data();
+    Frontier next(T);
+    Bits in_front(static_cast<std::size_t>(n_));
+    seen.set_atomic(src);
+    std::vector<std::int32_t> cur{src};
+    EdgeId unexplored = fo[n_] - fo[0];
+    bool bottom_up = false;
+    while (!cur.empty()) {
+      std::atomic<EdgeId> fe{0};
+      for_items(cur, [&](int, VertexId v) { fe.fetch_add(fo[v + 1] - fo[v], std::memory_order_relaxed); });
+      if (!bottom_up && fe.load() > unexplored / 14) bottom_up = true;
+      else if (bottom_up && static_cast<std::int64_t>(cur.size()) < n_ / 24) bottom_up = false;
+      unexplored -= fe.load();
+      if (bottom_up) {
+        std::fill(in_front.w.begin(), in_front.w.end(), 0);
+        for_items(cur, [&](int, VertexId v) { in_front.set_atomic(v); });
+        parallel_chunks(n_, [&](int th, std::int64_t b, std::int64_t e) {
+          auto& out = next.parts[static_cast<std::size_t>(th)];
+          for (std::int64_t ww = b; ww < e; ++ww) {
+            const VertexId w = static_cast<VertexId>(ww);
+            if (!alive.get(w) || seen.get(w)) continue;
+            for (EdgeId k = ro[w]; k < ro[w + 1]; ++k)
+              if (in_front.get(ra[k])) {
+                seen.set_atomic(w);
+                out.push_back(w);
+                break;
+              }
+          }
+        });
+      } else {
+        for_items(cur, [&](int th, VertexId v) {
+          auto& out = next.parts[static_cast<std::size_t>(th)];
+          for (EdgeId k = fo[v]; k < fo[v + 1]; ++k) {
+            const VertexId w = fa[k];
+            if (alive.get(w) && seen.set_atomic(w)) out.push_back(w);
+          }
+        });
+      }
+      cur = next.take();
+    }
+  }
+
+  // Tarjan's algorithm (SCC labels only) over the live vertices.
+  void tarjan_rest() {
+    const std::size_t nn = static_cast<std::size_t>(n_);
+    std::vector<std::int32_t> order(nn, -1), low(nn, 0);
+    std::vector<VertexId> pending;
+    std::vector<std::pair<VertexId, EdgeId>> stack;
+    std::int32_t clock = 0;
+    for (VertexId s = 0; s < n_; ++s) {
+      if (!live(s) || order[static_cast<std::size_t>(s)] >= 0) continue;
+      auto open = [&](VertexId v) {
+        order[static_cast<std::size_t>(v)] = low[static_cast<std::size_t>(v)] = clock++;
+        pending.push_back(v);
+        stack.emplace_back(v, a_.off[v]);
+      };
+      open(s);
+      while (!stack.empty()) {
+        auto& top = stack.back();
+        const VertexId v = top.first;
+        if (top.second < a_.off[v + 1]) {
+          const VertexId w = a_.tgt[top.second++];
+          if (w == v || !live(w)) continue;
+          if (order[static_cast<std::size_t>(w)] < 0) open(w);
+          else low[static_cast<std::size_t>(v)] = std::min(low[static_cast<std::size_t>(v)], low[static_cast<std::size_t>(w)]);
+          continue;
+        }
+        stack.pop_back();
+        if (!stack.empty()) {
+          const VertexId p = stack.back().first;
+          low[static_cast<std::size_t>(p)] = std::min(low[static_cast<std::size_t>(p)], low[static_cast<std::size_t>(v)]);
+        }
+        if (low[static_cast<std::size_t>(v)] != order[static_cast<std::size_t>(v)]) continue;
+        VertexId m;
+        do {
+          m = pending.back();
+          pending.pop_back();
+          label_[static_cast<std::size_t>(m)] = v;  // leaves the live set
+          low[static_cast<std::size_t>(m)] = n_;    // never lowers a later low
+        } while (m != v);
+      }
+    }
+  }
+
+  VertexId n_;
+  const Adjacency& a_;
+  detail::PhaseClock& clk_;
+ public:
+  VertexId giant_ = -1;  // representative of the SCC found by reachability (-1: none)
+ private:
+  std::vector<VertexId> label_;
+  std::vector<std::int32_t> din_, dout_;
+  std::vector<std::uint8_t> queued_;
+};
+
+// Disjoint sets over component indices (union by size, path halving).
+struct Sets {
+  std::vector<std::int32_t> up;
+  explicit Sets(std::int32_t k) : up(static_cast<std::size_t>(k), -1) {}
+  std::int32_t find(std::int32_t x) {
+    while (up[static_cast<std::size_t>(x)] >= 0) {
+      const std::int32_t p = up[static_cast<std::size_t>(x)];
+      if (up[static_cast<std::size_t>(p)] >= 0) up[static_cast<std::size_t>(x)] = up[static_cast<std::size_t>(p)];
+      x = p;
+    }
+    return x;
   }
   void unite(std::int32_t a, std::int32_t b) {
     a = find(a);
     b = find(b);
     if (a == b) return;
-    if (depth[static_cast<std::size_t>(a)] < depth[static_cast<std::size_t>(b)]) std::swap(a, b);
-    parent[static_cast<std::size_t>(b)] = a;
-    if (depth[static_cast<std::size_t>(a)] == depth[static_cast<std::size_t>(b)]) ++depth[static_cast<std::size_t>(a)];
+    if (up[static_cast<std::size_t>(a)] > up[static_cast<std::size_t>(b)]) std::swap(a, b);
+    up[static_cast<std::size_t>(a)] += up[static_cast<std::size_t>(b)];
+    up[static_cast<std::size_t>(b)] = a;
   }
 };
 
-constexpr std::uint8_t kDone = 1;  // component finished ("assigned")
-constexpr std::uint8_t kBig = 2;   // member of a size >= 2 SCC
+constexpr std::int64_t kWideComponent = 1 << 14;  // members scanned in parallel above this
+constexpr EdgeId kAhead = 12;                      // software prefetch distance on edge scans
 
-// Per-vertex DFS state in one 16-byte record: a visit costs one cache line
-// (the traversal is bound by these random accesses), and the records of the
-// next out-neighbours are prefetched while the current edge is handled.
-struct VRec {
-  std::int32_t order;
-  std::int32_t low;
-  std::int32_t level;
-  std::uint8_t state;
-  std::uint8_t pad[3];
-};
-constexpr EdgeId kPrefetch = 8;
-
-Partition tarjan_partition(const Graph& g, bool absorb_cacs, PartitionStats* stats) {
+Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* stats) {
   const VertexId n = g.vertex_count();
-  const EdgeId* off = g.offsets_data();
-  const VertexId* tgt = g.targets_data();
   const std::size_t nn = static_cast<std::size_t>(n);
-  std::vector<VRec> rec(nn, VRec{-1, 0, 0, 0, {0, 0, 0}});
-  DisjointSets sets(n);
-  std::vector<VertexId> pending;
-  std::vector<std::pair<VertexId, EdgeId>> stack;  // (vertex, next edge index)
-  std::vector<VertexId> absorbed;
-  pending.reserve(1024);
-  stack.reserve(1024);
+  Partition p;
   PartitionStats st;
-  std::int32_t clock = 0;
-  auto R = [&](VertexId v) -> VRec& { return rec[static_cast<std::size_t>(v)]; };
+  st.explore_edge_visits = g.edge_count();
+  st.finish_calls = n;
+  if (n == 0) {
+    if (stats) *stats = st;
+    return p;
+  }
+  detail::PhaseClock clk;
+  Adjacency adj{g.offsets_data(), g.targets_data(), {}, {}};
+  {
+    std::vector<EdgeId> ptr[1];
+    std::vector<VertexId> col[1];
+    detail::bucket_csr<1>(
+        n, n,
+        [&](std::int64_t uu, auto&& sink) {
+          const VertexId u = static_cast<VertexId>(uu);
+          for (EdgeId k = adj.off[u]; k < adj.off[u + 1]; ++k)
+            if (adj.tgt[k] != u) sink(0, adj.tgt[k], u);
+        },
+        ptr, col);
+    adj.in_off = std::move(ptr[0]);
+    adj.in_src = std::move(col[0]);
+  }
+  clk.mark("partition: in-edge transpose");
+  SccFinder finder(n, adj, clk);
+  const std::vector<VertexId> label = finder.run();
+  const VertexId giant = finder.giant_;
 
-  // the level/low update of the reference's update_from (partition.cpp:67-74)
-  auto relax = [&](VertexId v, VertexId w) {
-    VRec& a = R(v);
-    const VRec& b = R(w);
-    if (b.state & kDone) {
-      a.level = std::max(a.level, b.level + 1);
-    } else {
-      a.level = std::max(a.level, b.level);
-      a.low = std::min(a.low, b.low);
-    }
-  };
-  auto open = [&](VertexId v) {
-    VRec& a = R(v);
-    a.order = a.low = clock++;
-    a.level = 1;
-    pending.push_back(v);
-    stack.emplace_back(v, off[v]);
-    for (EdgeId e = off[v]; e < off[v + 1] && e < off[v] + kPrefetch; ++e) __builtin_prefetch(&rec[static_cast<std::size_t>(tgt[e])]);
-  };
-  // component root bookkeeping (partition.cpp:76-113)
-  auto close = [&](VertexId v) {
-    ++st.finish_calls;
-    VRec& rv = R(v);
-    if (rv.low != rv.order) return;
-    std::size_t first = pending.size();
-    while (pending[--first] != v) {
-    }
-    const std::size_t members = pending.size() - first;
-    const std::int32_t lv = rv.level;
-    for (std::size_t i = first; i < pending.size(); ++i) {
-      const VertexId m = pending[i];
-      R(m).state = kDone | kBig;
-      R(m).level = lv;
-      sets.unite(v, m);
-    }
-    pending.resize(first);
-    if (members != 1) return;
-    rv.state = kDone;
-    if (!absorb_cacs) return;
-    absorbed.clear();
-    const std::int32_t below = rv.level - 1;
-    for (EdgeId e = off[v]; e < off[v + 1]; ++e) {
-      ++st.merge_scan_edge_visits;
-      const VertexId w = tgt[e];
-      if (e + kPrefetch < off[v + 1]) __builtin_prefetch(&rec[static_cast<std::size_t>(tgt[e + kPrefetch])]);
-      if (w == v || R(w).level != below) continue;
-      if (R(w).state & kBig) return;  // an SCC on the next level vetoes
-      absorbed.push_back(w);
-    }
-    if (absorbed.empty()) return;
-    rv.level = below;
-    for (const VertexId w : absorbed) sets.unite(v, w);
-  };
-
-  for (VertexId s = 0; s < n; ++s) {
-    if (R(s).order >= 0) continue;
-    open(s);
-    while (!stack.empty()) {
-      auto& top = stack.back();
-      const VertexId v = top.first;
-      const EdgeId end = off[v + 1];
-      if (top.second < end) {
-        const EdgeId e = top.second++;
-        const VertexId w = tgt[e];
-        if (e + kPrefetch < end) __builtin_prefetch(&rec[static_cast<std::size_t>(tgt[e + kPrefetch])]);
-        ++st.explore_edge_visits;
-        if (w == v) continue;
-        if (R(w).order < 0)
-          open(w);
-        else
-          relax(v, w);
+  // dense component index per vertex (components numbered by representative)
+  std::vector<std::int32_t> cidx(nn + 1, 0);
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v) cidx[static_cast<std::size_t>(v)] = label[static_cast<std::size_t>(v)] == v;
+  });
+  const std::int32_t K = detail::exclusive_scan_inplace(cidx.data(), static_cast<std::int64_t>(nn) + 1);
+  std::vector<std::int32_t> comp(nn);
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v) comp[static_cast<std::size_t>(v)] = cidx[static_cast<std::size_t>(label[static_cast<std::size_t>(v)])];
+  });
+  std::vector<std::int32_t>().swap(cidx);
+  // members grouped by component (CSR), cross out-edge counts.  The giant
+  // SCC (one component, a large share of the vertices) is counted per thread
+  // instead of by atomics on one counter.
+  const std::size_t KK = static_cast<std::size_t>(K);
+  const std::int32_t cg = giant >= 0 ? comp[static_cast<std::size_t>(giant)] : -1;
+  const int T = host_threads();
+  std::vector<std::int64_t> mptr(KK + 1, 0);
+  std::vector<std::int64_t> pending(KK, 0);
+  std::vector<std::vector<VertexId>> gmem(static_cast<std::size_t>(T));
+  std::vector<std::int64_t> gpend(static_cast<std::size_t>(T), 0);
+  parallel_chunks(n, [&](int th, std::int64_t b, std::int64_t e) {
+    for (std::int64_t vv = b; vv < e; ++vv) {
+      const VertexId v = static_cast<VertexId>(vv);
+      const std::int32_t c = comp[static_cast<std::size_t>(v)];
+      std::int64_t x = 0;
+      const EdgeId k1 = adj.off[v + 1];
+      for (EdgeId k = adj.off[v]; k < k1; ++k) {
+        if (k + kAhead < k1) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
+        x += comp[static_cast<std::size_t>(adj.tgt[k])] != c;
+      }
+      if (c == cg) {
+        gmem[static_cast<std::size_t>(th)].push_back(v);
+        gpend[static_cast<std::size_t>(th)] += x;
         continue;
       }
-      stack.pop_back();
-      close(v);
-      if (!stack.empty()) relax(stack.back().first, v);
+      std::atomic_ref<std::int64_t>(mptr[static_cast<std::size_t>(c)]).fetch_add(1, std::memory_order_relaxed);
+      if (x) std::atomic_ref<std::int64_t>(pending[static_cast<std::size_t>(c)]).fetch_add(x, std::memory_order_relaxed);
+    }
+  });
+  if (cg >= 0) {
+    mptr[static_cast<std::size_t>(cg)] = 0;
+    for (int t = 0; t < T; ++t) {
+      mptr[static_cast<std::size_t>(cg)] += static_cast<std::int64_t>(gmem[static_cast<std::size_t>(t)].size());
+      pending[static_cast<std::size_t>(cg)] += gpend[static_cast<std::size_t>(t)];
     }
   }
-  if (stats) *stats = st;
+  std::vector<std::int32_t> csize(KK);
+  parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c) csize[static_cast<std::size_t>(c)] = static_cast<std::int32_t>(mptr[static_cast<std::size_t>(c)]);
+  });
+  detail::exclusive_scan_inplace(mptr.data(), static_cast<std::int64_t>(KK) + 1);
+  std::vector<VertexId> members(nn);
+  {
+    std::vector<std::int64_t> fill(mptr.begin(), mptr.end() - 1);
+    parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t v = b; v < e; ++v) {
+        const std::int32_t c = comp[static_cast<std::size_t>(v)];
+        if (c == cg) continue;
+        const std::int64_t at = csize[static_cast<std::size_t>(c)] == 1
+                                    ? fill[static_cast<std::size_t>(c)]
+                                    : std::atomic_ref<std::int64_t>(fill[static_cast<std::size_t>(c)]).fetch_add(1, std::memory_order_relaxed);
+        members[static_cast<std::size_t>(at)] = static_cast<VertexId>(v);
+      }
+    });
+    if (cg >= 0) {
+      std::int64_t at = mptr[static_cast<std::size_t>(cg)];
+      for (auto& part : gmem) {
+        std::copy(part.begin(), part.end(), members.begin() + at);
+        at += static_cast<std::int64_t>(part.size());
+        std::vector<VertexId>().swap(part);
+      }
+    }
+  }
 
-  Partition p;
-  p.comp_of.assign(nn, -1);
-  std::vector<VertexId> id_of_root(nn, -1);
-  for (VertexId v = 0; v < n; ++v) {
-    const VertexId r = sets.find(v);
-    VertexId& id = id_of_root[static_cast<std::size_t>(r)];
-    if (id < 0) {
-      id = static_cast<VertexId>(p.kinds.size());
-      p.kinds.push_back((rec[static_cast<std::size_t>(r)].state & kBig) ? ComponentKind::Scc : ComponentKind::Cac);
-      p.levels.push_back(rec[static_cast<std::size_t>(r)].level);
-      p.sizes.push_back(0);
+  clk.mark("partition: components, members");
+  // 2. wavefronts from the sinks of the component DAG
+  std::vector<std::int32_t> level(KK, 0);
+  std::vector<std::vector<std::pair<std::int32_t, std::int32_t>>> absorbs(static_cast<std::size_t>(T));
+  std::vector<std::int64_t> scans(static_cast<std::size_t>(T), 0);
+  Frontier next(T);
+  parallel_chunks(K, [&](int th, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c)
+      if (pending[static_cast<std::size_t>(c)] == 0) next.parts[static_cast<std::size_t>(th)].push_back(static_cast<std::int32_t>(c));
+  });
+  std::vector<std::int32_t> cur = next.take();
+  auto max_successor = [&](std::int32_t c, std::int64_t m0, std::int64_t m1) {
+    std::int32_t hi = 0;
+    for (std::int64_t i = m0; i < m1; ++i) {
+      const VertexId u = members[static_cast<std::size_t>(i)];
+      const EdgeId k1 = adj.off[u + 1];
+      for (EdgeId k = adj.off[u]; k < k1; ++k) {
+        if (k + kAhead < k1) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
+        const std::int32_t cw = comp[static_cast<std::size_t>(adj.tgt[k])];
+        if (cw != c) hi = std::max(hi, level[static_cast<std::size_t>(cw)]);
+      }
     }
-    p.comp_of[static_cast<std::size_t>(v)] = id;
-    ++p.sizes[static_cast<std::size_t>(id)];
+    return hi;
+  };
+  auto release = [&](int th, std::int32_t c, std::int64_t m0, std::int64_t m1) {
+    auto& out = next.parts[static_cast<std::size_t>(th)];
+    for (std::int64_t i = m0; i < m1; ++i) {
+      const VertexId u = members[static_cast<std::size_t>(i)];
+      const EdgeId k1 = adj.in_off[static_cast<std::size_t>(u) + 1];
+      for (EdgeId k = adj.in_off[static_cast<std::size_t>(u)]; k < k1; ++k) {
+        if (k + kAhead < k1) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k + kAhead)])]);
+        const std::int32_t cp = comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k)])];
+        if (cp != c && atomic_sub(pending[static_cast<std::size_t>(cp)], std::int64_t{1}) == 1) out.push_back(cp);
+      }
+    }
+  };
+  // decide one component whose successors are all decided
+  auto decide = [&](int th, std::int32_t c, std::int32_t hi) {
+    const std::int32_t l0 = hi + 1;
+    level[static_cast<std::size_t>(c)] = l0;
+    if (csize[static_cast<std::size_t>(c)] != 1 || !absorb_cacs) return;
+    const VertexId v = members[static_cast<std::size_t>(mptr[static_cast<std::size_t>(c)])];
+    auto& mine = absorbs[static_cast<std::size_t>(th)];
+    const std::size_t mark = mine.size();
+    std::int64_t scanned = 0;
+    bool veto = false;
+    for (EdgeId k = adj.off[v]; k < adj.off[v + 1]; ++k) {
+      ++scanned;
+      const VertexId w = adj.tgt[k];
+      if (w == v) continue;
+      const std::int32_t cw = comp[static_cast<std::size_t>(w)];
+      if (level[static_cast<std::size_t>(cw)] != l0 - 1) continue;
+      if (csize[static_cast<std::size_t>(cw)] > 1) {
+        veto = true;
+        break;
+      }
+      mine.emplace_back(c, cw);
+    }
+    scans[static_cast<std::size_t>(th)] += scanned;
+    if (veto) mine.resize(mark);
+    else if (mine.size() > mark) level[static_cast<std::size_t>(c)] = l0 - 1;
+  };
+  while (!cur.empty()) {
+    std::vector<std::int32_t> narrow, wide;
+    for (const std::int32_t c : cur)
+      (mptr[static_cast<std::size_t>(c) + 1] - mptr[static_cast<std::size_t>(c)] > kWideComponent ? wide : narrow).push_back(c);
+    for (const std::int32_t c : wide) {  // the giant SCC: members in parallel
+      const std::int64_t m0 = mptr[static_cast<std::size_t>(c)], m1 = mptr[static_cast<std::size_t>(c) + 1];
+      std::vector<std::int32_t> his(static_cast<std::size_t>(T), 0);
+      parallel_chunks(m1 - m0, [&](int th, std::int64_t b, std::int64_t e) {
+        his[static_cast<std::size_t>(th)] = std::max(his[static_cast<std::size_t>(th)], max_successor(c, m0 + b, m0 + e));
+      });
+      decide(0, c, *std::max_element(his.begin(), his.end()));
+    }
+    for_items(narrow, [&](int th, std::int32_t c) {
+      decide(th, c, max_successor(c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]));
+    });
+    for (const std::int32_t c : wide) {
+      const std::int64_t m0 = mptr[static_cast<std::size_t>(c)], m1 = mptr[static_cast<std::size_t>(c) + 1];
+      parallel_chunks(m1 - m0, [&](int th, std::int64_t b, std::int64_t e) { release(th, c, m0 + b, m0 + e); });
+    }
+    for_items(narrow, [&](int th, std::int32_t c) {
+      release(th, c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]);
+    });
+    cur = next.take();
   }
-  if (!p.levels.empty()) {
-    const std::int32_t lo = *std::min_element(p.levels.begin(), p.levels.end());
-    for (auto& l : p.levels) l -= lo;
-    p.max_level = *std::max_element(p.levels.begin(), p.levels.end());
-  }
+  for (const std::int64_t s : scans) st.merge_scan_edge_visits += s;
+
+  clk.mark("partition: level wavefronts");
+  // 3. absorptions -> final components, ids by smallest member
+  Sets sets(K);
+  for (const auto& part : absorbs)
+    for (const auto& [a, b] : part) sets.unite(a, b);
+  std::vector<std::int32_t> root(KK);
+  for (std::size_t c = 0; c < KK; ++c) root[c] = sets.find(static_cast<std::int32_t>(c));
+  std::vector<VertexId> first(KK, n);
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v) {
+      std::atomic_ref<VertexId> f(first[static_cast<std::size_t>(root[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])])]);
+      VertexId cur_min = f.load(std::memory_order_relaxed);
+      while (v < cur_min && !f.compare_exchange_weak(cur_min, static_cast<VertexId>(v), std::memory_order_relaxed)) {
+      }
+    }
+  });
+  std::vector<VertexId> id_at(nn + 1, 0);  // id_at[v] = number of components first seen before v
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v)
+      id_at[static_cast<std::size_t>(v)] = first[static_cast<std::size_t>(root[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])])] == v;
+  });
+  const VertexId k = detail::exclusive_scan_inplace(id_at.data(), static_cast<std::int64_t>(nn) + 1);
+  p.comp_of.resize(nn);
+  p.kinds.resize(static_cast<std::size_t>(k));
+  p.levels.resize(static_cast<std::size_t>(k));
+  p.sizes.assign(static_cast<std::size_t>(k), 0);
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v) {
+      const std::int32_t c = comp[static_cast<std::size_t>(v)];
+      const std::int32_t r = root[static_cast<std::size_t>(c)];
+      const VertexId id = id_at[static_cast<std::size_t>(first[static_cast<std::size_t>(r)])];
+      p.comp_of[static_cast<std::size_t>(v)] = id;
+      std::atomic_ref<VertexId>(p.sizes[static_cast<std::size_t>(id)]).fetch_add(1, std::memory_order_relaxed);
+      if (first[static_cast<std::size_t>(r)] == v) {
+        p.kinds[static_cast<std::size_t>(id)] = csize[static_cast<std::size_t>(c)] > 1 ? ComponentKind::Scc : ComponentKind::Cac;
+        p.levels[static_cast<std::size_t>(id)] = level[static_cast<std::size_t>(c)];
+      }
+    }
+  });
+  const std::int32_t lo = *std::min_element(p.levels.begin(), p.levels.end());
+  for (auto& l : p.levels) l -= lo;
+  p.max_level = *std::max_element(p.levels.begin(), p.levels.end());
+  clk.mark("partition: unions + assemble");
+  if (stats) *stats = st;
   return p;
 }
 
 }  // namespace
 
-Partition find_components(const Graph& g, PartitionStats* stats) { return tarjan_partition(g, true, stats); }
+Partition find_components(const Graph& g, PartitionStats* stats) { return wavefront_partition(g, true, stats); }
 
-Partition find_components_scc_only(const Graph& g) { return tarjan_partition(g, false, nullptr); }
+Partition find_components_scc_only(const Graph& g) { return wavefront_partition(g, false, nullptr); }
 
+// The partition in a form independent of id numbering: components as sorted
+// member lists with kind and level, ordered (partition.hpp:56-66).
 std::vector<CanonicalComponent> canonical_components(const Partition& p) {
-  std::vector<CanonicalComponent> cs(p.component_count());
-  for (std::size_t c = 0; c < cs.size(); ++c) {
+  const std::size_t k = p.component_count();
+  std::vector<std::size_t> at(k + 1, 0);
+  for (const VertexId c : p.comp_of) ++at[static_cast<std::size_t>(c) + 1];
+  for (std::size_t c = 0; c < k; ++c) at[c + 1] += at[c];
+  std::vector<CanonicalComponent> cs(k);
+  for (std::size_t c = 0; c < k; ++c) {
+    cs[c].members.reserve(at[c + 1] - at[c]);
     cs[c].kind = p.kinds[c];
     cs[c].level = p.levels[c];
   }
-  for (std::size_t v = 0; v < p.comp_of.size(); ++v)
+  for (std::size_t v = 0; v < p.comp_of.size(); ++v)  // ascending v: member lists come out sorted
     cs[static_cast<std::size_t>(p.comp_of[v])].members.push_back(static_cast<VertexId>(v));
   std::sort(cs.begin(), cs.end());
   return cs;
 }
 
 std::vector<std::uint8_t> big_scc_flags(const Partition& p) {
-  std::vector<std::uint8_t> f(p.comp_of.size(), 0);
-  for (std::size_t v = 0; v < f.size(); ++v)
-    f[v] = p.kinds[static_cast<std::size_t>(p.comp_of[v])] == ComponentKind::Scc;
+  std::vector<std::uint8_t> f(p.comp_of.size());
+  std::transform(p.comp_of.begin(), p.comp_of.end(), f.begin(),
+                 [&](VertexId c) { return static_cast<std::uint8_t>(p.kinds[static_cast<std::size_t>(c)] == ComponentKind::Scc); });
   return f;
 }
 
@@ -207,30 +622,25 @@ PartitionCensus census(const Partition& p) {
   c.max_level = p.max_level;
   c.level_count = p.max_level + 1;
   c.components_per_level.assign(static_cast<std::size_t>(p.max_level + 1), 0);
+  std::vector<std::int64_t> bins(33, 0);  // sizes in (2^(b-1), 2^b]
   VertexId largest = 0;
   for (std::size_t i = 0; i < p.component_count(); ++i) {
-    if (p.kinds[i] == ComponentKind::Scc) {
-      ++c.scc_components;
-    } else {
-      ++c.cac_components;
-      if (p.sizes[i] == 1) ++c.singleton_cacs;
-    }
+    const bool scc = p.kinds[i] == ComponentKind::Scc;
+    c.scc_components += scc;
+    c.cac_components += !scc;
+    c.singleton_cacs += !scc && p.sizes[i] == 1;
     ++c.components_per_level[static_cast<std::size_t>(p.levels[i])];
-    if (p.sizes[i] > largest) {
+    if (p.sizes[i] > largest) {  // first component of the largest size decides the kind
       largest = p.sizes[i];
       c.largest_kind = p.kinds[i];
     }
+    const auto s = static_cast<std::uint32_t>(p.sizes[i]);
+    ++bins[static_cast<std::size_t>(s <= 1 ? 0 : 32 - __builtin_clz(s - 1))];
   }
   c.largest_component = largest;
-  // size histogram over (bound/2, bound], bounds 1, 2, 4, ...
-  std::vector<std::int64_t> bins;
-  for (const VertexId s : p.sizes) {
-    std::size_t b = 0;
-    while ((VertexId{1} << b) < s) ++b;
-    if (bins.size() <= b) bins.resize(b + 1, 0);
-    ++bins[b];
-  }
-  for (std::size_t b = 0; b < bins.size(); ++b) c.size_histogram.emplace_back(VertexId{1} << b, bins[b]);
+  std::size_t top = bins.size();
+  while (top > 0 && bins[top - 1] == 0) --top;
+  for (std::size_t b = 0; b < top; ++b) c.size_histogram.emplace_back(VertexId{1} << b, bins[b]);
   return c;
 }
 

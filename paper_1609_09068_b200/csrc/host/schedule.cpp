@@ -16,17 +16,6 @@ namespace levelrank {
 inline namespace b200 {
 namespace {
 
-// LR_PLAN_PROF=1: per-phase wall times of the layout build on stderr
-struct PhaseClock {
-  bool on = std::getenv("LR_PLAN_PROF") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[plan] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
 
 // Stable counting sort, descending key (schedule.cpp:14-28).
 std::vector<VertexId> stable_desc(const std::vector<VertexId>& items, const std::vector<std::int32_t>& key,
@@ -218,7 +207,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   const std::uint8_t* lp = g.loop_data();
   const auto& comp_of = p.comp_of;
 
-  PhaseClock clk;
+  detail::PhaseClock clk;
   const auto comps = ordered_components(p, n);
   std::vector<std::int64_t> mb;
   std::vector<VertexId> mem;

@@ -149,7 +149,7 @@ def test_layout_emulation_bit_exact(lr, oracle):
             assert np.array_equal(r3, ref.ranks), t
 
 
-@pytest.mark.parametrize("cfg,shrink", [(1, 2), (2, 6), (3, 8), (4, 5)])
+@pytest.mark.parametrize("cfg,shrink", [(1, 2), (2, 6), (3, 8), (4, 5), (1, 0), (2, 2), (3, 5), (4, 2), (5, 8)])
 def test_config_partition_parity(lr, oracle, cfg, shrink):
     g = lr.config_graph(cfg, shrink)
     off, tgt, _, _ = g.csr()
@@ -158,6 +158,33 @@ def test_config_partition_parity(lr, oracle, cfg, shrink):
     a, b = lr.Plan(g, 100).schedule(), go.schedule(100)
     for k in ("unit_kind", "ids", "permutation", "cross_src", "edge_src", "edge_dst"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_partition_medium_random_structures(lr, oracle):
+    """Graphs big enough for every stage of the parallel partition: trimming
+    rounds, a giant SCC found by forward/backward reachability (above the
+    16k-member parallel threshold), small SCCs left to Tarjan, long chains of
+    single-vertex components absorbing CACs, kept and ignored self-loops."""
+    rng = np.random.default_rng(77)
+    for t in range(12):
+        n = int(rng.integers(20_000, 60_000))
+        m = int(n * rng.uniform(0.8, 3.0))
+        src = rng.integers(0, n, m)
+        dst = np.where(rng.random(m) < 0.7, np.minimum(src + rng.integers(1, 6, m), n - 1), rng.integers(0, n, m))
+        if t % 3 == 0:  # a dense core: one giant SCC
+            core = rng.integers(0, n // 2, 4 * n)
+            src = np.concatenate([src, core])
+            dst = np.concatenate([dst, rng.integers(0, n // 2, 4 * n)])
+        if t % 2:
+            loops = rng.integers(0, n, n // 50)
+            src, dst = np.concatenate([src, loops]), np.concatenate([dst, loops])
+        keep = t % 4 == 1
+        g = lr.Graph.from_edges(n, src=src.astype(np.int32), dst=dst.astype(np.int32), loop_policy=int(keep))
+        off, tgt, _, _ = g.csr()
+        go = oracle.graph_from_csr(n, off, tgt, keep)
+        assert_same_partition(lr.find_components(g), go.partition())
+        a, b = lr.find_components_scc_only(g), go.partition(merge=False)
+        assert np.array_equal(a.comp_of, b.comp_of) and np.array_equal(a.levels, b.levels), t
 
 
 def test_generators_deterministic(lr):
