@@ -18,6 +18,7 @@
 #include "levelrank/partition.hpp"
 #include "levelrank/schedule.hpp"
 #include "lr_cuda.h"
+#include "plan_internal.hpp"
 
 namespace levelrank {
 inline namespace b200 {
@@ -204,8 +205,9 @@ lr_status lr_plan_build(const lr_graph* gp, int32_t small_threshold, lr_plan** o
     auto plan = std::make_unique<lr_plan>();
     plan->g = &gp->g;
     plan->threshold = small_threshold;
-    plan->p = find_components(gp->g);
-    plan->L = build_layout(gp->g, plan->p, small_threshold);
+    detail::InEdges in;
+    plan->p = detail::find_components_with_in_edges(gp->g, nullptr, in);
+    plan->L = detail::build_layout_from(gp->g, plan->p, small_threshold, in);
     *out = plan.release();
   });
 }

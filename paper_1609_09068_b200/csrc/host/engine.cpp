@@ -3,11 +3,13 @@
 // exception types (engine.cpp:92-97, solvers.cpp:11-15,84-85,103-106,159).
 #include "levelrank/engine.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <stdexcept>
 #include <string>
 
 #include "lr_cuda.h"
+#include "plan_internal.hpp"
 
 namespace levelrank {
 inline namespace b200 {
@@ -54,9 +56,23 @@ void propagate_weights(std::span<const CrossEdge> cross, std::span<const double>
     d[i] = cross[i].dst;
     g[i] = cross[i].src_out_degree;
   }
-  if (ranks.size() != weights.size()) throw std::invalid_argument("ranks and weights differ in length");
-  check(lr_propagate_weights(device, s.data(), d.data(), g.data(), static_cast<std::int64_t>(cross.size()),
-                             ranks.data(), static_cast<std::int64_t>(ranks.size()), c, weights.data()));
+  // ranks are indexed by source, weights by destination: the two vectors may
+  // differ in length (engine.cpp:83-87); the C-ABI takes one length
+  const std::size_t nmax = std::max(ranks.size(), weights.size());
+  if (ranks.size() == weights.size()) {
+    check(lr_propagate_weights(device, s.data(), d.data(), g.data(), static_cast<std::int64_t>(cross.size()),
+                               ranks.data(), static_cast<std::int64_t>(ranks.size()), c, weights.data()));
+    return;
+  }
+  std::vector<double> r(nmax, 0.0), w(nmax, 0.0);
+  std::copy(ranks.begin(), ranks.end(), r.begin());
+  std::copy(weights.begin(), weights.end(), w.begin());
+  for (std::size_t i = 0; i < cross.size(); ++i)
+    if (static_cast<std::size_t>(d[i]) >= weights.size() || static_cast<std::size_t>(s[i]) >= ranks.size())
+      throw std::invalid_argument("cross edge out of range");
+  check(lr_propagate_weights(device, s.data(), d.data(), g.data(), static_cast<std::int64_t>(cross.size()), r.data(),
+                             static_cast<std::int64_t>(nmax), c, w.data()));
+  std::copy(w.begin(), w.begin() + static_cast<std::ptrdiff_t>(weights.size()), weights.begin());
 }
 
 struct PageRankEngine::Impl {
@@ -79,8 +95,11 @@ PageRankEngine::PageRankEngine(const Graph& g, VertexId small_threshold, int dev
   impl_->threshold = small_threshold;
   impl_->device = device;
   const auto t0 = std::chrono::steady_clock::now();
-  impl_->p = find_components(g);
-  impl_->L = build_layout(g, impl_->p, small_threshold);
+  {
+    detail::InEdges in;
+    impl_->p = detail::find_components_with_in_edges(g, nullptr, in);
+    impl_->L = detail::build_layout_from(g, impl_->p, small_threshold, in);
+  }
   const PartitionCensus c = census(impl_->p);
   impl_->census = lr_census{c.components, c.scc_components, c.cac_components, c.singleton_cacs, c.largest_component,
                             c.largest_kind == ComponentKind::Scc, c.max_level, c.level_count};

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "parallel.hpp"
+#include "plan_internal.hpp"
 
 namespace levelrank {
 inline namespace b200 {
@@ -342,7 +343,7 @@ struct Sets {
 constexpr std::int64_t kWideComponent = 1 << 14;  // members scanned in parallel above this
 constexpr EdgeId kAhead = 12;                      // software prefetch distance on edge scans
 
-Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* stats) {
+Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* stats, detail::InEdges* keep_in) {
   const VertexId n = g.vertex_count();
   const std::size_t nn = static_cast<std::size_t>(n);
   Partition p;
@@ -351,6 +352,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   st.finish_calls = n;
   if (n == 0) {
     if (stats) *stats = st;
+    if (keep_in) keep_in->off.assign(1, 0);
     return p;
   }
   detail::PhaseClock clk;
@@ -581,14 +583,24 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   p.max_level = *std::max_element(p.levels.begin(), p.levels.end());
   clk.mark("partition: unions + assemble");
   if (stats) *stats = st;
+  if (keep_in) {
+    keep_in->off = std::move(adj.in_off);
+    keep_in->src = std::move(adj.in_src);
+  }
   return p;
 }
 
 }  // namespace
 
-Partition find_components(const Graph& g, PartitionStats* stats) { return wavefront_partition(g, true, stats); }
+Partition find_components(const Graph& g, PartitionStats* stats) { return wavefront_partition(g, true, stats, nullptr); }
 
-Partition find_components_scc_only(const Graph& g) { return wavefront_partition(g, false, nullptr); }
+Partition find_components_scc_only(const Graph& g) { return wavefront_partition(g, false, nullptr, nullptr); }
+
+namespace detail {
+Partition find_components_with_in_edges(const Graph& g, PartitionStats* stats, InEdges& in) {
+  return wavefront_partition(g, true, stats, &in);
+}
+}  // namespace detail
 
 // The partition in a form independent of id numbering: components as sorted
 // member lists with kind and level, ordered (partition.hpp:56-66).

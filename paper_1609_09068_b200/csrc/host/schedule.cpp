@@ -11,6 +11,7 @@
 #include <stdexcept>
 
 #include "parallel.hpp"
+#include "plan_internal.hpp"
 
 namespace levelrank {
 inline namespace b200 {
@@ -187,7 +188,24 @@ Schedule build_schedule(const Graph& g, const Partition& p, VertexId small_thres
   return s;
 }
 
+namespace {
+Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_threshold, const detail::InEdges* in);
+}
+
 Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold) {
+  return build_layout_impl(g, p, small_threshold, nullptr);
+}
+
+namespace detail {
+Layout build_layout_from(const Graph& g, const Partition& p, VertexId small_threshold, const InEdges& in) {
+  return build_layout_impl(g, p, small_threshold, &in);
+}
+}  // namespace detail
+
+namespace {
+// in: the graph's in-edge lists when the partition already built them (then
+// the pull lists are gathered per row instead of transposing every edge again)
+Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_threshold, const detail::InEdges* in) {
   if (small_threshold < 1) throw std::invalid_argument("small_threshold must be at least 1");
   const VertexId n = g.vertex_count();
   const std::size_t nn = static_cast<std::size_t>(n);
@@ -324,17 +342,36 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   L.unit_row_begin[nu] = n;
   // Large SCC units: rows (= gather columns) by descending in-unit out-degree,
   // so the most-gathered s values sit together at the head of the unit.
+  // one scan of every out-edge: intra-component out-degree per vertex (kept
+  // self-loops count, ignored ones are dropped) -> SccLarge row order and the
+  // per-unit reference edge counts (unit.edges.size()); cross / dropped totals
   std::vector<std::int32_t> unit_out(nn, 0);
+  std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
   detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    EdgeId li = 0, lx = 0, ld = 0;
     for (std::int64_t uu = b; uu < e; ++uu) {
       const VertexId u = static_cast<VertexId>(uu);
-      if (plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)])].kind != UnitKind::SccLarge) continue;
       const VertexId cu = comp_of[static_cast<std::size_t>(u)];
       std::int32_t k = 0;
-      for (EdgeId q = off[u]; q < off[u + 1]; ++q)
-        k += comp_of[static_cast<std::size_t>(tgt[q])] == cu && (tgt[q] != u || keep);
+      const EdgeId q1 = off[u + 1];
+      for (EdgeId q = off[u]; q < q1; ++q) {
+        const VertexId v = tgt[q];
+        if (q + 12 < q1) __builtin_prefetch(&comp_of[static_cast<std::size_t>(tgt[q + 12])]);
+        if (v == u) {
+          if (keep) ++k;
+          else ++ld;
+        } else if (comp_of[static_cast<std::size_t>(v)] == cu) {
+          ++k;
+        } else {
+          ++lx;
+        }
+      }
       unit_out[static_cast<std::size_t>(u)] = k;
+      li += k;
     }
+    n_intra += li;
+    n_cross += lx;
+    n_dropped += ld;
   });
   detail::parallel_dynamic(static_cast<std::int64_t>(nu), 256, [&](std::int64_t b, std::int64_t e) {
     for (std::int64_t uu = b; uu < e; ++uu) {
@@ -374,33 +411,15 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
     }
   });
 
-  // per-unit reference edge counts (unit.edges.size()) and totals
+  // per-unit reference edge counts (unit.edges.size())
   std::vector<EdgeId> uedges(nu, 0);
-  std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
-  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    EdgeId li = 0, lx = 0, ld = 0;
-    for (std::int64_t uu = b; uu < e; ++uu) {
-      const VertexId u = static_cast<VertexId>(uu);
-      const VertexId cu = comp_of[static_cast<std::size_t>(u)];
-      const std::size_t un = static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)]);
-      EdgeId ue = 0;
-      for (EdgeId k = off[u]; k < off[u + 1]; ++k) {
-        const VertexId v = tgt[k];
-        if (v == u) {
-          if (keep) ++ue;
-          else ++ld;
-        } else if (comp_of[static_cast<std::size_t>(v)] == cu) {
-          ++ue;
-        } else {
-          ++lx;
-        }
-      }
-      li += ue;
-      if (ue) std::atomic_ref<EdgeId>(uedges[un]).fetch_add(ue, std::memory_order_relaxed);
+  detail::parallel_dynamic(static_cast<std::int64_t>(nu), 256, [&](std::int64_t b, std::int64_t e) {
+    for (std::int64_t u = b; u < e; ++u) {
+      EdgeId s = 0;
+      for (std::int64_t j = unit_mem_begin[static_cast<std::size_t>(u)]; j < unit_mem_begin[static_cast<std::size_t>(u) + 1]; ++j)
+        s += unit_out[static_cast<std::size_t>(umem[static_cast<std::size_t>(j)])];
+      uedges[static_cast<std::size_t>(u)] = s;
     }
-    n_intra += li;
-    n_cross += lx;
-    n_dropped += ld;
   });
   L.intra_edge_count = n_intra;
   L.cross_edge_count = n_cross;
@@ -408,43 +427,89 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   L.unit_edges = std::move(uedges);
   clk.mark("deg/loop + edge counts");
   // pull lists (sources as vertex ids, source ascending): intra = CSR 0
-  // (kept self-loops only in SCC rows), cross = CSR 1.  A target's row and
-  // component come from one packed 8-byte record: one cache miss per edge.
-  std::vector<std::uint64_t> rowcomp(nn);
-  detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t v = b; v < e; ++v)
-      rowcomp[static_cast<std::size_t>(v)] =
-          (static_cast<std::uint64_t>(static_cast<std::uint32_t>(comp_of[static_cast<std::size_t>(v)])) << 32) |
-          static_cast<std::uint32_t>(L.row_of[static_cast<std::size_t>(v)]);
-  });
-  std::vector<EdgeId> ptrs[2];
-  std::vector<VertexId> cols[2];
-  detail::bucket_csr<2>(
-      n, n,
-      [&](std::int64_t uu, auto&& sink) {
-        const VertexId u = static_cast<VertexId>(uu);
-        const std::uint32_t cu = static_cast<std::uint32_t>(comp_of[static_cast<std::size_t>(u)]);
-        const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)])].kind;
-        const bool scc = k == UnitKind::SccSmall || k == UnitKind::SccLarge;
-        const EdgeId q1 = off[u + 1];
-        for (EdgeId q = off[u]; q < q1; ++q) {
-          const VertexId v = tgt[q];
-          if (q + 8 < q1) __builtin_prefetch(&rowcomp[static_cast<std::size_t>(tgt[q + 8])]);
-          const std::uint64_t rc = rowcomp[static_cast<std::size_t>(v)];
-          const std::int64_t rv = static_cast<std::uint32_t>(rc);
-          if (v == u) {
-            if (keep && scc) sink(0, rv, u);
-          } else {
-            sink(static_cast<std::uint32_t>(rc >> 32) == cu ? 0 : 1, rv, u);
-          }
+  // (kept self-loops only in SCC rows), cross = CSR 1
+  std::vector<EdgeId> icnt, xcnt;
+  if (in) {  // gathered per row from the partition's in-edge lists
+    icnt.assign(nn + 1, 0);
+    xcnt.assign(nn + 1, 0);
+    auto row_loop = [&](VertexId v) {
+      const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(v)])].kind;
+      return keep && lp[v] && (k == UnitKind::SccSmall || k == UnitKind::SccLarge);
+    };
+    detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t r = b; r < e; ++r) {
+        const VertexId v = L.vertex_of[static_cast<std::size_t>(r)];
+        const VertexId cv = comp_of[static_cast<std::size_t>(v)];
+        EdgeId ni = row_loop(v) ? 1 : 0, nx = 0;
+        const EdgeId k1 = in->off[static_cast<std::size_t>(v) + 1];
+        for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
+          if (k + 12 < k1) __builtin_prefetch(&comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k + 12)])]);
+          if (comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k)])] == cv) ++ni;
+          else ++nx;
         }
-      },
-      ptrs, cols);
-  std::vector<std::uint64_t>().swap(rowcomp);
-  std::vector<EdgeId>& icnt = ptrs[0];
-  std::vector<EdgeId>& xcnt = ptrs[1];
-  L.isrc = std::move(cols[0]);
-  L.xsrc = std::move(cols[1]);
+        icnt[static_cast<std::size_t>(r)] = ni;
+        xcnt[static_cast<std::size_t>(r)] = nx;
+      }
+    });
+    L.isrc.resize(static_cast<std::size_t>(detail::exclusive_scan_inplace(icnt.data(), static_cast<std::int64_t>(nn) + 1)));
+    L.xsrc.resize(static_cast<std::size_t>(detail::exclusive_scan_inplace(xcnt.data(), static_cast<std::int64_t>(nn) + 1)));
+    detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t r = b; r < e; ++r) {
+        const VertexId v = L.vertex_of[static_cast<std::size_t>(r)];
+        const VertexId cv = comp_of[static_cast<std::size_t>(v)];
+        bool loop_due = row_loop(v);  // a kept self-loop sits at its place in source order
+        EdgeId ai = icnt[static_cast<std::size_t>(r)], ax = xcnt[static_cast<std::size_t>(r)];
+        const EdgeId k1 = in->off[static_cast<std::size_t>(v) + 1];
+        for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
+          const VertexId src = in->src[static_cast<std::size_t>(k)];
+          if (k + 12 < k1) __builtin_prefetch(&comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k + 12)])]);
+          if (loop_due && src > v) {
+            L.isrc[static_cast<std::size_t>(ai++)] = v;
+            loop_due = false;
+          }
+          if (comp_of[static_cast<std::size_t>(src)] == cv) L.isrc[static_cast<std::size_t>(ai++)] = src;
+          else L.xsrc[static_cast<std::size_t>(ax++)] = src;
+        }
+        if (loop_due) L.isrc[static_cast<std::size_t>(ai++)] = v;
+      }
+    });
+  } else {  // one stable bucketed transpose of every out-edge
+    // a target's row and component come from one packed 8-byte record
+    std::vector<std::uint64_t> rowcomp(nn);
+    detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t v = b; v < e; ++v)
+        rowcomp[static_cast<std::size_t>(v)] =
+            (static_cast<std::uint64_t>(static_cast<std::uint32_t>(comp_of[static_cast<std::size_t>(v)])) << 32) |
+            static_cast<std::uint32_t>(L.row_of[static_cast<std::size_t>(v)]);
+    });
+    std::vector<EdgeId> ptrs[2];
+    std::vector<VertexId> cols[2];
+    detail::bucket_csr<2>(
+        n, n,
+        [&](std::int64_t uu, auto&& sink) {
+          const VertexId u = static_cast<VertexId>(uu);
+          const std::uint32_t cu = static_cast<std::uint32_t>(comp_of[static_cast<std::size_t>(u)]);
+          const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(u)])].kind;
+          const bool scc = k == UnitKind::SccSmall || k == UnitKind::SccLarge;
+          const EdgeId q1 = off[u + 1];
+          for (EdgeId q = off[u]; q < q1; ++q) {
+            const VertexId v = tgt[q];
+            if (q + 8 < q1) __builtin_prefetch(&rowcomp[static_cast<std::size_t>(tgt[q + 8])]);
+            const std::uint64_t rc = rowcomp[static_cast<std::size_t>(v)];
+            const std::int64_t rv = static_cast<std::uint32_t>(rc);
+            if (v == u) {
+              if (keep && scc) sink(0, rv, u);
+            } else {
+              sink(static_cast<std::uint32_t>(rc >> 32) == cu ? 0 : 1, rv, u);
+            }
+          }
+        },
+        ptrs, cols);
+    icnt = std::move(ptrs[0]);
+    xcnt = std::move(ptrs[1]);
+    L.isrc = std::move(cols[0]);
+    L.xsrc = std::move(cols[1]);
+  }
   clk.mark("in-edge transpose");
   // per-row ordering = the reference's accumulation order, then vertex -> row
   std::vector<std::int32_t> level_idx_of(nn);
@@ -475,6 +540,7 @@ Layout build_layout(const Graph& g, const Partition& p, VertexId small_threshold
   L.xptr = std::move(xcnt);
   return L;
 }
+}  // namespace
 
 Layout build_baseline_layout(const Graph& g) {
   const VertexId n = g.vertex_count();
