@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <iosfwd>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -21,6 +22,28 @@ inline namespace b200 {
 
 using VertexId = std::int32_t;
 using EdgeId = std::int64_t;
+
+/// std::vector whose resize() leaves new elements default-initialised (no
+/// zero fill): the host builders size multi-GB arrays and then write every
+/// element from many threads, which also spreads the first-touch page faults.
+template <typename T>
+struct UninitAllocator : std::allocator<T> {
+  using value_type = T;
+  UninitAllocator() = default;
+  template <typename U>
+  UninitAllocator(const UninitAllocator<U>&) noexcept {}
+  template <typename U>
+  struct rebind {
+    using other = UninitAllocator<U>;
+  };
+  template <typename U, typename... Args>
+  void construct(U* p, Args&&... args) {
+    if constexpr (sizeof...(Args) == 0) ::new (static_cast<void*>(p)) U;
+    else ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <typename T>
+using uvector = std::vector<T, UninitAllocator<T>>;
 
 /// graph.hpp:19 -- n = max id + 1 must fit in VertexId.
 inline constexpr VertexId kMaxVertexId = 2147483646;

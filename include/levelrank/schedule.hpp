@@ -77,20 +77,20 @@ struct Layout {
   bool keep_loops = false;
   std::vector<std::int32_t> level_row_begin;   // n_levels + 1, level index 0 = max_level
   std::vector<std::int32_t> level_unit_begin;  // n_levels + 1
-  std::vector<VertexId> vertex_of;             // row -> vertex
-  std::vector<VertexId> row_of;                // vertex -> row
-  std::vector<VertexId> deg;                   // walk out-degree per row
+  uvector<VertexId> vertex_of;             // row -> vertex
+  uvector<VertexId> row_of;                // vertex -> row
+  uvector<VertexId> deg;                   // walk out-degree per row
   std::vector<std::uint8_t> loop;              // per row: keep && self-loop (singleton/CAC factor)
   // cross in-edges (pull) per row; sources as rows, ordered (source level
   // descending, source vertex ascending) = propagate_weights order.
-  std::vector<EdgeId> xptr;
-  std::vector<VertexId> xsrc;
+  uvector<EdgeId> xptr;
+  uvector<VertexId> xsrc;
   // intra-unit in-edges (pull) per row; sources as rows.  SCC rows: source
   // vertex ascending (the reference's push order over unit.edges); CAC rows:
   // source Kahn dequeue position (solve_cac's push order).  Self-loops appear
   // only in SCC rows under LoopPolicy::Keep.
-  std::vector<EdgeId> iptr;
-  std::vector<VertexId> isrc;
+  uvector<EdgeId> iptr;
+  uvector<VertexId> isrc;
   // units in schedule order
   std::vector<std::uint8_t> unit_kind;      // UnitKind
   std::vector<std::int32_t> unit_level;     // partition level

@@ -89,6 +89,9 @@ struct LevelTasks {
   int hot_begin = 0;
   long long hot_rows = 0, unit_rows = 0;
   int keep_stream = 0;  // L2 priority of the streamed SpMV operands (spmv.cu policy_stream)
+  // multi-GPU, one grid unit on the level: this rank's blocks per exchange
+  // chunk ([chunk_bk[j], chunk_bk[j+1]) relative to the level's blocks)
+  std::vector<int> chunk_bk;
 };
 
 // One depth slice of a large CAC: rows [r0, r1), heavy-row tasks [h0, h1).
@@ -218,6 +221,14 @@ struct lr_ctx {
   int shard = 0, nshards = 1;  // this process's rank / world size
   ncclComm_t comm = nullptr;
   std::vector<std::vector<int>> gu_bounds;  // per grid unit: world + 1 row bounds
+  // exchange chunks: per grid unit, world * xchunks + 1 row bounds (rank r's
+  // chunk j = [cuts[r * xchunks + j], cuts[r * xchunks + j + 1])), identical on
+  // every rank; a chunk's s' rows are broadcast while the next chunk computes
+  int xchunks = 1;
+  std::vector<std::vector<int>> gu_cuts;
+  cudaStream_t xstream = nullptr;            // NCCL exchange, concurrent with the SpMV chunks
+  std::vector<cudaEvent_t> xev;              // chunk j computed (compute stream -> exchange stream)
+  cudaEvent_t xdone = nullptr;               // iteration's exchange done (exchange -> compute stream)
   DevBuf<double> maxbuf;                     // per grid unit: shard max, all-reduced
   DevBuf<double> cacpv;                      // pushed terms of CACs swept by cac_sweep_compact (n, or empty)
 
@@ -238,6 +249,9 @@ struct lr_ctx {
   ~lr_ctx() {
     if (device >= 0) cudaSetDevice(device);
     drop_graphs();
+    for (cudaEvent_t e : xev) cudaEventDestroy(e);
+    if (xdone) cudaEventDestroy(xdone);
+    if (xstream) cudaStreamDestroy(xstream);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : lev)
@@ -428,6 +442,12 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   ctx->gu_rows.clear();
   ctx->gu_nnz.clear();
   ctx->gu_bounds.clear();
+  ctx->gu_cuts.clear();
+  ctx->xchunks = 1;
+  if (ctx->comm) {
+    const char* e = std::getenv("LR_XCHG_CHUNKS");
+    ctx->xchunks = std::max(1, std::min(64, e ? std::atoi(e) : 4));
+  }
   ctx->cac_slices.clear();
   int max_small = 0;
   bool small_needs_scratch = false;
@@ -456,6 +476,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.lc0 = static_cast<int>(lcta.size());
     T.gu0 = static_cast<int>(gstate.size());
     T.bk0 = static_cast<int>(blocks.size());
+    std::vector<int> pending_chunks;  // exchange chunks of the level's (last) grid unit
     for (int u = L->level_unit_begin[li]; u < L->level_unit_begin[li + 1]; ++u) {
       const int rb = L->unit_row_begin[u], re = L->unit_row_begin[u + 1];
       const int m = re - rb;
@@ -527,16 +548,32 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           ctx->gu_bounds.push_back(shard_bounds(L->iptr, rb, re, ctx->nshards));
           const int own0 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard)];
           const int own1 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard) + 1];
+          {  // exchange chunks of every rank's shard (nnz-balanced, whole rows)
+            const std::vector<int>& b = ctx->gu_bounds.back();
+            std::vector<int> cuts;
+            for (int q = 0; q < ctx->nshards; ++q) {
+              const std::vector<int> c = shard_bounds(L->iptr, b[static_cast<size_t>(q)], b[static_cast<size_t>(q) + 1],
+                                                      ctx->xchunks);
+              cuts.insert(cuts.end(), c.begin(), c.end() - 1);
+            }
+            cuts.push_back(re);
+            ctx->gu_cuts.push_back(std::move(cuts));
+          }
+          const std::vector<int>& my_cuts = ctx->gu_cuts.back();
+          std::vector<int> chunk_bk;
           // K4c chunks hold <= kChunkNnz in-edges and never put an empty row
           // inside a multi-row tile (its row-start flag would collide)
           const int tile_nnz = spmv_seg() ? kChunkNnz : kTileNnz;
           const int seg_nnz = spmv_seg() ? kChunkSegNnz : kSegNnz;
-          int r = own0;
-          while (r < own1) {
+          for (int xc = 0; xc < ctx->xchunks; ++xc) {
+          const int cend = my_cuts[static_cast<size_t>(ctx->shard * ctx->xchunks + xc) + 1];
+          chunk_bk.push_back(static_cast<int>(blocks.size()));
+          int r = my_cuts[static_cast<size_t>(ctx->shard * ctx->xchunks + xc)];
+          while (r < cend) {
             const long long len = L->iptr[r + 1] - L->iptr[r];
             if (len == 0 && spmv_seg()) {  // a run of rows without in-edges: y = 0
               const int start = r;
-              while (r < own1 && r - start < kTileRows && L->iptr[r + 1] == L->iptr[r]) ++r;
+              while (r < cend && r - start < kTileRows && L->iptr[r + 1] == L->iptr[r]) ++r;
               blocks.push_back(SpmvBlock{L->iptr[start], 0, start, r, gu, -1, 0});
               continue;
             }
@@ -559,7 +596,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             }
             const int start = r;
             long long acc = 0;
-            while (r < own1 && r - start < kTileRows) {
+            while (r < cend && r - start < kTileRows) {
               const long long l2 = L->iptr[r + 1] - L->iptr[r];
               if (l2 > tile_nnz || acc + l2 > tile_nnz || (l2 == 0 && spmv_seg())) break;
               acc += l2;
@@ -567,6 +604,9 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
             }
             blocks.push_back(SpmvBlock{L->iptr[start], static_cast<int>(acc), start, r, gu, -1, 0});
           }
+          }
+          chunk_bk.push_back(static_cast<int>(blocks.size()));
+          pending_chunks = std::move(chunk_bk);
           ctx->gu_rows.push_back(own1 - own0);  // roofline bookkeeping: this rank's share
           ctx->gu_nnz.push_back(L->iptr[own1] - L->iptr[own0]);
           GridUnitState g{};
@@ -594,6 +634,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.lc1 = static_cast<int>(lcta.size());
     T.gu1 = static_cast<int>(gstate.size());
     T.bk1 = static_cast<int>(blocks.size());
+    if (T.gu1 - T.gu0 == 1 && ctx->xchunks > 1)
+      for (const int bi : pending_chunks) T.chunk_bk.push_back(bi - T.bk0);
     // Hot head of the level's largest grid unit: its rows are ordered by
     // descending in-unit out-degree, so the first rows are the most gathered.
     // The head of s_in (read) and of s_out (written, read next iteration)
@@ -803,6 +845,53 @@ static lr_status exchange_shards(lr_ctx* ctx, const LevelTasks& T, double* buf, 
   return LR_OK;
 }
 
+// One power-series iteration of a level's single grid unit, row-sharded over
+// the ranks and cut into exchange chunks: SpMV chunk j on the compute stream,
+// then on the exchange stream the broadcasts of every rank's chunk j of s'
+// (and, after the last chunk, the all-reduce of the shard maxima) -- so the
+// exchange of chunk j overlaps the SpMV of chunk j + 1.  The chunks' maxima
+// accumulate in the unit state; only the last chunk publishes them.
+static lr_status chunked_iteration(lr_ctx* ctx, const LevelTasks& T, const DeviceLayout& L, const double* sin,
+                                   double* sout, int64_t& launches) {
+  cudaStream_t s = ctx->stream;
+  const int C = static_cast<int>(T.chunk_bk.size()) - 1;
+  if (!ctx->xstream) LR_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->xstream, cudaStreamNonBlocking));
+  if (!ctx->xdone) LR_CUDA_TRY(cudaEventCreateWithFlags(&ctx->xdone, cudaEventDisableTiming));
+  while (static_cast<int>(ctx->xev.size()) < C) {
+    cudaEvent_t e;
+    LR_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->xev.push_back(e);
+  }
+  const NcclApi& nc = nccl();
+  const std::vector<int>& cuts = ctx->gu_cuts[static_cast<size_t>(T.gu0)];
+  for (int j = 0; j < C; ++j) {
+    const int b0 = T.bk0 + T.chunk_bk[static_cast<size_t>(j)], b1 = T.bk0 + T.chunk_bk[static_cast<size_t>(j) + 1];
+    launch_grid_iter(L, ctx->blocks.p + b0, ctx->meta.p ? ctx->meta.p + static_cast<size_t>(b0) * 32 : nullptr, b1 - b0,
+                     T.gu0, 1, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p, ctx->heavy_cnt.p, ctx->params.p,
+                     ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p, ctx->status.p, T.hot_begin, T.hot_rows,
+                     T.unit_rows, T.keep_stream, ctx->maxbuf.p, s, j < C - 1 ? 1 : 0);
+    ++launches;
+    LR_CUDA_TRY(cudaEventRecord(ctx->xev[static_cast<size_t>(j)], s));
+    LR_CUDA_TRY(cudaStreamWaitEvent(ctx->xstream, ctx->xev[static_cast<size_t>(j)], 0));
+    LR_NCCL_TRY(nc.group_start());
+    for (int q = 0; q < ctx->nshards; ++q) {
+      const int r0 = cuts[static_cast<size_t>(q * C + j)], r1 = cuts[static_cast<size_t>(q * C + j) + 1];
+      if (r1 > r0)
+        LR_NCCL_TRY(nc.broadcast(sout + r0, sout + r0, static_cast<size_t>(r1 - r0), ncclDouble, q, ctx->comm,
+                                 ctx->xstream));
+    }
+    if (j == C - 1)
+      LR_NCCL_TRY(nc.all_reduce(ctx->maxbuf.p + T.gu0, ctx->maxbuf.p + T.gu0, 1, ncclDouble, ncclMax, ctx->comm,
+                                ctx->xstream));
+    LR_NCCL_TRY(nc.group_end());
+  }
+  LR_CUDA_TRY(cudaEventRecord(ctx->xdone, ctx->xstream));
+  LR_CUDA_TRY(cudaStreamWaitEvent(s, ctx->xdone, 0));
+  launch_grid_finish(ctx->gstate.p, T.gu0, 1, ctx->params.p, ctx->unit_iters.p, ctx->status.p, ctx->maxbuf.p, s);
+  ++launches;
+  return LR_OK;
+}
+
 static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, double tol, double* r3_dev,
                                  double* r1_dev, lr_solve_info* info, int64_t* unit_iters) {
   const lr_status pv = lr_validate_params(c, tol);
@@ -981,6 +1070,12 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           }
           if (k == 1) LR_CUDA_TRY(cudaEventRecord(ctx->lev[0], s));
           const bool sharded = ctx->comm != nullptr;
+          if (sharded && T.chunk_bk.size() > 2) {  // exchange overlapped chunk by chunk
+            if (const lr_status xs = chunked_iteration(ctx, T, L, sin, sout, launches); xs != LR_OK) return xs;
+            LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(k)], s));
+            ++spmv_launches;
+            continue;
+          }
           launch_grid_iter(L, ctx->blocks.p + T.bk0, ctx->meta.p ? ctx->meta.p + static_cast<size_t>(T.bk0) * 32 : nullptr,
                            T.bk1 - T.bk0, T.gu0, T.gu1 - T.gu0, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p,
                            ctx->heavy_cnt.p, ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p,

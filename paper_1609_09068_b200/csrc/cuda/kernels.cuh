@@ -245,7 +245,7 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* blocks, const unsi
                       const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p,
                       const double* pf, double* rank, const double* s_in, double* s_out, long long* unit_iters,
                       DevStatus* st, int hot_begin, long long hot_rows, long long unit_rows, int keep_stream,
-                      double* maxbuf, cudaStream_t s);
+                      double* maxbuf, cudaStream_t s, int hold = 0);
 // multi-GPU: close an iteration from the all-reduced shard maxima in maxbuf
 void launch_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
                         DevStatus* st, const double* maxbuf, cudaStream_t s);

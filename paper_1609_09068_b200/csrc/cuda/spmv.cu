@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kSpmvThreads)
                 const HeavyRow* __restrict__ heavy, double* heavy_part, int* heavy_cnt,
                 const SolveParams* __restrict__ p, const double* __restrict__ pf, double* __restrict__ rank,
                 const double* __restrict__ s_in, double* __restrict__ s_out, long long* unit_iters, DevStatus* st,
-                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, int keep_stream, double* maxbuf) {
+                int hot_begin, unsigned hot_bytes, unsigned unit_bytes, int nhead, int keep_stream, double* maxbuf, int hold) {
   extern __shared__ double dyn[];  // [kWarps][kTileNnz] staging, then the head
   double* head = dyn + kWarps * kTileNnz;
   __shared__ int wunit[kWarps];
@@ -357,7 +357,9 @@ __global__ void __launch_bounds__(kSpmvThreads)
   __syncthreads();
   if (last_cta && threadIdx.x == 0) {
     __threadfence();
-    if (maxbuf) {  // row-sharded: publish the shard max, decide after the all-reduce
+    if (hold) {  // an earlier chunk of a chunked (multi-GPU) iteration: maxima keep accumulating
+      st->ctas_done = 0;
+    } else if (maxbuf) {  // row-sharded: publish the shard max, decide after the all-reduce
       for (int i = gu0; i < gu0 + ngu; ++i) {
         maxbuf[i] = bitsd(atomicAdd(&gs[i].max_bits, 0ull));
         gs[i].max_bits = 0ull;
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
                double* heavy_part, int* heavy_cnt, const SolveParams* __restrict__ p, const double* __restrict__ pf,
                double* __restrict__ rank, const double* __restrict__ s_in, double* __restrict__ s_out,
                long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes, unsigned unit_bytes,
-               int nhead, int keep_stream, double* maxbuf) {
+               int nhead, int keep_stream, double* maxbuf, int hold) {
   constexpr int kW = kSegThreads / 32;
   extern __shared__ double dyn[];  // [kW][kTileRows] row totals, then the head
   double* head = dyn + kW * kTileRows;
@@ -680,7 +682,9 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   __syncthreads();
   if (last_cta && threadIdx.x == 0) {
     __threadfence();
-    if (maxbuf) {
+    if (hold) {  // an earlier chunk of a chunked (multi-GPU) iteration: maxima keep accumulating
+      st->ctas_done = 0;
+    } else if (maxbuf) {  // row-sharded: publish the shard max, decide after the all-reduce
       for (int i = gu0; i < gu0 + ngu; ++i) {
         maxbuf[i] = bitsd(atomicAdd(&gs[i].max_bits, 0ull));
         gs[i].max_bits = 0ull;
@@ -695,6 +699,16 @@ __global__ void __launch_bounds__(kSegThreads, 1)
 __global__ void k_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
                               DevStatus* st, const double* maxbuf) {
   if (threadIdx.x == 0 && blockIdx.x == 0) finish_iteration(gs, gu0, ngu, p, unit_iters, st, maxbuf);
+}
+
+// a shard whose last chunk of an iteration is empty: publish what the earlier
+// chunks accumulated
+__global__ void k_grid_publish(GridUnitState* gs, double* maxbuf, int gu0, int ngu) {
+  const int i = gu0 + static_cast<int>(threadIdx.x);
+  if (i < gu0 + ngu) {
+    maxbuf[i] = bitsd(gs[i].max_bits);
+    gs[i].max_bits = 0ull;
+  }
 }
 
 __global__ void k_grid_zero_max(double* maxbuf, int gu0, int ngu) {
@@ -765,9 +779,9 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
                       int ngu, GridUnitState* gs, const HeavyRow* heavy, double* heavy_part, int* heavy_cnt, const SolveParams* p, const double* pf,
                       double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
                       int hot_begin, long long hot_rows, long long unit_rows, int keep_stream, double* maxbuf,
-                      cudaStream_t s) {
-  if (ntasks == 0) {  // this rank owns no rows of the level's units: still publish a zero max
-    if (maxbuf) launch_grid_zero_max(maxbuf, gu0, ngu, s);
+                      cudaStream_t s, int hold) {
+  if (ntasks == 0) {  // no rows of the level's units in this launch
+    if (maxbuf && !hold) k_grid_publish<<<1, 1024, 0, s>>>(gs, maxbuf, gu0, ngu);
     return;
   }
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
@@ -785,11 +799,11 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
   if (spmv_seg()) {
     k_spmv_seg<<<grid, kSegThreads, static_cast<size_t>(nhead + (kSegThreads / 32) * kTileRows) * 8, s>>>(
         L, tasks, meta, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
-        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf);
+        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf, hold);
   } else {
     k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
         L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
-        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf);
+        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf, hold);
   }
 }
 

@@ -102,6 +102,58 @@ T exclusive_scan_inplace(T* v, std::int64_t n) {
   return part[static_cast<std::size_t>(t)];
 }
 
+// Stable parallel LSD radix sort of items[0, n) by a 32-bit key(item),
+// ascending (two 16-bit passes; the high pass is skipped when every key is
+// below 2^16).
+template <typename T, typename Key>
+void stable_radix_sort(T* items, std::int64_t n, Key&& key) {
+  if (n <= 1) return;
+  const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n / (1 << 15)) + 1));
+  uvector<T> tmp(static_cast<std::size_t>(n));
+  std::uint32_t hi_or = 0;
+  for (std::int64_t i = 0; i < n && !hi_or; i += std::max<std::int64_t>(1, n / 4096)) hi_or |= key(items[i]) >> 16;
+  std::vector<std::thread> pool;
+  auto run = [&](auto&& body) {
+    pool.clear();
+    for (int i = 0; i < t; ++i) pool.emplace_back(body, i);
+    for (auto& th : pool) th.join();
+  };
+  if (!hi_or) {  // the sample saw no high digit: check exactly
+    std::vector<std::uint32_t> any(static_cast<std::size_t>(t), 0);
+    run([&](int i) {
+      std::uint32_t a = 0;
+      for (std::int64_t k = n * i / t; k < n * (i + 1) / t; ++k) a |= key(items[k]) >> 16;
+      any[static_cast<std::size_t>(i)] = a;
+    });
+    for (const auto a : any) hi_or |= a;
+  }
+  std::vector<std::int64_t> off(static_cast<std::size_t>(t) << 16);
+  T* src = items;
+  T* dst = tmp.data();
+  for (int pass = 0; pass < (hi_or ? 2 : 1); ++pass) {
+    const int shift = 16 * pass;
+    std::fill(off.begin(), off.end(), 0);
+    run([&](int i) {
+      std::int64_t* h = off.data() + (static_cast<std::size_t>(i) << 16);
+      for (std::int64_t k = n * i / t; k < n * (i + 1) / t; ++k) ++h[(key(src[k]) >> shift) & 0xffffu];
+    });
+    std::int64_t acc = 0;
+    for (std::size_t x = 0; x < 65536; ++x)
+      for (int i = 0; i < t; ++i) {
+        std::int64_t& o = off[(static_cast<std::size_t>(i) << 16) + x];
+        const std::int64_t c = o;
+        o = acc;
+        acc += c;
+      }
+    run([&](int i) {
+      std::int64_t* h = off.data() + (static_cast<std::size_t>(i) << 16);
+      for (std::int64_t k = n * i / t; k < n * (i + 1) / t; ++k) dst[h[(key(src[k]) >> shift) & 0xffffu]++] = src[k];
+    });
+    std::swap(src, dst);
+  }
+  if (src != items) std::copy(src, src + n, items);
+}
+
 // Stable bucketed transpose into K CSRs over `nrows` rows, without atomics.
 // emit(u, sink) is called for every source u in [0, n_src) -- twice, with the
 // same calls both times -- and calls sink(k, row, value) for each entry of
@@ -109,9 +161,8 @@ T exclusive_scan_inplace(T* v, std::int64_t n) {
 // entries go to row buckets of 2^16 rows (per-thread cursors, sequential
 // writes), then each bucket is counting-sorted by row.  Every row's values end
 // up in emission order: source ascending, then the order emit produced them.
-template <int K, typename Emit>
-void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, std::vector<std::int64_t>* ptr,
-                std::vector<VertexId>* col) {
+template <int K, typename Emit, typename PtrVec, typename ColVec>
+void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr, ColVec* col) {
   constexpr int kShift = 16;
   const std::int64_t nb = (nrows >> kShift) + 1;
   const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n_src / 4096) + 1));
@@ -131,7 +182,7 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, std::vector
       emit(u, [&](int k, std::int64_t row, VertexId) { ++cur[at(k, th, row >> kShift)]; });
   });
   std::vector<std::int64_t> bstart(static_cast<std::size_t>(K) * static_cast<std::size_t>(nb + 1), 0);
-  std::vector<std::vector<std::uint64_t>> tmp(K);
+  std::vector<uvector<std::uint64_t>> tmp(K);
   for (int k = 0; k < K; ++k) {  // bucket-major, then thread: stable
     std::int64_t run_total = 0;
     for (std::int64_t b = 0; b < nb; ++b) {
@@ -144,7 +195,7 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, std::vector
     }
     bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(nb)] = run_total;
     tmp[static_cast<std::size_t>(k)].resize(static_cast<std::size_t>(run_total));
-    ptr[k].assign(static_cast<std::size_t>(nrows) + 1, 0);
+    ptr[k].resize(static_cast<std::size_t>(nrows) + 1);  // every entry written below
     col[k].resize(static_cast<std::size_t>(run_total));
   }
   run([&](int th) {  // 2. (row, value) pairs into their buckets

@@ -98,8 +98,8 @@ void for_items(const std::vector<std::int32_t>& items, F&& f) {
 struct Adjacency {
   const EdgeId* off;
   const VertexId* tgt;
-  std::vector<EdgeId> in_off;  // in-edges (self-loops left out), source-ascending rows
-  std::vector<VertexId> in_src;
+  uvector<EdgeId> in_off;  // in-edges (self-loops left out), source-ascending rows
+  uvector<VertexId> in_src;
 };
 
 // ------------------------------------------------------------- 1. SCC labels
@@ -341,7 +341,7 @@ struct Sets {
 };
 
 constexpr std::int64_t kWideComponent = 1 << 14;  // members scanned in parallel above this
-constexpr EdgeId kAhead = 12;                      // software prefetch distance on edge scans
+constexpr EdgeId kAhead = 16;                      // software prefetch distance on edge scans
 
 Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* stats, detail::InEdges* keep_in) {
   const VertexId n = g.vertex_count();
@@ -358,8 +358,8 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   detail::PhaseClock clk;
   Adjacency adj{g.offsets_data(), g.targets_data(), {}, {}};
   {
-    std::vector<EdgeId> ptr[1];
-    std::vector<VertexId> col[1];
+    uvector<EdgeId> ptr[1];
+    uvector<VertexId> col[1];
     detail::bucket_csr<1>(
         n, n,
         [&](std::int64_t uu, auto&& sink) {
@@ -372,6 +372,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     adj.in_src = std::move(col[0]);
   }
   clk.mark("partition: in-edge transpose");
+  const EdgeId m_all = adj.off[n], m_in = adj.in_off[nn];
   SccFinder finder(n, adj, clk);
   const std::vector<VertexId> label = finder.run();
   const VertexId giant = finder.giant_;
@@ -404,7 +405,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       std::int64_t x = 0;
       const EdgeId k1 = adj.off[v + 1];
       for (EdgeId k = adj.off[v]; k < k1; ++k) {
-        if (k + kAhead < k1) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
+        if (k + kAhead < m_all) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
         x += comp[static_cast<std::size_t>(adj.tgt[k])] != c;
       }
       if (c == cg) {
@@ -468,7 +469,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       const VertexId u = members[static_cast<std::size_t>(i)];
       const EdgeId k1 = adj.off[u + 1];
       for (EdgeId k = adj.off[u]; k < k1; ++k) {
-        if (k + kAhead < k1) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
+        if (k + kAhead < m_all) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
         const std::int32_t cw = comp[static_cast<std::size_t>(adj.tgt[k])];
         if (cw != c) hi = std::max(hi, level[static_cast<std::size_t>(cw)]);
       }
@@ -481,7 +482,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       const VertexId u = members[static_cast<std::size_t>(i)];
       const EdgeId k1 = adj.in_off[static_cast<std::size_t>(u) + 1];
       for (EdgeId k = adj.in_off[static_cast<std::size_t>(u)]; k < k1; ++k) {
-        if (k + kAhead < k1) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k + kAhead)])]);
+        if (k + kAhead < m_in) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k + kAhead)])]);
         const std::int32_t cp = comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k)])];
         if (cp != c && atomic_sub(pending[static_cast<std::size_t>(cp)], std::int64_t{1}) == 1) out.push_back(cp);
       }

@@ -15,8 +15,8 @@ inline namespace b200 {
 namespace detail {
 
 struct InEdges {
-  std::vector<EdgeId> off;    // n + 1
-  std::vector<VertexId> src;  // per target vertex: sources ascending, self-loops left out
+  uvector<EdgeId> off;    // n + 1
+  uvector<VertexId> src;  // per target vertex: sources ascending, self-loops left out
 };
 
 Partition find_components_with_in_edges(const Graph& g, PartitionStats* stats, InEdges& in);

@@ -189,6 +189,7 @@ Schedule build_schedule(const Graph& g, const Partition& p, VertexId small_thres
 }
 
 namespace {
+constexpr std::int64_t kParallelSortRows = 1 << 16;  // SccLarge units above this sort their rows in parallel
 Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_threshold, const detail::InEdges* in);
 }
 
@@ -347,6 +348,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   // per-unit reference edge counts (unit.edges.size()); cross / dropped totals
   std::vector<std::int32_t> unit_out(nn, 0);
   std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
+  const EdgeId m_all = off[n];
   detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     EdgeId li = 0, lx = 0, ld = 0;
     for (std::int64_t uu = b; uu < e; ++uu) {
@@ -356,7 +358,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
       const EdgeId q1 = off[u + 1];
       for (EdgeId q = off[u]; q < q1; ++q) {
         const VertexId v = tgt[q];
-        if (q + 12 < q1) __builtin_prefetch(&comp_of[static_cast<std::size_t>(tgt[q + 12])]);
+        if (q + 16 < m_all) __builtin_prefetch(&comp_of[static_cast<std::size_t>(tgt[q + 16])]);
         if (v == u) {
           if (keep) ++k;
           else ++ld;
@@ -379,7 +381,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
       const std::int64_t m0 = unit_mem_begin[u], m1 = unit_mem_begin[u + 1];
       VertexId* rows = L.vertex_of.data() + m0;
       std::copy(umem.begin() + m0, umem.begin() + m1, rows);
-      if (plan[u].kind == UnitKind::SccLarge)
+      if (plan[u].kind == UnitKind::SccLarge && m1 - m0 <= kParallelSortRows)
         std::stable_sort(rows, rows + (m1 - m0), [&](VertexId a, VertexId bb) {
           return unit_out[static_cast<std::size_t>(a)] > unit_out[static_cast<std::size_t>(bb)];
         });
@@ -392,9 +394,22 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
         dp[0] = static_cast<std::int32_t>(m0);
         for (std::int32_t d = 0; d < unit_depths[u]; ++d) dp[d + 1] += dp[d];
       }
+      if (plan[u].kind == UnitKind::SccLarge && m1 - m0 > kParallelSortRows) continue;  // below
       for (std::int64_t r = m0; r < m1; ++r) L.row_of[static_cast<std::size_t>(L.vertex_of[static_cast<std::size_t>(r)])] = static_cast<VertexId>(r);
     }
   });
+  // the giant units: a parallel stable radix sort by descending out-degree
+  for (std::size_t u = 0; u < nu; ++u) {
+    const std::int64_t m0 = unit_mem_begin[u], m1 = unit_mem_begin[u + 1];
+    if (plan[u].kind != UnitKind::SccLarge || m1 - m0 <= kParallelSortRows) continue;
+    VertexId* rows = L.vertex_of.data() + m0;
+    detail::stable_radix_sort(rows, m1 - m0, [&](VertexId v) {
+      return ~static_cast<std::uint32_t>(unit_out[static_cast<std::size_t>(v)]);
+    });
+    detail::parallel_chunks(m1 - m0, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t r = b; r < e; ++r) L.row_of[static_cast<std::size_t>(rows[r])] = static_cast<VertexId>(m0 + r);
+    });
+  }
   clk.mark("unit out-degrees + row order");
   L.level_row_begin.assign(static_cast<std::size_t>(nl) + 1, 0);
   for (std::int32_t li = 0; li <= nl; ++li)
@@ -428,41 +443,50 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   clk.mark("deg/loop + edge counts");
   // pull lists (sources as vertex ids, source ascending): intra = CSR 0
   // (kept self-loops only in SCC rows), cross = CSR 1
-  std::vector<EdgeId> icnt, xcnt;
+  uvector<EdgeId> icnt, xcnt;
   if (in) {  // gathered per row from the partition's in-edge lists
-    icnt.assign(nn + 1, 0);
-    xcnt.assign(nn + 1, 0);
+    icnt.resize(nn + 1);  // every row written below; [nn] receives the scan total
+    xcnt.resize(nn + 1);
+    icnt[nn] = xcnt[nn] = 0;
     auto row_loop = [&](VertexId v) {
       const UnitKind k = plan[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(v)])].kind;
       return keep && lp[v] && (k == UnitKind::SccSmall || k == UnitKind::SccLarge);
     };
+    // both passes walk vertices in id order, so the in-edge lists stream and
+    // the random component lookups are prefetched a fixed distance ahead
+    const EdgeId in_end = in->off[nn];
+    auto ahead = [&](EdgeId k) {
+      if (k + 16 < in_end) __builtin_prefetch(&comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k + 16)])]);
+    };
     detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-      for (std::int64_t r = b; r < e; ++r) {
-        const VertexId v = L.vertex_of[static_cast<std::size_t>(r)];
+      for (std::int64_t vv = b; vv < e; ++vv) {
+        const VertexId v = static_cast<VertexId>(vv);
         const VertexId cv = comp_of[static_cast<std::size_t>(v)];
         EdgeId ni = row_loop(v) ? 1 : 0, nx = 0;
         const EdgeId k1 = in->off[static_cast<std::size_t>(v) + 1];
         for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
-          if (k + 12 < k1) __builtin_prefetch(&comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k + 12)])]);
+          ahead(k);
           if (comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k)])] == cv) ++ni;
           else ++nx;
         }
-        icnt[static_cast<std::size_t>(r)] = ni;
-        xcnt[static_cast<std::size_t>(r)] = nx;
+        const std::size_t r = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
+        icnt[r] = ni;
+        xcnt[r] = nx;
       }
     });
     L.isrc.resize(static_cast<std::size_t>(detail::exclusive_scan_inplace(icnt.data(), static_cast<std::int64_t>(nn) + 1)));
     L.xsrc.resize(static_cast<std::size_t>(detail::exclusive_scan_inplace(xcnt.data(), static_cast<std::int64_t>(nn) + 1)));
     detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-      for (std::int64_t r = b; r < e; ++r) {
-        const VertexId v = L.vertex_of[static_cast<std::size_t>(r)];
+      for (std::int64_t vv = b; vv < e; ++vv) {
+        const VertexId v = static_cast<VertexId>(vv);
+        const std::size_t r = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
         const VertexId cv = comp_of[static_cast<std::size_t>(v)];
         bool loop_due = row_loop(v);  // a kept self-loop sits at its place in source order
-        EdgeId ai = icnt[static_cast<std::size_t>(r)], ax = xcnt[static_cast<std::size_t>(r)];
+        EdgeId ai = icnt[r], ax = xcnt[r];
         const EdgeId k1 = in->off[static_cast<std::size_t>(v) + 1];
         for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
           const VertexId src = in->src[static_cast<std::size_t>(k)];
-          if (k + 12 < k1) __builtin_prefetch(&comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k + 12)])]);
+          ahead(k);
           if (loop_due && src > v) {
             L.isrc[static_cast<std::size_t>(ai++)] = v;
             loop_due = false;
@@ -482,8 +506,8 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
             (static_cast<std::uint64_t>(static_cast<std::uint32_t>(comp_of[static_cast<std::size_t>(v)])) << 32) |
             static_cast<std::uint32_t>(L.row_of[static_cast<std::size_t>(v)]);
     });
-    std::vector<EdgeId> ptrs[2];
-    std::vector<VertexId> cols[2];
+    uvector<EdgeId> ptrs[2];
+    uvector<VertexId> cols[2];
     detail::bucket_csr<2>(
         n, n,
         [&](std::int64_t uu, auto&& sink) {
@@ -603,8 +627,8 @@ Layout build_baseline_layout(const Graph& g) {
     L.iptr[r + 1] = L.iptr[r] + indeg[static_cast<std::size_t>(v)].load(std::memory_order_relaxed);
   }
   // in-edges per row, source ascending (the reference's push order)
-  std::vector<EdgeId> ptrs[1];
-  std::vector<VertexId> cols[1];
+  uvector<EdgeId> ptrs[1];
+  uvector<VertexId> cols[1];
   detail::bucket_csr<1>(
       n, n,
       [&](std::int64_t uu, auto&& sink) {

@@ -58,10 +58,14 @@ def test_config_recipes(lr, oracle, cfg, shrink):
     assert res.report["total_edge_work"] == ref.report["total_edge_work"]
 
 
-def test_sharded_path_single_rank(lr):
-    """The multi-GPU code path (row shards + NCCL exchange + deferred stop
-    decision) on a one-rank communicator reproduces the unsharded solve."""
-    g = lr.config_graph(2, 6)
+@pytest.mark.parametrize("shrink,chunks", [(6, 1), (6, 4), (3, 4), (3, 7)])
+def test_sharded_path_single_rank(lr, monkeypatch, shrink, chunks):
+    """The multi-GPU code path (row shards, the s' exchange cut into chunks
+    that overlap the next chunk's SpMV on a second stream, deferred stop
+    decision) on a one-rank communicator reproduces the unsharded solve bit
+    for bit."""
+    monkeypatch.setenv("LR_XCHG_CHUNKS", str(chunks))
+    g = lr.config_graph(2, shrink)
     w = np.full(g.n, 1.0 / g.n)
     r3a, r1a, _, ita = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
     eng = lr.Engine(g, rank=0, world=1, nccl_id=lr.nccl_unique_id())
