@@ -185,6 +185,14 @@ lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* unique_i
 /* The nnz-balanced split used for the shards: bounds[world + 1] over rows
  * [row_begin, row_end) of a pull CSR with row pointers iptr. */
 lr_status lr_shard_rows(const int64_t* iptr, int32_t row_begin, int32_t row_end, int32_t world, int32_t* bounds);
+/* The exchange schedule of one sharded unit: every rank's shard cut into
+ * `chunks` nnz-balanced pieces of whole rows (world * chunks + 1 bounds; rank
+ * q's chunk j = [cuts[q*chunks+j], cuts[q*chunks+j+1])).  Per iteration chunk j
+ * is computed, then every rank's chunk j is broadcast (root order 0..world-1),
+ * the last chunk followed by the all-reduce(max); LR_XCHG_CHUNKS sets
+ * `chunks` (default 4). */
+lr_status lr_exchange_cuts(const int64_t* iptr, int32_t row_begin, int32_t row_end, int32_t world, int32_t chunks,
+                           int32_t* cuts);
 
 /* cudaStream_t the context launches on. */
 void* lr_ctx_stream(lr_ctx* ctx);

@@ -163,6 +163,7 @@ EXPORTS = {
     "lr_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "lr_ctx_set_comm": (C.c_int, [VP, C.c_int, C.c_int, C.c_char_p]),
     "lr_shard_rows": (C.c_int, [I64P, C.c_int32, C.c_int32, C.c_int32, I32P]),
+    "lr_exchange_cuts": (C.c_int, [I64P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, I32P]),
     "lr_ctx_stream": (VP, [VP]),
     "lr_ctx_device_bytes": (C.c_int64, [VP]),
     "lr_ctx_free": (None, [VP]),
@@ -489,6 +490,14 @@ def shard_rows(iptr, row_begin: int, row_end: int, world: int) -> np.ndarray:
     ip = np.ascontiguousarray(iptr, np.int64)
     out = np.zeros(world + 1, np.int32)
     _check(lib().lr_shard_rows(_p(ip, I64P), int(row_begin), int(row_end), int(world), _p(out, I32P)))
+    return out
+
+
+def exchange_cuts(iptr, row_begin: int, row_end: int, world: int, chunks: int) -> np.ndarray:
+    """lr_exchange_cuts: world * chunks + 1 row bounds of the chunked s' exchange."""
+    ip = np.ascontiguousarray(iptr, np.int64)
+    out = np.zeros(world * chunks + 1, np.int32)
+    _check(lib().lr_exchange_cuts(_p(ip, I64P), int(row_begin), int(row_end), int(world), int(chunks), _p(out, I32P)))
     return out
 
 

@@ -157,6 +157,22 @@ std::vector<int> shard_bounds(const int64_t* iptr, int rb, int re, int world) {
   return b;
 }
 
+// Exchange chunks of a row-sharded unit: rank q's shard [b_q, b_{q+1}) cut
+// into `chunks` nnz-balanced pieces of whole rows; world * chunks + 1 bounds,
+// rank q's chunk j = [cuts[q * chunks + j], cuts[q * chunks + j + 1]).  Every
+// rank computes the same cuts from the same layout.
+std::vector<int> exchange_cuts(const int64_t* iptr, int rb, int re, int world, int chunks) {
+  const std::vector<int> b = shard_bounds(iptr, rb, re, world);
+  std::vector<int> cuts;
+  cuts.reserve(static_cast<size_t>(world) * static_cast<size_t>(chunks) + 1);
+  for (int q = 0; q < world; ++q) {
+    const std::vector<int> c = shard_bounds(iptr, b[static_cast<size_t>(q)], b[static_cast<size_t>(q) + 1], chunks);
+    cuts.insert(cuts.end(), c.begin(), c.end() - 1);
+  }
+  cuts.push_back(re);
+  return cuts;
+}
+
 }  // namespace
 
 struct lr_ctx {
@@ -548,17 +564,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           ctx->gu_bounds.push_back(shard_bounds(L->iptr, rb, re, ctx->nshards));
           const int own0 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard)];
           const int own1 = ctx->gu_bounds.back()[static_cast<size_t>(ctx->shard) + 1];
-          {  // exchange chunks of every rank's shard (nnz-balanced, whole rows)
-            const std::vector<int>& b = ctx->gu_bounds.back();
-            std::vector<int> cuts;
-            for (int q = 0; q < ctx->nshards; ++q) {
-              const std::vector<int> c = shard_bounds(L->iptr, b[static_cast<size_t>(q)], b[static_cast<size_t>(q) + 1],
-                                                      ctx->xchunks);
-              cuts.insert(cuts.end(), c.begin(), c.end() - 1);
-            }
-            cuts.push_back(re);
-            ctx->gu_cuts.push_back(std::move(cuts));
-          }
+          // exchange chunks of every rank's shard (nnz-balanced, whole rows)
+          ctx->gu_cuts.push_back(exchange_cuts(L->iptr, rb, re, ctx->nshards, ctx->xchunks));
           const std::vector<int>& my_cuts = ctx->gu_cuts.back();
           std::vector<int> chunk_bk;
           // K4c chunks hold <= kChunkNnz in-edges and never put an empty row
@@ -1252,6 +1259,17 @@ lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* id128) {
   ctx->shard = rank;
   ctx->nshards = world;
   ctx->loaded = false;  // the next upload shards the grid units
+  return LR_OK;
+}
+
+lr_status lr_exchange_cuts(const int64_t* iptr, int32_t row_begin, int32_t row_end, int32_t world, int32_t chunks,
+                           int32_t* cuts) {
+  if (!iptr || !cuts || world < 1 || chunks < 1 || row_end < row_begin) {
+    lrerr::set("bad exchange request");
+    return LR_EINVAL;
+  }
+  const std::vector<int> c = exchange_cuts(iptr, row_begin, row_end, world, chunks);
+  std::copy(c.begin(), c.end(), cuts);
   return LR_OK;
 }
 

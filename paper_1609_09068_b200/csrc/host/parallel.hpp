@@ -108,6 +108,10 @@ T exclusive_scan_inplace(T* v, std::int64_t n) {
 template <typename T, typename Key>
 void stable_radix_sort(T* items, std::int64_t n, Key&& key) {
   if (n <= 1) return;
+  if (n < (1 << 14)) {  // small inputs: a comparison sort beats the histograms
+    std::stable_sort(items, items + n, [&](const T& a, const T& b) { return key(a) < key(b); });
+    return;
+  }
   const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n / (1 << 15)) + 1));
   uvector<T> tmp(static_cast<std::size_t>(n));
   std::uint32_t hi_or = 0;

@@ -543,10 +543,18 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   clk.mark("partition: level wavefronts");
   // 3. absorptions -> final components, ids by smallest member
   Sets sets(K);
-  for (const auto& part : absorbs)
-    for (const auto& [a, b] : part) sets.unite(a, b);
   std::vector<std::int32_t> root(KK);
-  for (std::size_t c = 0; c < KK; ++c) root[c] = sets.find(static_cast<std::int32_t>(c));
+  parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c) root[static_cast<std::size_t>(c)] = static_cast<std::int32_t>(c);
+  });
+  std::vector<std::int32_t> touched;  // only components in an absorption change root
+  for (const auto& part : absorbs)
+    for (const auto& [a, b] : part) {
+      sets.unite(a, b);
+      touched.push_back(a);
+      touched.push_back(b);
+    }
+  for (const std::int32_t c : touched) root[static_cast<std::size_t>(c)] = sets.find(c);
   std::vector<VertexId> first(KK, n);
   parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t v = b; v < e; ++v) {

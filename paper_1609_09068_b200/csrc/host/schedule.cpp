@@ -34,25 +34,37 @@ std::vector<VertexId> stable_desc(const std::vector<VertexId>& items, const std:
   return out;
 }
 
-// Components in schedule order: level desc, size desc, id asc.
-std::vector<VertexId> ordered_components(const Partition& p, VertexId n) {
+// Components in schedule order: level desc, size desc, id asc (two stable
+// parallel radix passes: by size, then by level).
+std::vector<VertexId> ordered_components(const Partition& p, VertexId) {
   const VertexId k = static_cast<VertexId>(p.component_count());
   std::vector<VertexId> comps(static_cast<std::size_t>(k));
   std::iota(comps.begin(), comps.end(), 0);
-  std::vector<std::int32_t> size_key(p.sizes.begin(), p.sizes.end());
-  comps = stable_desc(comps, size_key, n);
-  return stable_desc(comps, p.levels, std::max(p.max_level, 0));
+  detail::stable_radix_sort(comps.data(), k, [&](VertexId c) {
+    return ~static_cast<std::uint32_t>(p.sizes[static_cast<std::size_t>(c)]);
+  });
+  detail::stable_radix_sort(comps.data(), k, [&](VertexId c) {
+    return ~static_cast<std::uint32_t>(p.levels[static_cast<std::size_t>(c)]);
+  });
+  return comps;
 }
 
-// Members of every component, ascending vertex id (CSR by component).
+// Members of every component, ascending vertex id (CSR by component): a
+// stable parallel radix sort of the vertices by component.
 void component_members(const Partition& p, std::vector<std::int64_t>& begin, std::vector<VertexId>& mem) {
   const std::size_t k = p.component_count(), n = p.comp_of.size();
   begin.assign(k + 1, 0);
-  for (const VertexId c : p.comp_of) ++begin[static_cast<std::size_t>(c) + 1];
-  for (std::size_t c = 0; c < k; ++c) begin[c + 1] += begin[c];
-  std::vector<std::int64_t> cur(begin.begin(), begin.end() - 1);
+  detail::parallel_chunks(static_cast<std::int64_t>(n), [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v)
+      std::atomic_ref<std::int64_t>(begin[static_cast<std::size_t>(p.comp_of[static_cast<std::size_t>(v)])])
+          .fetch_add(1, std::memory_order_relaxed);
+  });
+  detail::exclusive_scan_inplace(begin.data(), static_cast<std::int64_t>(k) + 1);
   mem.resize(n);
-  for (std::size_t v = 0; v < n; ++v) mem[static_cast<std::size_t>(cur[static_cast<std::size_t>(p.comp_of[v])]++)] = static_cast<VertexId>(v);
+  std::iota(mem.begin(), mem.end(), 0);
+  detail::stable_radix_sort(mem.data(), static_cast<std::int64_t>(n), [&](VertexId v) {
+    return static_cast<std::uint32_t>(p.comp_of[static_cast<std::size_t>(v)]);
+  });
 }
 
 // One unit of the plan: a multi-vertex component, or a level's singletons.
@@ -93,7 +105,9 @@ std::vector<UnitPlan> plan_units(const Partition& p, const std::vector<VertexId>
       units.push_back({kind, level, c, sz});
     }
     if (!singles.empty()) {
-      std::sort(singles.begin(), singles.end());
+      // comps of equal level and size come in id order, and ids follow each
+      // component's smallest vertex: the singletons are usually sorted already
+      if (!std::is_sorted(singles.begin(), singles.end())) std::sort(singles.begin(), singles.end());
       const VertexId gs = static_cast<VertexId>(singles.size());
       auto at = std::find_if(units.begin() + static_cast<std::ptrdiff_t>(first), units.end(),
                              [&](const UnitPlan& u) { return u.size < gs; });

@@ -71,7 +71,14 @@ def test_sharded_path_single_rank(lr, monkeypatch, shrink, chunks):
     eng = lr.Engine(g, rank=0, world=1, nccl_id=lr.nccl_unique_id())
     r3b, r1b, _, itb = eng.solve(w, lr.SolverParams(0.85, 1e-12))
     assert np.array_equal(ita, itb)
-    assert np.array_equal(r3a, r3b) and np.array_equal(r1a, r1b)
+    if chunks == 1:
+        assert np.array_equal(r3a, r3b) and np.array_equal(r1a, r1b)
+    else:
+        # chunk cuts move K4c's tile boundaries, so rows spanning lanes are
+        # summed in a different tree (as in any row-sharded run): last-bit
+        # differences only, iteration counts identical
+        assert np.max(np.abs(r3a - r3b) / r3a) <= 1e-14
+        assert np.max(np.abs(r1a - r1b) / r1a) <= 1e-14
 
 
 def test_engine_reuse_and_zero_weights(lr):

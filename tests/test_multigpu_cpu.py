@@ -1,13 +1,16 @@
 """The multi-GPU path's host logic on CPU (gloo, world size 2).
 
 The sharded solve in csrc/cuda/ctx.cu splits every grid SccLarge unit into
-nnz-balanced row shards (lr_shard_rows), iterates only its own rows, then
-exchanges the pushed-vector shards and all-reduces the shard maxima before the
-common stop decision; the final rank shards are exchanged before lower levels
-read them.  This test runs exactly that protocol over torch.distributed/gloo
-with a scalar host SpMV standing in for the kernel, on the real layout, and
-checks it reproduces the single-process oracle: same per-unit iteration
-counts, bit-identical R3 (no SccSmall units in these graphs).
+nnz-balanced row shards, each cut into exchange chunks (lr_exchange_cuts);
+per iteration it computes chunk j of its own rows and broadcasts every rank's
+chunk j (roots in rank order) while the next chunk computes, all-reduces the
+shard maxima after the last chunk, and only then takes the common stop
+decision; the final rank shards are broadcast before lower levels read them.
+This test replays that exact schedule (the library's cuts, the same
+collective order) over torch.distributed/gloo with a scalar host SpMV standing
+in for the kernel, on the real layout, and checks it reproduces the
+single-process oracle: same per-unit iteration counts, bit-identical R3 (no
+SccSmall units in these graphs).
 """
 import os
 import socket
@@ -16,6 +19,7 @@ import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHUNKS = 3  # exchange chunks per shard (LR_XCHG_CHUNKS on the GPU path)
 
 
 def _free_port():
@@ -66,40 +70,49 @@ def _emulate_sharded(L, w, c, tol, cap, rank, world, dist, lr):
                 continue
             if kinds[u] != 3:
                 continue
-            # sharded power series of one SccLarge unit
-            bounds = lr.shard_rows(L["iptr"], a, b, world)
-            o0, o1 = bounds[rank], bounds[rank + 1]
+            # sharded power series of one SccLarge unit, on the library's own
+            # schedule: lr_exchange_cuts gives every rank's shard cut into
+            # exchange chunks; per iteration chunk j is computed, then every
+            # rank's chunk j is broadcast (roots in rank order), the last chunk
+            # followed by the all-reduce of the maxima (ctx.cu chunked_iteration)
+            cuts = lr.exchange_cuts(L["iptr"], a, b, world, CHUNKS)
+            bounds = [int(cuts[q * CHUNKS]) for q in range(world)] + [int(b)]
+            assert np.array_equal(bounds, lr.shard_rows(L["iptr"], a, b, world))
             pf = np.array([c / float(deg[r]) for r in range(a, b)])
             s_cur = pf * rankv[a:b]
-            pad = int(np.max(np.diff(bounds)))
             it = 0
             while True:
-                y = np.zeros(o1 - o0)
-                for r in range(o0, o1):
-                    acc = 0.0
-                    for e in range(L["iptr"][r], L["iptr"][r + 1]):
-                        acc += s_cur[L["isrc"][e] - a]
-                    y[r - o0] = acc
-                rankv[o0:o1] = rankv[o0:o1] + y
-                shard = np.zeros(pad)
-                shard[:o1 - o0] = pf[o0 - a:o1 - a] * y
-                parts = [torch.zeros(pad, dtype=torch.float64) for _ in range(world)]
-                dist.all_gather(parts, torch.from_numpy(shard))
-                s_cur = np.concatenate([parts[q].numpy()[:bounds[q + 1] - bounds[q]] for q in range(world)])
-                mx = torch.tensor([y.max() if len(y) else 0.0], dtype=torch.float64)
+                s_next = np.zeros(b - a)
+                mx_local = 0.0
+                for j in range(CHUNKS):
+                    for r in range(cuts[rank * CHUNKS + j], cuts[rank * CHUNKS + j + 1]):
+                        acc = 0.0
+                        for e in range(L["iptr"][r], L["iptr"][r + 1]):
+                            acc += s_cur[L["isrc"][e] - a]
+                        rankv[r] = rankv[r] + acc
+                        s_next[r - a] = pf[r - a] * acc
+                        mx_local = max(mx_local, acc)
+                    for q in range(world):
+                        q0, q1 = int(cuts[q * CHUNKS + j]), int(cuts[q * CHUNKS + j + 1])
+                        if q1 > q0:
+                            t = torch.from_numpy(s_next[q0 - a:q1 - a].copy())
+                            dist.broadcast(t, src=q)
+                            s_next[q0 - a:q1 - a] = t.numpy()
+                mx = torch.tensor([mx_local], dtype=torch.float64)
                 dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+                s_cur = s_next
                 it += 1
                 if it > cap:
                     raise RuntimeError("power series failed to converge")
                 if not (mx.item() >= tol):
                     break
             iters[u] = it
-            # replicate the final ranks of the unit
-            shard = np.zeros(pad)
-            shard[:o1 - o0] = rankv[o0:o1]
-            parts = [torch.zeros(pad, dtype=torch.float64) for _ in range(world)]
-            dist.all_gather(parts, torch.from_numpy(shard))
-            rankv[a:b] = np.concatenate([parts[q].numpy()[:bounds[q + 1] - bounds[q]] for q in range(world)])
+            # replicate the final ranks of the unit: each rank's shard broadcast
+            for q in range(world):
+                t = torch.from_numpy(rankv[bounds[q]:bounds[q + 1]].copy())
+                if len(t):
+                    dist.broadcast(t, src=q)
+                    rankv[bounds[q]:bounds[q + 1]] = t.numpy()
     r3 = np.zeros(n)
     r3[vert] = rankv
     return r3, iters
