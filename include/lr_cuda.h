@@ -257,6 +257,15 @@ lr_status lr_ranks_format(const double* ranks, int64_t n, char** out, int64_t* l
 lr_status lr_ranks_write(const double* ranks, int64_t n, const char* path);
 void lr_string_free(char* s);
 
+/* The unit solvers (proj/include/levelrank/solvers.hpp:31-54) on the GPU:
+ * kind 0 solve_singletons, 1 solve_cac, 2 solve_small_scc, 3 solve_large_scc;
+ * global_ids[m] the unit's vertices (local id = index), edge_src/dst[n_edges]
+ * its intra edges in local ids, w_local[m] its start weights.  ranks_out[m];
+ * iterations_out (kind 3) and edge_visits_out (kind 1) may be NULL. */
+lr_status lr_solve_unit(const lr_graph* g, int kind, const int32_t* global_ids, int32_t m, const int32_t* edge_src,
+                        const int32_t* edge_dst, int64_t n_edges, const double* w_local, double c, double tol,
+                        int device, double* ranks_out, int64_t* iterations_out, int64_t* edge_visits_out);
+
 /* ------------------------------------------------------- solver helpers */
 /* validate_params (proj/src/solvers.cpp:11-15). */
 lr_status lr_validate_params(double c, double tol);

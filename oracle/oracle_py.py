@@ -373,6 +373,8 @@ class Ref(_Lib):
         lib.lrref_ranks_format.argtypes = [F64P, C.c_int64, I64P]
         lib.lrref_ranks_format.restype = CPP
         lib.lrref_string_free.argtypes = [CPP]
+        lib.lrref_solve_unit.argtypes = [C.c_void_p, C.c_int, I32P, C.c_int32, I32P, I32P, C.c_int64, F64P, C.c_double,
+                                         C.c_double, F64P, I64P, I64P]
         lib.lrref_prep_new.argtypes = [C.c_void_p, C.c_int32]
         lib.lrref_prep_new.restype = C.c_void_p
         lib.lrref_prep_free.argtypes = [C.c_void_p]
@@ -488,6 +490,17 @@ class RefGraph:
                                 tuple(st) if mode == 0 else None)
         finally:
             self.r.lib.lrref_partition_free(h)
+
+    def solve_unit(self, kind, ids, es, ed, w, c, tol):
+        """The reference's solve_singletons / solve_cac / solve_small_scc /
+        solve_large_scc (kind 0-3) -> (ranks, iterations, edge_visits)."""
+        ids, es, ed, w = _i32(ids), _i32(es), _i32(ed), _f64(w)
+        out = np.zeros(len(ids))
+        it, vis = C.c_int64(), C.c_int64()
+        self.r._check(self.r.lib.lrref_solve_unit(self.h, int(kind), _p(ids, I32P), len(ids), _p(es, I32P),
+                                                  _p(ed, I32P), len(es), _p(w, F64P), c, tol, _p(out, F64P),
+                                                  C.byref(it), C.byref(vis)))
+        return out, it.value, vis.value
 
     def validate_partition(self):
         h = self._partition_handle(0)

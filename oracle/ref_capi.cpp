@@ -541,4 +541,36 @@ char* lrref_ranks_format(const double* ranks, int64_t n, int64_t* len) {
 
 void lrref_string_free(char* p) { std::free(p); }
 
+
+// The reference's unit solvers (proj/src/solvers.cpp:23-162) on a unit given
+// as global ids + local edges: kind 0 singletons, 1 cac, 2 small, 3 large.
+int lrref_solve_unit(void* gp, int kind, const int32_t* ids, int32_t m, const int32_t* es, const int32_t* ed,
+                     int64_t ne, const double* w, double c, double tol, double* out, int64_t* iters,
+                     int64_t* visits) {
+  try {
+    const Graph& g = *static_cast<Graph*>(gp);
+    SolveUnit unit;
+    unit.kind = static_cast<UnitKind>(kind);
+    unit.global_ids.assign(ids, ids + m);
+    for (int64_t i = 0; i < ne; ++i) unit.edges.emplace_back(es[i], ed[i]);
+    const Eigen::VectorXd wl = to_vec(w, m);
+    const SolverParams params{c, tol};
+    Eigen::VectorXd r;
+    std::int64_t it = 0;
+    EdgeId vis = 0;
+    switch (kind) {
+      case 0: r = solve_singletons(g, unit, wl, params); break;
+      case 1: r = solve_cac(g, unit, wl, params, &vis); break;
+      case 2: r = solve_small_scc(g, unit, wl, params); break;
+      default: r = solve_large_scc(g, unit, wl, params, it); break;
+    }
+    for (int32_t i = 0; i < m; ++i) out[i] = r(i);
+    *iters = it;
+    *visits = vis;
+    return 0;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
 }  // extern "C"

@@ -176,6 +176,8 @@ EXPORTS = {
     "lr_ranks_format": (C.c_int, [F64P, C.c_int64, C.POINTER(CP), C.POINTER(C.c_int64)]),
     "lr_ranks_write": (C.c_int, [F64P, C.c_int64, C.c_char_p]),
     "lr_string_free": (None, [CP]),
+    "lr_solve_unit": (C.c_int, [VP, C.c_int, I32P, C.c_int32, I32P, I32P, C.c_int64, F64P, C.c_double, C.c_double,
+                                C.c_int, F64P, I64P, I64P]),
     "lr_validate_params": (C.c_int, [C.c_double, C.c_double]),
     "lr_iteration_cap": (C.c_int64, [C.c_double, C.c_double]),
     "lr_error_bound": (None, [C.c_int64, C.c_int64, C.c_double, C.c_double, F64P]),
@@ -597,6 +599,25 @@ def compute_pagerank(g: Graph, weights, params: SolverParams = SolverParams(), m
     d["largest_component_kind"] = "scc" if d.pop("largest_is_scc") else "cac"
     d["all_weights_zero"] = bool(d["all_weights_zero"])
     return EngineResult(ranks, r1, d, it[: rep.n_units].copy())
+
+
+UNIT_KINDS = {"singletons": 0, "cac": 1, "small_scc": 2, "large_scc": 3}
+
+
+def solve_unit(g: Graph, kind, global_ids, edge_src, edge_dst, w_local, params: SolverParams = SolverParams(),
+               device: int = 0):
+    """The unit solvers solve_singletons / solve_cac / solve_small_scc /
+    solve_large_scc (solvers.hpp:31-54) on the GPU.  kind: 0-3 or a UNIT_KINDS
+    name; edges in local ids.  Returns (ranks, iterations, edge_visits)."""
+    k = UNIT_KINDS.get(kind, kind)
+    ids, es, ed = _i32(global_ids), _i32(edge_src), _i32(edge_dst)
+    w = _f64(w_local)
+    out = np.zeros(len(ids))
+    it, vis = C.c_int64(), C.c_int64()
+    _check(lib().lr_solve_unit(g._h, int(k), _p(ids, I32P), len(ids), _p(es, I32P), _p(ed, I32P), len(es), _p(w, F64P),
+                               float(params.c), float(params.tol), int(device), _p(out, F64P), C.byref(it),
+                               C.byref(vis)))
+    return out, it.value, vis.value
 
 
 def compute_baseline(g: Graph, weights, params: SolverParams = SolverParams(), device: int = 0) -> EngineResult:

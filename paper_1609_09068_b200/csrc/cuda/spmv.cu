@@ -518,10 +518,17 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       const long long base = off < static_cast<unsigned>(nhead) ? head_base : glob_base;
       const double* src = reinterpret_cast<const double*>(base + (static_cast<long long>(idx[k]) << 3));
       double v = 0.0;
+#ifdef LR_GATHER_L1  // experiment: gathers allocate in L1
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+          : "+d"(v)
+          : "l"(src), "r"(vm & (1u << k)), "l"(keep));
+#else
       asm volatile(
           "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
           : "+d"(v)
           : "l"(src), "r"(vm & (1u << k)), "l"(keep));
+#endif
       S.g[k] = v;
     }
     const bool tile = S.b.heavy < 0 && S.b.nnz <= kChunkNnz;

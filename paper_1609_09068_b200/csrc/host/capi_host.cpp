@@ -691,3 +691,35 @@ lr_status lr_ranks_write(const double* ranks, int64_t n, const char* path) {
 void lr_string_free(char* s) { std::free(s); }
 
 }  // extern "C"
+
+extern "C" lr_status lr_solve_unit(const lr_graph* g, int kind, const int32_t* global_ids, int32_t m,
+                                   const int32_t* edge_src, const int32_t* edge_dst, int64_t n_edges,
+                                   const double* w_local, double c, double tol, int device, double* ranks_out,
+                                   int64_t* iterations_out, int64_t* edge_visits_out) {
+  if (!g || m < 0 || n_edges < 0 || (m > 0 && (!global_ids || !w_local || !ranks_out)) ||
+      (n_edges > 0 && (!edge_src || !edge_dst)) || kind < 0 || kind > 3) {
+    lrerr::set("bad unit solve request");
+    return LR_EINVAL;
+  }
+  return guarded([&] {
+    SolveUnit unit;
+    unit.kind = static_cast<UnitKind>(kind);
+    unit.global_ids.assign(global_ids, global_ids + m);
+    unit.edges.resize(static_cast<std::size_t>(n_edges));
+    for (int64_t i = 0; i < n_edges; ++i) unit.edges[static_cast<std::size_t>(i)] = {edge_src[i], edge_dst[i]};
+    const std::span<const double> w(w_local, static_cast<std::size_t>(m));
+    const SolverParams params{c, tol};
+    std::vector<double> r;
+    std::int64_t it = 0;
+    EdgeId visits = 0;
+    switch (kind) {
+      case 0: r = solve_singletons(g->g, unit, w, params, device); break;
+      case 1: r = solve_cac(g->g, unit, w, params, &visits, device); break;
+      case 2: r = solve_small_scc(g->g, unit, w, params, device); break;
+      default: r = solve_large_scc(g->g, unit, w, params, it, device); break;
+    }
+    std::copy(r.begin(), r.end(), ranks_out);
+    if (iterations_out) *iterations_out = it;
+    if (edge_visits_out) *edge_visits_out = visits;
+  });
+}

@@ -1,0 +1,33 @@
+"""K4c A/B driver: one graph and plan, then device solves under several
+LR_SPMV_HEAD values (read at every launch); prints K4c's algorithmic GB/s
+(12 B/edge + 32 B/row per launch over the CUDA-event time of the active
+launches).  Run once per library build (LR_LIB selects a variant)."""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1609_09068_b200 as lr  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=5)
+ap.add_argument("--shrink", type=int, default=0)
+ap.add_argument("--heads", default="8192")
+ap.add_argument("--solves", type=int, default=3)
+a = ap.parse_args()
+t = time.time()
+g = lr.config_graph(a.config, a.shrink)
+eng = lr.Engine(g)
+print(f"lib {lr.library_path()} setup {time.time() - t:.0f}s", flush=True)
+w = np.full(g.n, 1.0 / g.n)
+for h in a.heads.split(","):
+    os.environ["LR_SPMV_HEAD"] = h
+    rates = []
+    for _ in range(a.solves):
+        _, _, info, _ = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+        rates.append(info["spmv_bytes"] / (info["spmv_active_ms"] / 1e3) / 1e9)
+    print(f"head {h}: K4c {np.median(rates):.0f} GB/s (runs {', '.join(f'{r:.0f}' for r in rates)}), "
+          f"device {info['device_ms']:.1f} ms", flush=True)
