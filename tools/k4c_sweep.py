@@ -17,12 +17,33 @@ ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--shrink", type=int, default=0)
 ap.add_argument("--heads", default="8192")
 ap.add_argument("--solves", type=int, default=3)
+ap.add_argument("--hot", default="", help="LR_L2_HOT_FRAC values (re-upload per value)")
+ap.add_argument("--keep", default="", help="LR_SPMV_KEEP values (re-upload per value)")
 a = ap.parse_args()
 t = time.time()
 g = lr.config_graph(a.config, a.shrink)
 eng = lr.Engine(g)
 print(f"lib {lr.library_path()} setup {time.time() - t:.0f}s", flush=True)
 w = np.full(g.n, 1.0 / g.n)
+
+
+def reupload():
+    import ctypes as C
+    lr._check(lr.lib().lr_ctx_upload(eng._h, C.byref(eng._layout)))
+
+
+for var, vals in (("LR_L2_HOT_FRAC", a.hot), ("LR_SPMV_KEEP", a.keep)):
+    for v in [x for x in vals.split(",") if x]:
+        os.environ[var] = v
+        reupload()
+        rates = []
+        for _ in range(a.solves):
+            _, _, info, _ = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+            rates.append(info["spmv_bytes"] / (info["spmv_active_ms"] / 1e3) / 1e9)
+        print(f"{var}={v}: K4c {np.median(rates):.0f} GB/s (runs {', '.join(f'{r:.0f}' for r in rates)})", flush=True)
+        del os.environ[var]
+    if vals:
+        reupload()
 for h in a.heads.split(","):
     os.environ["LR_SPMV_HEAD"] = h
     rates = []
