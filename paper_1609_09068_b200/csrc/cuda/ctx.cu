@@ -927,6 +927,11 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   DevBuf<long long> prof_buf;
   double prof_max[5] = {0, 0, 0, 0, 0}, prof_crit[5] = {0, 0, 0, 0, 0}, prof_span = 0;
   long long prof_cnt[5] = {0, 0, 0, 0, 0};
+  cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
+  double side_main = 0, side_side = 0, side_crit = 0;
+  long long side_longer = 0, side_levels = 0;
+  if (prof_on)
+    for (auto& e : pev) LR_CUDA_TRY(cudaEventCreate(&e));
   if (prof_on) {
     int most = 1;
     for (const LevelTasks& T : ctx->lt) most = std::max({most, T.lt1 - T.lt0, T.xb1 - T.xb0});
@@ -957,6 +962,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     // stream, concurrently with the level's k_level: units of one level are
     // independent, both only read ranks of the levels above
     const bool fork = T.cac_b1 > T.cac_b0;
+    if (prof_on && fork) LR_CUDA_TRY(cudaEventRecord(pev[0], s));
     if (fork) {
       LR_CUDA_TRY(cudaEventRecord(ctx->fork_ev, s));
       LR_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
@@ -968,6 +974,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       }
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
                      ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side);
+      if (prof_on) LR_CUDA_TRY(cudaEventRecord(pev[2], ctx->side));
       LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));
       ++nl;
     }
@@ -977,6 +984,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
                    ctx->unit_iters.p, ctx->status.p, T.sm1 > T.sm0 || T.lc1 > T.lc0, s);
       ++nl;
+      if (prof_on && fork) LR_CUDA_TRY(cudaEventRecord(pev[1], s));
       if (prof_on) {  // LR_LEVEL_PROF: per task type, the longest CTA of this level
         const int nt = T.lt1 - T.lt0;
         std::vector<long long> h(static_cast<size_t>(3 * nt));
@@ -1004,6 +1012,17 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       }
     }
     if (fork) LR_CUDA_TRY(cudaStreamWaitEvent(s, ctx->join_ev, 0));
+    if (prof_on && fork && T.lt1 > T.lt0) {  // main-stream level kernel vs the side stream's large CACs
+      LR_CUDA_TRY(cudaStreamSynchronize(s));
+      float mm = 0.f, ss = 0.f;
+      cudaEventElapsedTime(&mm, pev[0], pev[1]);
+      cudaEventElapsedTime(&ss, pev[0], pev[2]);
+      side_main += mm;
+      side_side += ss;
+      side_crit += std::max(mm, ss);
+      side_longer += ss > mm;
+      ++side_levels;
+    }
     if (T.sb1 > T.sb0) {
       launch_small(L, ctx->small_big.p + T.sb0, T.sb1 - T.sb0, ctx->small_scratch_ld - 1, ctx->pf.p, ctx->rank.p,
                    ctx->small_scratch.p, ctx->status.p, s);
@@ -1152,6 +1171,12 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     LR_CUDA_TRY(set_level_prof(nullptr));
     static const char* names[5] = {"rows", "cac_warps", "cac_block", "small", "lcta"};
     std::fprintf(stderr, "[LR_LEVEL_PROF] k_level span sum %.1f us over %zu levels\n", prof_span, ctx->lt.size());
+    if (side_levels)
+      std::fprintf(stderr,
+                   "[LR_LEVEL_PROF] %lld levels with a side stream: main %.1f us, side (row tasks + k_cac_big) %.1f us, "
+                   "sum of per-level max %.1f us, side longer in %lld levels\n",
+                   side_levels, side_main * 1e3, side_side * 1e3, side_crit * 1e3, side_longer);
+    for (auto& e : pev) cudaEventDestroy(e);
     for (int ty = 0; ty < 5; ++ty)
       std::fprintf(stderr, "  %-10s ctas %8lld  sum of per-level max %9.1f us  critical in levels: %9.1f us\n",
                    names[ty], prof_cnt[ty], prof_max[ty], prof_crit[ty]);
