@@ -266,6 +266,21 @@ lr_status lr_solve_unit(const lr_graph* g, int kind, const int32_t* global_ids, 
                         const int32_t* edge_dst, int64_t n_edges, const double* w_local, double c, double tol,
                         int device, double* ranks_out, int64_t* iterations_out, int64_t* edge_visits_out);
 
+/* solve_large_scc with PowerSeriesStats (solvers.cpp:128-162, solvers.hpp:23-27)
+ * in its instrumented GPU form, on a unit given as a pull CSR (row i's in-edge
+ * sources ascending; kept self-loops included), push factors pf = c/deg and
+ * start weights w.  ranks[m]; *iterations; l1[k] = ||inc_k||_1 for the first
+ * min(iterations, l1_cap) iterations; *min_entry = smallest increment entry.
+ * LR_ENOCONV past `cap` iterations. */
+lr_status lr_series_stats_csr(int device, int32_t m, const long long* ptr, const int32_t* src, const double* pf,
+                              const double* w, double tol, int64_t cap, double* ranks, int64_t* iterations,
+                              double* l1, int64_t l1_cap, double* min_entry);
+/* The same from a unit of a graph (global ids, local edges), as solve_unit. */
+lr_status lr_solve_large_scc_stats(const lr_graph* g, const int32_t* global_ids, int32_t m, const int32_t* edge_src,
+                                   const int32_t* edge_dst, int64_t n_edges, const double* w_local, double c,
+                                   double tol, int device, double* ranks_out, int64_t* iterations_out, double* l1,
+                                   int64_t l1_cap, int64_t* l1_len, double* min_entry);
+
 /* ------------------------------------------------------- solver helpers */
 /* validate_params (proj/src/solvers.cpp:11-15). */
 lr_status lr_validate_params(double c, double tol);

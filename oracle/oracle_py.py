@@ -375,6 +375,8 @@ class Ref(_Lib):
         lib.lrref_string_free.argtypes = [CPP]
         lib.lrref_solve_unit.argtypes = [C.c_void_p, C.c_int, I32P, C.c_int32, I32P, I32P, C.c_int64, F64P, C.c_double,
                                          C.c_double, F64P, I64P, I64P]
+        lib.lrref_large_scc_stats.argtypes = [C.c_void_p, I32P, C.c_int32, I32P, I32P, C.c_int64, F64P, C.c_double,
+                                              C.c_double, F64P, I64P, F64P, C.c_int64, I64P, F64P]
         lib.lrref_prep_new.argtypes = [C.c_void_p, C.c_int32]
         lib.lrref_prep_new.restype = C.c_void_p
         lib.lrref_prep_free.argtypes = [C.c_void_p]
@@ -501,6 +503,16 @@ class RefGraph:
                                                   _p(ed, I32P), len(es), _p(w, F64P), c, tol, _p(out, F64P),
                                                   C.byref(it), C.byref(vis)))
         return out, it.value, vis.value
+
+    def large_scc_stats(self, ids, es, ed, w, c, tol, cap=4096):
+        """solve_large_scc with PowerSeriesStats -> (ranks, iterations, l1 norms, min entry)."""
+        ids, es, ed, w = _i32(ids), _i32(es), _i32(ed), _f64(w)
+        out, l1 = np.zeros(len(ids)), np.zeros(cap)
+        it, n1, mn = C.c_int64(), C.c_int64(), C.c_double()
+        self.r._check(self.r.lib.lrref_large_scc_stats(self.h, _p(ids, I32P), len(ids), _p(es, I32P), _p(ed, I32P),
+                                                       len(es), _p(w, F64P), c, tol, _p(out, F64P), C.byref(it),
+                                                       _p(l1, F64P), cap, C.byref(n1), C.byref(mn)))
+        return out, it.value, l1[:min(n1.value, cap)].copy(), mn.value
 
     def validate_partition(self):
         h = self._partition_handle(0)

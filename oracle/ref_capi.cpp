@@ -573,4 +573,30 @@ int lrref_solve_unit(void* gp, int kind, const int32_t* ids, int32_t m, const in
   }
 }
 
+
+// solve_large_scc with PowerSeriesStats (solvers.cpp:128-162).
+int lrref_large_scc_stats(void* gp, const int32_t* ids, int32_t m, const int32_t* es, const int32_t* ed, int64_t ne,
+                          const double* w, double c, double tol, double* out, int64_t* iters, double* l1,
+                          int64_t l1cap, int64_t* l1len, double* mn) {
+  try {
+    const Graph& g = *static_cast<Graph*>(gp);
+    SolveUnit unit;
+    unit.kind = UnitKind::SccLarge;
+    unit.global_ids.assign(ids, ids + m);
+    for (int64_t i = 0; i < ne; ++i) unit.edges.emplace_back(es[i], ed[i]);
+    PowerSeriesStats st;
+    std::int64_t it = 0;
+    const Eigen::VectorXd r = solve_large_scc(g, unit, to_vec(w, m), SolverParams{c, tol}, it, &st);
+    for (int32_t i = 0; i < m; ++i) out[i] = r(i);
+    *iters = it;
+    const int64_t k = std::min<int64_t>(l1cap, static_cast<int64_t>(st.increment_l1_norms.size()));
+    for (int64_t i = 0; i < k; ++i) l1[i] = st.increment_l1_norms[static_cast<std::size_t>(i)];
+    *l1len = static_cast<int64_t>(st.increment_l1_norms.size());
+    *mn = st.min_increment_entry;
+    return 0;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
 }  // extern "C"

@@ -178,6 +178,10 @@ EXPORTS = {
     "lr_string_free": (None, [CP]),
     "lr_solve_unit": (C.c_int, [VP, C.c_int, I32P, C.c_int32, I32P, I32P, C.c_int64, F64P, C.c_double, C.c_double,
                                 C.c_int, F64P, I64P, I64P]),
+    "lr_series_stats_csr": (C.c_int, [C.c_int, C.c_int32, I64P, I32P, F64P, F64P, C.c_double, C.c_int64, F64P, I64P,
+                                      F64P, C.c_int64, F64P]),
+    "lr_solve_large_scc_stats": (C.c_int, [VP, I32P, C.c_int32, I32P, I32P, C.c_int64, F64P, C.c_double, C.c_double,
+                                           C.c_int, F64P, I64P, F64P, C.c_int64, I64P, F64P]),
     "lr_validate_params": (C.c_int, [C.c_double, C.c_double]),
     "lr_iteration_cap": (C.c_int64, [C.c_double, C.c_double]),
     "lr_error_bound": (None, [C.c_int64, C.c_int64, C.c_double, C.c_double, F64P]),
@@ -618,6 +622,20 @@ def solve_unit(g: Graph, kind, global_ids, edge_src, edge_dst, w_local, params: 
                                float(params.c), float(params.tol), int(device), _p(out, F64P), C.byref(it),
                                C.byref(vis)))
     return out, it.value, vis.value
+
+
+def solve_large_scc_stats(g: Graph, global_ids, edge_src, edge_dst, w_local, params: SolverParams = SolverParams(),
+                          device: int = 0, cap: int = 1 << 16):
+    """solve_large_scc with PowerSeriesStats (solvers.hpp:23-27, :48-51):
+    returns (ranks, iterations, increment L1 norms, smallest increment entry)."""
+    ids, es, ed = _i32(global_ids), _i32(edge_src), _i32(edge_dst)
+    w = _f64(w_local)
+    out, l1 = np.zeros(len(ids)), np.zeros(cap)
+    it, n1, mn = C.c_int64(), C.c_int64(), C.c_double()
+    _check(lib().lr_solve_large_scc_stats(g._h, _p(ids, I32P), len(ids), _p(es, I32P), _p(ed, I32P), len(es),
+                                          _p(w, F64P), float(params.c), float(params.tol), int(device), _p(out, F64P),
+                                          C.byref(it), _p(l1, F64P), cap, C.byref(n1), C.byref(mn)))
+    return out, it.value, l1[:min(n1.value, cap)].copy(), mn.value
 
 
 def compute_baseline(g: Graph, weights, params: SolverParams = SolverParams(), device: int = 0) -> EngineResult:

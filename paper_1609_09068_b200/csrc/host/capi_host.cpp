@@ -716,10 +716,40 @@ extern "C" lr_status lr_solve_unit(const lr_graph* g, int kind, const int32_t* g
       case 0: r = solve_singletons(g->g, unit, w, params, device); break;
       case 1: r = solve_cac(g->g, unit, w, params, &visits, device); break;
       case 2: r = solve_small_scc(g->g, unit, w, params, device); break;
-      default: r = solve_large_scc(g->g, unit, w, params, it, device); break;
+      default: r = solve_large_scc(g->g, unit, w, params, it, nullptr, device); break;
     }
     std::copy(r.begin(), r.end(), ranks_out);
     if (iterations_out) *iterations_out = it;
     if (edge_visits_out) *edge_visits_out = visits;
+  });
+}
+
+extern "C" lr_status lr_solve_large_scc_stats(const lr_graph* g, const int32_t* global_ids, int32_t m,
+                                              const int32_t* edge_src, const int32_t* edge_dst, int64_t n_edges,
+                                              const double* w_local, double c, double tol, int device,
+                                              double* ranks_out, int64_t* iterations_out, double* l1, int64_t l1_cap,
+                                              int64_t* l1_len, double* min_entry) {
+  if (!g || m < 0 || n_edges < 0 || (m > 0 && (!global_ids || !w_local || !ranks_out)) ||
+      (n_edges > 0 && (!edge_src || !edge_dst)) || !iterations_out || !min_entry) {
+    lrerr::set("bad unit solve request");
+    return LR_EINVAL;
+  }
+  return guarded([&] {
+    SolveUnit unit;
+    unit.kind = UnitKind::SccLarge;
+    unit.global_ids.assign(global_ids, global_ids + m);
+    unit.edges.resize(static_cast<std::size_t>(n_edges));
+    for (int64_t i = 0; i < n_edges; ++i) unit.edges[static_cast<std::size_t>(i)] = {edge_src[i], edge_dst[i]};
+    PowerSeriesStats st;
+    std::int64_t it = 0;
+    const std::vector<double> r =
+        solve_large_scc(g->g, unit, std::span<const double>(w_local, static_cast<std::size_t>(m)), SolverParams{c, tol},
+                        it, &st, device);
+    std::copy(r.begin(), r.end(), ranks_out);
+    *iterations_out = it;
+    const int64_t k = std::min<int64_t>(l1_cap, static_cast<int64_t>(st.increment_l1_norms.size()));
+    if (l1) std::copy(st.increment_l1_norms.begin(), st.increment_l1_norms.begin() + k, l1);
+    if (l1_len) *l1_len = static_cast<int64_t>(st.increment_l1_norms.size());
+    *min_entry = st.min_increment_entry;
   });
 }

@@ -10,6 +10,7 @@
 // SccSmall, 1 for SccLarge), and the power series reports its iterations.
 #include <algorithm>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "levelrank/engine.hpp"
@@ -110,8 +111,49 @@ std::vector<double> solve_small_scc(const Graph& g, const SolveUnit& unit, std::
 }
 
 std::vector<double> solve_large_scc(const Graph& g, const SolveUnit& unit, std::span<const double> w_local,
-                                    const SolverParams& params, std::int64_t& iterations, int device) {
-  return solve_as_graph(g, unit, w_local, params, 1, &iterations, device);
+                                    const SolverParams& params, std::int64_t& iterations, PowerSeriesStats* stats,
+                                    int device) {
+  if (!stats) return solve_as_graph(g, unit, w_local, params, 1, &iterations, device);
+  validate_params(params);
+  const VertexId m = unit.size();
+  if (static_cast<VertexId>(w_local.size()) != m)
+    throw std::invalid_argument("weight vector does not match the unit size");
+  // pull CSR: row b's sources a in ascending order = solve_large_scc's
+  // accumulation order over unit.edges (sorted by source, then target)
+  const bool keep = g.loop_policy() == LoopPolicy::Keep;
+  std::vector<std::pair<VertexId, VertexId>> e;
+  e.reserve(unit.edges.size());
+  for (const auto& [a, b] : unit.edges) {
+    if (a < 0 || a >= m || b < 0 || b >= m) throw std::invalid_argument("unit edge out of range");
+    if (a == b && !keep) continue;
+    e.emplace_back(b, a);
+  }
+  std::stable_sort(e.begin(), e.end());
+  std::vector<long long> ptr(static_cast<std::size_t>(m) + 1, 0);
+  std::vector<std::int32_t> src(e.size());
+  for (std::size_t k = 0; k < e.size(); ++k) {
+    ++ptr[static_cast<std::size_t>(e[k].first) + 1];
+    src[k] = e[k].second;
+  }
+  for (VertexId i = 0; i < m; ++i) ptr[static_cast<std::size_t>(i) + 1] += ptr[static_cast<std::size_t>(i)];
+  std::vector<double> pf(static_cast<std::size_t>(m));
+  for (VertexId i = 0; i < m; ++i)
+    pf[static_cast<std::size_t>(i)] = params.c / static_cast<double>(g.walk_out_degree(unit.global_ids[static_cast<std::size_t>(i)]));
+  const std::int64_t cap = iteration_cap(params);
+  std::vector<double> ranks(static_cast<std::size_t>(m)), l1(static_cast<std::size_t>(cap) + 1);
+  double mn = 0.0;
+  const lr_status st = lr_series_stats_csr(device, m, ptr.data(), src.data(), pf.data(), w_local.data(), params.tol,
+                                           cap, ranks.data(), &iterations, l1.data(),
+                                           static_cast<std::int64_t>(l1.size()), &mn);
+  if (st != LR_OK) {
+    const std::string msg = lr_last_error();
+    if (st == LR_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+  }
+  l1.resize(static_cast<std::size_t>(std::min<std::int64_t>(iterations, static_cast<std::int64_t>(l1.size()))));
+  stats->increment_l1_norms = std::move(l1);
+  stats->min_increment_entry = m > 0 ? mn : 0.0;
+  return ranks;
 }
 
 }  // namespace b200

@@ -53,3 +53,29 @@ def test_cac_solver_rejects_a_cycle(lr):
     g = lr.Graph.from_edges(3, [(0, 1), (1, 2), (2, 0)])
     with pytest.raises(lr.CycleError):
         lr.solve_unit(g, "cac", [0, 1, 2], [0, 1, 2], [1, 2, 0], np.ones(3), lr.SolverParams(0.85, 1e-9))
+
+
+def test_power_series_stats_match_reference(lr, ref):
+    """solve_large_scc with PowerSeriesStats: iteration count exact, ranks
+    bit-exact (rows pulled in source order), the increments' L1 norms and the
+    smallest increment entry equal to the reference's up to summation order."""
+    rng = np.random.default_rng(5)
+    done = 0
+    for t in range(12):
+        n = int(rng.integers(20, 300))
+        s, d = random_graph(rng, n, float(rng.uniform(0.02, 0.08)), loops=t % 2 == 0)
+        keep = t % 3 == 0
+        g = lr.Graph.from_edges(n, src=s, dst=d, loop_policy=int(keep))
+        rg = ref.graph(n, s, d, keep)
+        for kind, ids, es, ed in _units(rg.schedule(1)):
+            if kind != 3:
+                continue
+            w = rng.uniform(0.1, 2.0, len(ids))
+            want, wit, wl1, wmin = rg.large_scc_stats(ids, es, ed, w, 0.85, 1e-12)
+            got, it, l1, mn = lr.solve_large_scc_stats(g, ids, es, ed, w, lr.SolverParams(0.85, 1e-12))
+            assert it == wit and len(l1) == len(wl1) == it
+            assert np.array_equal(got, want)
+            np.testing.assert_allclose(l1, wl1, rtol=1e-13)
+            assert mn == wmin
+            done += 1
+    assert done > 5
