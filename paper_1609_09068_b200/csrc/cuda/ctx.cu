@@ -78,6 +78,8 @@ struct LevelTasks {
   int sb0 = 0, sb1 = 0, sb_max = 0;  // SccSmall units beyond shared memory
   int lt0 = 0, lt1 = 0;  // CTA tasks of the fused level kernel
   int xb0 = 0, xb1 = 0;  // row tasks: start weights of the level's largest k_cac_big CACs (side stream)
+  bool xb_fin = false;   // ... split: kTaskRowsFin tasks finishing sums begun one level earlier
+  int pt0 = 0, pt1 = 0;  // kTaskRowsPart tasks for the NEXT level's large CACs (pre stream, this level)
   size_t smem = 0;       // its dynamic shared memory
   size_t big_smem = 0;   // dynamic shared memory of the k_cac_big launch
   size_t sm_tile = 0;    // largest small_solve_tile footprint of the level
@@ -196,6 +198,10 @@ struct lr_ctx {
   }
   cudaStream_t side = nullptr;  // large CACs, concurrent with each level's k_level
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // early partial start-weight sums of the next level's large CACs (kTaskRowsPart)
+  cudaStream_t pre = nullptr;
+  cudaEvent_t pre_fork = nullptr, pre_done = nullptr;
+  DevBuf<double> xpart;
   int n = 0;
   int n_levels = 0;
   int64_t n_units = 0;
@@ -274,6 +280,9 @@ struct lr_ctx {
       if (e) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
+    if (pre_fork) cudaEventDestroy(pre_fork);
+    if (pre_done) cudaEventDestroy(pre_done);
+    if (pre) cudaStreamDestroy(pre);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
     if (h_params) cudaFreeHost(h_params);
@@ -397,7 +406,10 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->pre, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->pre_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->pre_done, cudaEventDisableTiming) != cudaSuccess) {
     lrerr::set("CUDA side stream creation failed");
     return fail(LR_ECUDA);
   }
@@ -771,6 +783,34 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->cac.upload(cac_w.data(), cac_w.size(), s));
   LR_CUDA_TRY(ctx->small.upload(small.data(), small.size(), s));
   LR_CUDA_TRY(ctx->small_big.upload(small_big.data(), small_big.size(), s));
+  // Large CACs' start weights in two halves (config-4 shaped chains of narrow
+  // levels): each row's cross list is ordered by source level, so the terms from
+  // levels solved at least two levels earlier are a prefix -- summed while the
+  // previous level solves (kTaskRowsPart on the pre stream), the rest added at
+  // the row's own level (kTaskRowsFin): same order, same rounding, off the
+  // side stream's critical path.  Both levels must be captured together (no
+  // grid SpMV between them).  LR_XSPLIT=0 keeps the one-level gather.
+  {
+    const char* e = std::getenv("LR_XSPLIT");
+    const bool on = !(e && std::atoi(e) == 0);
+    bool any = false;
+    for (size_t li = 1; on && li < ctx->lt.size(); ++li) {
+      LevelTasks& T = ctx->lt[li];
+      LevelTasks& P = ctx->lt[li - 1];
+      if (T.xb1 <= T.xb0 || T.gu1 > T.gu0 || P.gu1 > P.gu0) continue;
+      P.pt0 = static_cast<int>(ltasks.size());
+      for (int i = T.xb0; i < T.xb1; ++i) {
+        LevelTask& t = ltasks[static_cast<size_t>(i)];
+        t.type = kTaskRowsFin;
+        t.split = P.rb;
+        ltasks.push_back(LevelTask{kTaskRowsPart, t.a, t.b, P.rb});
+      }
+      P.pt1 = static_cast<int>(ltasks.size());
+      T.xb_fin = true;
+      any = true;
+    }
+    if (any) LR_CUDA_TRY(ctx->xpart.alloc(static_cast<size_t>(ctx->n)));
+  }
   LR_CUDA_TRY(ctx->ltasks.upload(ltasks.data(), ltasks.size(), s));
   LR_CUDA_TRY(ctx->lcta.upload(lcta.data(), lcta.size(), s));
   LR_CUDA_TRY(ctx->gstate.upload(gstate.data(), gstate.size(), s));
@@ -952,6 +992,18 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   // everything of one level that the host does not steer: enqueued directly, or
   // captured into a segment graph
   auto static_level = [&](const LevelTasks& T, int64_t& nl) -> lr_status {
+    // the previous level's early partial sums of this level's large CACs
+    if (T.xb_fin) LR_CUDA_TRY(cudaStreamWaitEvent(s, ctx->pre_done, 0));
+    // early partial sums of the NEXT level's large CACs, concurrent with this level
+    if (T.pt1 > T.pt0) {
+      LR_CUDA_TRY(cudaEventRecord(ctx->pre_fork, s));
+      LR_CUDA_TRY(cudaStreamWaitEvent(ctx->pre, ctx->pre_fork, 0));
+      launch_level(L, ctx->ltasks.p + T.pt0, T.pt1 - T.pt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p, 0,
+                   0, kRowTaskSmem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, ctx->unit_iters.p,
+                   ctx->status.p, true, ctx->pre, /*profile=*/false, ctx->xpart.p);
+      LR_CUDA_TRY(cudaEventRecord(ctx->pre_done, ctx->pre));
+      ++nl;
+    }
     // K1 for rows with more than kCrossSplit cross in-edges (split over warps)
     if (T.xh1 > T.xh0) {
       launch_cross_heavy(L, ctx->xheavy.p + T.xh0, T.xh1 - T.xh0, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p,
@@ -969,7 +1021,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       if (T.xb1 > T.xb0) {
         launch_level(L, ctx->ltasks.p + T.xb0, T.xb1 - T.xb0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                      0, 0, kRowTaskSmem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, ctx->unit_iters.p,
-                     ctx->status.p, false, ctx->side, /*profile=*/false);
+                     ctx->status.p, T.xb_fin, ctx->side, /*profile=*/false, ctx->xpart.p);
         ++nl;
       }
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,

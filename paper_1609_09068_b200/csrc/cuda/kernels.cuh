@@ -115,12 +115,25 @@ constexpr int kCacPregatherRows = 1024;  // larger CACs (all of k_cac_big's): st
                                          // (config 4: 34.6 ms at 4096, 32.1 ms at 2048 and 1024)
 
 // One CTA of the fused per-level kernel (level.cu).
-enum LevelTaskType : int { kTaskRows = 0, kTaskCacWarps = 1, kTaskCacBlock = 2, kTaskSmall = 3, kTaskLcta = 4 };
+enum LevelTaskType : int {
+  kTaskRows = 0,
+  kTaskCacWarps = 1,
+  kTaskCacBlock = 2,
+  kTaskSmall = 3,
+  kTaskLcta = 4,
+  // start weights split across two levels (config-4 shaped chains): the terms
+  // from sources in rows below `split` (levels solved at least two levels
+  // earlier, a prefix of every row's ordered cross list) summed one level
+  // early into xpart; the rest added from xpart at the row's own level
+  kTaskRowsPart = 5,
+  kTaskRowsFin = 6,
+};
+constexpr int kTaskTypes = 7;
 struct LevelTask {
   int type;
-  int a;  // rows: first row; CAC warps: first CacTask; others: task index
-  int b;  // rows: end row; CAC warps: end CacTask
-  int pad;
+  int a;      // rows: first row; CAC warps: first CacTask; others: task index
+  int b;      // rows: end row; CAC warps: end CacTask
+  int split;  // kTaskRowsPart / kTaskRowsFin: first row of the level solved just before the rows' own
 };
 constexpr int kCacBlockMaxRows = 32768;  // larger CACs: one grid-wide launch per depth slice
 #ifndef LR_SPMV_THREADS
@@ -221,7 +234,8 @@ cudaError_t set_level_prof(long long* buf);
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile = true);
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile = true,
+                  double* xpart = nullptr);
 
 // launch wrappers (stream-ordered)
 void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,

@@ -14,6 +14,8 @@
 // in-edges by the separate segment kernel (k_pull_heavy) launched before.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include <cstdint>
 #include <cstdio>
 
@@ -101,9 +103,14 @@ __device__ void cross_rows(const DeviceLayout& L, int r0, int r1, const double* 
 // more than kTiledCrossMax edges takes the per-row path.
 constexpr int kTiledCrossMax = 2048;
 
-// rows [rb, re), re - rb <= 32, by the calling warp
+// rows [rb, re), re - rb <= 32, by the calling warp.  mode 0: whole rows;
+// kTaskRowsPart: only the terms of sources in rows below `split`, the partial
+// sum stored in xpart; kTaskRowsFin: xpart plus the remaining terms.  Every
+// row owner adds its terms in list order, so the split changes no rounding.
+template <int mode = 0>
 __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const double* __restrict__ w, double c,
-                                const double* __restrict__ pf, double* rank, double* s0, double* stage) {
+                                const double* __restrict__ pf, double* rank, double* s0, double* stage,
+                                int split = 0, double* xpart = nullptr) {
   const int lane = threadIdx.x & 31;
   const int row = rb + lane;
   const bool mine = row < re;
@@ -112,14 +119,33 @@ __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const dou
     lo = L.xptr[row];
     hi = L.xptr[row + 1];
   }
-  const long long base = __shfl_sync(0xffffffffu, lo, 0);
-  const long long end = L.xptr[re];
-  if (end - base > kTiledCrossMax) {
-    cross_rows(L, rb, re, w, c, pf, rank, s0, lane, 32);
-    return;
-  }
+  long long base = __shfl_sync(0xffffffffu, lo, 0);
+  long long end = L.xptr[re];
+  if constexpr (mode == 0)
+    if (end - base > kTiledCrossMax) {
+      cross_rows(L, rb, re, w, c, pf, rank, s0, lane, 32);
+      return;
+    }
   const bool light = mine && hi - lo <= kCrossLight;  // heavier rows: k_pull_heavy
-  double acc = light ? w[L.vertex_of[row]] : 0.0;
+  if constexpr (mode != 0) {  // this pass covers [lo, cut) or [cut, hi) of each row
+    long long cut = lo;
+    if (light)
+      while (cut < hi && L.xsrc[cut] < split) ++cut;
+    if constexpr (mode == kTaskRowsPart) hi = cut;
+    else lo = cut;
+    base = light ? lo : LLONG_MAX;  // the warp's edge window: every light row's range
+    end = light ? hi : LLONG_MIN;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      base = min(base, __shfl_xor_sync(0xffffffffu, base, o));
+      end = max(end, __shfl_xor_sync(0xffffffffu, end, o));
+    }
+  }
+  double acc = 0.0;
+  if (light) {
+    if constexpr (mode == kTaskRowsFin) acc = xpart[row];
+    else acc = w[L.vertex_of[row]];
+  }
   // the finish's per-row operands, loaded now (off the gather chain)
   std::uint8_t kind = 0, lp = 0;
   int dg = 1;
@@ -157,7 +183,9 @@ __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const dou
     }
     __syncwarp();
   }
-  if (light) {  // row_finish with the prefetched operands
+  if constexpr (mode == kTaskRowsPart) {
+    if (light) xpart[row] = acc;
+  } else if (light) {  // row_finish with the prefetched operands
     if (kind == kSingle && lp) acc /= 1.0 - c / static_cast<double>(dg);
     rank[row] = acc;
     if (kind == kLargeGrid) s0[row] = pfr * acc;
@@ -165,10 +193,12 @@ __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const dou
 }
 
 // a row task: 32 rows per warp of the CTA
+template <int mode = 0>
 __device__ void cross_rows_tiled(const DeviceLayout& L, int r0, int r1, const double* __restrict__ w, double c,
-                                 const double* __restrict__ pf, double* rank, double* s0, double* stage) {
+                                 const double* __restrict__ pf, double* rank, double* s0, double* stage,
+                                 int split = 0, double* xpart = nullptr) {
   const int rb = r0 + 32 * static_cast<int>(threadIdx.x >> 5);
-  if (rb < r1) cross_warp_rows(L, rb, min(rb + 32, r1), w, c, pf, rank, s0, stage);
+  if (rb < r1) cross_warp_rows<mode>(L, rb, min(rb + 32, r1), w, c, pf, rank, s0, stage, split, xpart);
 }
 
 // The start weights of a unit's rows [r0, r1) by a whole CTA of `nwarps` warps
@@ -1510,7 +1540,7 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
             const int* __restrict__ depth_ptr, const SccTask* __restrict__ smalls, const SccTask* __restrict__ lctas,
             int small_ld, int lcta_rows, const double* __restrict__ w, const SolveParams* __restrict__ p,
             const double* __restrict__ pf, double* rank, double* s0, long long* unit_iters, DevStatus* st,
-            size_t smem_bytes, long long* prof) {
+            size_t smem_bytes, long long* prof, double* xpart) {
   extern __shared__ double sm[];
   __shared__ double red[2][32];
   const LevelTask t = tasks[blockIdx.x];
@@ -1522,6 +1552,16 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
         cross_rows_tiled(L, t.a, t.b, w, c, pf, rank, s0, sm + (threadIdx.x >> 5) * kTileNnzCross);
       else
         cross_rows(L, t.a, t.b, w, c, pf, rank, s0, threadIdx.x, kThreads);
+      break;
+    case kTaskRowsPart:  // heavy instantiation only, launched with kRowTaskSmem or more
+      if constexpr (HEAVY)
+        cross_rows_tiled<kTaskRowsPart>(L, t.a, t.b, w, c, pf, rank, s0, sm + (threadIdx.x >> 5) * kTileNnzCross,
+                                        t.split, xpart);
+      break;
+    case kTaskRowsFin:
+      if constexpr (HEAVY)
+        cross_rows_tiled<kTaskRowsFin>(L, t.a, t.b, w, c, pf, rank, s0, sm + (threadIdx.x >> 5) * kTileNnzCross,
+                                       t.split, xpart);
       break;
     case kTaskCacWarps: {
       const int ci = t.a + static_cast<int>(threadIdx.x >> 5);
@@ -1672,15 +1712,15 @@ cudaError_t set_level_prof(long long* buf) {
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile) {
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile, double* xpart) {
   if (ntasks == 0) return;
   long long* prof = profile ? g_level_prof : nullptr;  // one launch per level owns the buffer
   if (heavy)
     k_level<true><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
-                                                 pf, rank, s0, unit_iters, st, smem, prof);
+                                                 pf, rank, s0, unit_iters, st, smem, prof, xpart);
   else
     k_level<false><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
-                                                  pf, rank, s0, unit_iters, st, smem, prof);
+                                                  pf, rank, s0, unit_iters, st, smem, prof, xpart);
 }
 
 }  // namespace lrk

@@ -221,3 +221,19 @@ def test_dense_small_scc_shared_memory_cap(lr, oracle, m, th, keep):
     d = np.concatenate([d, np.roll(ring, -1), [m]])
     w = np.random.default_rng(m).uniform(0.1, 2.0, m + 40)
     check(lr, oracle, m + 40, s, d, w=w, th=th, keep=keep)
+
+
+@pytest.mark.parametrize("cfg,shrink", [(4, 3), (1, 1)])
+def test_split_start_weights_bit_identical(lr, monkeypatch, cfg, shrink):
+    """Large CACs' start weights summed in two halves across consecutive
+    levels (kTaskRowsPart one level early, kTaskRowsFin at the row's level)
+    give exactly the one-pass gather's ranks: the split is a prefix of each
+    row's ordered cross list, so the additions and their order are unchanged."""
+    g = lr.config_graph(cfg, shrink)
+    w = np.full(g.n, 1.0 / g.n)
+    monkeypatch.setenv("LR_XSPLIT", "0")
+    a = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
+    monkeypatch.setenv("LR_XSPLIT", "1")
+    b = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(a[3], b[3])
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
