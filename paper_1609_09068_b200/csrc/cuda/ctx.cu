@@ -783,13 +783,15 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   // Large CACs' start weights in two halves (config-4 shaped chains of narrow
   // levels): each row's cross list is ordered by source level, so the terms from
   // levels solved at least two levels earlier are a prefix -- summed while the
-  // previous level solves (kTaskRowsPart on the pre stream), the rest added by
-  // k_cac_big itself before its sweep (kTaskRowsFin order): same order, same
-  // rounding, one launch fewer on the side stream's critical path.  Both levels must be captured together (no
-  // grid SpMV between them).  LR_XSPLIT=0 keeps the one-level gather.
+  // previous level solves (kTaskRowsPart on the pre stream), the rest added at
+  // the row's own level (kTaskRowsFin): same order, same rounding, off the
+  // side stream's critical path.  Both levels must be captured together (no
+  // grid SpMV between them).  Measured at config 4: 31.2 ms without, 31.9 ms with (the
+  // finish tasks' latency is the same as the full gather's); off by default,
+  // LR_XSPLIT=1 enables it.
   {
     const char* e = std::getenv("LR_XSPLIT");
-    const bool on = !(e && std::atoi(e) == 0);
+    const bool on = e && std::atoi(e) != 0;
     bool any = false;
     for (size_t li = 1; on && li < ctx->lt.size(); ++li) {
       LevelTasks& T = ctx->lt[li];
@@ -797,19 +799,12 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
       if (T.xb1 <= T.xb0 || T.gu1 > T.gu0 || P.gu1 > P.gu0) continue;
       P.pt0 = static_cast<int>(ltasks.size());
       for (int i = T.xb0; i < T.xb1; ++i) {
-        const LevelTask t = ltasks[static_cast<size_t>(i)];
+        LevelTask& t = ltasks[static_cast<size_t>(i)];
+        t.type = kTaskRowsFin;
+        t.split = P.rb;
         ltasks.push_back(LevelTask{kTaskRowsPart, t.a, t.b, P.rb});
       }
       P.pt1 = static_cast<int>(ltasks.size());
-      // the rest of each sum is added by k_cac_big itself: no row-task launch
-      for (int i = T.cac_b0; i < T.cac_b1; ++i) {
-        CacTask& ct = cac_w[static_cast<size_t>(i)];
-        if (ct.pregathered == 1) {
-          ct.pregathered = 2;
-          ct.split = P.rb;
-        }
-      }
-      T.xb0 = T.xb1;
       T.xb_fin = true;
       any = true;
     }
@@ -1032,8 +1027,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
         ++nl;
       }
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
-                     ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side,
-                     ctx->xpart.p);
+                     ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side);
       if (prof_on) LR_CUDA_TRY(cudaEventRecord(pev[2], ctx->side));
       LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));
       ++nl;

@@ -3,6 +3,27 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
+// Device-side bounds checks of the gathers (compute-sanitizer is closed on the
+// GPU pool): build with -DLR_DEVICE_CHECKS (tools/build_variant.sh dchecks
+// -DLR_DEVICE_CHECKS) and run the GPU suite with LR_LIB pointing at it; a failed
+// check prints its site and traps the kernel.  Compiled out otherwise.
+#ifdef LR_DEVICE_CHECKS
+#define LR_DCHECK(cond)                                                                     \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("LR_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                 \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define LR_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace lrk {
 namespace dev {
 

@@ -83,12 +83,7 @@ struct CacTask {
   int row_end;
   long long depth_begin;  // into depth_ptr
   int ndepth;
-  // 0: k_cac_big gathers the start weights; 1: row tasks launched before did;
-  // 2: partial sums from the level before (xpart), k_cac_big adds the terms of
-  // sources in rows >= split (kTaskRowsFin order)
-  int pregathered;
-  int split;
-  int pad;
+  int pregathered;  // start weights gathered by row tasks launched before (k_cac_big skips its own)
 };
 struct SccTask {
   int row_begin;
@@ -227,7 +222,7 @@ cudaError_t configure_level_kernel();
 // large CACs, 1024-thread CTAs, meant for a second stream (level.cu)
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
                     const SolveParams* p, const double* pf, double* rank, double* s0, double* pv, size_t smem,
-                    cudaStream_t s, double* xpart = nullptr);
+                    cudaStream_t s);
 // shared-memory bytes a CAC of `rows` rows and `edges` in-edges needs to be swept from shared memory
 size_t cac_stage_need(long long rows, long long edges);
 size_t cac_compact_need(long long rows, long long edges);  // k_cac_big's structure-only staging

@@ -163,6 +163,7 @@ __device__ void cross_warp_rows(const DeviceLayout& L, int rb, int re, const dou
     for (int k = 0; k < kTileNnzCross / 32; ++k) {
       const int e = lane + 32 * k;
       src[k] = e < n ? __ldg(L.xsrc + cb + e) : 0;
+      LR_DCHECK(src[k] >= 0 && src[k] < L.n);
     }
     double rv[kTileNnzCross / 32];
     int dv[kTileNnzCross / 32];
@@ -227,6 +228,7 @@ __device__ __forceinline__ double cac_row(const DeviceLayout& L, int r, double c
 #pragma unroll 4
   for (long long e = e0; e < e1; ++e) {
     const int s = L.isrc[e];
+    LR_DCHECK(s >= 0 && s < L.n);
     acc += rank[s] * c / static_cast<double>(L.deg[s]);
   }
   return acc;
@@ -349,6 +351,7 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       double acc = sr[i];
       for (int e = e0; e < e1; ++e) {
         const int sp = es[e];
+        LR_DCHECK(sp >= 0 && sp < m);
         acc += sr[sp] * c / static_cast<double>(rd[sp]);
       }
       sr[i] = lp[i] ? acc / (1.0 - c / static_cast<double>(rd[i])) : acc;
@@ -1629,27 +1632,14 @@ __global__ void __launch_bounds__(kThreads, HEAVY ? LR_LEVEL_MINB : LR_LIGHT_MIN
 // level, ~20 us, formerly serialised after k_level).
 constexpr int kBigThreads = 1024;
 
-// (kept out of line: k_cac_big runs at 64 registers per thread)
-__device__ __noinline__ void big_cac_finish_weights(const DeviceLayout& L, const CacTask& ct,
-                                                    const double* __restrict__ w, double c,
-                                                    const double* __restrict__ pf, double* rank, double* s0,
-                                                    double* sm, double* xpart) {
-  const int warp = threadIdx.x >> 5;
-  for (int rb = ct.row_begin + 32 * warp; rb < ct.row_end; rb += 32 * (kBigThreads / 32))
-    cross_warp_rows<kTaskRowsFin>(L, rb, min(rb + 32, ct.row_end), w, c, pf, rank, s0, sm + warp * kTileNnzCross,
-                                  ct.split, xpart);
-}
 
 __global__ void __launch_bounds__(kBigThreads)
     k_cac_big(DeviceLayout L, const CacTask* __restrict__ cacs, const int* __restrict__ depth_ptr,
               const double* __restrict__ w, const SolveParams* __restrict__ p, const double* __restrict__ pf,
-              double* rank, double* s0, double* pv, size_t smem_bytes, double* xpart) {
+              double* rank, double* s0, double* pv, size_t smem_bytes) {
   extern __shared__ double sm[];
   const CacTask ct = cacs[blockIdx.x];
-  if (ct.pregathered == 2) {  // finish start weights begun one level earlier (warp-tiled, in order)
-    big_cac_finish_weights(L, ct, w, p->c, pf, rank, s0, sm, xpart);
-    __syncthreads();
-  }
+
   // the CAC's own start weights (rows above kCrossSplit cross in-edges were
   // done by k_pull_heavy before the level), so the launch runs concurrently
   // with the level's k_level on a side stream
@@ -1671,7 +1661,7 @@ __global__ void __launch_bounds__(kBigThreads)
 
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
                     const SolveParams* p, const double* pf, double* rank, double* s0, double* pv, size_t smem,
-                    cudaStream_t s, double* xpart) {
+                    cudaStream_t s) {
   if (n == 0) return;
   // highest launch priority (kept by graph capture): its 1024-thread CTAs need a
   // whole SM and must be placed before the level's k_level CTAs fill them
@@ -1690,7 +1680,7 @@ void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int
   attr[0].val.priority = prio;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, pv, smem, xpart);
+  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, pv, smem);
 }
 
 size_t cac_stage_need(long long rows, long long edges) { return cac_stage_bytes(rows, edges); }

@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     for (int k = 0; k < 8; ++k) {
       // one generic load: the shared-memory head or the global pushed vector
       const unsigned off = static_cast<unsigned>(idx[k] - hot_begin);
+      LR_DCHECK(!(vm & (1u << k)) || (idx[k] >= 0 && idx[k] < L.n));
       const long long base = off < static_cast<unsigned>(nhead) ? head_base : glob_base;
       const double* src = reinterpret_cast<const double*>(base + (static_cast<long long>(idx[k]) << 3));
       double v = 0.0;

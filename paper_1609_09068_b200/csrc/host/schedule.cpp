@@ -18,22 +18,6 @@ inline namespace b200 {
 namespace {
 
 
-// Stable counting sort, descending key (schedule.cpp:14-28).
-std::vector<VertexId> stable_desc(const std::vector<VertexId>& items, const std::vector<std::int32_t>& key,
-                                  std::int32_t max_key) {
-  std::vector<std::int64_t> slot(static_cast<std::size_t>(max_key) + 2, 0);
-  for (const VertexId it : items) ++slot[static_cast<std::size_t>(key[static_cast<std::size_t>(it)])];
-  std::int64_t acc = 0;
-  for (std::int32_t k = max_key; k >= 0; --k) {
-    const std::int64_t c = slot[static_cast<std::size_t>(k)];
-    slot[static_cast<std::size_t>(k)] = acc;
-    acc += c;
-  }
-  std::vector<VertexId> out(items.size());
-  for (const VertexId it : items) out[static_cast<std::size_t>(slot[static_cast<std::size_t>(key[static_cast<std::size_t>(it)])]++)] = it;
-  return out;
-}
-
 // Components in schedule order: level desc, size desc, id asc (two stable
 // parallel radix passes: by size, then by level).
 std::vector<VertexId> ordered_components(const Partition& p, VertexId) {
