@@ -340,11 +340,19 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       __syncwarp();
     }
   };
-  sync();
+  // slice bounds: dp[d + 1] is the next slice's start, so only one new bound
+  // per slice, loaded a slice ahead (off the barrier-to-barrier chain)
   const int* dp = depth_ptr + t.depth_begin;
-  for (int d = 0; d < t.ndepth; ++d) {
+  const int nd = t.ndepth;
+  int b0 = __ldg(dp) - rb, b1 = nd > 0 ? __ldg(dp + 1) - rb : b0;
+  sync();
+  for (int d = 0; d < nd; ++d) {
     if (d > 0) sync();
-    const int s0 = dp[d] - rb, s1 = dp[d + 1] - rb;
+    const int s0 = b0, s1 = b1;
+    if (d + 1 < nd) {
+      b0 = s1;
+      b1 = __ldg(dp + d + 2) - rb;
+    }
     for (int i = s0 + tid; i < s1; i += width) {
       const int e0 = rp[i], e1 = rp[i + 1];
       if (e1 - e0 > kCrossLight) continue;
