@@ -137,14 +137,15 @@ Schedule build_schedule(const Graph& g, const Partition& p, VertexId small_thres
   const auto plan = plan_units(p, comps, small_threshold, lub, singles, mb, mem);
   const std::size_t nl = static_cast<std::size_t>(p.max_level) + 1;
   s.levels.resize(nl);
-  std::vector<std::pair<std::size_t, std::size_t>> unit_of_comp(p.component_count());
   std::vector<VertexId> local_of(static_cast<std::size_t>(n));
+  std::vector<SolveUnit*> flat;  // every unit, schedule order
   for (std::size_t li = 0; li < nl; ++li) {
     auto& L = s.levels[li];
     L.level = p.max_level - static_cast<std::int32_t>(li);
+    L.units.resize(static_cast<std::size_t>(lub[li + 1] - lub[li]));
     for (std::int32_t ui = lub[li]; ui < lub[li + 1]; ++ui) {
       const UnitPlan& up = plan[static_cast<std::size_t>(ui)];
-      SolveUnit u;
+      SolveUnit& u = L.units[static_cast<std::size_t>(ui - lub[li])];
       u.kind = up.kind;
       u.level = up.level;
       if (up.comp >= 0)
@@ -152,37 +153,55 @@ Schedule build_schedule(const Graph& g, const Partition& p, VertexId small_thres
                             mem.begin() + mb[static_cast<std::size_t>(up.comp) + 1]);
       else
         u.global_ids = singles[li];
-      const std::size_t idx = L.units.size();
-      for (std::size_t i = 0; i < u.global_ids.size(); ++i) {
-        const VertexId v = u.global_ids[i];
-        local_of[static_cast<std::size_t>(v)] = static_cast<VertexId>(i);
-        unit_of_comp[static_cast<std::size_t>(p.comp_of[static_cast<std::size_t>(v)])] = {li, idx};
-      }
-      L.units.push_back(std::move(u));
+      flat.push_back(&u);
     }
   }
-  for (VertexId u = 0; u < n; ++u) {
-    const VertexId cu = p.comp_of[static_cast<std::size_t>(u)];
-    const auto [li, ui] = unit_of_comp[static_cast<std::size_t>(cu)];
-    for (const VertexId v : g.out_neighbors(u)) {
-      if (u == v) {
-        if (g.loop_policy() == LoopPolicy::Keep) {
-          s.levels[li].units[ui].edges.emplace_back(local_of[static_cast<std::size_t>(u)], local_of[static_cast<std::size_t>(u)]);
-          ++s.intra_edge_count;
-        } else {
-          ++s.dropped_loop_count;
+  // Intra edges unit by unit (in parallel): the unit's vertices ascending and
+  // each row's targets ascending give the (local src, local dst) order the
+  // reference's single pass over all vertices produces (schedule.cpp:112-135).
+  const bool keep = g.loop_policy() == LoopPolicy::Keep;
+  std::atomic<EdgeId> intra{0}, dropped{0};
+  detail::parallel_dynamic(static_cast<std::int64_t>(flat.size()), 64, [&](std::int64_t b, std::int64_t e) {
+    EdgeId li = 0, ld = 0;
+    for (std::int64_t k = b; k < e; ++k) {
+      SolveUnit& u = *flat[static_cast<std::size_t>(k)];
+      for (std::size_t a = 0; a < u.global_ids.size(); ++a) local_of[static_cast<std::size_t>(u.global_ids[a])] = static_cast<VertexId>(a);
+      for (std::size_t a = 0; a < u.global_ids.size(); ++a) {
+        const VertexId v = u.global_ids[a];
+        const VertexId cv = p.comp_of[static_cast<std::size_t>(v)];
+        for (const VertexId t : g.out_neighbors(v)) {
+          if (t == v) {
+            if (keep) u.edges.emplace_back(static_cast<VertexId>(a), static_cast<VertexId>(a));
+            else ++ld;
+          } else if (p.comp_of[static_cast<std::size_t>(t)] == cv) {
+            u.edges.emplace_back(static_cast<VertexId>(a), local_of[static_cast<std::size_t>(t)]);
+          }
         }
-        continue;
       }
-      if (cu == p.comp_of[static_cast<std::size_t>(v)]) {
-        s.levels[li].units[ui].edges.emplace_back(local_of[static_cast<std::size_t>(u)], local_of[static_cast<std::size_t>(v)]);
-        ++s.intra_edge_count;
-      } else {
-        s.levels[li].cross_edges.push_back({u, v, g.walk_out_degree(u)});
-        ++s.cross_edge_count;
-      }
+      li += static_cast<EdgeId>(u.edges.size());
     }
-  }
+    intra += li;
+    dropped += ld;
+  });
+  // Cross edges per source level (in parallel over levels), sources ascending.
+  std::atomic<EdgeId> cross{0};
+  detail::parallel_dynamic(static_cast<std::int64_t>(nl), 1, [&](std::int64_t b, std::int64_t e) {
+    for (std::int64_t li = b; li < e; ++li) {
+      auto& L = s.levels[static_cast<std::size_t>(li)];
+      std::vector<VertexId> sources;
+      for (const SolveUnit& u : L.units) sources.insert(sources.end(), u.global_ids.begin(), u.global_ids.end());
+      std::sort(sources.begin(), sources.end());
+      for (const VertexId v : sources) {
+        const VertexId cv = p.comp_of[static_cast<std::size_t>(v)];
+        for (const VertexId t : g.out_neighbors(v))
+          if (t != v && p.comp_of[static_cast<std::size_t>(t)] != cv) L.cross_edges.push_back({v, t, g.walk_out_degree(v)});
+      }
+      cross += static_cast<EdgeId>(L.cross_edges.size());
+    }
+  });
+  s.intra_edge_count = intra;
+  s.dropped_loop_count = dropped;
+  s.cross_edge_count = cross;
   return s;
 }
 

@@ -237,3 +237,19 @@ def test_split_start_weights_bit_identical(lr, monkeypatch, cfg, shrink):
     b = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
     assert np.array_equal(a[3], b[3])
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_cta_series_source_order_iteration_counts(lr, oracle, monkeypatch):
+    """The CTA power series sums each row's first twelve in-edges pairwise and,
+    by default, reorders in-edges for shared-memory banks; with the layout's
+    source order (LR_BANK_ORDER=0) and by default, per-unit iteration counts
+    equal the reference's and ranks agree to 1e-10."""
+    g = lr.config_graph(1, 2)
+    off, tgt, _, _ = g.csr()
+    w = np.full(g.n, 1.0 / g.n)
+    ref = oracle.graph_from_csr(g.n, off, tgt).compute_pagerank(w, 0.85, 1e-12, 100)
+    for order in ("0", "1"):
+        monkeypatch.setenv("LR_BANK_ORDER", order)
+        res = lr.compute_pagerank(g, w, lr.SolverParams(0.85, 1e-12))
+        assert np.array_equal(res.unit_iters, ref.unit_iters), order
+        assert (np.abs(res.ranks - ref.ranks) / ref.ranks).max() <= 1e-10, order
