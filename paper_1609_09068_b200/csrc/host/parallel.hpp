@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdint>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "levelrank/graph.hpp"
@@ -29,6 +30,15 @@ struct PhaseClock {
 };
 
 
+// Runs f(i) for i in [0, t) on t threads of the persistent host pool (the
+// caller is thread 0; pool.cpp).
+void pool_run_impl(int t, void (*fn)(void*, int), void* arg);
+template <typename F>
+void pool_run(int t, F&& f) {
+  using Fn = std::remove_reference_t<F>;
+  pool_run_impl(t, [](void* a, int i) { (*static_cast<Fn*>(a))(i); }, static_cast<void*>(&f));
+}
+
 // Calls f(tid, begin, end) on contiguous chunks of [0, n) from up to
 // host_threads() threads (serial below `grain`).
 template <typename F>
@@ -40,13 +50,7 @@ void parallel_chunks(std::int64_t n, F&& f, std::int64_t grain = 1 << 15) {
     return;
   }
   t = static_cast<int>(std::min<std::int64_t>(t, (n + grain - 1) / grain));
-  std::vector<std::thread> pool;
-  pool.reserve(static_cast<std::size_t>(t));
-  for (int i = 0; i < t; ++i) {
-    const std::int64_t b = n * i / t, e = n * (i + 1) / t;
-    pool.emplace_back([&f, i, b, e] { f(i, b, e); });
-  }
-  for (auto& th : pool) th.join();
+  pool_run(t, [&](int i) { f(i, n * i / t, n * (i + 1) / t); });
 }
 
 // Dynamic scheduling over [0, n) in blocks of `block` (for skewed work).
@@ -59,16 +63,13 @@ void parallel_dynamic(std::int64_t n, std::int64_t block, F&& f) {
     return;
   }
   std::atomic<std::int64_t> next{0};
-  std::vector<std::thread> pool;
-  for (int i = 0; i < t; ++i)
-    pool.emplace_back([&] {
-      for (;;) {
-        const std::int64_t b = next.fetch_add(block);
-        if (b >= n) return;
-        f(b, std::min(n, b + block));
-      }
-    });
-  for (auto& th : pool) th.join();
+  pool_run(t, [&](int) {
+    for (;;) {
+      const std::int64_t b = next.fetch_add(block);
+      if (b >= n) return;
+      f(b, std::min(n, b + block));
+    }
+  });
 }
 
 // Exclusive prefix sum in place over v[0..n); returns the total.  v has n+1
@@ -77,12 +78,7 @@ template <typename T>
 T exclusive_scan_inplace(T* v, std::int64_t n) {
   const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n / (1 << 16)) + 1));
   std::vector<T> part(static_cast<std::size_t>(t) + 1, 0);
-  std::vector<std::thread> pool;
-  auto run = [&](auto&& body) {
-    pool.clear();
-    for (int i = 0; i < t; ++i) pool.emplace_back(body, i);
-    for (auto& th : pool) th.join();
-  };
+  auto run = [&](auto&& body) { pool_run(t, body); };
   run([&](int i) {
     const std::int64_t b = n * i / t, e = n * (i + 1) / t;
     T s = 0;
@@ -116,12 +112,7 @@ void stable_radix_sort(T* items, std::int64_t n, Key&& key) {
   uvector<T> tmp(static_cast<std::size_t>(n));
   std::uint32_t hi_or = 0;
   for (std::int64_t i = 0; i < n && !hi_or; i += std::max<std::int64_t>(1, n / 4096)) hi_or |= key(items[i]) >> 16;
-  std::vector<std::thread> pool;
-  auto run = [&](auto&& body) {
-    pool.clear();
-    for (int i = 0; i < t; ++i) pool.emplace_back(body, i);
-    for (auto& th : pool) th.join();
-  };
+  auto run = [&](auto&& body) { pool_run(t, body); };
   if (!hi_or) {  // the sample saw no high digit: check exactly
     std::vector<std::uint32_t> any(static_cast<std::size_t>(t), 0);
     run([&](int i) {
@@ -175,11 +166,7 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr
                static_cast<std::size_t>(nb) + static_cast<std::size_t>(b);
   };
   std::vector<std::int64_t> cur(static_cast<std::size_t>(K) * static_cast<std::size_t>(t) * static_cast<std::size_t>(nb), 0);
-  auto run = [&](auto&& body) {
-    std::vector<std::thread> pool;
-    for (int i = 0; i < t; ++i) pool.emplace_back(body, i);
-    for (auto& th : pool) th.join();
-  };
+  auto run = [&](auto&& body) { pool_run(t, body); };
   run([&](int th) {  // 1. per-(thread, bucket) counts
     const std::int64_t b = n_src * th / t, e = n_src * (th + 1) / t;
     for (std::int64_t u = b; u < e; ++u)

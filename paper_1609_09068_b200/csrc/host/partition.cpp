@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <thread>
 #include <vector>
 
@@ -85,15 +86,21 @@ struct Bits {
   }
 };
 
-// parallel_chunks with the thread index bounded by host_threads()
+// parallel_chunks with the thread index bounded by host_threads(): the items
+// are components or vertices whose edge scans are random-access bound, so even
+// a deep DAG's small wavefronts (~2k components) are spread over every thread
+// (the pool keeps a phase's overhead to microseconds)
 template <typename F>
-void for_items(const std::vector<std::int32_t>& items, F&& f) {
+void for_items(const std::vector<std::int32_t>& items, F&& f, std::int64_t grain) {
   parallel_chunks(static_cast<std::int64_t>(items.size()),
                   [&](int th, std::int64_t b, std::int64_t e) {
                     for (std::int64_t i = b; i < e; ++i) f(th, items[static_cast<std::size_t>(i)]);
                   },
-                  256);
+                  grain);
 }
+// items per thread: small on big graphs (each item's scan misses cache), large
+// on small graphs (where a phase is shorter than waking the workers)
+inline std::int64_t item_grain(std::int64_t n) { return n >= (1 << 22) ? 64 : 4096; }
 
 struct Adjacency {
   const EdgeId* off;
@@ -163,7 +170,7 @@ class SccFinder {
           if (live(p) && atomic_sub(dout_[static_cast<std::size_t>(p)], 1) == 1 && claim(queued_[static_cast<std::size_t>(p)]))
             out.push_back(p);
         }
-      });
+      }, item_grain(n_));
       cur = next.take();
     }
   }
@@ -180,7 +187,8 @@ class SccFinder {
         const std::int64_t s = static_cast<std::int64_t>(din_[static_cast<std::size_t>(v)]) * dout_[static_cast<std::size_t>(v)];
         if (s > best) best = s, pivot = v;
       }
-    if (pivot < 0) return;
+    // no hub (a deep DAG of small components, planted SCCs): Tarjan alone
+    if (pivot < 0 || best < kMinHubDegreeProduct) return;
     const std::size_t nn = static_cast<std::size_t>(n_);
     Bits alive(nn), fw(nn), bw(nn);
     parallel_chunks((n_ + 63) / 64, [&](int, std::int64_t b, std::int64_t e) {
@@ -190,8 +198,10 @@ class SccFinder {
         alive.w[static_cast<std::size_t>(wd)] = x;
       }
     });
-    bfs(pivot, alive, fw, false);
-    bfs(pivot, alive, bw, true);
+    // a pivot whose reach needs more than kMaxReachLevels BFS levels sits in a
+    // deep DAG of small components (config 4), not in a giant SCC: leave it
+    // to Tarjan (the result is the same, only the order of work changes)
+    if (!bfs(pivot, alive, fw, false) || !bfs(pivot, alive, bw, true)) return;
     giant_ = pivot;
     // the SCC's members leave the graph: recount live degrees without them
     parallel_chunks(n_, [&](int, std::int64_t b, std::int64_t e) {
@@ -218,7 +228,9 @@ class SccFinder {
   // Level-synchronous BFS over the live vertices, direction-optimising
   // (Beamer et al.): a large frontier switches to the bottom-up step, where
   // every unvisited vertex looks for one parent in the frontier and stops.
-  void bfs(VertexId src, const Bits& alive, Bits& seen, bool backward) {
+  static constexpr int kMaxReachLevels = 128;
+  static constexpr std::int64_t kMinHubDegreeProduct = 1024;
+  bool bfs(VertexId src, const Bits& alive, Bits& seen, bool backward) {
     const int T = host_threads();
     const EdgeId* fo = backward ? a_.in_off.data() : a_.off;  // search direction
     const VertexId* fa = backward ? a_.in_src.data() : a_.tgt;
@@ -230,15 +242,16 @@ class SccFinder {
     std::vector<std::int32_t> cur{src};
     EdgeId unexplored = fo[n_] - fo[0];
     bool bottom_up = false;
+    int levels = 0;
     while (!cur.empty()) {
       std::atomic<EdgeId> fe{0};
-      for_items(cur, [&](int, VertexId v) { fe.fetch_add(fo[v + 1] - fo[v], std::memory_order_relaxed); });
+      for_items(cur, [&](int, VertexId v) { fe.fetch_add(fo[v + 1] - fo[v], std::memory_order_relaxed); }, item_grain(n_));
       if (!bottom_up && fe.load() > unexplored / 14) bottom_up = true;
       else if (bottom_up && static_cast<std::int64_t>(cur.size()) < n_ / 24) bottom_up = false;
       unexplored -= fe.load();
       if (bottom_up) {
         std::fill(in_front.w.begin(), in_front.w.end(), 0);
-        for_items(cur, [&](int, VertexId v) { in_front.set_atomic(v); });
+        for_items(cur, [&](int, VertexId v) { in_front.set_atomic(v); }, item_grain(n_));
         parallel_chunks(n_, [&](int th, std::int64_t b, std::int64_t e) {
           auto& out = next.parts[static_cast<std::size_t>(th)];
           for (std::int64_t ww = b; ww < e; ++ww) {
@@ -259,10 +272,12 @@ class SccFinder {
             const VertexId w = fa[k];
             if (alive.get(w) && seen.set_atomic(w)) out.push_back(w);
           }
-        });
+        }, item_grain(n_));
       }
       cur = next.take();
+      if (++levels > kMaxReachLevels && !cur.empty()) return false;
     }
+    return true;
   }
 
   // Tarjan's algorithm (SCC labels only) over the live vertices.
@@ -514,7 +529,10 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     if (veto) mine.resize(mark);
     else if (mine.size() > mark) level[static_cast<std::size_t>(c)] = l0 - 1;
   };
+  long long n_waves = 0, n_items = 0;
   while (!cur.empty()) {
+    ++n_waves;
+    n_items += static_cast<long long>(cur.size());
     std::vector<std::int32_t> narrow, wide;
     for (const std::int32_t c : cur)
       (mptr[static_cast<std::size_t>(c) + 1] - mptr[static_cast<std::size_t>(c)] > kWideComponent ? wide : narrow).push_back(c);
@@ -528,18 +546,19 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     }
     for_items(narrow, [&](int th, std::int32_t c) {
       decide(th, c, max_successor(c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]));
-    });
+    }, item_grain(n));
     for (const std::int32_t c : wide) {
       const std::int64_t m0 = mptr[static_cast<std::size_t>(c)], m1 = mptr[static_cast<std::size_t>(c) + 1];
       parallel_chunks(m1 - m0, [&](int th, std::int64_t b, std::int64_t e) { release(th, c, m0 + b, m0 + e); });
     }
     for_items(narrow, [&](int th, std::int32_t c) {
       release(th, c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]);
-    });
+    }, item_grain(n));
     cur = next.take();
   }
   for (const std::int64_t s : scans) st.merge_scan_edge_visits += s;
 
+  if (clk.on) std::fprintf(stderr, "[plan] partition: %lld wavefronts, %lld components\n", n_waves, n_items);
   clk.mark("partition: level wavefronts");
   // 3. absorptions -> final components, ids by smallest member
   Sets sets(K);
