@@ -43,3 +43,25 @@ def test_baseline_layout_large(lr, keep):
     for r in range(n):
         v = vo[r]
         np.testing.assert_array_equal(got[iptr[r]:iptr[r + 1]], want[want_start[v]:want_start[v + 1]])
+
+
+def test_concurrent_plan_builds_agree(lr):
+    """Two host threads building plans at once (the C-ABI releases the GIL):
+    one gets the persistent worker pool, the other falls back to its own
+    threads; both layouts equal a plan built alone."""
+    import threading
+    g = lr.config_graph(2, 2)
+    want = lr.Plan(g).layout()
+    out = [None, None]
+
+    def build(i):
+        out[i] = lr.Plan(g).layout()
+
+    ts = [threading.Thread(target=build, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for got in out:
+        for k in ("vertex_of", "iptr", "isrc", "xptr", "xsrc", "unit_kind", "unit_row_begin"):
+            assert np.array_equal(got[k], want[k]), k
