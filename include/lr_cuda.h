@@ -191,6 +191,16 @@ lr_status lr_shard_rows(const int64_t* iptr, int32_t row_begin, int32_t row_end,
  * is computed, then every rank's chunk j is broadcast (root order 0..world-1),
  * the last chunk followed by the all-reduce(max); LR_XCHG_CHUNKS sets
  * `chunks` (default 4). */
+/* The rows of one level's units [unit_begin, unit_end) split over `world`
+ * ranks for its CTA-solved units (world + 1 row bounds over the layout's
+ * iptr / xptr / unit_row_begin / unit_kind): each rank solves the units
+ * starting in its range (singleton groups and grid rows cut anywhere), the
+ * ranges are then broadcast from their owners.  Applied to levels of at least
+ * LR_DIST_MIN_ROWS rows (default 65536) when a communicator is set;
+ * LR_DIST_LEVELS=0 replicates every level. */
+lr_status lr_split_level_rows(const int64_t* iptr, const int64_t* xptr, const int32_t* unit_row_begin,
+                              const uint8_t* unit_kind, int32_t unit_begin, int32_t unit_end, int32_t world,
+                              int32_t* bounds);
 lr_status lr_exchange_cuts(const int64_t* iptr, int32_t row_begin, int32_t row_end, int32_t world, int32_t chunks,
                            int32_t* cuts);
 

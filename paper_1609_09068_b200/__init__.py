@@ -164,6 +164,7 @@ EXPORTS = {
     "lr_ctx_set_comm": (C.c_int, [VP, C.c_int, C.c_int, C.c_char_p]),
     "lr_shard_rows": (C.c_int, [I64P, C.c_int32, C.c_int32, C.c_int32, I32P]),
     "lr_exchange_cuts": (C.c_int, [I64P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, I32P]),
+    "lr_split_level_rows": (C.c_int, [I64P, I64P, I32P, U8P, C.c_int32, C.c_int32, C.c_int32, I32P]),
     "lr_ctx_stream": (VP, [VP]),
     "lr_ctx_device_bytes": (C.c_int64, [VP]),
     "lr_ctx_free": (None, [VP]),
@@ -496,6 +497,19 @@ def shard_rows(iptr, row_begin: int, row_end: int, world: int) -> np.ndarray:
     ip = np.ascontiguousarray(iptr, np.int64)
     out = np.zeros(world + 1, np.int32)
     _check(lib().lr_shard_rows(_p(ip, I64P), int(row_begin), int(row_end), int(world), _p(out, I32P)))
+    return out
+
+
+def split_level_rows(layout: dict, level: int, world: int) -> np.ndarray:
+    """lr_split_level_rows on a Plan.layout(): world + 1 row bounds of one level."""
+    ip = np.ascontiguousarray(layout["iptr"], np.int64)
+    xp = np.ascontiguousarray(layout["xptr"], np.int64)
+    urb = np.ascontiguousarray(layout["unit_row_begin"], np.int32)
+    uk = np.ascontiguousarray(layout["unit_kind"], np.uint8)
+    lub = layout["level_unit_begin"]
+    out = np.zeros(world + 1, np.int32)
+    _check(lib().lr_split_level_rows(_p(ip, I64P), _p(xp, I64P), _p(urb, I32P), _p(uk, U8P), int(lub[level]),
+                                     int(lub[level + 1]), int(world), _p(out, I32P)))
     return out
 
 

@@ -91,6 +91,9 @@ struct LevelTasks {
   int hot_begin = 0;
   long long hot_rows = 0, unit_rows = 0;
   int keep_stream = 0;  // L2 priority of the streamed SpMV operands (spmv.cu policy_stream)
+  // multi-GPU, large levels: rows split over the ranks for the CTA-solved
+  // units (world + 1 bounds; empty = every rank solves the whole level)
+  std::vector<int> dist_bounds;
   // multi-GPU, one grid unit on the level: this rank's blocks per exchange
   // chunk ([chunk_bk[j], chunk_bk[j+1]) relative to the level's blocks)
   std::vector<int> chunk_bk;
@@ -175,6 +178,53 @@ std::vector<int> exchange_cuts(const int64_t* iptr, int rb, int re, int world, i
   return cuts;
 }
 
+// Rows of one level split over `world` ranks for the level's CTA-solved units
+// (multi-GPU, lr_split_level_rows): contiguous row ranges balanced by a cost
+// of rows + cross in-edges + intra in-edges (x32 for units small enough for
+// the CTA power series, whose edges are walked every iteration); singleton
+// groups and grid units are cut anywhere (their rows are independent row
+// tasks), every other unit is kept whole.  world + 1 bounds.
+std::vector<int> split_level_rows(const int64_t* iptr, const int64_t* xptr, const int32_t* unit_row_begin,
+                                  const std::uint8_t* unit_kind, int u0, int u1, int world) {
+  const int rb = unit_row_begin[u0], re = unit_row_begin[u1];
+  std::vector<int> b(static_cast<size_t>(world) + 1, rb);
+  b[static_cast<size_t>(world)] = re;
+  if (world <= 1 || re <= rb) return b;
+  auto cost = [&](int u) {
+    const int a = unit_row_begin[u], e = unit_row_begin[u + 1];
+    const long long intra = iptr[e] - iptr[a];
+    const bool cta_series = unit_kind[u] == 3 && e - a <= kCtaLargeMaxRows && intra <= kCtaLargeMaxNnz;
+    return static_cast<double>(e - a) + static_cast<double>(xptr[e] - xptr[a]) +
+           static_cast<double>(intra) * (cta_series ? 32.0 : 1.0);
+  };
+  double total = 0.0;
+  for (int u = u0; u < u1; ++u) total += cost(u);
+  double acc = 0.0;
+  int q = 1;
+  for (int u = u0; u < u1 && q < world; ++u) {
+    const int a = unit_row_begin[u], e = unit_row_begin[u + 1];
+    const double c = cost(u);
+    const bool divisible = unit_kind[u] == 0 ||
+                           (unit_kind[u] == 3 && !(e - a <= kCtaLargeMaxRows && iptr[e] - iptr[a] <= kCtaLargeMaxNnz));
+    while (q < world && acc + c >= total * q / world) {
+      const double target = total * q / world;
+      int cut = e;
+      if (divisible && e > a) {
+        const double per_row = c / static_cast<double>(e - a);
+        cut = a + static_cast<int>(std::ceil((target - acc) / per_row));
+        cut = std::min(std::max(cut, a), e);
+      } else if (target - acc < acc + c - target) {
+        cut = a;
+      }
+      b[static_cast<size_t>(q)] = std::max(cut, b[static_cast<size_t>(q) - 1]);
+      ++q;
+    }
+    acc += c;
+  }
+  for (; q < world; ++q) b[static_cast<size_t>(q)] = re;
+  return b;
+}
+
 }  // namespace
 
 struct lr_ctx {
@@ -248,6 +298,9 @@ struct lr_ctx {
   // every rank; a chunk's s' rows are broadcast while the next chunk computes
   int xchunks = 1;
   std::vector<std::vector<int>> gu_cuts;
+  bool dist_any = false;                     // some level's CTA units are split over the ranks
+  std::vector<std::uint8_t> h_unit_kind;     // host copies for the report of a split solve
+  std::vector<long long> h_unit_edges;
   cudaStream_t xstream = nullptr;            // NCCL exchange, concurrent with the SpMV chunks
   std::vector<cudaEvent_t> xev;              // chunk j computed (compute stream -> exchange stream)
   cudaEvent_t xdone = nullptr;               // iteration's exchange done (exchange -> compute stream)
@@ -477,6 +530,19 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     ctx->xchunks = std::max(1, std::min(64, e ? std::atoi(e) : 4));
   }
   ctx->cac_slices.clear();
+  // multi-GPU: the CTA-solved units of large levels split over the ranks
+  // (LR_DIST_LEVELS=0 replicates them; LR_DIST_MIN_ROWS sets "large")
+  ctx->dist_any = false;
+  const bool dist_on = ctx->comm && [] {
+    const char* e = std::getenv("LR_DIST_LEVELS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const long long dist_min_rows = [] {
+    const char* e = std::getenv("LR_DIST_MIN_ROWS");
+    return e ? std::atoll(e) : (1ll << 16);
+  }();
+  ctx->h_unit_kind.assign(L->unit_kind, L->unit_kind + L->n_units);
+  ctx->h_unit_edges.assign(L->unit_edges, L->unit_edges + L->n_units);
   int max_small = 0;
   bool small_needs_scratch = false;
   for (int li = 0; li < L->n_levels; ++li) {
@@ -505,6 +571,20 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
     T.gu0 = static_cast<int>(gstate.size());
     T.bk0 = static_cast<int>(blocks.size());
     std::vector<int> pending_chunks;  // exchange chunks of the level's (last) grid unit
+    // this rank's rows of the level's CTA-solved units
+    int my0 = T.rb, my1 = T.re;
+    if (dist_on && T.re - T.rb >= dist_min_rows) {
+      T.dist_bounds = split_level_rows(L->iptr, L->xptr, L->unit_row_begin, L->unit_kind, L->level_unit_begin[li],
+                                       L->level_unit_begin[li + 1], ctx->nshards);
+      my0 = T.dist_bounds[static_cast<size_t>(ctx->shard)];
+      my1 = T.dist_bounds[static_cast<size_t>(ctx->shard) + 1];
+      ctx->dist_any = true;
+    }
+    auto mine = [&](int a) { return a >= my0 && a < my1; };  // a whole unit starting at row a
+    auto clip = [&](int a, int e) {  // this rank's part of a row-divisible range
+      const int c0 = std::max(a, my0), c1 = std::min(e, my1);
+      if (c1 > c0) rowranges[static_cast<size_t>(li)].emplace_back(c0, c1);
+    };
     for (int u = L->level_unit_begin[li]; u < L->level_unit_begin[li + 1]; ++u) {
       const int rb = L->unit_row_begin[u], re = L->unit_row_begin[u + 1];
       const int m = re - rb;
@@ -538,7 +618,8 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           }
         } else {
           // (large CACs gather their own start weights in k_cac_big)
-          (m > kCacMidMaxRows ? lb : m > kCacWarpMaxRows ? lm : lw).push_back(CacTask{rb, re, db, nd, 0});
+          if (m > kCacMidMaxRows) lb.push_back(CacTask{rb, re, db, nd, 0});  // side stream: every rank
+          else if (mine(rb)) (m > kCacWarpMaxRows ? lm : lw).push_back(CacTask{rb, re, db, nd, 0});
         }
       } else if (kind == 2) {
         rk = kSmall;
@@ -547,7 +628,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
         // m: those go to the global-scratch kernel like the large ones
         if (m <= kSmallSmemMaxM && small_unit_smem_bytes(m, ne) <= kSmallSmemCap &&
             static_cast<size_t>(m + 1) * static_cast<size_t>(m + 2) * sizeof(double) <= kSmallSmemCap) {
-          small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
+          if (mine(rb)) small.push_back(SccTask{rb, re, u, 0, L->unit_edges[u]});
           T.sm_tile = std::max(T.sm_tile, small_unit_smem_bytes(m, ne));
           T.sm_max = std::max(T.sm_max, m);
         } else {  // beyond shared memory: global-scratch kernel after the level kernel
@@ -563,13 +644,13 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           rk = kLargeCta;
           int has_heavy = 0;
           for (int r = rb; r < re && !has_heavy; ++r) has_heavy = L->iptr[r + 1] - L->iptr[r] > kCrossLight;
-          lcta.push_back(SccTask{rb, re, u, has_heavy, L->unit_edges[u]});
+          if (mine(rb)) lcta.push_back(SccTask{rb, re, u, has_heavy, L->unit_edges[u]});
           // a multiple of 16 doubles (the 32 banks) above m: same bank map for
           // both pushed vectors, and room for the register path's zero slot
           T.lc_max = std::max(T.lc_max, (m + 2 + 15) & ~15);
         } else {
           rk = kLargeGrid;
-          rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
+          clip(rb, re);  // start values s0 = pf * w of the rows (exchanged after the level)
           const int gu = static_cast<int>(gstate.size());
           const size_t first_block = blocks.size();
           // multi-GPU: this rank owns rows [own0, own1) of the unit (nnz-balanced)
@@ -635,7 +716,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
           gstate.push_back(g);
         }
       }
-      if (kind == 0) rowranges[static_cast<size_t>(li)].emplace_back(rb, re);
+      if (kind == 0) clip(rb, re);
       for (int r = rb; r < re; ++r) rowkind[static_cast<size_t>(r)] = rk;
     }
     T.cac_w0 = static_cast<int>(cac_w.size());
@@ -941,6 +1022,28 @@ static lr_status chunked_iteration(lr_ctx* ctx, const LevelTasks& T, const Devic
   return LR_OK;
 }
 
+// A level whose CTA-solved units are split over the ranks: each rank's row
+// range (its units' ranks, and the start values s0 of grid rows) broadcast to
+// every rank -- grouped in-place broadcasts, an all-gather with uneven parts.
+// Rows in the range that every rank computed (large CACs, global-scratch small
+// SCCs, CAC slices) carry the same values everywhere, so overwriting them is
+// harmless.
+static lr_status exchange_level(lr_ctx* ctx, const LevelTasks& T) {
+  const NcclApi& nc = nccl();
+  LR_NCCL_TRY(nc.group_start());
+  for (int q = 0; q < ctx->nshards; ++q) {
+    const int r0 = T.dist_bounds[static_cast<size_t>(q)], r1 = T.dist_bounds[static_cast<size_t>(q) + 1];
+    if (r1 <= r0) continue;
+    LR_NCCL_TRY(nc.broadcast(ctx->rank.p + r0, ctx->rank.p + r0, static_cast<size_t>(r1 - r0), ncclDouble, q,
+                             ctx->comm, ctx->stream));
+    if (T.gu1 > T.gu0)
+      LR_NCCL_TRY(nc.broadcast(ctx->s0.p + r0, ctx->s0.p + r0, static_cast<size_t>(r1 - r0), ncclDouble, q, ctx->comm,
+                               ctx->stream));
+  }
+  LR_NCCL_TRY(nc.group_end());
+  return LR_OK;
+}
+
 static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, double tol, double* r3_dev,
                                  double* r1_dev, lr_solve_info* info, int64_t* unit_iters) {
   const lr_status pv = lr_validate_params(c, tol);
@@ -1095,13 +1198,16 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     return LR_OK;
   };
   if (use_graphs && !ctx->segs_built) {
+    // a level with a grid SpMV or with an exchange of split units is enqueued
+    // directly every solve; runs of the others are captured
+    auto capturable = [&](size_t q) { return ctx->lt[q].gu1 == ctx->lt[q].gu0 && ctx->lt[q].dist_bounds.empty(); };
     for (size_t li = 0; li < ctx->lt.size();) {
-      if (ctx->lt[li].gu1 > ctx->lt[li].gu0) {
+      if (!capturable(li)) {
         ++li;
         continue;
       }
       size_t lj = li;
-      while (lj < ctx->lt.size() && ctx->lt[lj].gu1 == ctx->lt[lj].gu0) ++lj;
+      while (lj < ctx->lt.size() && capturable(lj)) ++lj;
       lr_ctx::Segment seg{static_cast<int>(li), static_cast<int>(lj), 0, nullptr};
       LR_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       lr_status cst = LR_OK;
@@ -1129,6 +1235,8 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     }
     const LevelTasks& T = ctx->lt[li];
     if (const lr_status ls = static_level(T, launches); ls != LR_OK) return ls;
+    if (!T.dist_bounds.empty())  // every rank's rows of the split units to every rank
+      if (const lr_status xs = exchange_level(ctx, T); xs != LR_OK) return xs;
     if (T.gu1 > T.gu0) {
       launch_grid_reset(ctx->gstate.p + T.gu0, T.gu1 - T.gu0, ctx->status.p, s);
       ++launches;
@@ -1235,10 +1343,37 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       std::fprintf(stderr, "  %-10s ctas %8lld  sum of per-level max %9.1f us  critical in levels: %9.1f us\n",
                    names[ty], prof_cnt[ty], prof_max[ty], prof_crit[ty]);
   }
+  if (ctx->dist_any) {
+    // split units' iteration counts live on their owners (others hold 0; grid
+    // units the same value everywhere), errors on whichever rank saw them
+    const NcclApi& nc = nccl();
+    LR_NCCL_TRY(nc.group_start());
+    if (ctx->n_units > 0)
+      LR_NCCL_TRY(nc.all_reduce(ctx->unit_iters.p, ctx->unit_iters.p, static_cast<size_t>(ctx->n_units), ncclInt64,
+                                ncclMax, ctx->comm, s));
+    LR_NCCL_TRY(nc.all_reduce(&ctx->status.p->err, &ctx->status.p->err, 1, ncclUint32, ncclMax, ctx->comm, s));
+    LR_NCCL_TRY(nc.group_end());
+  }
   LR_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-  if (unit_iters && ctx->n_units > 0)
-    LR_CUDA_TRY(cudaMemcpyAsync(unit_iters, ctx->unit_iters.p, ctx->unit_iters.bytes(), cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> dist_iters;
+  int64_t* iters_out = unit_iters;
+  if (ctx->dist_any && ctx->n_units > 0 && !iters_out) {
+    dist_iters.resize(static_cast<size_t>(ctx->n_units));
+    iters_out = dist_iters.data();
+  }
+  if (iters_out && ctx->n_units > 0)
+    LR_CUDA_TRY(cudaMemcpyAsync(iters_out, ctx->unit_iters.p, ctx->unit_iters.bytes(), cudaMemcpyDeviceToHost, s));
   LR_CUDA_TRY(cudaStreamSynchronize(s));
+  if (ctx->dist_any) {  // the power-series totals from the reduced per-unit counts
+    DevStatus& hs = *ctx->h_status;
+    hs.total_iterations = 0;
+    hs.iterative_edge_work = 0;
+    for (int64_t u = 0; u < ctx->n_units; ++u)
+      if (ctx->h_unit_kind[static_cast<size_t>(u)] == 3) {
+        hs.total_iterations += iters_out[u];
+        hs.iterative_edge_work += iters_out[u] * ctx->h_unit_edges[static_cast<size_t>(u)];
+      }
+  }
   float dev_ms = 0.f;
   cudaEventElapsedTime(&dev_ms, ctx->ev[0], ctx->ev[1]);
   ctx->launches += launches;
@@ -1338,6 +1473,18 @@ lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* id128) {
   ctx->shard = rank;
   ctx->nshards = world;
   ctx->loaded = false;  // the next upload shards the grid units
+  return LR_OK;
+}
+
+lr_status lr_split_level_rows(const int64_t* iptr, const int64_t* xptr, const int32_t* unit_row_begin,
+                              const uint8_t* unit_kind, int32_t unit_begin, int32_t unit_end, int32_t world,
+                              int32_t* bounds) {
+  if (!iptr || !xptr || !unit_row_begin || !unit_kind || !bounds || world < 1 || unit_end < unit_begin) {
+    lrerr::set("bad level split request");
+    return LR_EINVAL;
+  }
+  const std::vector<int> b = split_level_rows(iptr, xptr, unit_row_begin, unit_kind, unit_begin, unit_end, world);
+  std::copy(b.begin(), b.end(), bounds);
   return LR_OK;
 }
 

@@ -124,3 +124,22 @@ def test_graph_replay_with_new_weights_and_params(lr, oracle):
         finally:
             os.environ.pop("LR_GRAPHS", None)
         assert np.array_equal(r3n, r3) and np.array_equal(r1n, r1), trial
+
+
+@pytest.mark.parametrize("cfg,shrink", [(3, 6), (1, 2), (4, 5)])
+def test_split_levels_single_rank(lr, monkeypatch, cfg, shrink):
+    """Levels whose CTA-solved units are split over the ranks (every level here:
+    LR_DIST_MIN_ROWS=0), on a one-rank communicator: the owner-only task lists,
+    the per-level range broadcasts and the reduced iteration counts reproduce
+    the replicated solve bit for bit."""
+    monkeypatch.setenv("LR_XCHG_CHUNKS", "1")
+    monkeypatch.setenv("LR_DIST_MIN_ROWS", "0")
+    g = lr.config_graph(cfg, shrink)
+    w = np.full(g.n, 1.0 / g.n)
+    r3a, r1a, ia, ita = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
+    eng = lr.Engine(g, rank=0, world=1, nccl_id=lr.nccl_unique_id())
+    r3b, r1b, ib, itb = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(ita, itb)
+    assert np.array_equal(r3a, r3b) and np.array_equal(r1a, r1b)
+    assert ia["total_iterations"] == ib["total_iterations"]
+    assert ia["iterative_edge_work"] == ib["iterative_edge_work"]

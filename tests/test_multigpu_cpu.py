@@ -1,6 +1,9 @@
 """The multi-GPU path's host logic on CPU (gloo, world size 2).
 
-The sharded solve in csrc/cuda/ctx.cu splits every grid SccLarge unit into
+Per level the rows of the CTA-solved units are split over the ranks
+(lr_split_level_rows), each rank solving its range, and the ranges are
+broadcast from their owners (exchange_level).  The sharded solve in
+csrc/cuda/ctx.cu splits every grid SccLarge unit into
 nnz-balanced row shards, each cut into exchange chunks (lr_exchange_cuts);
 per iteration it computes chunk j of its own rows and broadcasts every rank's
 chunk j (roots in rank order) while the next chunk computes, all-reduces the
@@ -44,7 +47,12 @@ def _emulate_sharded(L, w, c, tol, cap, rank, world, dist, lr):
         kind_of_row = np.zeros(re - rb, np.int64)
         for u in range(L["level_unit_begin"][li], L["level_unit_begin"][li + 1]):
             kind_of_row[urb[u] - rb:urb[u + 1] - rb] = kinds[u]
-        for r in range(rb, re):  # replicated on every rank
+        # the level's rows split over the ranks (lr_split_level_rows, as the
+        # device does with LR_DIST_MIN_ROWS=0): each rank computes the start
+        # weights and solves the one-pass units of its range ...
+        split = lr.split_level_rows(L, li, world)
+        my0, my1 = int(split[rank]), int(split[rank + 1])
+        for r in range(my0, my1):
             acc = w[vert[r]]
             for e in range(L["xptr"][r], L["xptr"][r + 1]):
                 s = L["xsrc"][e]
@@ -54,6 +62,8 @@ def _emulate_sharded(L, w, c, tol, cap, rank, world, dist, lr):
             rankv[r] = acc
         for u in range(L["level_unit_begin"][li], L["level_unit_begin"][li + 1]):
             a, b = urb[u], urb[u + 1]
+            if kinds[u] == 1 and not my0 <= a < my1:
+                continue
             if kinds[u] == 1:
                 dp = L["depth_ptr"][L["cac_depth_begin"][u]:]
                 d = 0
@@ -68,6 +78,15 @@ def _emulate_sharded(L, w, c, tol, cap, rank, world, dist, lr):
                         rankv[r] = acc
                     d += 1
                 continue
+        # ... then every range is broadcast from its owner (ctx.cu exchange_level)
+        for q in range(world):
+            q0, q1 = int(split[q]), int(split[q + 1])
+            if q1 > q0:
+                t = torch.from_numpy(rankv[q0:q1].copy())
+                dist.broadcast(t, src=q)
+                rankv[q0:q1] = t.numpy()
+        for u in range(L["level_unit_begin"][li], L["level_unit_begin"][li + 1]):
+            a, b = urb[u], urb[u + 1]
             if kinds[u] != 3:
                 continue
             # sharded power series of one SccLarge unit, on the library's own
