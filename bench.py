@@ -486,8 +486,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args.config, args.shrink, n, g.m),
-            "parallelism": (f"giant-SCC rows sharded over {world} GPUs (NCCL exchange per iteration), "
-                            "other units replicated") if world > 1 else "1 GPU",
+            "parallelism": (f"giant-SCC rows sharded over {world} GPUs (chunked NCCL exchange per iteration), "
+                            "large levels' other units split over the GPUs") if world > 1 else "1 GPU",
             "workload_stats": {"edge_updates_per_step": work, "iterative_edge_work": int(info0["iterative_edge_work"]),
                                "large_scc_iterations": int(iters[large].max()) if large.any() else 0,
                                "levels": n_levels, "units": n_units},
