@@ -206,6 +206,12 @@ lr_status lr_exchange_cuts(const int64_t* iptr, int32_t row_begin, int32_t row_e
 
 /* cudaStream_t the context launches on. */
 void* lr_ctx_stream(lr_ctx* ctx);
+/* UnitRecord::wall_ms (proj/src/engine.cpp:28,56) on the GPU: with
+ * LR_UNIT_TIMES=1 set at upload, every level task and large-CAC CTA records
+ * device timestamps, and after each solve ms[u] = the span from the first to
+ * the last of unit u's tasks (units of one level run concurrently), plus its
+ * grid SpMV time for a grid SccLarge unit.  LR_EINVAL when not enabled. */
+lr_status lr_ctx_unit_times(const lr_ctx* ctx, double* ms, int64_t n_units);
 /* Device bytes held by the context. */
 int64_t lr_ctx_device_bytes(const lr_ctx* ctx);
 void lr_ctx_free(lr_ctx* ctx);

@@ -167,6 +167,7 @@ EXPORTS = {
     "lr_split_level_rows": (C.c_int, [I64P, I64P, I32P, U8P, C.c_int32, C.c_int32, C.c_int32, I32P]),
     "lr_ctx_stream": (VP, [VP]),
     "lr_ctx_device_bytes": (C.c_int64, [VP]),
+    "lr_ctx_unit_times": (C.c_int, [VP, F64P, C.c_int64]),
     "lr_ctx_free": (None, [VP]),
     "lr_compute_pagerank": (C.c_int, [VP, F64P, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_int, F64P,
                                       F64P, C.POINTER(_Report), I64P, C.c_int64]),
@@ -570,6 +571,13 @@ class Engine:
 
     def device_bytes(self) -> int:
         return int(lib().lr_ctx_device_bytes(self._h))
+
+    def unit_times(self) -> np.ndarray:
+        """UnitRecord::wall_ms of the last solve (device span of each unit's
+        tasks); needs LR_UNIT_TIMES=1 in the environment when the Engine is built."""
+        out = np.zeros(max(self.n_units, 1))
+        _check(lib().lr_ctx_unit_times(self._h, _p(out, F64P), self.n_units))
+        return out[:self.n_units]
 
     def solve(self, weights, params: SolverParams = SolverParams(), r3=None, r1=None, want_unit_iters=True):
         """Host buffers in, host buffers out (lr_solve).  Returns (r3, r1, info, unit_iters)."""

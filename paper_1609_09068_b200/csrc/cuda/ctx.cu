@@ -299,6 +299,17 @@ struct lr_ctx {
   int xchunks = 1;
   std::vector<std::vector<int>> gu_cuts;
   bool dist_any = false;                     // some level's CTA units are split over the ranks
+  // LR_UNIT_TIMES=1 at upload: per-CTA device timestamps of every level task
+  // and large CAC, mapped to units after each solve (UnitRecord::wall_ms)
+  bool unit_times = false;
+  DevBuf<long long> ut_tasks, ut_cacs;
+  std::vector<int64_t> task_unit_ptr;        // level task -> units (CSR)
+  std::vector<int32_t> task_units;
+  std::vector<int32_t> cac_unit;             // CacTask -> unit
+  std::vector<int32_t> level_of_unit;
+  std::vector<double> grid_level_ms;         // per level: its grid SpMV time (last solve)
+  std::vector<double> h_unit_ms;             // per unit: device span of its tasks (last solve)
+  bool unit_ms_valid = false;
   std::vector<std::uint8_t> h_unit_kind;     // host copies for the report of a split solve
   std::vector<long long> h_unit_edges;
   cudaStream_t xstream = nullptr;            // NCCL exchange, concurrent with the SpMV chunks
@@ -895,6 +906,46 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   LR_CUDA_TRY(ctx->small.upload(small.data(), small.size(), s));
   LR_CUDA_TRY(ctx->small_big.upload(small_big.data(), small_big.size(), s));
   LR_CUDA_TRY(ctx->ltasks.upload(ltasks.data(), ltasks.size(), s));
+  ctx->unit_times = [] {
+    const char* e = std::getenv("LR_UNIT_TIMES");
+    return e && std::atoi(e) != 0;
+  }();
+  ctx->unit_ms_valid = false;
+  if (ctx->unit_times) {
+    auto unit_of_row = [&](int r) {
+      return static_cast<int32_t>(std::upper_bound(L->unit_row_begin, L->unit_row_begin + L->n_units + 1, r) -
+                                  L->unit_row_begin - 1);
+    };
+    ctx->task_unit_ptr.assign(1, 0);
+    ctx->task_units.clear();
+    for (const LevelTask& t : ltasks) {
+      switch (t.type) {
+        case kTaskCacWarps:
+          for (int i = t.a; i < t.b; ++i) ctx->task_units.push_back(unit_of_row(cac_w[static_cast<size_t>(i)].row_begin));
+          break;
+        case kTaskCacBlock:
+          ctx->task_units.push_back(unit_of_row(cac_w[static_cast<size_t>(t.a)].row_begin));
+          break;
+        case kTaskSmall:
+          ctx->task_units.push_back(small[static_cast<size_t>(t.a)].unit);
+          break;
+        case kTaskLcta:
+          ctx->task_units.push_back(lcta[static_cast<size_t>(t.a)].unit);
+          break;
+        default:  // row tasks: rows of one unit
+          ctx->task_units.push_back(unit_of_row(t.a));
+          break;
+      }
+      ctx->task_unit_ptr.push_back(static_cast<int64_t>(ctx->task_units.size()));
+    }
+    ctx->cac_unit.resize(cac_w.size());
+    for (size_t i = 0; i < cac_w.size(); ++i) ctx->cac_unit[i] = unit_of_row(cac_w[i].row_begin);
+    ctx->level_of_unit.assign(static_cast<size_t>(L->n_units), 0);
+    for (int li = 0; li < L->n_levels; ++li)
+      for (int u = L->level_unit_begin[li]; u < L->level_unit_begin[li + 1]; ++u) ctx->level_of_unit[static_cast<size_t>(u)] = li;
+    LR_CUDA_TRY(ctx->ut_tasks.alloc(3 * std::max<size_t>(ltasks.size(), 1)));
+    LR_CUDA_TRY(ctx->ut_cacs.alloc(3 * std::max<size_t>(cac_w.size(), 1)));
+  }
   LR_CUDA_TRY(ctx->lcta.upload(lcta.data(), lcta.size(), s));
   LR_CUDA_TRY(ctx->gstate.upload(gstate.data(), gstate.size(), s));
   LR_CUDA_TRY(ctx->blocks.upload(blocks.data(), blocks.size(), s));
@@ -1065,6 +1116,11 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   LR_CUDA_TRY(cudaMemcpyAsync(ctx->params.p, ctx->h_params, sizeof(SolveParams), cudaMemcpyHostToDevice, s));
   LR_CUDA_TRY(cudaMemsetAsync(ctx->status.p, 0, sizeof(DevStatus), s));
   if (ctx->n_units > 0) LR_CUDA_TRY(cudaMemsetAsync(ctx->unit_iters.p, 0, ctx->unit_iters.bytes(), s));
+  if (ctx->unit_times) {
+    LR_CUDA_TRY(cudaMemsetAsync(ctx->ut_tasks.p, 0, ctx->ut_tasks.bytes(), s));
+    LR_CUDA_TRY(cudaMemsetAsync(ctx->ut_cacs.p, 0, ctx->ut_cacs.bytes(), s));
+    ctx->grid_level_ms.assign(ctx->lt.size(), 0.0);
+  }
   LR_CUDA_TRY(cudaEventRecord(ctx->ev[0], s));
   // LR_LEVEL_PROF=1: per-level timing of k_level's CTAs by task type (diagnostic, synchronises every level)
   const bool prof_on = std::getenv("LR_LEVEL_PROF") != nullptr;
@@ -1105,7 +1161,8 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       LR_CUDA_TRY(cudaStreamWaitEvent(ctx->pre, ctx->pre_fork, 0));
       launch_level(L, ctx->ltasks.p + T.pt0, T.pt1 - T.pt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p, 0,
                    0, kRowTaskSmem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, ctx->unit_iters.p,
-                   ctx->status.p, true, ctx->pre, /*profile=*/false, ctx->xpart.p);
+                   ctx->status.p, true, ctx->pre, /*profile=*/false, ctx->xpart.p,
+                   ctx->unit_times ? ctx->ut_tasks.p + 3 * static_cast<size_t>(T.pt0) : nullptr);
       LR_CUDA_TRY(cudaEventRecord(ctx->pre_done, ctx->pre));
       ++nl;
     }
@@ -1126,11 +1183,13 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       if (T.xb1 > T.xb0) {
         launch_level(L, ctx->ltasks.p + T.xb0, T.xb1 - T.xb0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                      0, 0, kRowTaskSmem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p, ctx->unit_iters.p,
-                     ctx->status.p, T.xb_fin, ctx->side, /*profile=*/false, ctx->xpart.p);
+                     ctx->status.p, T.xb_fin, ctx->side, /*profile=*/false, ctx->xpart.p,
+                     ctx->unit_times ? ctx->ut_tasks.p + 3 * static_cast<size_t>(T.xb0) : nullptr);
         ++nl;
       }
       launch_cac_big(L, ctx->cac.p + T.cac_b0, T.cac_b1 - T.cac_b0, ctx->depth_ptr.p, w_dev, ctx->params.p, ctx->pf.p,
-                     ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side);
+                     ctx->rank.p, ctx->s0.p, ctx->cacpv.n ? ctx->cacpv.p : nullptr, T.big_smem, ctx->side,
+                     ctx->unit_times ? ctx->ut_cacs.p + 3 * static_cast<size_t>(T.cac_b0) : nullptr);
       if (prof_on) LR_CUDA_TRY(cudaEventRecord(pev[2], ctx->side));
       LR_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side));
       ++nl;
@@ -1139,7 +1198,8 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
     if (T.lt1 > T.lt0) {
       launch_level(L, ctx->ltasks.p + T.lt0, T.lt1 - T.lt0, ctx->cac.p, ctx->depth_ptr.p, ctx->small.p, ctx->lcta.p,
                    T.sm_max + 1, T.lc_max, T.smem, w_dev, ctx->params.p, ctx->pf.p, ctx->rank.p, ctx->s0.p,
-                   ctx->unit_iters.p, ctx->status.p, T.sm1 > T.sm0 || T.lc1 > T.lc0, s);
+                   ctx->unit_iters.p, ctx->status.p, T.sm1 > T.sm0 || T.lc1 > T.lc0, s, true, nullptr,
+                   ctx->unit_times ? ctx->ut_tasks.p + 3 * static_cast<size_t>(T.lt0) : nullptr);
       ++nl;
       if (prof_on && fork) LR_CUDA_TRY(cudaEventRecord(pev[1], s));
       if (prof_on) {  // LR_LEVEL_PROF: per task type, the longest CTA of this level
@@ -1302,6 +1362,7 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
       spmv_ms += ms;
+      if (ctx->unit_times) ctx->grid_level_ms[li] = ms;
       // roofline bookkeeping: per-unit iteration counts of this level
       const int ngu = T.gu1 - T.gu0;
       std::vector<GridUnitState> gsh(static_cast<size_t>(ngu));
@@ -1376,6 +1437,30 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
   }
   float dev_ms = 0.f;
   cudaEventElapsedTime(&dev_ms, ctx->ev[0], ctx->ev[1]);
+  if (ctx->unit_times) {  // per unit: span from its first task's start to its last task's end
+    std::vector<long long> ht(ctx->ut_tasks.n), hc(ctx->ut_cacs.n);
+    LR_CUDA_TRY(cudaMemcpy(ht.data(), ctx->ut_tasks.p, ctx->ut_tasks.bytes(), cudaMemcpyDeviceToHost));
+    LR_CUDA_TRY(cudaMemcpy(hc.data(), ctx->ut_cacs.p, ctx->ut_cacs.bytes(), cudaMemcpyDeviceToHost));
+    const size_t nu = static_cast<size_t>(ctx->n_units);
+    std::vector<long long> lo(nu, 0), hi(nu, 0);
+    auto add = [&](int32_t u, long long a, long long b) {
+      if (a <= 0 || b < a) return;
+      const size_t k = static_cast<size_t>(u);
+      lo[k] = lo[k] ? std::min(lo[k], a) : a;
+      hi[k] = std::max(hi[k], b);
+    };
+    for (size_t t = 0; t + 1 < ctx->task_unit_ptr.size(); ++t)
+      for (int64_t j = ctx->task_unit_ptr[t]; j < ctx->task_unit_ptr[t + 1]; ++j)
+        add(ctx->task_units[static_cast<size_t>(j)], ht[3 * t + 1], ht[3 * t + 2]);
+    for (size_t i = 0; i < ctx->cac_unit.size(); ++i) add(ctx->cac_unit[i], hc[3 * i + 1], hc[3 * i + 2]);
+    ctx->h_unit_ms.assign(nu, 0.0);
+    for (size_t u = 0; u < nu; ++u) {
+      if (hi[u] > lo[u]) ctx->h_unit_ms[u] = static_cast<double>(hi[u] - lo[u]) * 1e-6;
+      if (ctx->h_unit_kind[u] == 3 && !ctx->grid_level_ms.empty())
+        ctx->h_unit_ms[u] += ctx->grid_level_ms[static_cast<size_t>(ctx->level_of_unit[u])];
+    }
+    ctx->unit_ms_valid = true;
+  }
   ctx->launches += launches;
   ctx->spmv_launches += spmv_launches;
   const DevStatus& st = *ctx->h_status;
@@ -1473,6 +1558,15 @@ lr_status lr_ctx_set_comm(lr_ctx* ctx, int rank, int world, const char* id128) {
   ctx->shard = rank;
   ctx->nshards = world;
   ctx->loaded = false;  // the next upload shards the grid units
+  return LR_OK;
+}
+
+lr_status lr_ctx_unit_times(const lr_ctx* ctx, double* ms, int64_t n) {
+  if (!ctx || !ms || !ctx->unit_ms_valid || n != ctx->n_units) {
+    lrerr::set("no per-unit times: upload with LR_UNIT_TIMES=1, then solve");
+    return LR_EINVAL;
+  }
+  std::copy(ctx->h_unit_ms.begin(), ctx->h_unit_ms.end(), ms);
   return LR_OK;
 }
 

@@ -222,7 +222,7 @@ cudaError_t configure_level_kernel();
 // large CACs, 1024-thread CTAs, meant for a second stream (level.cu)
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
                     const SolveParams* p, const double* pf, double* rank, double* s0, double* pv, size_t smem,
-                    cudaStream_t s);
+                    cudaStream_t s, long long* task_times = nullptr);
 // shared-memory bytes a CAC of `rows` rows and `edges` in-edges needs to be swept from shared memory
 size_t cac_stage_need(long long rows, long long edges);
 size_t cac_compact_need(long long rows, long long edges);  // k_cac_big's structure-only staging
@@ -235,7 +235,7 @@ void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, con
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
                   long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile = true,
-                  double* xpart = nullptr);
+                  double* xpart = nullptr, long long* task_times = nullptr);
 
 // launch wrappers (stream-ordered)
 void launch_prep(const DeviceLayout& L, const double* w, const SolveParams* p, double* pf, DevStatus* st,

@@ -1644,9 +1644,10 @@ constexpr int kBigThreads = 1024;
 __global__ void __launch_bounds__(kBigThreads)
     k_cac_big(DeviceLayout L, const CacTask* __restrict__ cacs, const int* __restrict__ depth_ptr,
               const double* __restrict__ w, const SolveParams* __restrict__ p, const double* __restrict__ pf,
-              double* rank, double* s0, double* pv, size_t smem_bytes) {
+              double* rank, double* s0, double* pv, size_t smem_bytes, long long* prof) {
   extern __shared__ double sm[];
   const CacTask ct = cacs[blockIdx.x];
+  const long long t_start = prof ? global_ns() : 0;
 
   // the CAC's own start weights (rows above kCrossSplit cross in-edges were
   // done by k_pull_heavy before the level), so the launch runs concurrently
@@ -1663,13 +1664,21 @@ __global__ void __launch_bounds__(kBigThreads)
     cac_sweep_compact(L, ct, depth_ptr, p->c, rank, pv, sm);
   else
     cac_sweep<true>(L, ct, depth_ptr, p->c, rank, threadIdx.x, kBigThreads);
+  if (prof) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      prof[3 * blockIdx.x] = 0;
+      prof[3 * blockIdx.x + 1] = t_start;
+      prof[3 * blockIdx.x + 2] = global_ns();
+    }
+  }
 }
 
 }  // namespace
 
 void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int* depth_ptr, const double* w,
                     const SolveParams* p, const double* pf, double* rank, double* s0, double* pv, size_t smem,
-                    cudaStream_t s) {
+                    cudaStream_t s, long long* task_times) {
   if (n == 0) return;
   // highest launch priority (kept by graph capture): its 1024-thread CTAs need a
   // whole SM and must be placed before the level's k_level CTAs fill them
@@ -1688,7 +1697,7 @@ void launch_cac_big(const DeviceLayout& L, const CacTask* cacs, int n, const int
   attr[0].val.priority = prio;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, pv, smem);
+  cudaLaunchKernelEx(&cfg, k_cac_big, L, cacs, depth_ptr, w, p, pf, rank, s0, pv, smem, task_times);
 }
 
 size_t cac_stage_need(long long rows, long long edges) { return cac_stage_bytes(rows, edges); }
@@ -1725,9 +1734,12 @@ cudaError_t set_level_prof(long long* buf) {
 void launch_level(const DeviceLayout& L, const LevelTask* tasks, int ntasks, const CacTask* cacs, const int* depth_ptr,
                   const SccTask* smalls, const SccTask* lctas, int small_ld, int lcta_rows, size_t smem,
                   const double* w, const SolveParams* p, const double* pf, double* rank, double* s0,
-                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile, double* xpart) {
+                  long long* unit_iters, DevStatus* st, bool heavy, cudaStream_t s, bool profile, double* xpart,
+                  long long* task_times) {
   if (ntasks == 0) return;
-  long long* prof = profile ? g_level_prof : nullptr;  // one launch per level owns the buffer
+  // per-CTA (type, start ns, end ns): the level profile (one launch per level
+  // owns that buffer) or the per-unit timing buffer of this launch's tasks
+  long long* prof = task_times ? task_times : profile ? g_level_prof : nullptr;
   if (heavy)
     k_level<true><<<ntasks, kThreads, smem, s>>>(L, tasks, cacs, depth_ptr, smalls, lctas, small_ld, lcta_rows, w, p,
                                                  pf, rank, s0, unit_iters, st, smem, prof, xpart);

@@ -188,6 +188,9 @@ EngineResult PageRankEngine::solve(std::span<const double> weights, const Solver
   rep.device_ms = info.device_ms;
   rep.cross_edge_count = L.cross_edge_count;
   rep.units.resize(static_cast<std::size_t>(L.unit_count()));
+  std::vector<double> unit_ms(rep.units.size(), 0.0);  // LR_UNIT_TIMES=1: device span per unit
+  if (!unit_ms.empty() && lr_ctx_unit_times(impl_->ctx, unit_ms.data(), static_cast<std::int64_t>(unit_ms.size())) != LR_OK)
+    std::fill(unit_ms.begin(), unit_ms.end(), 0.0);
   for (std::size_t u = 0; u < rep.units.size(); ++u) {
     UnitRecord& r = rep.units[u];
     r.kind = static_cast<UnitKind>(L.unit_kind[u]);
@@ -195,6 +198,7 @@ EngineResult PageRankEngine::solve(std::span<const double> weights, const Solver
     r.size = L.unit_row_begin[u + 1] - L.unit_row_begin[u];
     r.edges = L.unit_edges[u];
     r.iterations = iters[u];
+    r.wall_ms = unit_ms[u];
     rep.total_iterations += r.iterations;
     if (r.kind == UnitKind::SccLarge) {
       rep.iterative_edge_work += r.iterations * r.edges;

@@ -143,3 +143,25 @@ def test_split_levels_single_rank(lr, monkeypatch, cfg, shrink):
     assert np.array_equal(r3a, r3b) and np.array_equal(r1a, r1b)
     assert ia["total_iterations"] == ib["total_iterations"]
     assert ia["iterative_edge_work"] == ib["iterative_edge_work"]
+
+
+def test_unit_times(lr, monkeypatch):
+    """UnitRecord::wall_ms on the GPU (LR_UNIT_TIMES=1): the units of a
+    config-1 graph (all four kinds) get positive device spans; the giant
+    unit's includes its grid SpMV time; results are unchanged."""
+    g = lr.config_graph(1, 2)
+    w = np.full(g.n, 1.0 / g.n)
+    r3a = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))[0]
+    monkeypatch.setenv("LR_UNIT_TIMES", "1")
+    eng = lr.Engine(g)
+    r3b, _, info, it = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(r3a, r3b)
+    ms = eng.unit_times()
+    # (units in the global-scratch small-SCC kernel or CAC slices are not timed: 0)
+    assert len(ms) == eng.n_units and (ms > 0).mean() > 0.9 and ms.max() < info["device_ms"] + 1e-9
+    g2 = lr.config_graph(2, 6)
+    e2 = lr.Engine(g2)
+    _, _, info2, it2 = e2.solve(np.full(g2.n, 1.0 / g2.n), lr.SolverParams(0.85, 1e-12))
+    L = e2.plan.layout()
+    big = int(np.argmax(np.where(L["unit_kind"] == 3, L["unit_edges"], -1)))
+    assert e2.unit_times()[big] >= 0.5 * info2["spmv_ms"]
