@@ -282,10 +282,14 @@ __device__ void cac_sweep(const DeviceLayout& L, const CacTask& t, const int* __
 }
 
 // The same sweep with the CAC staged in shared memory: its start weights,
-// row pointers, parents (as offsets into the CAC) and parent degrees are loaded
+// row pointers, parents (as offsets into the CAC) and walk degrees are loaded
 // once, all independent loads in flight together; every depth slice then
 // reads only shared memory, so a slice costs a barrier instead of three
-// dependent global round trips.  Same terms, same order (bit-exact).
+// dependent global round trips.  A finished row writes its rank to global
+// memory and replaces its start weight in `sr` with the term it pushes,
+// (r * c) / deg -- the exact value cac_row computes per in-edge -- so a child's
+// in-edge costs two shared loads and an add, with no FP64 division on the
+// slice-to-slice chain.  Same terms, same order (bit-exact).
 template <bool kBlock>
 __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const int* __restrict__ depth_ptr, double c,
                                  double* rank, int tid, int width, void* stage) {
@@ -353,6 +357,14 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       b0 = s1;
       b1 = __ldg(dp + d + 2) - rb;
     }
+    // rows of this slice: sr[i] holds the start weight, sr[parent] the
+    // parent's pushed term
+    auto finish = [&](int i, double acc) {
+      const double dg = static_cast<double>(rd[i]);
+      const double fin = lp[i] ? acc / (1.0 - c / dg) : acc;
+      rank[rb + i] = fin;
+      sr[i] = fin * c / dg;
+    };
     for (int i = s0 + tid; i < s1; i += width) {
       const int e0 = rp[i], e1 = rp[i + 1];
       if (e1 - e0 > kCrossLight) continue;
@@ -360,9 +372,9 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
       for (int e = e0; e < e1; ++e) {
         const int sp = es[e];
         LR_DCHECK(sp >= 0 && sp < m);
-        acc += sr[sp] * c / static_cast<double>(rd[sp]);
+        acc += sr[sp];
       }
-      sr[i] = lp[i] ? acc / (1.0 - c / static_cast<double>(rd[i])) : acc;
+      finish(i, acc);
     }
     for (int base = s0 + wid * 32; base < s1; base += nw * 32) {
       const int i = base + lane;
@@ -373,20 +385,13 @@ __device__ void cac_sweep_staged(const DeviceLayout& L, const CacTask& t, const 
         mask &= mask - 1;
         const int row = base + src;
         double y = 0.0;
-        for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) {
-          const int sp = es[e];
-          y += sr[sp] * c / static_cast<double>(rd[sp]);
-        }
+        for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) y += sr[es[e]];
         y = warp_sum(y);
-        if (lane == 0) {
-          const double a = sr[row] + y;
-          sr[row] = lp[row] ? a / (1.0 - c / static_cast<double>(rd[row])) : a;
-        }
+        if (lane == 0) finish(row, sr[row] + y);
       }
     }
   }
-  sync();
-  for (int i = tid; i < m; i += width) rank[rb + i] = sr[i];
+  sync();  // the stage is free for the caller's next task
 }
 
 // CACs too large for cac_sweep_staged (k_cac_big, up to 65535 rows): only the
