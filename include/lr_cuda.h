@@ -214,6 +214,10 @@ void* lr_ctx_stream(lr_ctx* ctx);
 lr_status lr_ctx_unit_times(const lr_ctx* ctx, double* ms, int64_t n_units);
 /* Device bytes held by the context. */
 int64_t lr_ctx_device_bytes(const lr_ctx* ctx);
+/* Levels whose grid power series runs as K5 (k_spmv_blk: dest-row blocks,
+   source-sorted in-edges, built at upload); no reference counterpart -- an
+   introspection hook for tests and the bench. */
+int32_t lr_ctx_blk_units(const lr_ctx* ctx);
 void lr_ctx_free(lr_ctx* ctx);
 
 /* ------------------------------------------------- one-call drop-in */

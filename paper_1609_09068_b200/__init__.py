@@ -167,6 +167,7 @@ EXPORTS = {
     "lr_split_level_rows": (C.c_int, [I64P, I64P, I32P, U8P, C.c_int32, C.c_int32, C.c_int32, I32P]),
     "lr_ctx_stream": (VP, [VP]),
     "lr_ctx_device_bytes": (C.c_int64, [VP]),
+    "lr_ctx_blk_units": (C.c_int32, [VP]),
     "lr_ctx_unit_times": (C.c_int, [VP, F64P, C.c_int64]),
     "lr_ctx_free": (None, [VP]),
     "lr_compute_pagerank": (C.c_int, [VP, F64P, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_int, F64P,
@@ -571,6 +572,10 @@ class Engine:
 
     def device_bytes(self) -> int:
         return int(lib().lr_ctx_device_bytes(self._h))
+
+    def blk_units(self) -> int:
+        """Levels whose grid SpMV runs as K5 (k_spmv_blk, dest-row blocks)."""
+        return int(lib().lr_ctx_blk_units(self._h))
 
     def unit_times(self) -> np.ndarray:
         """UnitRecord::wall_ms of the last solve (device span of each unit's

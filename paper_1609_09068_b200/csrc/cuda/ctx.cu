@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -91,6 +92,7 @@ struct LevelTasks {
   int hot_begin = 0;
   long long hot_rows = 0, unit_rows = 0;
   int keep_stream = 0;  // L2 priority of the streamed SpMV operands (spmv.cu policy_stream)
+  int blk = -1;         // K5: index into lr_ctx::blk (the level's one grid unit by dest-row blocks), or -1
   // multi-GPU, large levels: rows split over the ranks for the CTA-solved
   // units (world + 1 bounds; empty = every rank solves the whole level)
   std::vector<int> dist_bounds;
@@ -317,6 +319,17 @@ struct lr_ctx {
   cudaEvent_t xdone = nullptr;               // iteration's exchange done (exchange -> compute stream)
   DevBuf<double> maxbuf;                     // per grid unit: shard max, all-reduced
   DevBuf<double> cacpv;                      // pushed terms of CACs swept by cac_sweep_compact (n, or empty)
+  // K5 (k_spmv_blk): dest-blocked, source-sorted in-edges of large grid units
+  struct BlkUnit {
+    DevBuf<unsigned> esrc;
+    DevBuf<unsigned short> edst;
+    DevBuf<BlkPart> parts;
+    DevBuf<double> yacc;
+    DevBuf<int> bcnt;
+    BlkUnitDev dev{};
+    size_t bytes() const { return esrc.bytes() + edst.bytes() + parts.bytes() + yacc.bytes() + bcnt.bytes(); }
+  };
+  std::vector<std::unique_ptr<BlkUnit>> blk;
 
   DeviceLayout dl() const {
     DeviceLayout L;
@@ -489,6 +502,8 @@ lr_status lr_ctx_create(int device, lr_ctx** out) {
 
 void lr_ctx_free(lr_ctx* ctx) { delete ctx; }
 
+int32_t lr_ctx_blk_units(const lr_ctx* ctx) { return ctx ? static_cast<int32_t>(ctx->blk.size()) : 0; }
+
 void* lr_ctx_stream(lr_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int64_t lr_ctx_device_bytes(const lr_ctx* c) {
@@ -499,8 +514,81 @@ int64_t lr_ctx_device_bytes(const lr_ctx* c) {
                               c->lcta.bytes() + c->gstate.bytes() + c->blocks.bytes() + c->meta.bytes() + c->heavy.bytes() +
                               c->heavy_part.bytes() + c->heavy_cnt.bytes() + c->small_scratch.bytes() +
                               c->w.bytes() + c->rank.bytes() + c->s0.bytes() + c->s1.bytes() + c->pf.bytes() +
-                              c->r3.bytes() + c->r1.bytes() + c->partial.bytes() + c->unit_iters.bytes());
+                              c->r3.bytes() + c->r1.bytes() + c->partial.bytes() + c->unit_iters.bytes() +
+                              [c] {
+                                size_t b = 0;
+                                for (const auto& u : c->blk) b += u->bytes();
+                                return b;
+                              }());
 }
+
+}  // extern "C"
+
+// K5 for every level whose grid SpMV is one large unit on one GPU: its in-edges
+// by dest-row blocks of BR rows, sorted by source (built on the device from the
+// uploaded CSR, spmv.cu k_spmv_blk).  LR_BLK=0 keeps K4c everywhere;
+// LR_BLK_MIN_ROWS (default 2^22) sets "large", LR_BLK_ROWS the block rows
+// (default 16384), LR_BLK_PART the entries per part (default: about eight parts
+// per SM).
+static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vector<GridUnitState>& gstate,
+                                 cudaStream_t s) {
+  ctx->blk.clear();
+  const char* e_on = std::getenv("LR_BLK");
+  if ((e_on && std::atoi(e_on) == 0) || ctx->comm || !spmv_seg()) return LR_OK;
+  const char* e_min = std::getenv("LR_BLK_MIN_ROWS");
+  const long long min_rows = e_min ? std::atoll(e_min) : (1ll << 22);
+  const char* e_br = std::getenv("LR_BLK_ROWS");
+  const int BR = std::max(32, std::min(e_br ? std::atoi(e_br) : 16384, (kMaxDynSmem / 8) - 64));
+  int sms = 0;
+  LR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  for (LevelTasks& T : ctx->lt) {
+    if (T.gu1 - T.gu0 != 1) continue;
+    const int u = gstate[static_cast<size_t>(T.gu0)].unit;
+    const int u0 = L->unit_row_begin[u], R = L->unit_row_begin[u + 1] - u0;
+    if (R < min_rows || R <= 0) continue;
+    const long long e_begin = L->iptr[u0], E = L->iptr[u0 + R] - e_begin;
+    const int nb = static_cast<int>((static_cast<long long>(R) + BR - 1) / BR);
+    std::vector<long long> pad_off(static_cast<size_t>(nb) + 1, 0);
+    for (int b = 0; b < nb; ++b) {
+      const long long cnt = L->iptr[u0 + std::min(R, (b + 1) * BR)] - L->iptr[u0 + b * BR];
+      pad_off[static_cast<size_t>(b) + 1] = pad_off[static_cast<size_t>(b)] + (cnt + kBlkChunk - 1) / kBlkChunk * kBlkChunk;
+    }
+    const long long total = pad_off.back();
+    const char* e_part = std::getenv("LR_BLK_PART");
+    long long P = e_part ? std::atoll(e_part) : total / (8ll * sms);
+    P = std::max<long long>(kBlkChunk, (P + kBlkChunk - 1) / kBlkChunk * kBlkChunk);
+    P = std::min<long long>(P, 1ll << 30);
+    std::vector<BlkPart> parts;
+    int nslots = 0;
+    for (int b = 0; b < nb; ++b) {
+      const long long a = pad_off[static_cast<size_t>(b)], n = pad_off[static_cast<size_t>(b) + 1] - a;
+      const int np = static_cast<int>(std::max<long long>(1, (n + P - 1) / P));
+      const int slot = np > 1 ? nslots++ : -1;
+      for (int q = 0; q < np; ++q) {
+        const long long lo = a + static_cast<long long>(q) * P, hi = std::min(a + n, lo + P);
+        parts.push_back(BlkPart{lo, static_cast<int>(hi - lo), b, slot, np});
+      }
+    }
+    // heaviest parts first: the launch's tail is made of the light ones
+    std::stable_sort(parts.begin(), parts.end(), [](const BlkPart& x, const BlkPart& y) { return x.n > y.n; });
+    auto U = std::make_unique<lr_ctx::BlkUnit>();
+    LR_CUDA_TRY(U->esrc.alloc(static_cast<size_t>(total)));
+    LR_CUDA_TRY(U->edst.alloc(static_cast<size_t>(total)));
+    LR_CUDA_TRY(U->parts.upload(parts.data(), parts.size(), s));
+    LR_CUDA_TRY(U->yacc.alloc(static_cast<size_t>(nslots) * BR));
+    LR_CUDA_TRY(U->bcnt.alloc(static_cast<size_t>(nslots)));
+    LR_CUDA_TRY(cudaMemsetAsync(U->yacc.p, 0, U->yacc.bytes(), s));
+    LR_CUDA_TRY(cudaMemsetAsync(U->bcnt.p, 0, U->bcnt.bytes(), s));
+    LR_CUDA_TRY(build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, R, BR, pad_off, U->esrc.p, U->edst.p, s));
+    U->dev = BlkUnitDev{U->esrc.p, U->edst.p, U->parts.p, static_cast<int>(parts.size()), u0, R, BR, U->yacc.p,
+                        U->bcnt.p};
+    T.blk = static_cast<int>(ctx->blk.size());
+    ctx->blk.push_back(std::move(U));
+  }
+  return LR_OK;
+}
+
+extern "C" {
 
 lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
   if (!ctx || !L) {
@@ -872,6 +960,7 @@ lr_status lr_ctx_upload(lr_ctx* ctx, const lr_layout* L) {
                                     cudaMemcpyHostToDevice, s));
     }
   LR_CUDA_TRY(ctx->depth_ptr.upload(L->depth_ptr, static_cast<size_t>(L->depth_ptr_len), s));
+  if (const lr_status bs = build_blk_units(ctx, L, gstate, s); bs != LR_OK) return bs;
   // Large CACs' start weights in two halves (config-4 shaped chains of narrow
   // levels): each row's cross list is ordered by source level, so the terms from
   // levels solved at least two levels earlier are a prefix -- summed while the
@@ -1321,6 +1410,15 @@ static lr_status solve_on_device(lr_ctx* ctx, const double* w_dev, double c, dou
           if (sharded && T.chunk_bk.size() > 2) {  // exchange overlapped chunk by chunk
             if (const lr_status xs = chunked_iteration(ctx, T, L, sin, sout, launches); xs != LR_OK) return xs;
             LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(k)], s));
+            ++spmv_launches;
+            continue;
+          }
+          if (T.blk >= 0 && !sharded) {
+            launch_spmv_blk(ctx->blk[static_cast<size_t>(T.blk)]->dev, T.gu0, ctx->gstate.p, ctx->params.p, ctx->pf.p,
+                            ctx->rank.p, sin, sout, ctx->unit_iters.p, ctx->status.p, T.hot_begin, T.hot_rows,
+                            T.unit_rows, s);
+            LR_CUDA_TRY(cudaEventRecord(ctx->lev[static_cast<size_t>(k)], s));
+            ++launches;
             ++spmv_launches;
             continue;
           }

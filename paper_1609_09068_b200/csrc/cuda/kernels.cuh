@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
+#include <vector>
 
 namespace lrk {
 
@@ -270,6 +271,45 @@ void launch_normalize(const double* r3, double* r1, int n, const double* partial
                       cudaStream_t s);
 void launch_propagate(const int* dst_order, const long long* seg_ptr, int nseg, const int* src, const int* dst,
                       const int* deg, const double* ranks, double c, double* weights, cudaStream_t s);
+
+// K5 (k_spmv_blk, spmv.cu): the power-series SpMV of one large grid unit in
+// dest-row blocks.  Block b = unit rows [b*BR, (b+1)*BR); its in-edges sorted by
+// source (esrc: source row in the unit, edst: dest row in the block), padded to
+// a multiple of kBlkChunk entries with (src 0, dst BR) dummies.  A part is a
+// contiguous range of one block's entries; blocks with several parts add their
+// partial rows into yacc (slot) and the last part to finish closes the rows.
+#ifndef LR_BLK_THREADS
+#define LR_BLK_THREADS 1024
+#endif
+constexpr int kBlkThreads = LR_BLK_THREADS;
+constexpr int kBlkChunk = 256;  // entries per warp step (8 per lane, lane-strided)
+struct BlkPart {
+  long long e0;  // first entry (into esrc/edst)
+  int n;         // entries (multiple of kBlkChunk)
+  int blk;       // dest block
+  int slot;      // split blocks: partial-row slot, else -1
+  int nsplit;    // parts of the block
+};
+struct BlkUnitDev {
+  const unsigned* esrc;
+  const unsigned short* edst;
+  const BlkPart* parts;
+  int nparts;
+  int u0;  // first row of the unit
+  int R;   // rows of the unit
+  int BR;  // rows per block
+  double* yacc;  // [split blocks][BR]
+  int* bcnt;     // [split blocks]
+};
+// entries of rows [u0, u0 + R) (CSR iptr/isrc on the device, in-edges
+// [e_begin, e_begin + E)) sorted by (block, source) and padded: block b's
+// entries land at pad_off[b] (host array, NB + 1 entries, multiples of kBlkChunk)
+cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long e_begin, long long E, int u0, int R,
+                              int BR, const std::vector<long long>& pad_off, unsigned* esrc, unsigned short* edst,
+                              cudaStream_t s);
+void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
+                     double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
+                     int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s);
 
 constexpr int kOutBlock = 1024;  // rows per partial sum of the R1 normalisation
 

@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
                double* heavy_part, int* heavy_cnt, const SolveParams* __restrict__ p, const double* __restrict__ pf,
                double* __restrict__ rank, const double* __restrict__ s_in, double* __restrict__ s_out,
                long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes, unsigned unit_bytes,
-               int nhead, int keep_stream, double* maxbuf, int hold) {
+               int nhead, int nwarm, int keep_stream, double* maxbuf, int hold) {
   constexpr int kW = kSegThreads / 32;
   extern __shared__ double dyn[];  // [kW][kTileRows] row totals, then the head
   double* head = dyn + kW * kTileRows;
@@ -519,17 +519,18 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       const long long base = off < static_cast<unsigned>(nhead) ? head_base : glob_base;
       const double* src = reinterpret_cast<const double*>(base + (static_cast<long long>(idx[k]) << 3));
       double v = 0.0;
-#ifdef LR_GATHER_L1  // experiment: gathers allocate in L1
-      asm volatile(
-          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
-          : "+d"(v)
-          : "l"(src), "r"(vm & (1u << k)), "l"(keep));
-#else
+      // the warm window [nhead, nhead + nwarm) past the head: gathers that
+      // allocate in L1 (evict-last), so its lines are served without an L2 request
+      const unsigned warm = off - static_cast<unsigned>(nhead) < static_cast<unsigned>(nwarm);
+      const unsigned valid = (vm >> k) & 1u;
       asm volatile(
           "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
           : "+d"(v)
-          : "l"(src), "r"(vm & (1u << k)), "l"(keep));
-#endif
+          : "l"(src), "r"(valid & (warm ^ 1u)), "l"(keep));
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+          : "+d"(v)
+          : "l"(src), "r"(valid & warm), "l"(keep));
       S.g[k] = v;
     }
     const bool tile = S.b.heavy < 0 && S.b.nnz <= kChunkNnz;
@@ -704,6 +705,127 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   }
 }
 
+// K5: one power-series iteration of a large grid unit by dest-row blocks
+// (DESIGN.md §4.1 "K5").  A CTA claims parts (a contiguous range of one
+// block's in-edges, sorted by source) from a global counter; its warps walk the
+// part 256 entries at a time, lane l taking entries l, l+32, ..., so each
+// gather instruction reads 32 CONSECUTIVE sources of the sorted list: where the
+// sources are dense (the high-degree rows that carry most in-edges) they share
+// 128-byte lines and one L2 request serves many in-edges -- the pull SpMV's
+// one-request-per-in-edge ceiling does not apply.  Rows accumulate in shared
+// memory (y[BR + 1], slot BR absorbs the padding); a whole block is finished by
+// its CTA (rank += y, s' = pf y, max), a split block's parts add their rows into
+// yacc and the last one to arrive finishes them.  Summation order depends on
+// the atomics' arrival order (rows agree to ~1e-16; iteration counts asserted).
+__device__ __forceinline__ unsigned ld_stream_u32(const unsigned* p, std::uint64_t pol) {
+  unsigned v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_stream_u16(const unsigned short* p, std::uint64_t pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <int GATHER_L1>
+__device__ __forceinline__ double ld_blk_gather(const double* p, std::uint64_t pol) {
+  double v;
+  if (GATHER_L1)
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+template <int GATHER_L1>
+__global__ void __launch_bounds__(kBlkThreads, 1)
+    k_spmv_blk(BlkUnitDev B, int gu, GridUnitState* gs, const SolveParams* __restrict__ p,
+               const double* __restrict__ pf, double* __restrict__ rank, const double* __restrict__ s_in,
+               double* __restrict__ s_out, long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes,
+               unsigned unit_bytes) {
+  constexpr int kW = kBlkThreads / 32;
+  extern __shared__ double y[];  // [BR + 1]
+  __shared__ int s_part;
+  __shared__ int s_last;
+  __shared__ double wmax[kW];
+  if (gs[gu].done) return;  // launches past convergence exit at once
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint64_t stream = policy_stream(0);
+  const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
+  const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
+  const double* sb = s_in + B.u0;
+  double lmax = 0.0;
+  auto finish_row = [&](int r, double v) {
+    const long long g = static_cast<long long>(B.u0) + r;
+    rank[g] += v;
+    st_keep(s_out + g, pf[g] * v, keep_out);
+    lmax = fmax(lmax, v);
+  };
+  for (;;) {
+    if (threadIdx.x == 0) s_part = atomicAdd(&st->next_task, 1);
+    for (int i = threadIdx.x; i <= B.BR; i += kBlkThreads) y[i] = 0.0;
+    __syncthreads();
+    const int pi = s_part;
+    if (pi >= B.nparts) break;
+    const BlkPart P = B.parts[pi];
+    const unsigned* es = B.esrc + P.e0;
+    const unsigned short* ed = B.edst + P.e0;
+    for (int c = warp * kBlkChunk; c < P.n; c += kW * kBlkChunk) {
+      unsigned j[8], d[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) j[k] = ld_stream_u32(es + c + lane + 32 * k, stream);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d[k] = ld_stream_u16(ed + c + lane + 32 * k, stream);
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        LR_DCHECK(j[k] < static_cast<unsigned>(B.R) && d[k] <= static_cast<unsigned>(B.BR));
+        v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) atomicAdd(y + d[k], v[k]);
+    }
+    __syncthreads();
+    const int r0 = P.blk * B.BR, nr = min(B.BR, B.R - r0);
+    if (P.slot < 0) {
+      for (int i = threadIdx.x; i < nr; i += kBlkThreads) finish_row(r0 + i, y[i]);
+    } else {
+      double* ya = B.yacc + static_cast<size_t>(P.slot) * B.BR;
+      for (int i = threadIdx.x; i < nr; i += kBlkThreads) atomicAdd(ya + i, y[i]);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = atomicAdd(B.bcnt + P.slot, 1) == P.nsplit - 1;
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        for (int i = threadIdx.x; i < nr; i += kBlkThreads) {
+          const double v = __ldcg(ya + i);
+          ya[i] = 0.0;
+          finish_row(r0 + i, v);
+        }
+        if (threadIdx.x == 0) B.bcnt[P.slot] = 0;
+      }
+    }
+    __syncthreads();  // y is zeroed for the next part
+  }
+  const double m = warp_max(lmax);
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = 0.0;
+    for (int w = 0; w < kW; ++w) mm = fmax(mm, wmax[w]);
+    if (mm > 0.0) atomicMax(&gs[gu].max_bits, dbits(mm));
+    __threadfence();
+    s_last = atomicAdd(&st->ctas_done, 1) == static_cast<int>(gridDim.x) - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    st->next_task = 0;
+    finish_iteration(gs, gu, 1, p, unit_iters, st);
+  }
+}
+
 __global__ void k_grid_finish(GridUnitState* gs, int gu0, int ngu, const SolveParams* p, long long* unit_iters,
                               DevStatus* st, const double* maxbuf) {
   if (threadIdx.x == 0 && blockIdx.x == 0) finish_iteration(gs, gu0, ngu, p, unit_iters, st, maxbuf);
@@ -804,15 +926,49 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
   int want_head = spmv_seg() ? (unit_rows * 8 <= (48ll << 20) ? kHeadRowsSeg : kHeadRows) : kHeadRows;
   if (const char* e = std::getenv("LR_SPMV_HEAD")) want_head = std::max(0, std::atoi(e));
   const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
+  int nwarm = 0;
+  if (const char* e = std::getenv("LR_SPMV_WARM")) nwarm = std::max(0, std::atoi(e));
+  nwarm = static_cast<int>(std::min<long long>(nwarm, unit_rows - nhead));
   if (spmv_seg()) {
     k_spmv_seg<<<grid, kSegThreads, static_cast<size_t>(nhead + (kSegThreads / 32) * kTileRows) * 8, s>>>(
         L, tasks, meta, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
-        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf, hold);
+        hot_begin, hot_bytes, unit_bytes, nhead, nwarm, keep_stream, maxbuf, hold);
   } else {
     k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
         L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
         hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf, hold);
   }
+}
+
+// K5 launch: one persistent CTA per SM (y takes BR + 1 doubles of shared memory).
+// LR_BLK_L1=0 makes the gathers skip L1 (default: allocate, consecutive warps
+// of a CTA read neighbouring lines of the sorted sources).
+void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
+                     double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
+                     int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
+  const char* e_l1 = std::getenv("LR_BLK_L1");
+  const bool l1 = !(e_l1 && std::atoi(e_l1) == 0);
+  static int sms = 0;
+  static size_t smem_set = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = static_cast<size_t>(B.BR + 1) * sizeof(double);
+  if (smem > smem_set) {  // opt in to the block's y (static shared memory comes on top)
+    cudaFuncSetAttribute(k_spmv_blk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_spmv_blk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    smem_set = smem;
+  }
+  const int grid = std::max(1, std::min(sms, B.nparts));
+  const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
+  if (l1)
+    k_spmv_blk<1><<<grid, kBlkThreads, smem, s>>>(B, gu, gs, p, pf, rank, s_in, s_out, unit_iters, st, hot_begin,
+                                                  hot_bytes, unit_bytes);
+  else
+    k_spmv_blk<0><<<grid, kBlkThreads, smem, s>>>(B, gu, gs, p, pf, rank, s_in, s_out, unit_iters, st, hot_begin,
+                                                  hot_bytes, unit_bytes);
 }
 
 void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s) {

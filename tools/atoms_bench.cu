@@ -1,0 +1,86 @@
+// Shared-memory fp64 accumulation rates on the running GPU: random
+// y[d] += v into a per-CTA array of BR doubles (atomicAdd on shared doubles
+// compiles to an LDS + DADD + ATOMS.CAST.SPIN.64 loop on sm_100a), against
+// plain random STS and LDS, 148 CTAs x T threads, 8 independent updates per
+// thread in flight.  Decides whether a dest-blocked SpMV can accumulate its
+// rows with shared-memory atomics.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/atoms_bench.cu -o build/atoms_bench
+#include <cstdio>
+#include <cstdlib>
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                          \
+      std::printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      std::exit(1);                                                                   \
+    }                                                                                 \
+  } while (0)
+
+template <int MODE>
+__global__ void k(int iters, int br, double* out) {
+  extern __shared__ double y[];
+  for (int i = threadIdx.x; i < br; i += blockDim.x) y[i] = 0.0;
+  __syncthreads();
+  unsigned s = 0x9E3779B9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    unsigned d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s = s * 1664525u + 1013904223u;
+      d[q] = (s >> 8) % br;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (MODE == 0) atomicAdd(&y[d[q]], 1.0 + q);
+      if (MODE == 1) y[d[q]] = 1.0 + q;
+      if (MODE == 2) acc += y[d[q]];
+    }
+  }
+  __syncthreads();
+  double t = acc;
+  for (int i = threadIdx.x; i < br; i += blockDim.x) t += y[i];
+  if (t == -1.0) out[0] = t;
+}
+
+int main() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  double* out;
+  CK(cudaMalloc(&out, 8));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const char* names[3] = {"atomicAdd f64 (CAS loop)", "random STS.64", "random LDS.64"};
+  for (int mode = 0; mode < 3; ++mode)
+    for (int threads : {512, 768, 1024})
+      for (int br : {8192, 16384, 24576}) {
+        const size_t smem = br * 8;
+        const int iters = 2000;
+        auto launch = [&] {
+          if (mode == 0) k<0><<<sms, threads, smem>>>(iters, br, out);
+          if (mode == 1) k<1><<<sms, threads, smem>>>(iters, br, out);
+          if (mode == 2) k<2><<<sms, threads, smem>>>(iters, br, out);
+        };
+        CK(cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        launch();
+        CK(cudaDeviceSynchronize());
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+          cudaEventRecord(e0);
+          launch();
+          cudaEventRecord(e1);
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best) best = ms;
+        }
+        const double ops = (double)sms * threads * iters * 8;
+        std::printf("%-26s %4d thr  y %5d: %.3f ms  %.1f G ops/s  %.2f ops/SM-clk@1.9GHz\n", names[mode], threads, br,
+                    best, ops / best / 1e6, ops / best / 1e6 / sms / 1.9);
+      }
+  return 0;
+}

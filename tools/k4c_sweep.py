@@ -19,6 +19,8 @@ ap.add_argument("--heads", default="8192")
 ap.add_argument("--solves", type=int, default=3)
 ap.add_argument("--hot", default="", help="LR_L2_HOT_FRAC values (re-upload per value)")
 ap.add_argument("--keep", default="", help="LR_SPMV_KEEP values (re-upload per value)")
+ap.add_argument("--env", action="append", default=[],
+                help="VAR=v1,v2,...: per-launch knobs (no re-upload), swept at the first --heads value")
 a = ap.parse_args()
 t = time.time()
 g = lr.config_graph(a.config, a.shrink)
@@ -44,6 +46,18 @@ for var, vals in (("LR_L2_HOT_FRAC", a.hot), ("LR_SPMV_KEEP", a.keep)):
         del os.environ[var]
     if vals:
         reupload()
+for spec in a.env:
+    var, vals = spec.split("=", 1)
+    os.environ["LR_SPMV_HEAD"] = a.heads.split(",")[0]
+    for v in vals.split(","):
+        os.environ[var] = v
+        rates = []
+        for _ in range(a.solves):
+            _, _, info, _ = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+            rates.append(info["spmv_bytes"] / (info["spmv_active_ms"] / 1e3) / 1e9)
+        print(f"{var}={v}: K4c {np.median(rates):.0f} GB/s (runs {', '.join(f'{r:.0f}' for r in rates)}), "
+              f"device {info['device_ms']:.1f} ms", flush=True)
+    del os.environ[var]
 for h in a.heads.split(","):
     os.environ["LR_SPMV_HEAD"] = h
     rates = []
