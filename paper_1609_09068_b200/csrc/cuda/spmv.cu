@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
                double* heavy_part, int* heavy_cnt, const SolveParams* __restrict__ p, const double* __restrict__ pf,
                double* __restrict__ rank, const double* __restrict__ s_in, double* __restrict__ s_out,
                long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes, unsigned unit_bytes,
-               int nhead, int nwarm, int keep_stream, double* maxbuf, int hold) {
+               int nhead, int keep_stream, double* maxbuf, int hold) {
   constexpr int kW = kSegThreads / 32;
   extern __shared__ double dyn[];  // [kW][kTileRows] row totals, then the head
   double* head = dyn + kW * kTileRows;
@@ -519,18 +519,10 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       const long long base = off < static_cast<unsigned>(nhead) ? head_base : glob_base;
       const double* src = reinterpret_cast<const double*>(base + (static_cast<long long>(idx[k]) << 3));
       double v = 0.0;
-      // the warm window [nhead, nhead + nwarm) past the head: gathers that
-      // allocate in L1 (evict-last), so its lines are served without an L2 request
-      const unsigned warm = off - static_cast<unsigned>(nhead) < static_cast<unsigned>(nwarm);
-      const unsigned valid = (vm >> k) & 1u;
       asm volatile(
           "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
           : "+d"(v)
-          : "l"(src), "r"(valid & (warm ^ 1u)), "l"(keep));
-      asm volatile(
-          "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
-          : "+d"(v)
-          : "l"(src), "r"(valid & warm), "l"(keep));
+          : "l"(src), "r"(vm & (1u << k)), "l"(keep));
       S.g[k] = v;
     }
     const bool tile = S.b.heavy < 0 && S.b.nnz <= kChunkNnz;
@@ -737,7 +729,7 @@ __device__ __forceinline__ double ld_blk_gather(const double* p, std::uint64_t p
   return v;
 }
 
-template <int GATHER_L1>
+template <int GATHER_L1, int PIPE>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     k_spmv_blk(BlkUnitDev B, int gu, GridUnitState* gs, const SolveParams* __restrict__ p,
                const double* __restrict__ pf, double* __restrict__ rank, const double* __restrict__ s_in,
@@ -770,20 +762,55 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const BlkPart P = B.parts[pi];
     const unsigned* es = B.esrc + P.e0;
     const unsigned short* ed = B.edst + P.e0;
-    for (int c = warp * kBlkChunk; c < P.n; c += kW * kBlkChunk) {
+    if (PIPE) {
+      // the next chunk's indices load while this chunk's gathers are in flight
+      int c = warp * kBlkChunk;
       unsigned j[8], d[8];
+      if (c < P.n) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) j[k] = ld_stream_u32(es + c + lane + 32 * k, stream);
+        for (int k = 0; k < 8; ++k) j[k] = ld_stream_u32(es + c + lane + 32 * k, stream);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) d[k] = ld_stream_u16(ed + c + lane + 32 * k, stream);
-      double v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        LR_DCHECK(j[k] < static_cast<unsigned>(B.R) && d[k] <= static_cast<unsigned>(B.BR));
-        v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
+        for (int k = 0; k < 8; ++k) d[k] = ld_stream_u16(ed + c + lane + 32 * k, stream);
       }
+      for (; c < P.n; c += kW * kBlkChunk) {
+        double v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) atomicAdd(y + d[k], v[k]);
+        for (int k = 0; k < 8; ++k) {
+          LR_DCHECK(j[k] < static_cast<unsigned>(B.R) && d[k] <= static_cast<unsigned>(B.BR));
+          v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
+        }
+        const int cn = c + kW * kBlkChunk;
+        unsigned jn[8], dn[8];
+        if (cn < P.n) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) jn[k] = ld_stream_u32(es + cn + lane + 32 * k, stream);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dn[k] = ld_stream_u16(ed + cn + lane + 32 * k, stream);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) atomicAdd(y + d[k], v[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          j[k] = jn[k];
+          d[k] = dn[k];
+        }
+      }
+    } else {
+      for (int c = warp * kBlkChunk; c < P.n; c += kW * kBlkChunk) {
+        unsigned j[8], d[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) j[k] = ld_stream_u32(es + c + lane + 32 * k, stream);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) d[k] = ld_stream_u16(ed + c + lane + 32 * k, stream);
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          LR_DCHECK(j[k] < static_cast<unsigned>(B.R) && d[k] <= static_cast<unsigned>(B.BR));
+          v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) atomicAdd(y + d[k], v[k]);
+      }
     }
     __syncthreads();
     const int r0 = P.blk * B.BR, nr = min(B.BR, B.R - r0);
@@ -926,13 +953,10 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
   int want_head = spmv_seg() ? (unit_rows * 8 <= (48ll << 20) ? kHeadRowsSeg : kHeadRows) : kHeadRows;
   if (const char* e = std::getenv("LR_SPMV_HEAD")) want_head = std::max(0, std::atoi(e));
   const int nhead = static_cast<int>(std::min<long long>({head_capacity(), want_head, unit_rows}));
-  int nwarm = 0;
-  if (const char* e = std::getenv("LR_SPMV_WARM")) nwarm = std::max(0, std::atoi(e));
-  nwarm = static_cast<int>(std::min<long long>(nwarm, unit_rows - nhead));
   if (spmv_seg()) {
     k_spmv_seg<<<grid, kSegThreads, static_cast<size_t>(nhead + (kSegThreads / 32) * kTileRows) * 8, s>>>(
         L, tasks, meta, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
-        hot_begin, hot_bytes, unit_bytes, nhead, nwarm, keep_stream, maxbuf, hold);
+        hot_begin, hot_bytes, unit_bytes, nhead, keep_stream, maxbuf, hold);
   } else {
     k_grid_iter<<<grid, kSpmvThreads, static_cast<size_t>(nhead + kWarps * kTileNnz) * 8, s>>>(
         L, tasks, ntasks, gu0, ngu, gs, heavy, heavy_part, heavy_cnt, p, pf, rank, s_in, s_out, unit_iters, st,
@@ -941,13 +965,15 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
 }
 
 // K5 launch: one persistent CTA per SM (y takes BR + 1 doubles of shared memory).
-// LR_BLK_L1=0 makes the gathers skip L1 (default: allocate, consecutive warps
-// of a CTA read neighbouring lines of the sorted sources).
+// LR_BLK_L1=1 makes the gathers allocate in L1 (measured slightly slower at
+// config 5: 3924 vs 3952 GB/s); LR_BLK_PIPE=0 drops the index prefetch.
 void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
                      double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
                      int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
   const char* e_l1 = std::getenv("LR_BLK_L1");
-  const bool l1 = !(e_l1 && std::atoi(e_l1) == 0);
+  const bool l1 = e_l1 && std::atoi(e_l1) != 0;
+  const char* e_pipe = std::getenv("LR_BLK_PIPE");
+  const bool pipe = !(e_pipe && std::atoi(e_pipe) == 0);
   static int sms = 0;
   static size_t smem_set = 0;
   if (sms == 0) {
@@ -957,18 +983,17 @@ void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const Solve
   }
   const size_t smem = static_cast<size_t>(B.BR + 1) * sizeof(double);
   if (smem > smem_set) {  // opt in to the block's y (static shared memory comes on top)
-    cudaFuncSetAttribute(k_spmv_blk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_spmv_blk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_spmv_blk<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_spmv_blk<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_spmv_blk<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_spmv_blk<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     smem_set = smem;
   }
   const int grid = std::max(1, std::min(sms, B.nparts));
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
-  if (l1)
-    k_spmv_blk<1><<<grid, kBlkThreads, smem, s>>>(B, gu, gs, p, pf, rank, s_in, s_out, unit_iters, st, hot_begin,
-                                                  hot_bytes, unit_bytes);
-  else
-    k_spmv_blk<0><<<grid, kBlkThreads, smem, s>>>(B, gu, gs, p, pf, rank, s_in, s_out, unit_iters, st, hot_begin,
-                                                  hot_bytes, unit_bytes);
+  auto kern = l1 ? (pipe ? k_spmv_blk<1, 1> : k_spmv_blk<1, 0>) : (pipe ? k_spmv_blk<0, 1> : k_spmv_blk<0, 0>);
+  kern<<<grid, kBlkThreads, smem, s>>>(B, gu, gs, p, pf, rank, s_in, s_out, unit_iters, st, hot_begin, hot_bytes,
+                                       unit_bytes);
 }
 
 void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s) {

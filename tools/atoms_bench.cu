@@ -30,10 +30,12 @@ __global__ void k(int iters, int br, double* out) {
     for (int q = 0; q < 8; ++q) {
       s = s * 1664525u + 1013904223u;
       d[q] = (s >> 8) % br;
+      if (MODE >= 3) d[q] = (d[q] & ~15u) | (threadIdx.x & 15u);  // each half-warp: 16 distinct bank pairs
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if (MODE == 0) atomicAdd(&y[d[q]], 1.0 + q);
+      if (MODE == 0 || MODE == 3) atomicAdd(&y[d[q]], 1.0 + q);
+      if (MODE == 4) acc += y[d[q]];
       if (MODE == 1) y[d[q]] = 1.0 + q;
       if (MODE == 2) acc += y[d[q]];
     }
@@ -52,20 +54,25 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[3] = {"atomicAdd f64 (CAS loop)", "random STS.64", "random LDS.64"};
-  for (int mode = 0; mode < 3; ++mode)
-    for (int threads : {512, 768, 1024})
-      for (int br : {8192, 16384, 24576}) {
+  const char* names[5] = {"atomicAdd f64 (CAS loop)", "random STS.64", "random LDS.64", "atomicAdd, no conflicts",
+                          "LDS.64, no conflicts"};
+  for (int mode = 0; mode < 5; ++mode)
+    for (int threads : {1024})
+      for (int br : {16384}) {
         const size_t smem = br * 8;
         const int iters = 2000;
         auto launch = [&] {
           if (mode == 0) k<0><<<sms, threads, smem>>>(iters, br, out);
           if (mode == 1) k<1><<<sms, threads, smem>>>(iters, br, out);
           if (mode == 2) k<2><<<sms, threads, smem>>>(iters, br, out);
+          if (mode == 3) k<3><<<sms, threads, smem>>>(iters, br, out);
+          if (mode == 4) k<4><<<sms, threads, smem>>>(iters, br, out);
         };
         CK(cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         launch();
         CK(cudaDeviceSynchronize());
         float best = 1e30f;
