@@ -394,7 +394,12 @@ def run_ours(args):
         setup_thread = threading.Thread(target=leg.setup, daemon=True)
         setup_thread.start()
     # parity spot check of the timed path vs the host-API result
-    assert torch.equal(r3_h, torch.from_numpy(r3h)), "device-resident and host-API solves differ"
+    # (K5 accumulates rows with shared-memory atomics, whose arrival order varies
+    # from launch to launch: results agree to rounding, iteration counts exactly)
+    ref_t = torch.from_numpy(r3h)
+    rel = float(((r3_h - ref_t).abs() / ref_t.abs().clamp_min(1e-300)).max())
+    assert rel <= 1e-12, f"device-resident and host-API solves differ: max relative {rel:.3e}"
+    assert all(i["total_iterations"] == info0["total_iterations"] for i in infos), "iteration totals differ between solves"
 
     inf = infos[-1]
     peak, peak_kind = peaks()
@@ -409,7 +414,9 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "frac_vs_nominal_8000": (achieved / 8000.0) if achieved else None,
-                "kernel": "k_spmv_seg (K4c: SccLarge power-series SpMV)", "peak_kind": peak_kind,
+                "kernel": ("k_spmv_blk (K5: SccLarge power-series SpMV by dest-row blocks, source-sorted in-edges)"
+                           if eng.blk_units() > 0 else "k_spmv_seg (K4c: SccLarge power-series SpMV)"),
+                "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": (inf["spmv_bytes"] / inf["spmv_active_launches"])
                 if inf["spmv_active_launches"] else None,
                 "avg_launch_ms": (inf["spmv_active_ms"] / inf["spmv_active_launches"])
@@ -417,7 +424,7 @@ def run_ours(args):
                 "spmv_share_of_step": inf["spmv_active_ms"] / ms if ms > 0 else None}
     # the bound that applies (profiles/r01_gather_ceiling.md): every in-edge not
     # served by the shared-memory head is one random 8-byte gather = one L2 sector
-    if achieved and head_share is not None and inf["spmv_edges"]:
+    if achieved and head_share is not None and inf["spmv_edges"] and eng.blk_units() == 0:
         g_per_s = inf["spmv_edges"] * (1.0 - head_share) / (inf["spmv_active_ms"] / 1e3)
         roofline["gathers"] = {"head_share_of_in_edges": head_share, "global_gathers_per_s": g_per_s,
                                "ceiling_l2_resident_per_s": 195e9, "ceiling_171MB_uniform_per_s": 86e9,

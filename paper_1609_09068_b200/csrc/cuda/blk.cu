@@ -36,23 +36,31 @@ __global__ void k_blk_keys(const long long* __restrict__ iptr, const int* __rest
   }
 }
 
-// CTA per block (grid-stride): sorted run -> padded slot
+// thread per padded slot: sorted run -> padded slot (the slot's block by binary
+// search in pad_off; the heaviest block holds a large share of all entries, so
+// the work is split by slots, not by blocks)
 __global__ void k_blk_pack(const long long* __restrict__ iptr, long long e_begin, int u0, int R, int BR,
                            const long long* __restrict__ pad_off, int nb, unsigned long long smask,
                            const unsigned long long* __restrict__ keys, const unsigned short* __restrict__ vals,
                            unsigned* __restrict__ esrc, unsigned short* __restrict__ edst) {
-  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int r0 = b * BR, r1 = min(R, r0 + BR);
+  const long long total = pad_off[nb];
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = nb;  // last block with pad_off[b] <= i (empty blocks share their successor's offset)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pad_off[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    const int r0 = lo * BR, r1 = min(R, r0 + BR);
     const long long s0 = iptr[u0 + r0] - e_begin, cnt = iptr[u0 + r1] - iptr[u0 + r0];
-    const long long p0 = pad_off[b], pn = pad_off[b + 1] - p0;
-    for (long long i = threadIdx.x; i < pn; i += blockDim.x) {
-      if (i < cnt) {
-        esrc[p0 + i] = static_cast<unsigned>(keys[s0 + i] & smask);
-        edst[p0 + i] = vals[s0 + i];
-      } else {
-        esrc[p0 + i] = 0u;
-        edst[p0 + i] = static_cast<unsigned short>(BR);
-      }
+    const long long j = i - pad_off[lo];
+    if (j < cnt) {
+      esrc[i] = static_cast<unsigned>(keys[s0 + j] & smask);
+      edst[i] = vals[s0 + j];
+    } else {
+      esrc[i] = 0u;
+      edst[i] = static_cast<unsigned short>(BR);
     }
   }
 }
@@ -152,10 +160,10 @@ cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long 
     if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<std::int64_t>(E), 0, end_bit, s)) !=
         cudaSuccess)
       return done(e);
-    k_blk_pack<<<std::min(nb, 4096), 256, 0, s>>>(iptr, e_begin, u0, R, BR, poff, nb, (1ull << sbits) - 1,
+    k_blk_pack<<<2368, 256, 0, s>>>(iptr, e_begin, u0, R, BR, poff, nb, (1ull << sbits) - 1,
                                                   kb.Current(), vb.Current(), esrc, edst);
   } else {
-    k_blk_pack<<<std::min(nb, 4096), 256, 0, s>>>(iptr, e_begin, u0, R, BR, poff, nb, (1ull << sbits) - 1, k0, v0,
+    k_blk_pack<<<2368, 256, 0, s>>>(iptr, e_begin, u0, R, BR, poff, nb, (1ull << sbits) - 1, k0, v0,
                                                   esrc, edst);
   }
   {

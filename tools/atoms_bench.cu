@@ -30,7 +30,8 @@ __global__ void k(int iters, int br, double* out) {
     for (int q = 0; q < 8; ++q) {
       s = s * 1664525u + 1013904223u;
       d[q] = (s >> 8) % br;
-      if (MODE >= 3) d[q] = (d[q] & ~15u) | (threadIdx.x & 15u);  // each half-warp: 16 distinct bank pairs
+      if (MODE == 3 || MODE == 4) d[q] = (d[q] & ~15u) | (threadIdx.x & 15u);  // each half-warp: 16 distinct bank pairs
+      if (MODE >= 5) d[q] = (d[q] & ~31u) | (threadIdx.x & 31u);  // and 32 distinct rows per warp instruction
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -38,6 +39,17 @@ __global__ void k(int iters, int br, double* out) {
       if (MODE == 4) acc += y[d[q]];
       if (MODE == 1) y[d[q]] = 1.0 + q;
       if (MODE == 2) acc += y[d[q]];
+      if (MODE == 5) {  // take the row (exchange with a sentinel), add, put it back
+        unsigned long long* a = reinterpret_cast<unsigned long long*>(&y[d[q]]);
+        unsigned long long old;
+        do old = atomicExch(a, ~0ull);
+        while (old == ~0ull);
+        *reinterpret_cast<volatile double*>(a) = __longlong_as_double(static_cast<long long>(old)) + (1.0 + q);
+      }
+      if (MODE == 6) {  // not atomic: the lower bound (LDS + DADD + STS)
+        volatile double* a = &y[d[q]];
+        *a = *a + (1.0 + q);
+      }
     }
   }
   __syncthreads();
@@ -54,9 +66,9 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[5] = {"atomicAdd f64 (CAS loop)", "random STS.64", "random LDS.64", "atomicAdd, no conflicts",
-                          "LDS.64, no conflicts"};
-  for (int mode = 0; mode < 5; ++mode)
+  const char* names[7] = {"atomicAdd f64 (CAS loop)", "random STS.64", "random LDS.64", "atomicAdd, no conflicts",
+                          "LDS.64, no conflicts", "exchange-lock add, no conflicts", "LDS+DADD+STS, no conflicts"};
+  for (int mode = 0; mode < 7; ++mode)
     for (int threads : {1024})
       for (int br : {16384}) {
         const size_t smem = br * 8;
@@ -67,12 +79,16 @@ int main() {
           if (mode == 2) k<2><<<sms, threads, smem>>>(iters, br, out);
           if (mode == 3) k<3><<<sms, threads, smem>>>(iters, br, out);
           if (mode == 4) k<4><<<sms, threads, smem>>>(iters, br, out);
+          if (mode == 5) k<5><<<sms, threads, smem>>>(iters, br, out);
+          if (mode == 6) k<6><<<sms, threads, smem>>>(iters, br, out);
         };
         CK(cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         launch();
         CK(cudaDeviceSynchronize());
         float best = 1e30f;
