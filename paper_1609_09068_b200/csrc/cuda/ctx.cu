@@ -528,11 +528,16 @@ int64_t lr_ctx_device_bytes(const lr_ctx* c) {
 // by dest-row blocks of BR rows, sorted by source (built on the device from the
 // uploaded CSR, spmv.cu k_spmv_blk).  LR_BLK=0 keeps K4c everywhere;
 // LR_BLK_MIN_ROWS (default 2^22) sets "large", LR_BLK_ROWS the block rows
-// (default 16384), LR_BLK_PART the entries per part (default: about eight parts
-// per SM).
+// (default 16384), LR_BLK_PART the slots per part (default: about eight parts
+// per SM), LR_BLK_WIN the bank-balance window (0 or LR_BLK_BANKS=0: none),
+// LR_BLK_SLACK the rows of entries per empty row (0: none).
 static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vector<GridUnitState>& gstate,
                                  cudaStream_t s) {
   ctx->blk.clear();
+  auto env_int = [](const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+  };
   const char* e_on = std::getenv("LR_BLK");
   if ((e_on && std::atoi(e_on) == 0) || ctx->comm || !spmv_seg()) return LR_OK;
   const char* e_min = std::getenv("LR_BLK_MIN_ROWS");
@@ -548,10 +553,19 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     if (R < min_rows || R <= 0) continue;
     const long long e_begin = L->iptr[u0], E = L->iptr[u0 + R] - e_begin;
     const int nb = static_cast<int>((static_cast<long long>(R) + BR - 1) / BR);
+    // slots of a block's run: its entries in rows of 32 (one K5 gather
+    // instruction), one empty row after every `slack` rows (free slots for the
+    // bank balance), padded to whole chunks
+    const int slack = std::max(0, env_int("LR_BLK_SLACK", kBlkSlack));
+    int win = env_int("LR_BLK_BANKS", 1) == 0 ? 0 : env_int("LR_BLK_WIN", kBlkWindow);
+    if (win != 0 && win != 256 && win != 1024 && win != 2048 && win != 4096 && win != 8192) win = kBlkWindow;
     std::vector<long long> pad_off(static_cast<size_t>(nb) + 1, 0);
     for (int b = 0; b < nb; ++b) {
       const long long cnt = L->iptr[u0 + std::min(R, (b + 1) * BR)] - L->iptr[u0 + b * BR];
-      pad_off[static_cast<size_t>(b) + 1] = pad_off[static_cast<size_t>(b)] + (cnt + kBlkChunk - 1) / kBlkChunk * kBlkChunk;
+      long long rows = (cnt + 31) / 32;
+      if (slack > 0 && rows > 0) rows += (rows - 1) / slack;
+      const long long slots = rows * 32;
+      pad_off[static_cast<size_t>(b) + 1] = pad_off[static_cast<size_t>(b)] + (slots + kBlkChunk - 1) / kBlkChunk * kBlkChunk;
     }
     const long long total = pad_off.back();
     const char* e_part = std::getenv("LR_BLK_PART");
@@ -579,7 +593,8 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     LR_CUDA_TRY(U->bcnt.alloc(static_cast<size_t>(nslots)));
     LR_CUDA_TRY(cudaMemsetAsync(U->yacc.p, 0, U->yacc.bytes(), s));
     LR_CUDA_TRY(cudaMemsetAsync(U->bcnt.p, 0, U->bcnt.bytes(), s));
-    LR_CUDA_TRY(build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, R, BR, pad_off, U->esrc.p, U->edst.p, s));
+    LR_CUDA_TRY(build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, R, BR, pad_off, slack, win, U->esrc.p,
+                                  U->edst.p, s));
     U->dev = BlkUnitDev{U->esrc.p, U->edst.p, U->parts.p, static_cast<int>(parts.size()), u0, R, BR, U->yacc.p,
                         U->bcnt.p};
     T.blk = static_cast<int>(ctx->blk.size());

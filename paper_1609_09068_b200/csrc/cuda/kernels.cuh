@@ -274,15 +274,19 @@ void launch_propagate(const int* dst_order, const long long* seg_ptr, int nseg, 
 
 // K5 (k_spmv_blk, spmv.cu): the power-series SpMV of one large grid unit in
 // dest-row blocks.  Block b = unit rows [b*BR, (b+1)*BR); its in-edges sorted by
-// source (esrc: source row in the unit, edst: dest row in the block), padded to
-// a multiple of kBlkChunk entries with (src 0, dst BR) dummies.  A part is a
-// contiguous range of one block's entries; blocks with several parts add their
+// source (esrc: source row in the unit, edst: dest row in the block) in slots of
+// kBlkChunk; unused slots hold (src 0, dst BR) dummies, which K5 skips.  Inside
+// a window of kBlkWindow slots the entries are placed so that each half-warp's
+// dest rows fall on distinct shared-memory bank pairs (blk.cu).  A part is a
+// contiguous range of one block's slots; blocks with several parts add their
 // partial rows into yacc (slot) and the last part to finish closes the rows.
 #ifndef LR_BLK_THREADS
 #define LR_BLK_THREADS 1024
 #endif
 constexpr int kBlkThreads = LR_BLK_THREADS;
-constexpr int kBlkChunk = 256;  // entries per warp step (8 per lane, lane-strided)
+constexpr int kBlkChunk = 256;    // slots per warp step (8 per lane, lane-strided)
+constexpr int kBlkWindow = 8192;  // slots the bank balance looks at together (blk.cu k_blk_banks)
+constexpr int kBlkSlack = 0;      // rows of 32 entries per empty row (0: none)
 struct BlkPart {
   long long e0;  // first entry (into esrc/edst)
   int n;         // entries (multiple of kBlkChunk)
@@ -302,11 +306,12 @@ struct BlkUnitDev {
   int* bcnt;     // [split blocks]
 };
 // entries of rows [u0, u0 + R) (CSR iptr/isrc on the device, in-edges
-// [e_begin, e_begin + E)) sorted by (block, source) and padded: block b's
-// entries land at pad_off[b] (host array, NB + 1 entries, multiples of kBlkChunk)
+// [e_begin, e_begin + E)) sorted by (block, source): block b's run lands at
+// pad_off[b] (host array, NB + 1 entries, multiples of kBlkChunk), one empty row
+// of 32 slots after every `slack` rows, bank-balanced in windows of `win` slots
 cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long e_begin, long long E, int u0, int R,
-                              int BR, const std::vector<long long>& pad_off, unsigned* esrc, unsigned short* edst,
-                              cudaStream_t s);
+                              int BR, const std::vector<long long>& pad_off, int slack, int win, unsigned* esrc,
+                              unsigned short* edst, cudaStream_t s);
 void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
                      double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
                      int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s);

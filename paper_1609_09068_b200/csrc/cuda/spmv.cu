@@ -705,7 +705,9 @@ __global__ void __launch_bounds__(kSegThreads, 1)
 // sources are dense (the high-degree rows that carry most in-edges) they share
 // 128-byte lines and one L2 request serves many in-edges -- the pull SpMV's
 // one-request-per-in-edge ceiling does not apply.  Rows accumulate in shared
-// memory (y[BR + 1], slot BR absorbs the padding); a whole block is finished by
+// memory (y[BR]; unused slots carry dst = BR and are skipped; the entries are
+// placed so that a half-warp's dest rows lie on distinct bank pairs, blk.cu); a
+// whole block is finished by
 // its CTA (rank += y, s' = pf y, max), a split block's parts add their rows into
 // yacc and the last one to arrive finishes them.  Summation order depends on
 // the atomics' arrival order (rows agree to ~1e-16; iteration counts asserted).
@@ -746,6 +748,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   const std::uint64_t keep = policy_hot_head(s_in + hot_begin, hot_bytes, unit_bytes);
   const std::uint64_t keep_out = policy_hot_head(s_out + hot_begin, hot_bytes, unit_bytes);
   const double* sb = s_in + B.u0;
+  const unsigned ubr = static_cast<unsigned>(B.BR);
   double lmax = 0.0;
   auto finish_row = [&](int r, double v) {
     const long long g = static_cast<long long>(B.u0) + r;
@@ -788,7 +791,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
           for (int k = 0; k < 8; ++k) dn[k] = ld_stream_u16(ed + cn + lane + 32 * k, stream);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) atomicAdd(y + d[k], v[k]);
+        for (int k = 0; k < 8; ++k)
+          if (d[k] != ubr) atomicAdd(y + d[k], v[k]);  // dummies (unused slots) add nothing
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           j[k] = jn[k];
@@ -809,7 +813,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
           v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) atomicAdd(y + d[k], v[k]);
+        for (int k = 0; k < 8; ++k)
+          if (d[k] != ubr) atomicAdd(y + d[k], v[k]);  // dummies (unused slots) add nothing
       }
     }
     __syncthreads();
