@@ -71,8 +71,14 @@ __global__ void k_blk_pack(const long long* __restrict__ iptr, long long e_begin
   }
 }
 
-// Shared-memory bank balance, one thread per window of W slots (several chunks
-// of one block).  K5 lane l of a warp handles slots l + 32 k of a chunk; its
+// Slot i of a window (instruction row i / 32, lane i % 32; windows and chunks
+// start at multiples of 256) -> its place in memory: K5 stores a chunk
+// lane-major (lane * 8 + row within the chunk), so a lane's 8 slots are one
+// vector load.
+__device__ __forceinline__ int blk_slot_pos(int i) { return (i & ~255) | ((i & 31) << 3) | ((i >> 5) & 7); }
+
+// Shared-memory bank balance, one CTA per window of W slots (several chunks of
+// one block), the window staged in shared memory.  K5 lane l of a warp handles slots l + 32 k of a chunk; its
 // atomic add to y[dst] (LDS + DADD + ATOMS.CAST.SPIN.64) hits the bank pair
 // dst mod 16 (8-byte words), and a half-warp whose 16 adds use 16 distinct bank
 // pairs takes the fewest shared-memory wavefronts -- the L1/shared data pipe is
@@ -88,83 +94,162 @@ __global__ void k_blk_pack(const long long* __restrict__ iptr, long long e_begin
 // placement cascades instead (an entry pushed into a neighbour pushes the
 // neighbour's own entries on: measured 4,700 vs 5,050 GB/s at config 5).
 template <int W>
-__global__ void k_blk_banks(unsigned* __restrict__ esrc, unsigned short* __restrict__ edst,
-                            const long long* __restrict__ wstart, const int* __restrict__ wlen, long long nwin,
-                            int BR) {
-  constexpr int G = W / 16;
-  for (long long wi = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; wi < nwin;
-       wi += static_cast<long long>(gridDim.x) * blockDim.x) {
+__global__ void __launch_bounds__(256, 1)
+    k_blk_banks(unsigned* __restrict__ esrc, unsigned short* __restrict__ edst, const long long* __restrict__ wstart,
+                const int* __restrict__ wlen, long long nwin, int BR, int reach) {
+  constexpr int NI = W / 32;  // instruction rows of a full window
+  static_assert(NI <= 256, "one thread per row in pass 1");
+  extern __shared__ unsigned char blk_smem[];
+  unsigned* s = reinterpret_cast<unsigned*>(blk_smem);        // [W] entries as packed (slot order)
+  unsigned* os = s + W;                                       // [W] placed
+  unsigned short* d = reinterpret_cast<unsigned short*>(os + W);
+  unsigned short* od = d + W;
+  unsigned short* to = od + W;    // slot an entry goes to
+  unsigned short* left = to + W;  // pass 1 left-overs, 32 per row
+  unsigned short* rest = left + W;  // pass 2 left-overs
+  unsigned short* occ = rest + W;   // [2 NI] bank pairs taken per half-warp
+  unsigned* rownear = reinterpret_cast<unsigned*>(occ + 2 * NI);  // [NI]
+  unsigned char* fill = reinterpret_cast<unsigned char*>(rownear + NI);  // [2 NI]
+  unsigned char* lcnt = fill + 2 * NI;                                    // [NI]
+  __shared__ int s_nrest;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (long long wi = blockIdx.x; wi < nwin; wi += gridDim.x) {
     unsigned* es = esrc + wstart[wi];
     unsigned short* ed = edst + wstart[wi];
     const int len = wlen[wi], ni = len / 32;
-    unsigned s[W];
-    unsigned short d[W], to[W], left[W];
-    unsigned short occ[G];
-    unsigned char fill[G];
-    for (int i = 0; i < len; ++i) {
+    for (int i = tid; i < len; i += 256) {
       s[i] = es[i];
       d[i] = ed[i];
-      es[i] = 0u;
-      ed[i] = static_cast<unsigned short>(BR);
+      os[i] = 0u;
+      od[i] = static_cast<unsigned short>(BR);
     }
-    for (int h = 0; h < 2 * ni; ++h) occ[h] = 0, fill[h] = 0;
-    auto put = [&](int i, int h) {
-      occ[h] = static_cast<unsigned short>(occ[h] | (1u << (d[i] & 15)));
-      to[i] = static_cast<unsigned short>((h >> 1) * 32 + (h & 1) * 16 + fill[h]++);
-    };
-    int nleft = 0;
-    for (int i = 0; i < len; ++i) {
-      if (d[i] == BR) continue;  // a dummy: its slot is free
-      const int c = d[i] & 15, a = (i >> 5) * 2;
-      if (!((occ[a] >> c) & 1)) put(i, a);
-      else if (!((occ[a + 1] >> c) & 1)) put(i, a + 1);
-      else left[nleft++] = static_cast<unsigned short>(i);
-    }
-    int nrest = 0;
-    for (int q = 0; q < nleft; ++q) {
-      const int i = left[q], c = d[i] & 15, i0 = i >> 5;
-      int best = -1;
-      for (int dist = 1; dist < ni && best < 0; ++dist)
-        for (int sg = 0; sg < 2 && best < 0; ++sg) {
-          const int in = sg ? i0 - dist : i0 + dist;
-          if (in < 0 || in >= ni) continue;
-          for (int h = 2 * in; h < 2 * in + 2 && best < 0; ++h)
-            if (fill[h] < 16 && !((occ[h] >> c) & 1)) best = h;
+    __syncthreads();
+    // pass 1: a row keeps what fits its two half-warps (thread per row)
+    if (tid < ni) {
+      unsigned oa = 0, ob = 0;
+      int fa = 0, fb = 0, nl = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int i = tid * 32 + l;
+        if (d[i] == BR) continue;  // a dummy: its slot is free
+        const unsigned bit = 1u << (d[i] & 15);
+        if (!(oa & bit)) {
+          oa |= bit;
+          to[i] = static_cast<unsigned short>(tid * 32 + fa++);
+        } else if (!(ob & bit)) {
+          ob |= bit;
+          to[i] = static_cast<unsigned short>(tid * 32 + 16 + fb++);
+        } else {
+          left[tid * 32 + nl++] = static_cast<unsigned short>(i);
         }
-      if (best < 0) left[nrest++] = static_cast<unsigned short>(i);
-      else put(i, best);
-    }
-    for (int q = 0; q < nrest; ++q) {
-      const int i = left[q], i0 = i >> 5;
-      int best = -1;
-      for (int dist = 0; dist < ni && best < 0; ++dist)
-        for (int sg = 0; sg < 2 && best < 0; ++sg) {
-          const int in = sg ? i0 - dist : i0 + dist;
-          if ((sg && dist == 0) || in < 0 || in >= ni) continue;
-          for (int h = 2 * in; h < 2 * in + 2 && best < 0; ++h)
-            if (fill[h] < 16) best = h;
-        }
-      put(i, best);
-    }
-    for (int i = 0; i < len; ++i)
-      if (d[i] != BR) {
-        es[to[i]] = s[i];
-        ed[to[i]] = d[i];
       }
+      occ[2 * tid] = static_cast<unsigned short>(oa);
+      occ[2 * tid + 1] = static_cast<unsigned short>(ob);
+      fill[2 * tid] = static_cast<unsigned char>(fa);
+      fill[2 * tid + 1] = static_cast<unsigned char>(fb);
+      lcnt[tid] = static_cast<unsigned char>(nl);
+    }
+    __syncthreads();
+    // passes 2 and 3 (warp 0; lane l looks at the row at distance base + l / 2,
+    // after (even l) or before (odd l): the lowest lane that fits is the nearest)
+    if (tid < 32) {
+      int nrest = 0;
+      for (int r = 0; r < ni; ++r)
+        for (int q = 0; q < lcnt[r]; ++q) {
+          const int i = left[r * 32 + q];
+          const unsigned bit = 1u << (d[i] & 15);
+          int h = -1;
+          for (int base = 1; base < min(ni, reach) && h < 0; base += 16) {
+            const int dist = base + (lane >> 1), in = (lane & 1) ? r - dist : r + dist;
+            int mine = -1;
+            if (dist < ni && in >= 0 && in < ni) {
+              if (fill[2 * in] < 16 && !(occ[2 * in] & bit)) mine = 2 * in;
+              else if (fill[2 * in + 1] < 16 && !(occ[2 * in + 1] & bit)) mine = 2 * in + 1;
+            }
+            const unsigned vote = __ballot_sync(0xffffffffu, mine >= 0);
+            if (vote) h = __shfl_sync(0xffffffffu, mine, __ffs(vote) - 1);
+          }
+          if (lane == 0) {
+            if (h < 0) {
+              rest[nrest] = static_cast<unsigned short>(i);
+            } else {
+              occ[h] = static_cast<unsigned short>(occ[h] | bit);
+              to[i] = static_cast<unsigned short>((h >> 1) * 32 + (h & 1) * 16 + fill[h]++);
+            }
+          }
+          nrest += h < 0;
+          __syncwarp();
+        }
+      for (int q = 0; q < nrest; ++q) {
+        const int i = rest[q], r = i >> 5;
+        int h = -1;
+        for (int base = 0; base < ni && h < 0; base += 16) {
+          const int dist = base + (lane >> 1), in = (lane & 1) ? r - dist : r + dist;
+          int mine = -1;
+          if (dist < ni && !((lane & 1) && dist == 0) && in >= 0 && in < ni) {
+            if (fill[2 * in] < 16) mine = 2 * in;
+            else if (fill[2 * in + 1] < 16) mine = 2 * in + 1;
+          }
+          const unsigned vote = __ballot_sync(0xffffffffu, mine >= 0);
+          if (vote) h = __shfl_sync(0xffffffffu, mine, __ffs(vote) - 1);
+        }
+        if (lane == 0) to[i] = static_cast<unsigned short>((h >> 1) * 32 + (h & 1) * 16 + fill[h]++);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < len; i += 256)
+      if (d[i] != BR) {
+        os[to[i]] = s[i];
+        od[to[i]] = d[i];
+      }
+    __syncthreads();
     // a dummy gathers what a neighbour gathers: every unused slot reading source
     // 0 would send one request per instruction to the same L2 sector from all
     // SMs (measured: 3 % dummies with source 0 halve K5's rate)
-    unsigned near = 0u;
-    for (int i = 0; i < len && near == 0u; ++i)
-      if (d[i] != BR) near = s[i];
-    for (int r = 0; r < ni; ++r) {
-      for (int l = 0; l < 32; ++l)
-        if (ed[r * 32 + l] != BR) {
-          near = es[r * 32 + l];
+    if (tid < ni) {
+      unsigned first = 0xffffffffu;
+      for (int l = 0; l < 32 && first == 0xffffffffu; ++l)
+        if (od[tid * 32 + l] != BR) first = os[tid * 32 + l];
+      rownear[tid] = first;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned near = 0u;
+      for (int r = 0; r < ni; ++r)
+        if (rownear[r] != 0xffffffffu) {
+          near = rownear[r];
           break;
         }
-      for (int l = 0; l < 32; ++l)
-        if (ed[r * 32 + l] == BR) es[r * 32 + l] = near;
+      for (int r = 0; r < ni; ++r) {
+        if (rownear[r] != 0xffffffffu) near = rownear[r];
+        rownear[r] = near;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < len; i += 256) {
+      const int p = blk_slot_pos(i);
+      es[p] = od[i] != BR ? os[i] : rownear[i >> 5];
+      ed[p] = od[i];
+    }
+    __syncthreads();
+  }
+}
+
+// without the bank balance: slot order -> K5's lane-major order, chunk by chunk
+__global__ void k_blk_lane_major(unsigned* __restrict__ esrc, unsigned short* __restrict__ edst, long long nchunks) {
+  for (long long ch = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; ch < nchunks;
+       ch += static_cast<long long>(gridDim.x) * blockDim.x) {
+    unsigned* es = esrc + ch * kBlkChunk;
+    unsigned short* ed = edst + ch * kBlkChunk;
+    unsigned s[kBlkChunk];
+    unsigned short d[kBlkChunk];
+    for (int i = 0; i < kBlkChunk; ++i) {
+      s[i] = es[i];
+      d[i] = ed[i];
+    }
+    for (int i = 0; i < kBlkChunk; ++i) {
+      es[blk_slot_pos(i)] = s[i];
+      ed[blk_slot_pos(i)] = d[i];
     }
   }
 }
@@ -241,12 +326,21 @@ cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long 
         (e = cudaMemcpyAsync(wsd, ws.data(), ws.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
         (e = cudaMemcpyAsync(wld, wl.data(), wl.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       return done(e);
-    if (win == 256) k_blk_banks<256><<<592, 64, 0, s>>>(esrc, edst, wsd, wld, nw, BR);
-    else if (win == 1024) k_blk_banks<1024><<<592, 64, 0, s>>>(esrc, edst, wsd, wld, nw, BR);
-    else if (win == 2048) k_blk_banks<2048><<<592, 64, 0, s>>>(esrc, edst, wsd, wld, nw, BR);
-    else if (win == 4096) k_blk_banks<4096><<<592, 32, 0, s>>>(esrc, edst, wsd, wld, nw, BR);
-    else k_blk_banks<8192><<<592, 32, 0, s>>>(esrc, edst, wsd, wld, nw, BR);
+    auto balance = [&](auto kern, int w) {
+      const size_t smem = static_cast<size_t>(w) * 18 + static_cast<size_t>(w / 32) * 11;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      const char* er = std::getenv("LR_BLK_REACH");
+      kern<<<static_cast<unsigned>(std::min<long long>(nw, 4 * 148)), 256, smem, s>>>(esrc, edst, wsd, wld, nw, BR,
+                                                                                   er ? std::atoi(er) : kBlkReach);
+    };
+    if (win == 256) balance(k_blk_banks<256>, 256);
+    else if (win == 1024) balance(k_blk_banks<1024>, 1024);
+    else if (win == 2048) balance(k_blk_banks<2048>, 2048);
+    else if (win == 4096) balance(k_blk_banks<4096>, 4096);
+    else balance(k_blk_banks<8192>, 8192);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return done(e);  // ws / wl are host temporaries
+  } else if (!pad_off.empty() && pad_off.back() > 0) {
+    k_blk_lane_major<<<1184, 128, 0, s>>>(esrc, edst, pad_off.back() / kBlkChunk);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return done(e);
   return done(cudaStreamSynchronize(s));

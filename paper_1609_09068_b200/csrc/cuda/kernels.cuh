@@ -286,7 +286,8 @@ void launch_propagate(const int* dst_order, const long long* seg_ptr, int nseg, 
 constexpr int kBlkThreads = LR_BLK_THREADS;
 constexpr int kBlkChunk = 256;    // slots per warp step (8 per lane, lane-strided)
 constexpr int kBlkWindow = 8192;  // slots the bank balance looks at together (blk.cu k_blk_banks)
-constexpr int kBlkSlack = 0;      // rows of 32 entries per empty row (0: none)
+constexpr int kBlkSlack = 32;     // rows of 32 entries per empty row (0: none)
+constexpr int kBlkReach = 1 << 20;  // rows a left-over entry looks at on either side for a conflict-free slot
 struct BlkPart {
   long long e0;  // first entry (into esrc/edst)
   int n;         // entries (multiple of kBlkChunk)

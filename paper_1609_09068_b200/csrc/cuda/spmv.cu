@@ -700,7 +700,8 @@ __global__ void __launch_bounds__(kSegThreads, 1)
 // K5: one power-series iteration of a large grid unit by dest-row blocks
 // (DESIGN.md §4.1 "K5").  A CTA claims parts (a contiguous range of one
 // block's in-edges, sorted by source) from a global counter; its warps walk the
-// part 256 entries at a time, lane l taking entries l, l+32, ..., so each
+// part 256 slots at a time, lane l taking slots l, l+32, ... (stored lane-major,
+// so its 8 sources and 8 dest rows are two vector loads), so each
 // gather instruction reads 32 CONSECUTIVE sources of the sorted list: where the
 // sources are dense (the high-degree rows that carry most in-edges) they share
 // 128-byte lines and one L2 request serves many in-edges -- the pull SpMV's
@@ -711,15 +712,22 @@ __global__ void __launch_bounds__(kSegThreads, 1)
 // its CTA (rank += y, s' = pf y, max), a split block's parts add their rows into
 // yacc and the last one to arrive finishes them.  Summation order depends on
 // the atomics' arrival order (rows agree to ~1e-16; iteration counts asserted).
-__device__ __forceinline__ unsigned ld_stream_u32(const unsigned* p, std::uint64_t pol) {
-  unsigned v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ unsigned ld_stream_u16(const unsigned short* p, std::uint64_t pol) {
-  unsigned short v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
-  return v;
+// a lane's 8 slots of a chunk (slot lane + 32 k, stored at lane * 8 + k): 8
+// sources with one 256-bit load, 8 dest rows with one 128-bit load
+__device__ __forceinline__ void ld_blk_idx(const unsigned* es, const unsigned short* ed, int lane,
+                                           std::uint64_t pol, unsigned (&j)[8], unsigned (&d)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(j[0]), "=r"(j[1]), "=r"(j[2]), "=r"(j[3]), "=r"(j[4]), "=r"(j[5]), "=r"(j[6]), "=r"(j[7])
+               : "l"(es + lane * 8), "l"(pol));
+  unsigned q[4];
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
+               : "l"(ed + lane * 8), "l"(pol));
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    d[2 * m] = q[m] & 0xffffu;
+    d[2 * m + 1] = q[m] >> 16;
+  }
 }
 template <int GATHER_L1>
 __device__ __forceinline__ double ld_blk_gather(const double* p, std::uint64_t pol) {
@@ -769,12 +777,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       // the next chunk's indices load while this chunk's gathers are in flight
       int c = warp * kBlkChunk;
       unsigned j[8], d[8];
-      if (c < P.n) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) j[k] = ld_stream_u32(es + c + lane + 32 * k, stream);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) d[k] = ld_stream_u16(ed + c + lane + 32 * k, stream);
-      }
+      if (c < P.n) ld_blk_idx(es + c, ed + c, lane, stream, j, d);
       for (; c < P.n; c += kW * kBlkChunk) {
         double v[8];
 #pragma unroll
@@ -784,12 +787,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         }
         const int cn = c + kW * kBlkChunk;
         unsigned jn[8], dn[8];
-        if (cn < P.n) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) jn[k] = ld_stream_u32(es + cn + lane + 32 * k, stream);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) dn[k] = ld_stream_u16(ed + cn + lane + 32 * k, stream);
-        }
+        if (cn < P.n) ld_blk_idx(es + cn, ed + cn, lane, stream, jn, dn);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (d[k] != ubr) atomicAdd(y + d[k], v[k]);  // dummies (unused slots) add nothing
@@ -802,10 +800,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     } else {
       for (int c = warp * kBlkChunk; c < P.n; c += kW * kBlkChunk) {
         unsigned j[8], d[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) j[k] = ld_stream_u32(es + c + lane + 32 * k, stream);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) d[k] = ld_stream_u16(ed + c + lane + 32 * k, stream);
+        ld_blk_idx(es + c, ed + c, lane, stream, j, d);
         double v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -970,13 +965,15 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
 }
 
 // K5 launch: one persistent CTA per SM (y takes BR + 1 doubles of shared memory).
-// LR_BLK_L1=1 makes the gathers allocate in L1 (measured slightly slower at
-// config 5: 3924 vs 3952 GB/s); LR_BLK_PIPE=0 drops the index prefetch.
+// The gathers allocate in L1 (LR_BLK_L1=0: not): with the bank balance an entry
+// moved to a neighbouring row finds its line already fetched by that row
+// (5,110 -> 5,189 GB/s at config 5; before the balance it measured slightly
+// slower, 3,924 vs 3,952); LR_BLK_PIPE=0 drops the index prefetch.
 void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
                      double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
                      int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
   const char* e_l1 = std::getenv("LR_BLK_L1");
-  const bool l1 = e_l1 && std::atoi(e_l1) != 0;
+  const bool l1 = !(e_l1 && std::atoi(e_l1) == 0);
   const char* e_pipe = std::getenv("LR_BLK_PIPE");
   const bool pipe = !(e_pipe && std::atoi(e_pipe) == 0);
   static int sms = 0;
