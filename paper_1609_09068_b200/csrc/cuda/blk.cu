@@ -93,31 +93,35 @@ __device__ __forceinline__ int blk_slot_pos(int i) { return (i & ~255) | ((i & 3
 // gather instruction keeps most of its 32 adjacent sources; an in-order greedy
 // placement cascades instead (an entry pushed into a neighbour pushes the
 // neighbour's own entries on: measured 4,700 vs 5,050 GB/s at config 5).
+// The bank pairs do not interact in pass 2: a half-warp that lacks a bank pair
+// has a free slot (16 slots, at most one entry per pair until pass 3), so warp c
+// places the left-overs of bank pair c on its own, in order, and an entry's lane
+// inside its half-warp is the rank of its bank pair among the half's pairs --
+// the layout does not depend on how the warps interleave.
+constexpr int kBanksThreads = 512;  // 16 warps: one per bank pair in pass 2
 template <int W>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kBanksThreads, 1)
     k_blk_banks(unsigned* __restrict__ esrc, unsigned short* __restrict__ edst, const long long* __restrict__ wstart,
                 const int* __restrict__ wlen, long long nwin, int BR, int reach) {
   constexpr int NI = W / 32;  // instruction rows of a full window
-  static_assert(NI <= 256, "one thread per row in pass 1");
+  static_assert(NI <= kBanksThreads, "one thread per row in pass 1");
   extern __shared__ unsigned char blk_smem[];
-  unsigned* s = reinterpret_cast<unsigned*>(blk_smem);        // [W] entries as packed (slot order)
-  unsigned* os = s + W;                                       // [W] placed
-  unsigned short* d = reinterpret_cast<unsigned short*>(os + W);
+  unsigned* s = reinterpret_cast<unsigned*>(blk_smem);  // [W] entries as packed (slot order)
+  unsigned* os = s + W;                                 // [W] placed
+  unsigned* occ = os + W;                               // [2 NI] bank pairs taken per half-warp (low 16 bits)
+  unsigned* rownear = occ + 2 * NI;                     // [NI]
+  unsigned short* d = reinterpret_cast<unsigned short*>(rownear + NI);
   unsigned short* od = d + W;
-  unsigned short* to = od + W;    // slot an entry goes to
-  unsigned short* left = to + W;  // pass 1 left-overs, 32 per row
-  unsigned short* rest = left + W;  // pass 2 left-overs
-  unsigned short* occ = rest + W;   // [2 NI] bank pairs taken per half-warp
-  unsigned* rownear = reinterpret_cast<unsigned*>(occ + 2 * NI);  // [NI]
-  unsigned char* fill = reinterpret_cast<unsigned char*>(rownear + NI);  // [2 NI]
-  unsigned char* lcnt = fill + 2 * NI;                                    // [NI]
-  __shared__ int s_nrest;
-  const int tid = threadIdx.x, lane = tid & 31;
+  unsigned short* half = od + W;    // half-warp an entry goes to (0xffff: pass 3 decides)
+  unsigned short* left = half + W;  // pass 1 left-overs, 32 per row
+  unsigned char* extra = reinterpret_cast<unsigned char*>(left + W);  // [2 NI] pass 3 entries per half-warp
+  unsigned char* lcnt = extra + 2 * NI;                               // [NI]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (long long wi = blockIdx.x; wi < nwin; wi += gridDim.x) {
     unsigned* es = esrc + wstart[wi];
     unsigned short* ed = edst + wstart[wi];
     const int len = wlen[wi], ni = len / 32;
-    for (int i = tid; i < len; i += 256) {
+    for (int i = tid; i < len; i += kBanksThreads) {
       s[i] = es[i];
       d[i] = ed[i];
       os[i] = 0u;
@@ -127,80 +131,90 @@ __global__ void __launch_bounds__(256, 1)
     // pass 1: a row keeps what fits its two half-warps (thread per row)
     if (tid < ni) {
       unsigned oa = 0, ob = 0;
-      int fa = 0, fb = 0, nl = 0;
+      int nl = 0;
       for (int l = 0; l < 32; ++l) {
         const int i = tid * 32 + l;
         if (d[i] == BR) continue;  // a dummy: its slot is free
         const unsigned bit = 1u << (d[i] & 15);
         if (!(oa & bit)) {
           oa |= bit;
-          to[i] = static_cast<unsigned short>(tid * 32 + fa++);
+          half[i] = static_cast<unsigned short>(2 * tid);
         } else if (!(ob & bit)) {
           ob |= bit;
-          to[i] = static_cast<unsigned short>(tid * 32 + 16 + fb++);
+          half[i] = static_cast<unsigned short>(2 * tid + 1);
         } else {
           left[tid * 32 + nl++] = static_cast<unsigned short>(i);
         }
       }
-      occ[2 * tid] = static_cast<unsigned short>(oa);
-      occ[2 * tid + 1] = static_cast<unsigned short>(ob);
-      fill[2 * tid] = static_cast<unsigned char>(fa);
-      fill[2 * tid + 1] = static_cast<unsigned char>(fb);
+      occ[2 * tid] = oa;
+      occ[2 * tid + 1] = ob;
+      extra[2 * tid] = extra[2 * tid + 1] = 0;
       lcnt[tid] = static_cast<unsigned char>(nl);
     }
     __syncthreads();
-    // passes 2 and 3 (warp 0; lane l looks at the row at distance base + l / 2,
-    // after (even l) or before (odd l): the lowest lane that fits is the nearest)
-    if (tid < 32) {
-      int nrest = 0;
+    // pass 2 (warp c = bank pair c; lane l looks at the row at distance
+    // base + l / 2, after (even l) or before (odd l): the lowest lane that fits
+    // is the nearest)
+    if (warp < 16) {
+      const unsigned bit = 1u << warp;
       for (int r = 0; r < ni; ++r)
         for (int q = 0; q < lcnt[r]; ++q) {
           const int i = left[r * 32 + q];
-          const unsigned bit = 1u << (d[i] & 15);
+          if ((d[i] & 15) != warp) continue;
           int h = -1;
           for (int base = 1; base < min(ni, reach) && h < 0; base += 16) {
             const int dist = base + (lane >> 1), in = (lane & 1) ? r - dist : r + dist;
             int mine = -1;
             if (dist < ni && in >= 0 && in < ni) {
-              if (fill[2 * in] < 16 && !(occ[2 * in] & bit)) mine = 2 * in;
-              else if (fill[2 * in + 1] < 16 && !(occ[2 * in + 1] & bit)) mine = 2 * in + 1;
+              if (!(occ[2 * in] & bit)) mine = 2 * in;
+              else if (!(occ[2 * in + 1] & bit)) mine = 2 * in + 1;
             }
             const unsigned vote = __ballot_sync(0xffffffffu, mine >= 0);
             if (vote) h = __shfl_sync(0xffffffffu, mine, __ffs(vote) - 1);
           }
           if (lane == 0) {
-            if (h < 0) {
-              rest[nrest] = static_cast<unsigned short>(i);
-            } else {
-              occ[h] = static_cast<unsigned short>(occ[h] | bit);
-              to[i] = static_cast<unsigned short>((h >> 1) * 32 + (h & 1) * 16 + fill[h]++);
-            }
+            if (h >= 0) atomicOr(&occ[h], bit);  // other warps set other bits of the same word
+            half[i] = static_cast<unsigned short>(h >= 0 ? h : 0xffff);
           }
-          nrest += h < 0;
           __syncwarp();
         }
-      for (int q = 0; q < nrest; ++q) {
-        const int i = rest[q], r = i >> 5;
-        int h = -1;
-        for (int base = 0; base < ni && h < 0; base += 16) {
-          const int dist = base + (lane >> 1), in = (lane & 1) ? r - dist : r + dist;
-          int mine = -1;
-          if (dist < ni && !((lane & 1) && dist == 0) && in >= 0 && in < ni) {
-            if (fill[2 * in] < 16) mine = 2 * in;
-            else if (fill[2 * in + 1] < 16) mine = 2 * in + 1;
-          }
-          const unsigned vote = __ballot_sync(0xffffffffu, mine >= 0);
-          if (vote) h = __shfl_sync(0xffffffffu, mine, __ffs(vote) - 1);
-        }
-        if (lane == 0) to[i] = static_cast<unsigned short>((h >> 1) * 32 + (h & 1) * 16 + fill[h]++);
-        __syncwarp();
-      }
     }
     __syncthreads();
-    for (int i = tid; i < len; i += 256)
+    // pass 3 (warp 0): entries without a conflict-free half-warp anywhere in the
+    // window take the nearest free slot, in order
+    if (warp == 0)
+      for (int i0 = 0; i0 < len; i0 += 32) {
+        unsigned todo = __ballot_sync(0xffffffffu, d[i0 + lane] != BR && half[i0 + lane] == 0xffffu);
+        for (; todo; todo &= todo - 1) {
+          const int i = i0 + __ffs(todo) - 1, r = i >> 5;
+          int h = -1;
+          for (int base = 0; base < ni && h < 0; base += 16) {
+            const int dist = base + (lane >> 1), in = (lane & 1) ? r - dist : r + dist;
+            int mine = -1;
+            if (dist < ni && !((lane & 1) && dist == 0) && in >= 0 && in < ni) {
+              if (__popc(occ[2 * in]) + extra[2 * in] < 16) mine = 2 * in;
+              else if (__popc(occ[2 * in + 1]) + extra[2 * in + 1] < 16) mine = 2 * in + 1;
+            }
+            const unsigned vote = __ballot_sync(0xffffffffu, mine >= 0);
+            if (vote) h = __shfl_sync(0xffffffffu, mine, __ffs(vote) - 1);
+          }
+          if (lane == 0) {  // behind the half-warp's conflict-free entries
+            half[i] = static_cast<unsigned short>(h | 0x8000);
+            left[i] = static_cast<unsigned short>(extra[h]++);
+          }
+          __syncwarp();
+        }
+      }
+    __syncthreads();
+    for (int i = tid; i < len; i += kBanksThreads)
       if (d[i] != BR) {
-        os[to[i]] = s[i];
-        od[to[i]] = d[i];
+        const int h = half[i] & 0x7fff;
+        const unsigned o = occ[h], bit = 1u << (d[i] & 15);
+        // conflict-free entries by the rank of their bank pair, pass 3 entries behind them
+        const int lane_in_half = (half[i] & 0x8000) ? __popc(o) + left[i] : __popc(o & (bit - 1));
+        const int slot = (h >> 1) * 32 + (h & 1) * 16 + lane_in_half;
+        os[slot] = s[i];
+        od[slot] = d[i];
       }
     __syncthreads();
     // a dummy gathers what a neighbour gathers: every unused slot reading source
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     __syncthreads();
-    for (int i = tid; i < len; i += 256) {
+    for (int i = tid; i < len; i += kBanksThreads) {
       const int p = blk_slot_pos(i);
       es[p] = od[i] != BR ? os[i] : rownear[i >> 5];
       ed[p] = od[i];
@@ -327,10 +341,10 @@ cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long 
         (e = cudaMemcpyAsync(wld, wl.data(), wl.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       return done(e);
     auto balance = [&](auto kern, int w) {
-      const size_t smem = static_cast<size_t>(w) * 18 + static_cast<size_t>(w / 32) * 11;
+      const size_t smem = static_cast<size_t>(w) * 16 + static_cast<size_t>(w / 32) * 15;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       const char* er = std::getenv("LR_BLK_REACH");
-      kern<<<static_cast<unsigned>(std::min<long long>(nw, 4 * 148)), 256, smem, s>>>(esrc, edst, wsd, wld, nw, BR,
+      kern<<<static_cast<unsigned>(std::min<long long>(nw, 4 * 148)), kBanksThreads, smem, s>>>(esrc, edst, wsd, wld, nw, BR,
                                                                                    er ? std::atoi(er) : kBlkReach);
     };
     if (win == 256) balance(k_blk_banks<256>, 256);
