@@ -527,7 +527,7 @@ int64_t lr_ctx_device_bytes(const lr_ctx* c) {
 // K5 for every level whose grid SpMV is one large unit on one GPU: its in-edges
 // by dest-row blocks of BR rows, sorted by source (built on the device from the
 // uploaded CSR, spmv.cu k_spmv_blk).  LR_BLK=0 keeps K4c everywhere;
-// LR_BLK_MIN_ROWS (default 2^22) sets "large", LR_BLK_ROWS the block rows
+// LR_BLK_MIN_ROWS (default 2^21) sets "large", LR_BLK_ROWS the block rows
 // (default 16384), LR_BLK_PART the slots per part (default: about eight parts
 // per SM), LR_BLK_WIN the bank-balance window (0 or LR_BLK_BANKS=0: none),
 // LR_BLK_SLACK the rows of entries per empty row (0: none).
@@ -541,7 +541,7 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
   const char* e_on = std::getenv("LR_BLK");
   if ((e_on && std::atoi(e_on) == 0) || ctx->comm || !spmv_seg()) return LR_OK;
   const char* e_min = std::getenv("LR_BLK_MIN_ROWS");
-  const long long min_rows = e_min ? std::atoll(e_min) : (1ll << 22);
+  const long long min_rows = e_min ? std::atoll(e_min) : (1ll << 21);
   const char* e_br = std::getenv("LR_BLK_ROWS");
   const int BR = std::max(32, std::min(e_br ? std::atoi(e_br) : 16384, (kMaxDynSmem / 8) - 64));
   int sms = 0;
