@@ -527,7 +527,8 @@ int64_t lr_ctx_device_bytes(const lr_ctx* c) {
 // K5 for every level whose grid SpMV is one large unit on one GPU: its in-edges
 // by dest-row blocks of BR rows, sorted by source (built on the device from the
 // uploaded CSR, spmv.cu k_spmv_blk).  LR_BLK=0 keeps K4c everywhere;
-// LR_BLK_MIN_ROWS (default 2^21) sets "large", LR_BLK_ROWS the block rows
+// LR_BLK_MIN_ROWS (default 2^21) and LR_BLK_MIN_DEG (in-edges per row, default
+// 8) set "large", LR_BLK_ROWS the block rows
 // (default 16384), LR_BLK_PART the slots per part (default: about eight parts
 // per SM), LR_BLK_WIN the bank-balance window (0 or LR_BLK_BANKS=0: none),
 // LR_BLK_SLACK the rows of entries per empty row (0: none).
@@ -552,6 +553,9 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     const int u0 = L->unit_row_begin[u], R = L->unit_row_begin[u + 1] - u0;
     if (R < min_rows || R <= 0) continue;
     const long long e_begin = L->iptr[u0], E = L->iptr[u0 + R] - e_begin;
+    // sparse units (config 3's whole-graph baseline: 5.6 in-edges per row) have too
+    // few entries per block for the sorted gathers to share lines: K4c
+    if (E < static_cast<long long>(env_int("LR_BLK_MIN_DEG", 8)) * R) continue;
     const int nb = static_cast<int>((static_cast<long long>(R) + BR - 1) / BR);
     // slots of a block's run: its entries in rows of 32 (one K5 gather
     // instruction), one empty row after every `slack` rows (free slots for the

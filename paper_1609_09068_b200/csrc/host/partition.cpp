@@ -403,6 +403,11 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     for (std::int64_t v = b; v < e; ++v) comp[static_cast<std::size_t>(v)] = cidx[static_cast<std::size_t>(label[static_cast<std::size_t>(v)])];
   });
   std::vector<std::int32_t>().swap(cidx);
+  // edges that leave their SCC, one bit each (plan_internal.hpp): recorded by the
+  // two scans below that look every edge's components up anyway
+  uvector<std::uint64_t> cross_out(static_cast<std::size_t>((m_all + 63) / 64)), cross_in(static_cast<std::size_t>((m_in + 63) / 64));
+  parallel_chunks(static_cast<std::int64_t>(cross_out.size()), [&](int, std::int64_t b, std::int64_t e) { std::fill(cross_out.begin() + b, cross_out.begin() + e, 0); });
+  parallel_chunks(static_cast<std::int64_t>(cross_in.size()), [&](int, std::int64_t b, std::int64_t e) { std::fill(cross_in.begin() + b, cross_in.begin() + e, 0); });
   // members grouped by component (CSR), cross out-edge counts.  The giant
   // SCC (one component, a large share of the vertices) is counted per thread
   // instead of by atomics on one counter.
@@ -414,6 +419,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   std::vector<std::vector<VertexId>> gmem(static_cast<std::size_t>(T));
   std::vector<std::int64_t> gpend(static_cast<std::size_t>(T), 0);
   parallel_chunks(n, [&](int th, std::int64_t b, std::int64_t e) {
+    detail::CrossBits bits(cross_out.data());
     for (std::int64_t vv = b; vv < e; ++vv) {
       const VertexId v = static_cast<VertexId>(vv);
       const std::int32_t c = comp[static_cast<std::size_t>(v)];
@@ -421,7 +427,10 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       const EdgeId k1 = adj.off[v + 1];
       for (EdgeId k = adj.off[v]; k < k1; ++k) {
         if (k + kAhead < m_all) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
-        x += comp[static_cast<std::size_t>(adj.tgt[k])] != c;
+        if (comp[static_cast<std::size_t>(adj.tgt[k])] != c) {
+          ++x;
+          bits.set(k);
+        }
       }
       if (c == cg) {
         gmem[static_cast<std::size_t>(th)].push_back(v);
@@ -482,24 +491,25 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     std::int32_t hi = 0;
     for (std::int64_t i = m0; i < m1; ++i) {
       const VertexId u = members[static_cast<std::size_t>(i)];
-      const EdgeId k1 = adj.off[u + 1];
-      for (EdgeId k = adj.off[u]; k < k1; ++k) {
-        if (k + kAhead < m_all) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
-        const std::int32_t cw = comp[static_cast<std::size_t>(adj.tgt[k])];
-        if (cw != c) hi = std::max(hi, level[static_cast<std::size_t>(cw)]);
-      }
+      detail::for_cross_bits(cross_out.data(), adj.off[u], adj.off[u + 1], [&](EdgeId k) {
+        hi = std::max(hi, level[static_cast<std::size_t>(comp[static_cast<std::size_t>(adj.tgt[k])])]);
+      });
     }
+    (void)c;
     return hi;
   };
   auto release = [&](int th, std::int32_t c, std::int64_t m0, std::int64_t m1) {
     auto& out = next.parts[static_cast<std::size_t>(th)];
+    detail::CrossBits bits(cross_in.data());
     for (std::int64_t i = m0; i < m1; ++i) {
       const VertexId u = members[static_cast<std::size_t>(i)];
       const EdgeId k1 = adj.in_off[static_cast<std::size_t>(u) + 1];
       for (EdgeId k = adj.in_off[static_cast<std::size_t>(u)]; k < k1; ++k) {
         if (k + kAhead < m_in) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k + kAhead)])]);
         const std::int32_t cp = comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k)])];
-        if (cp != c && atomic_sub(pending[static_cast<std::size_t>(cp)], std::int64_t{1}) == 1) out.push_back(cp);
+        if (cp == c) continue;
+        bits.set(k);
+        if (atomic_sub(pending[static_cast<std::size_t>(cp)], std::int64_t{1}) == 1) out.push_back(cp);
       }
     }
   };
@@ -614,6 +624,8 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   if (keep_in) {
     keep_in->off = std::move(adj.in_off);
     keep_in->src = std::move(adj.in_src);
+    keep_in->cross_out = std::move(cross_out);
+    keep_in->cross_in = std::move(cross_in);
   }
   return p;
 }

@@ -366,6 +366,10 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   std::vector<std::int32_t> unit_out(nn, 0);
   std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
   const EdgeId m_all = off[n];
+  // with the partition's cross-edge bits only the edges that leave their SCC need
+  // their components looked up (a clear bit: same SCC, same component)
+  const std::uint64_t* xo_bits = in && !in->cross_out.empty() ? in->cross_out.data() : nullptr;
+  const std::uint64_t* xi_bits = in && !in->cross_in.empty() ? in->cross_in.data() : nullptr;
   detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     EdgeId li = 0, lx = 0, ld = 0;
     for (std::int64_t uu = b; uu < e; ++uu) {
@@ -373,6 +377,22 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
       const VertexId cu = comp_of[static_cast<std::size_t>(u)];
       std::int32_t k = 0;
       const EdgeId q1 = off[u + 1];
+      if (xo_bits) {
+        EdgeId self = 0;
+        if (lp[u])
+          for (EdgeId q = off[u]; q < q1; ++q) self += tgt[q] == u;
+        EdgeId leaving = 0, merged = 0;  // out of the SCC; of those, inside the final component
+        detail::for_cross_bits(xo_bits, off[u], q1, [&](EdgeId q) {
+          ++leaving;
+          merged += comp_of[static_cast<std::size_t>(tgt[q])] == cu;
+        });
+        k = static_cast<std::int32_t>((q1 - off[u]) - self - leaving + merged + (keep ? self : 0));
+        if (!keep) ld += self;
+        lx += leaving - merged;
+        unit_out[static_cast<std::size_t>(u)] = k;
+        li += k;
+        continue;
+      }
       for (EdgeId q = off[u]; q < q1; ++q) {
         const VertexId v = tgt[q];
         if (q + 16 < m_all) __builtin_prefetch(&comp_of[static_cast<std::size_t>(tgt[q + 16])]);
@@ -481,10 +501,17 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
         const VertexId cv = comp_of[static_cast<std::size_t>(v)];
         EdgeId ni = row_loop(v) ? 1 : 0, nx = 0;
         const EdgeId k1 = in->off[static_cast<std::size_t>(v) + 1];
-        for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
-          ahead(k);
-          if (comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k)])] == cv) ++ni;
-          else ++nx;
+        if (xi_bits) {
+          detail::for_cross_bits(xi_bits, in->off[static_cast<std::size_t>(v)], k1, [&](EdgeId k) {
+            nx += comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k)])] != cv;
+          });
+          ni += (k1 - in->off[static_cast<std::size_t>(v)]) - nx;
+        } else {
+          for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
+            ahead(k);
+            if (comp_of[static_cast<std::size_t>(in->src[static_cast<std::size_t>(k)])] == cv) ++ni;
+            else ++nx;
+          }
         }
         const std::size_t r = static_cast<std::size_t>(L.row_of[static_cast<std::size_t>(v)]);
         icnt[r] = ni;
@@ -503,12 +530,15 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
         const EdgeId k1 = in->off[static_cast<std::size_t>(v) + 1];
         for (EdgeId k = in->off[static_cast<std::size_t>(v)]; k < k1; ++k) {
           const VertexId src = in->src[static_cast<std::size_t>(k)];
-          ahead(k);
+          if (!xi_bits) ahead(k);
           if (loop_due && src > v) {
             L.isrc[static_cast<std::size_t>(ai++)] = v;
             loop_due = false;
           }
-          if (comp_of[static_cast<std::size_t>(src)] == cv) L.isrc[static_cast<std::size_t>(ai++)] = src;
+          const bool intra = xi_bits && !((xi_bits[k >> 6] >> (k & 63)) & 1)
+                                 ? true
+                                 : comp_of[static_cast<std::size_t>(src)] == cv;
+          if (intra) L.isrc[static_cast<std::size_t>(ai++)] = src;
           else L.xsrc[static_cast<std::size_t>(ax++)] = src;
         }
         if (loop_due) L.isrc[static_cast<std::size_t>(ai++)] = v;

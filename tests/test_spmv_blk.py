@@ -21,6 +21,7 @@ CASES = [  # (block rows, entries per part)
 def _force(monkeypatch, br, part):
     monkeypatch.setenv("LR_BLK", "1")
     monkeypatch.setenv("LR_BLK_MIN_ROWS", "0")
+    monkeypatch.setenv("LR_BLK_MIN_DEG", "0")
     monkeypatch.setenv("LR_BLK_ROWS", str(br))
     if part:
         monkeypatch.setenv("LR_BLK_PART", str(part))
