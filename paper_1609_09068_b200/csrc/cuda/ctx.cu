@@ -589,16 +589,29 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     }
     // heaviest parts first: the launch's tail is made of the light ones
     std::stable_sort(parts.begin(), parts.end(), [](const BlkPart& x, const BlkPart& y) { return x.n > y.n; });
+    // the layout and its build (sort keys, double buffers: ~20 B per in-edge of
+    // scratch) may not fit next to a graph close to the HBM capacity: that unit
+    // keeps K4c, which needs nothing beyond the CSR
     auto U = std::make_unique<lr_ctx::BlkUnit>();
-    LR_CUDA_TRY(U->esrc.alloc(static_cast<size_t>(total)));
-    LR_CUDA_TRY(U->edst.alloc(static_cast<size_t>(total)));
-    LR_CUDA_TRY(U->parts.upload(parts.data(), parts.size(), s));
-    LR_CUDA_TRY(U->yacc.alloc(static_cast<size_t>(nslots) * BR));
-    LR_CUDA_TRY(U->bcnt.alloc(static_cast<size_t>(nslots)));
-    LR_CUDA_TRY(cudaMemsetAsync(U->yacc.p, 0, U->yacc.bytes(), s));
-    LR_CUDA_TRY(cudaMemsetAsync(U->bcnt.p, 0, U->bcnt.bytes(), s));
-    LR_CUDA_TRY(build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, R, BR, pad_off, slack, win, U->esrc.p,
-                                  U->edst.p, s));
+    auto build = [&]() -> cudaError_t {
+      cudaError_t e;
+      if ((e = U->esrc.alloc(static_cast<size_t>(total))) != cudaSuccess) return e;
+      if ((e = U->edst.alloc(static_cast<size_t>(total))) != cudaSuccess) return e;
+      if ((e = U->parts.upload(parts.data(), parts.size(), s)) != cudaSuccess) return e;
+      if ((e = U->yacc.alloc(static_cast<size_t>(nslots) * BR)) != cudaSuccess) return e;
+      if ((e = U->bcnt.alloc(static_cast<size_t>(nslots))) != cudaSuccess) return e;
+      if ((e = cudaMemsetAsync(U->yacc.p, 0, U->yacc.bytes(), s)) != cudaSuccess) return e;
+      if ((e = cudaMemsetAsync(U->bcnt.p, 0, U->bcnt.bytes(), s)) != cudaSuccess) return e;
+      return build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, R, BR, pad_off, slack, win, U->esrc.p,
+                               U->edst.p, s);
+    };
+    if (const cudaError_t e = build(); e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();  // cleared: not sticky
+      cudaStreamSynchronize(s);
+      continue;
+    } else {
+      LR_CUDA_TRY(e);
+    }
     U->dev = BlkUnitDev{U->esrc.p, U->edst.p, U->parts.p, static_cast<int>(parts.size()), u0, R, BR, U->yacc.p,
                         U->bcnt.p};
     T.blk = static_cast<int>(ctx->blk.size());

@@ -53,6 +53,19 @@ void parallel_chunks(std::int64_t n, F&& f, std::int64_t grain = 1 << 15) {
   pool_run(t, [&](int i) { f(i, n * i / t, n * (i + 1) / t); });
 }
 
+// A multi-hundred-MB array filled by one thread costs as much as a parallel
+// pass over the edges that use it: fill (and first-touch) from all threads.
+template <typename T>
+void parallel_fill(T* p, std::int64_t n, T value) {
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) { std::fill(p + b, p + e, value); }, 1 << 18);
+}
+template <typename T>
+uvector<T> filled(std::size_t n, T value) {
+  uvector<T> v(n);
+  parallel_fill(v.data(), static_cast<std::int64_t>(n), value);
+  return v;
+}
+
 // Dynamic scheduling over [0, n) in blocks of `block` (for skewed work).
 template <typename F>
 void parallel_dynamic(std::int64_t n, std::int64_t block, F&& f) {

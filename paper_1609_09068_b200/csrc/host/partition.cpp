@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <thread>
@@ -105,6 +106,7 @@ inline std::int64_t item_grain(std::int64_t n) { return n >= (1 << 22) ? 64 : 40
 struct Adjacency {
   const EdgeId* off;
   const VertexId* tgt;
+  const std::uint8_t* loop;  // vertex has a self-loop among its out-edges
   uvector<EdgeId> in_off;  // in-edges (self-loops left out), source-ascending rows
   uvector<VertexId> in_src;
 };
@@ -113,19 +115,20 @@ struct Adjacency {
 class SccFinder {
  public:
   SccFinder(VertexId n, const Adjacency& a, detail::PhaseClock& clk)
-      : n_(n), a_(a), clk_(clk), label_(static_cast<std::size_t>(n), -1) {}
+      : n_(n), a_(a), clk_(clk), label_(detail::filled<VertexId>(static_cast<std::size_t>(n), -1)) {}
 
   // label[v] = a representative vertex of v's SCC
-  std::vector<VertexId> run() {
+  uvector<VertexId> run() {
     const std::size_t nn = static_cast<std::size_t>(n_);
-    din_.assign(nn, 0);
-    dout_.assign(nn, 0);
-    queued_.assign(nn, 0);
+    din_.resize(nn);  // both written for every vertex below
+    dout_.resize(nn);
+    queued_ = detail::filled<std::uint8_t>(nn, 0);
     parallel_chunks(n_, [&](int, std::int64_t b, std::int64_t e) {
       for (std::int64_t v = b; v < e; ++v) {
         din_[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(a_.in_off[static_cast<std::size_t>(v) + 1] - a_.in_off[static_cast<std::size_t>(v)]);
-        std::int32_t d = 0;
-        for (EdgeId k = a_.off[v]; k < a_.off[v + 1]; ++k) d += a_.tgt[k] != v;
+        std::int32_t d = static_cast<std::int32_t>(a_.off[v + 1] - a_.off[v]);
+        if (a_.loop[v])  // only looped vertices need their out-edges counted
+          for (EdgeId k = a_.off[v]; k < a_.off[v + 1]; ++k) d -= a_.tgt[k] == v;
         dout_[static_cast<std::size_t>(v)] = d;
       }
     });
@@ -283,7 +286,7 @@ class SccFinder {
   // Tarjan's algorithm (SCC labels only) over the live vertices.
   void tarjan_rest() {
     const std::size_t nn = static_cast<std::size_t>(n_);
-    std::vector<std::int32_t> order(nn, -1), low(nn, 0);
+    uvector<std::int32_t> order = detail::filled<std::int32_t>(nn, -1), low(nn);  // low is set when a vertex opens
     std::vector<VertexId> pending;
     std::vector<std::pair<VertexId, EdgeId>> stack;
     std::int32_t clock = 0;
@@ -328,15 +331,15 @@ class SccFinder {
  public:
   VertexId giant_ = -1;  // representative of the SCC found by reachability (-1: none)
  private:
-  std::vector<VertexId> label_;
-  std::vector<std::int32_t> din_, dout_;
-  std::vector<std::uint8_t> queued_;
+  uvector<VertexId> label_;
+  uvector<std::int32_t> din_, dout_;
+  uvector<std::uint8_t> queued_;
 };
 
 // Disjoint sets over component indices (union by size, path halving).
 struct Sets {
-  std::vector<std::int32_t> up;
-  explicit Sets(std::int32_t k) : up(static_cast<std::size_t>(k), -1) {}
+  uvector<std::int32_t> up;
+  explicit Sets(std::int32_t k) : up(detail::filled<std::int32_t>(static_cast<std::size_t>(k), -1)) {}
   std::int32_t find(std::int32_t x) {
     while (up[static_cast<std::size_t>(x)] >= 0) {
       const std::int32_t p = up[static_cast<std::size_t>(x)];
@@ -371,7 +374,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     return p;
   }
   detail::PhaseClock clk;
-  Adjacency adj{g.offsets_data(), g.targets_data(), {}, {}};
+  Adjacency adj{g.offsets_data(), g.targets_data(), g.loop_data(), {}, {}};
   {
     uvector<EdgeId> ptr[1];
     uvector<VertexId> col[1];
@@ -389,20 +392,21 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   clk.mark("partition: in-edge transpose");
   const EdgeId m_all = adj.off[n], m_in = adj.in_off[nn];
   SccFinder finder(n, adj, clk);
-  const std::vector<VertexId> label = finder.run();
+  const uvector<VertexId> label = finder.run();
   const VertexId giant = finder.giant_;
 
   // dense component index per vertex (components numbered by representative)
-  std::vector<std::int32_t> cidx(nn + 1, 0);
+  uvector<std::int32_t> cidx(nn + 1);
+  cidx[nn] = 0;
   parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t v = b; v < e; ++v) cidx[static_cast<std::size_t>(v)] = label[static_cast<std::size_t>(v)] == v;
   });
   const std::int32_t K = detail::exclusive_scan_inplace(cidx.data(), static_cast<std::int64_t>(nn) + 1);
-  std::vector<std::int32_t> comp(nn);
+  uvector<std::int32_t> comp(nn);
   parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t v = b; v < e; ++v) comp[static_cast<std::size_t>(v)] = cidx[static_cast<std::size_t>(label[static_cast<std::size_t>(v)])];
   });
-  std::vector<std::int32_t>().swap(cidx);
+  uvector<std::int32_t>().swap(cidx);
   // edges that leave their SCC, one bit each (plan_internal.hpp): recorded by the
   // two scans below that look every edge's components up anyway
   uvector<std::uint64_t> cross_out(static_cast<std::size_t>((m_all + 63) / 64)), cross_in(static_cast<std::size_t>((m_in + 63) / 64));
@@ -414,8 +418,8 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   const std::size_t KK = static_cast<std::size_t>(K);
   const std::int32_t cg = giant >= 0 ? comp[static_cast<std::size_t>(giant)] : -1;
   const int T = host_threads();
-  std::vector<std::int64_t> mptr(KK + 1, 0);
-  std::vector<std::int64_t> pending(KK, 0);
+  uvector<std::int64_t> mptr = detail::filled<std::int64_t>(KK + 1, 0);
+  uvector<std::int64_t> pending = detail::filled<std::int64_t>(KK, 0);
   std::vector<std::vector<VertexId>> gmem(static_cast<std::size_t>(T));
   std::vector<std::int64_t> gpend(static_cast<std::size_t>(T), 0);
   parallel_chunks(n, [&](int th, std::int64_t b, std::int64_t e) {
@@ -448,14 +452,15 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       pending[static_cast<std::size_t>(cg)] += gpend[static_cast<std::size_t>(t)];
     }
   }
-  std::vector<std::int32_t> csize(KK);
+  uvector<std::int32_t> csize(KK);
   parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t c = b; c < e; ++c) csize[static_cast<std::size_t>(c)] = static_cast<std::int32_t>(mptr[static_cast<std::size_t>(c)]);
   });
   detail::exclusive_scan_inplace(mptr.data(), static_cast<std::int64_t>(KK) + 1);
-  std::vector<VertexId> members(nn);
+  uvector<VertexId> members(nn);
   {
-    std::vector<std::int64_t> fill(mptr.begin(), mptr.end() - 1);
+    uvector<std::int64_t> fill(KK);
+    parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) { std::copy(mptr.begin() + b, mptr.begin() + e, fill.begin() + b); });
     parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
       for (std::int64_t v = b; v < e; ++v) {
         const std::int32_t c = comp[static_cast<std::size_t>(v)];
@@ -478,7 +483,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
 
   clk.mark("partition: components, members");
   // 2. wavefronts from the sinks of the component DAG
-  std::vector<std::int32_t> level(KK, 0);
+  uvector<std::int32_t> level = detail::filled<std::int32_t>(KK, 0);
   std::vector<std::vector<std::pair<std::int32_t, std::int32_t>>> absorbs(static_cast<std::size_t>(T));
   std::vector<std::int64_t> scans(static_cast<std::size_t>(T), 0);
   Frontier next(T);
@@ -572,7 +577,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   clk.mark("partition: level wavefronts");
   // 3. absorptions -> final components, ids by smallest member
   Sets sets(K);
-  std::vector<std::int32_t> root(KK);
+  uvector<std::int32_t> root(KK);
   parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t c = b; c < e; ++c) root[static_cast<std::size_t>(c)] = static_cast<std::int32_t>(c);
   });
@@ -584,7 +589,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       touched.push_back(b);
     }
   for (const std::int32_t c : touched) root[static_cast<std::size_t>(c)] = sets.find(c);
-  std::vector<VertexId> first(KK, n);
+  uvector<VertexId> first = detail::filled<VertexId>(KK, n);
   parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t v = b; v < e; ++v) {
       std::atomic_ref<VertexId> f(first[static_cast<std::size_t>(root[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])])]);
@@ -593,7 +598,8 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       }
     }
   });
-  std::vector<VertexId> id_at(nn + 1, 0);  // id_at[v] = number of components first seen before v
+  uvector<VertexId> id_at(nn + 1);  // id_at[v] = number of components first seen before v
+  id_at[nn] = 0;
   parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t v = b; v < e; ++v)
       id_at[static_cast<std::size_t>(v)] = first[static_cast<std::size_t>(root[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])])] == v;
@@ -616,9 +622,20 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       }
     }
   });
-  const std::int32_t lo = *std::min_element(p.levels.begin(), p.levels.end());
-  for (auto& l : p.levels) l -= lo;
-  p.max_level = *std::max_element(p.levels.begin(), p.levels.end());
+  {  // shift the lowest level to 0
+    const int T2 = host_threads();
+    std::vector<std::int32_t> los(static_cast<std::size_t>(T2), INT32_MAX), his(static_cast<std::size_t>(T2), INT32_MIN);
+    parallel_chunks(k, [&](int th, std::int64_t b, std::int64_t e) {
+      const auto [mn, mx] = std::minmax_element(p.levels.begin() + b, p.levels.begin() + e);
+      los[static_cast<std::size_t>(th)] = std::min(los[static_cast<std::size_t>(th)], *mn);
+      his[static_cast<std::size_t>(th)] = std::max(his[static_cast<std::size_t>(th)], *mx);
+    });
+    const std::int32_t lo = *std::min_element(los.begin(), los.end());
+    parallel_chunks(k, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t i = b; i < e; ++i) p.levels[static_cast<std::size_t>(i)] -= lo;
+    });
+    p.max_level = *std::max_element(his.begin(), his.end()) - lo;
+  }
   clk.mark("partition: unions + assemble");
   if (stats) *stats = st;
   if (keep_in) {

@@ -255,9 +255,9 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   const std::int32_t nl = p.max_level + 1;
 
   // unit of every vertex, local index (= position in ascending members)
-  std::vector<std::int32_t> unit_of(nn), local_of(nn);
+  uvector<std::int32_t> unit_of(nn), local_of(nn);  // every vertex is in a unit: written below
   std::vector<std::int64_t> unit_mem_begin(nu + 1, 0);  // into `umem`
-  std::vector<VertexId> umem(nn);
+  uvector<VertexId> umem(nn);
   {
     std::int64_t pos = 0;
     for (std::int32_t li = 0; li < nl; ++li)
@@ -286,7 +286,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   clk.mark("unit_of / local_of");
   // CAC units: Kahn pass of solve_cac (solvers.cpp:43-83) to get each vertex's
   // dequeue position and its depth (longest path from the unit's sources).
-  std::vector<std::int32_t> kahn_pos(nn, 0), depth(nn, 0);
+  uvector<std::int32_t> kahn_pos(nn), depth(nn);  // written and read for CAC vertices only
   std::vector<std::int32_t> unit_depths(nu, 0);
   std::atomic<bool> cycle{false};
   detail::parallel_dynamic(static_cast<std::int64_t>(nu), 64, [&](std::int64_t b, std::int64_t e) {
@@ -363,7 +363,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   // one scan of every out-edge: intra-component out-degree per vertex (kept
   // self-loops count, ignored ones are dropped) -> SccLarge row order and the
   // per-unit reference edge counts (unit.edges.size()); cross / dropped totals
-  std::vector<std::int32_t> unit_out(nn, 0);
+  uvector<std::int32_t> unit_out(nn);
   std::atomic<EdgeId> n_intra{0}, n_cross{0}, n_dropped{0};
   const EdgeId m_all = off[n];
   // with the partition's cross-edge bits only the edges that leave their SCC need
@@ -583,7 +583,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   }
   clk.mark("in-edge transpose");
   // per-row ordering = the reference's accumulation order, then vertex -> row
-  std::vector<std::int32_t> level_idx_of(nn);
+  uvector<std::int32_t> level_idx_of(nn);
   detail::parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
     for (std::int64_t v = b; v < e; ++v)
       level_idx_of[static_cast<std::size_t>(v)] = p.max_level - p.levels[static_cast<std::size_t>(comp_of[static_cast<std::size_t>(v)])];
