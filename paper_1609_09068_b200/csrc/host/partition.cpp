@@ -548,9 +548,17 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   while (!cur.empty()) {
     ++n_waves;
     n_items += static_cast<long long>(cur.size());
-    std::vector<std::int32_t> narrow, wide;
-    for (const std::int32_t c : cur)
-      (mptr[static_cast<std::size_t>(c) + 1] - mptr[static_cast<std::size_t>(c)] > kWideComponent ? wide : narrow).push_back(c);
+    // the few components with many members (the giant SCC) are scanned member-parallel;
+    // the rest one component per item (the item loops below skip the wide ones)
+    auto is_wide = [&](std::int32_t c) { return csize[static_cast<std::size_t>(c)] > kWideComponent; };
+    const std::vector<std::int32_t>& narrow = cur;
+    std::vector<std::int32_t> wide;
+    {
+      std::vector<std::vector<std::int32_t>> found(static_cast<std::size_t>(T));
+      for_items(cur, [&](int th, std::int32_t c) { if (is_wide(c)) found[static_cast<std::size_t>(th)].push_back(c); }, 1 << 16);
+      for (const auto& f : found) wide.insert(wide.end(), f.begin(), f.end());
+      std::sort(wide.begin(), wide.end());
+    }
     for (const std::int32_t c : wide) {  // the giant SCC: members in parallel
       const std::int64_t m0 = mptr[static_cast<std::size_t>(c)], m1 = mptr[static_cast<std::size_t>(c) + 1];
       std::vector<std::int32_t> his(static_cast<std::size_t>(T), 0);
@@ -560,6 +568,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       decide(0, c, *std::max_element(his.begin(), his.end()));
     }
     for_items(narrow, [&](int th, std::int32_t c) {
+      if (is_wide(c)) return;
       decide(th, c, max_successor(c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]));
     }, item_grain(n));
     for (const std::int32_t c : wide) {
@@ -567,6 +576,7 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       parallel_chunks(m1 - m0, [&](int th, std::int64_t b, std::int64_t e) { release(th, c, m0 + b, m0 + e); });
     }
     for_items(narrow, [&](int th, std::int32_t c) {
+      if (is_wide(c)) return;
       release(th, c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]);
     }, item_grain(n));
     cur = next.take();
