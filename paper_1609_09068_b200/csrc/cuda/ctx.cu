@@ -529,8 +529,9 @@ int64_t lr_ctx_device_bytes(const lr_ctx* c) {
 // uploaded CSR, spmv.cu k_spmv_blk).  LR_BLK=0 keeps K4c everywhere;
 // LR_BLK_MIN_ROWS (default 2^21) and LR_BLK_MIN_DEG (in-edges per row, default
 // 8) set "large", LR_BLK_ROWS the block rows
-// (default 16384), LR_BLK_PART the slots per part (default: about eight parts
-// per SM), LR_BLK_WIN the bank-balance window (0 or LR_BLK_BANKS=0: none),
+// (default 16384), LR_BLK_PART the slots per part (default: about three parts
+// per SM -- a block that is not split adds nothing to global memory; measured
+// 5,238 / 5,365 / 5,422 / 5,421 GB/s at 8 / 4 / 2.7 / 1 parts per SM), LR_BLK_WIN the bank-balance window (0 or LR_BLK_BANKS=0: none),
 // LR_BLK_SLACK the rows of entries per empty row (0: none).
 static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vector<GridUnitState>& gstate,
                                  cudaStream_t s) {
@@ -573,7 +574,7 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     }
     const long long total = pad_off.back();
     const char* e_part = std::getenv("LR_BLK_PART");
-    long long P = e_part ? std::atoll(e_part) : total / (8ll * sms);
+    long long P = e_part ? std::atoll(e_part) : total * 10 / (27ll * sms);
     P = std::max<long long>(kBlkChunk, (P + kBlkChunk - 1) / kBlkChunk * kBlkChunk);
     P = std::min<long long>(P, 1ll << 30);
     std::vector<BlkPart> parts;
