@@ -617,6 +617,15 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
                         U->bcnt.p};
     T.blk = static_cast<int>(ctx->blk.size());
     ctx->blk.push_back(std::move(U));
+    // K5 streams its indices evict-first and gathers the pushed vector block after
+    // block: a larger evict-last window than K4c's pays (measured at config 5:
+    // 0 / 0.3 / 0.6 / 0.85 / 1.0 / 1.3 / 1.6 / 2.0 / 3.0 of L2 -> 4311 / 4978 /
+    // 5276 / 5419 / 5451 / 5472 / 5484 / 5479 / 5462 GB/s)
+    if (std::getenv("LR_L2_HOT_FRAC") == nullptr) {
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+      T.hot_rows = std::min<long long>(T.unit_rows, static_cast<long long>(1.6 * l2 / 16.0));
+    }
   }
   return LR_OK;
 }

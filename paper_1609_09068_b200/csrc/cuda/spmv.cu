@@ -760,8 +760,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   double lmax = 0.0;
   auto finish_row = [&](int r, double v) {
     const long long g = static_cast<long long>(B.u0) + r;
-    rank[g] += v;
-    st_keep(s_out + g, pf[g] * v, keep_out);
+    // rank and pf pass through once per iteration: first out of L2
+    double rk;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(rk) : "l"(rank + g), "l"(stream));
+    st_keep(rank + g, rk + v, stream);
+    st_keep(s_out + g, ld_stream(pf + g, stream) * v, keep_out);
     lmax = fmax(lmax, v);
   };
   for (;;) {
