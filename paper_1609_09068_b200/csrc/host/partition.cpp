@@ -422,6 +422,20 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
   uvector<std::int64_t> pending = detail::filled<std::int64_t>(KK, 0);
   std::vector<std::vector<VertexId>> gmem(static_cast<std::size_t>(T));
   std::vector<std::int64_t> gpend(static_cast<std::size_t>(T), 0);
+  // Membership in the giant SCC as a bitmap (8 MB at 2^26 vertices: cache
+  // resident, unlike comp[]): an edge with an end in the giant SCC is classified
+  // without looking its components up -- both ends inside: not cross; one end
+  // inside: cross, and the inside end's component is cg.  On a scale-free graph
+  // that covers nearly every edge.
+  Bits in_giant(cg >= 0 ? nn : 0);
+  if (cg >= 0)
+    parallel_chunks((n + 63) / 64, [&](int, std::int64_t b, std::int64_t e) {
+      for (std::int64_t wd = b; wd < e; ++wd) {
+        std::uint64_t x = 0;
+        for (std::int64_t v = wd * 64, k = 0; k < 64 && v < n; ++v, ++k) x |= static_cast<std::uint64_t>(comp[static_cast<std::size_t>(v)] == cg) << k;
+        in_giant.w[static_cast<std::size_t>(wd)] = x;
+      }
+    });
   parallel_chunks(n, [&](int th, std::int64_t b, std::int64_t e) {
     detail::CrossBits bits(cross_out.data());
     for (std::int64_t vv = b; vv < e; ++vv) {
@@ -429,11 +443,23 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       const std::int32_t c = comp[static_cast<std::size_t>(v)];
       std::int64_t x = 0;
       const EdgeId k1 = adj.off[v + 1];
-      for (EdgeId k = adj.off[v]; k < k1; ++k) {
-        if (k + kAhead < m_all) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
-        if (comp[static_cast<std::size_t>(adj.tgt[k])] != c) {
-          ++x;
-          bits.set(k);
+      if (cg >= 0) {
+        const bool vg = c == cg;
+        for (EdgeId k = adj.off[v]; k < k1; ++k) {
+          const VertexId w = adj.tgt[k];
+          const bool wg = in_giant.get(w);
+          if (vg ? !wg : (wg || comp[static_cast<std::size_t>(w)] != c)) {
+            ++x;
+            bits.set(k);
+          }
+        }
+      } else {
+        for (EdgeId k = adj.off[v]; k < k1; ++k) {
+          if (k + kAhead < m_all) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.tgt[k + kAhead])]);
+          if (comp[static_cast<std::size_t>(adj.tgt[k])] != c) {
+            ++x;
+            bits.set(k);
+          }
         }
       }
       if (c == cg) {
@@ -509,6 +535,19 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
     for (std::int64_t i = m0; i < m1; ++i) {
       const VertexId u = members[static_cast<std::size_t>(i)];
       const EdgeId k1 = adj.in_off[static_cast<std::size_t>(u) + 1];
+      if (cg >= 0) {
+        const bool ug = c == cg;
+        for (EdgeId k = adj.in_off[static_cast<std::size_t>(u)]; k < k1; ++k) {
+          const VertexId src = adj.in_src[static_cast<std::size_t>(k)];
+          const bool sg = in_giant.get(src);
+          if (ug && sg) continue;  // inside the giant SCC
+          const std::int32_t cp = sg ? cg : comp[static_cast<std::size_t>(src)];
+          if (cp == c) continue;
+          bits.set(k);
+          if (atomic_sub(pending[static_cast<std::size_t>(cp)], std::int64_t{1}) == 1) out.push_back(cp);
+        }
+        continue;
+      }
       for (EdgeId k = adj.in_off[static_cast<std::size_t>(u)]; k < k1; ++k) {
         if (k + kAhead < m_in) __builtin_prefetch(&comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k + kAhead)])]);
         const std::int32_t cp = comp[static_cast<std::size_t>(adj.in_src[static_cast<std::size_t>(k)])];
