@@ -1,10 +1,13 @@
 // Device-side build of K5's dest-blocked layout (kernels.cuh BlkUnitDev) from
-// the unit's in-edge CSR already on the device: key every in-edge by
-// (dest block, source), radix-sort the keys with the in-block dest row as
-// payload (CUB, one-time setup at upload), then scatter each block's sorted run
-// into its padded slot, dummies (src 0, dst BR) in the padding.  Rows are in
-// unit order, so block b's in-edges occupy the same CSR range before and after
-// the sort: the sort only reorders inside blocks.
+// the unit's in-edge CSR already on the device (one-time setup at upload):
+//   1. k_blk_keys + CUB radix sort: every in-edge keyed by (dest block, source),
+//      the in-block dest row as payload.  Rows are in unit order, so block b's
+//      in-edges occupy the same CSR range before and after the sort.
+//   2. k_blk_pack: each block's sorted run into its slots (rows of 32 slots, one
+//      empty row per `slack` rows, padded to whole chunks; unused slots = dummies).
+//   3. k_blk_banks: entries placed inside windows of `win` slots so that each
+//      half-warp of K5 adds to 16 distinct shared-memory bank pairs, chunks
+//      stored lane-major (k_blk_lane_major alone when the balance is off).
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
