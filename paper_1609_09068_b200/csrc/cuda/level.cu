@@ -827,6 +827,14 @@ __device__ __forceinline__ void stage_row_edges(const DeviceLayout& L, const dou
 // registers (no pivoting: the blocks are strictly diagonally dominant by
 // columns).  Lane (g, tq) holds P[g][2tq], P[g][2tq+1]; returns its A fragments
 // of P^-1 for DMMA m8n8k4 (row g, columns tq and 4 + tq).
+// Division-free elimination: step pv replaces row g != pv by
+// piv * row_g - P[g][pv] * row_pv (any nonzero multiple of a row is a valid row
+// operation), which leaves the pivot row alone and keeps the reciprocal off the
+// eight-step dependent chain (shuffle + multiply + fma per step instead of
+// shuffle + reciprocal + two Newton steps + multiply + fma: ~190 -> ~80 cycles).
+// The left block ends up diagonal; each row is divided by its diagonal entry
+// once at the end (eight independent reciprocals).  Entries scale by at most the
+// product of the pivots, which lie in (1 - c, 1 + c): no overflow in 8 steps.
 __device__ __forceinline__ void pivot_block_inverse(double p0, double p1, int g, int tq, double& ia, double& ib) {
   double q0 = g == 2 * tq ? 1.0 : 0.0, q1 = g == 2 * tq + 1 ? 1.0 : 0.0;
 #pragma unroll
@@ -836,25 +844,21 @@ __device__ __forceinline__ void pivot_block_inverse(double p0, double p1, int g,
     const double rq0 = __shfl_sync(0xffffffffu, q0, src), rq1 = __shfl_sync(0xffffffffu, q1, src);
     const double piv = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, pv * 4 + (pv >> 1));
     const double f = __shfl_sync(0xffffffffu, (pv & 1) ? p1 : p0, g * 4 + (pv >> 1));  // P[g][pv]
-    // 1 / piv: hardware reciprocal plus two Newton steps (~1 ulp; a division is
-    // ~90 cycles on this chain)
-    double inv;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(piv));
-    inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
-    inv = __fma_rn(inv, __fma_rn(-piv, inv, 1.0), inv);
-    if (g == pv) {
-      p0 = rp0 * inv;
-      p1 = rp1 * inv;
-      q0 = rq0 * inv;
-      q1 = rq1 * inv;
-    } else {
-      const double r = f * inv;
-      p0 = __fma_rn(-r, rp0, p0);
-      p1 = __fma_rn(-r, rp1, p1);
-      q0 = __fma_rn(-r, rq0, q0);
-      q1 = __fma_rn(-r, rq1, q1);
+    if (g != pv) {
+      p0 = __fma_rn(piv, p0, -(f * rp0));
+      p1 = __fma_rn(piv, p1, -(f * rp1));
+      q0 = __fma_rn(piv, q0, -(f * rq0));
+      q1 = __fma_rn(piv, q1, -(f * rq1));
     }
   }
+  // 1 / P[g][g]: hardware reciprocal plus two Newton steps (~1 ulp)
+  const double dg = __shfl_sync(0xffffffffu, (g & 1) ? p1 : p0, g * 4 + (g >> 1));
+  double inv;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(dg));
+  inv = __fma_rn(inv, __fma_rn(-dg, inv, 1.0), inv);
+  inv = __fma_rn(inv, __fma_rn(-dg, inv, 1.0), inv);
+  q0 *= inv;
+  q1 *= inv;
   const double u0 = __shfl_sync(0xffffffffu, q0, g * 4 + (tq >> 1)), u1 = __shfl_sync(0xffffffffu, q1, g * 4 + (tq >> 1));
   const double v0 = __shfl_sync(0xffffffffu, q0, g * 4 + 2 + (tq >> 1)),
                v1 = __shfl_sync(0xffffffffu, q1, g * 4 + 2 + (tq >> 1));
