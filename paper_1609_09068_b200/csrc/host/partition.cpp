@@ -611,6 +611,34 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       decide(th, c, max_successor(c, mptr[static_cast<std::size_t>(c)], mptr[static_cast<std::size_t>(c) + 1]));
     }, item_grain(n));
     for (const std::int32_t c : wide) {
+      if (c == cg) {
+        // The giant SCC's cross in-edges, found from their sources: only the
+        // vertices outside it can hold one, and those carry a small share of the
+        // edges -- no pass over the giant's own in-edge lists.  The edge's place in
+        // its target's (source-ascending) in-list, for the cross-edge bit, is a
+        // binary search.
+        parallel_chunks(n, [&](int th, std::int64_t b, std::int64_t e) {
+          auto& out = next.parts[static_cast<std::size_t>(th)];
+          for (std::int64_t pp = b; pp < e; ++pp) {
+            const VertexId pv = static_cast<VertexId>(pp);
+            if (in_giant.get(pv)) continue;
+            std::int64_t cnt = 0;
+            for (EdgeId k = adj.off[pv]; k < adj.off[pv + 1]; ++k) {
+              const VertexId w = adj.tgt[k];
+              if (!in_giant.get(w)) continue;
+              ++cnt;
+              const VertexId* lo = adj.in_src.data() + adj.in_off[static_cast<std::size_t>(w)];
+              const VertexId* hi = adj.in_src.data() + adj.in_off[static_cast<std::size_t>(w) + 1];
+              const EdgeId pos = std::lower_bound(lo, hi, pv) - adj.in_src.data();
+              __atomic_fetch_or(&cross_in[static_cast<std::size_t>(pos >> 6)], std::uint64_t{1} << (pos & 63), __ATOMIC_RELAXED);
+            }
+            if (cnt == 0) continue;
+            const std::int32_t cp = comp[static_cast<std::size_t>(pv)];
+            if (atomic_sub(pending[static_cast<std::size_t>(cp)], cnt) == cnt) out.push_back(cp);
+          }
+        });
+        continue;
+      }
       const std::int64_t m0 = mptr[static_cast<std::size_t>(c)], m1 = mptr[static_cast<std::size_t>(c) + 1];
       parallel_chunks(m1 - m0, [&](int th, std::int64_t b, std::int64_t e) { release(th, c, m0 + b, m0 + e); });
     }
