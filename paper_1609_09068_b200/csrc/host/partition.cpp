@@ -444,11 +444,13 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       std::int64_t x = 0;
       const EdgeId k1 = adj.off[v + 1];
       if (cg >= 0) {
-        const bool vg = c == cg;
+        if (c == cg) {  // its cross out-edges are found from their targets below
+          gmem[static_cast<std::size_t>(th)].push_back(v);
+          continue;
+        }
         for (EdgeId k = adj.off[v]; k < k1; ++k) {
           const VertexId w = adj.tgt[k];
-          const bool wg = in_giant.get(w);
-          if (vg ? !wg : (wg || comp[static_cast<std::size_t>(w)] != c)) {
+          if (in_giant.get(w) || comp[static_cast<std::size_t>(w)] != c) {
             ++x;
             bits.set(k);
           }
@@ -471,6 +473,26 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       if (x) std::atomic_ref<std::int64_t>(pending[static_cast<std::size_t>(c)]).fetch_add(x, std::memory_order_relaxed);
     }
   });
+  // The giant SCC's cross out-edges, found from their targets: only a vertex
+  // outside it can receive one, and those hold a small share of the in-edges --
+  // no pass over the giant's own out-edge lists.  The edge's place in its source's
+  // (target-ascending) row, for the cross-edge bit, is a binary search.
+  if (cg >= 0)
+    parallel_chunks(n, [&](int th, std::int64_t b, std::int64_t e) {
+      std::int64_t found = 0;
+      for (std::int64_t ww = b; ww < e; ++ww) {
+        const VertexId w = static_cast<VertexId>(ww);
+        if (in_giant.get(w)) continue;
+        for (EdgeId k = adj.in_off[static_cast<std::size_t>(w)]; k < adj.in_off[static_cast<std::size_t>(w) + 1]; ++k) {
+          const VertexId src = adj.in_src[static_cast<std::size_t>(k)];
+          if (!in_giant.get(src)) continue;
+          ++found;
+          const EdgeId pos = std::lower_bound(adj.tgt + adj.off[src], adj.tgt + adj.off[src + 1], w) - adj.tgt;
+          __atomic_fetch_or(&cross_out[static_cast<std::size_t>(pos >> 6)], std::uint64_t{1} << (pos & 63), __ATOMIC_RELAXED);
+        }
+      }
+      gpend[static_cast<std::size_t>(th)] += found;
+    });
   if (cg >= 0) {
     mptr[static_cast<std::size_t>(cg)] = 0;
     for (int t = 0; t < T; ++t) {
