@@ -688,38 +688,49 @@ Partition wavefront_partition(const Graph& g, bool absorb_cacs, PartitionStats* 
       touched.push_back(b);
     }
   for (const std::int32_t c : touched) root[static_cast<std::size_t>(c)] = sets.find(c);
-  uvector<VertexId> first = detail::filled<VertexId>(KK, n);
-  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t v = b; v < e; ++v) {
-      std::atomic_ref<VertexId> f(first[static_cast<std::size_t>(root[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])])]);
+  // Everything below walks the components, not the vertices: a component's
+  // smallest member, the smallest member of its final component (`first`), the
+  // final id, its size; the vertices then take their id with one lookup each.
+  uvector<VertexId> first = detail::filled<VertexId>(KK, n), minv(KK);
+  parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c) {
+      const std::int64_t m0 = mptr[static_cast<std::size_t>(c)], m1 = mptr[static_cast<std::size_t>(c) + 1];
+      VertexId mn = members[static_cast<std::size_t>(m0)];
+      for (std::int64_t i = m0 + 1; i < m1; ++i) mn = std::min(mn, members[static_cast<std::size_t>(i)]);
+      minv[static_cast<std::size_t>(c)] = mn;
+      std::atomic_ref<VertexId> f(first[static_cast<std::size_t>(root[static_cast<std::size_t>(c)])]);
       VertexId cur_min = f.load(std::memory_order_relaxed);
-      while (v < cur_min && !f.compare_exchange_weak(cur_min, static_cast<VertexId>(v), std::memory_order_relaxed)) {
+      while (mn < cur_min && !f.compare_exchange_weak(cur_min, mn, std::memory_order_relaxed)) {
       }
     }
-  });
-  uvector<VertexId> id_at(nn + 1);  // id_at[v] = number of components first seen before v
-  id_at[nn] = 0;
-  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t v = b; v < e; ++v)
-      id_at[static_cast<std::size_t>(v)] = first[static_cast<std::size_t>(root[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])])] == v;
-  });
+  }, 1 << 12);
+  uvector<VertexId> id_at = detail::filled<VertexId>(nn + 1, 0);  // id_at[v] = number of components first seen before v
+  parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c)
+      if (minv[static_cast<std::size_t>(c)] == first[static_cast<std::size_t>(root[static_cast<std::size_t>(c)])])
+        id_at[static_cast<std::size_t>(minv[static_cast<std::size_t>(c)])] = 1;
+  }, 1 << 12);
   const VertexId k = detail::exclusive_scan_inplace(id_at.data(), static_cast<std::int64_t>(nn) + 1);
   p.comp_of.resize(nn);
   p.kinds.resize(static_cast<std::size_t>(k));
   p.levels.resize(static_cast<std::size_t>(k));
   p.sizes.assign(static_cast<std::size_t>(k), 0);
-  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t v = b; v < e; ++v) {
-      const std::int32_t c = comp[static_cast<std::size_t>(v)];
-      const std::int32_t r = root[static_cast<std::size_t>(c)];
-      const VertexId id = id_at[static_cast<std::size_t>(first[static_cast<std::size_t>(r)])];
-      p.comp_of[static_cast<std::size_t>(v)] = id;
-      std::atomic_ref<VertexId>(p.sizes[static_cast<std::size_t>(id)]).fetch_add(1, std::memory_order_relaxed);
-      if (first[static_cast<std::size_t>(r)] == v) {
+  uvector<VertexId> fid(KK);  // final id of every SCC-level component
+  parallel_chunks(K, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c) {
+      const VertexId f = first[static_cast<std::size_t>(root[static_cast<std::size_t>(c)])];
+      const VertexId id = id_at[static_cast<std::size_t>(f)];
+      fid[static_cast<std::size_t>(c)] = id;
+      std::atomic_ref<VertexId>(p.sizes[static_cast<std::size_t>(id)]).fetch_add(csize[static_cast<std::size_t>(c)], std::memory_order_relaxed);
+      if (minv[static_cast<std::size_t>(c)] == f) {  // the component of the final component's first vertex
         p.kinds[static_cast<std::size_t>(id)] = csize[static_cast<std::size_t>(c)] > 1 ? ComponentKind::Scc : ComponentKind::Cac;
         p.levels[static_cast<std::size_t>(id)] = level[static_cast<std::size_t>(c)];
       }
     }
+  }, 1 << 12);
+  parallel_chunks(n, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t v = b; v < e; ++v)
+      p.comp_of[static_cast<std::size_t>(v)] = fid[static_cast<std::size_t>(comp[static_cast<std::size_t>(v)])];
   });
   {  // shift the lowest level to 0
     const int T2 = host_threads();
