@@ -33,21 +33,52 @@ std::vector<VertexId> ordered_components(const Partition& p, VertexId) {
   return comps;
 }
 
-// Members of every component, ascending vertex id (CSR by component): a
-// stable parallel radix sort of the vertices by component.
+// Members of every component, ascending vertex id (CSR by component).  The
+// offsets are the scan of the sizes; a single-vertex component's member goes
+// straight to its slot, and only the vertices of larger components (in vertex
+// order) are sorted by component, stably -- the slots of those components, in
+// slot order, take the sorted vertices one to one.
 void component_members(const Partition& p, std::vector<std::int64_t>& begin, std::vector<VertexId>& mem) {
   const std::size_t k = p.component_count(), n = p.comp_of.size();
-  begin.assign(k + 1, 0);
-  detail::parallel_chunks(static_cast<std::int64_t>(n), [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t v = b; v < e; ++v)
-      std::atomic_ref<std::int64_t>(begin[static_cast<std::size_t>(p.comp_of[static_cast<std::size_t>(v)])])
-          .fetch_add(1, std::memory_order_relaxed);
+  begin.resize(k + 1);
+  begin[k] = 0;
+  uvector<std::int64_t> singles_before(k + 1);  // single-vertex components with a smaller id
+  singles_before[k] = 0;
+  detail::parallel_chunks(static_cast<std::int64_t>(k), [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t c = b; c < e; ++c) {
+      begin[static_cast<std::size_t>(c)] = p.sizes[static_cast<std::size_t>(c)];
+      singles_before[static_cast<std::size_t>(c)] = p.sizes[static_cast<std::size_t>(c)] == 1;
+    }
   });
   detail::exclusive_scan_inplace(begin.data(), static_cast<std::int64_t>(k) + 1);
+  detail::exclusive_scan_inplace(singles_before.data(), static_cast<std::int64_t>(k) + 1);
   mem.resize(n);
-  std::iota(mem.begin(), mem.end(), 0);
-  detail::stable_radix_sort(mem.data(), static_cast<std::int64_t>(n), [&](VertexId v) {
+  const int T = host_threads();
+  std::vector<uvector<VertexId>> found(static_cast<std::size_t>(T));
+  detail::parallel_chunks(static_cast<std::int64_t>(n), [&](int th, std::int64_t b, std::int64_t e) {
+    auto& mine = found[static_cast<std::size_t>(th)];
+    for (std::int64_t v = b; v < e; ++v) {
+      const std::size_t c = static_cast<std::size_t>(p.comp_of[static_cast<std::size_t>(v)]);
+      if (p.sizes[c] == 1) mem[static_cast<std::size_t>(begin[c])] = static_cast<VertexId>(v);
+      else mine.push_back(static_cast<VertexId>(v));
+    }
+  });
+  std::vector<std::size_t> at(static_cast<std::size_t>(T) + 1, 0);
+  for (int t = 0; t < T; ++t) at[static_cast<std::size_t>(t) + 1] = at[static_cast<std::size_t>(t)] + found[static_cast<std::size_t>(t)].size();
+  uvector<VertexId> multi(at[static_cast<std::size_t>(T)]);  // chunks are ascending vertex ranges: vertex order
+  detail::parallel_chunks(T, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t t = b; t < e; ++t)
+      std::copy(found[static_cast<std::size_t>(t)].begin(), found[static_cast<std::size_t>(t)].end(), multi.begin() + static_cast<std::ptrdiff_t>(at[static_cast<std::size_t>(t)]));
+  }, 1);
+  detail::stable_radix_sort(multi.data(), static_cast<std::int64_t>(multi.size()), [&](VertexId v) {
     return static_cast<std::uint32_t>(p.comp_of[static_cast<std::size_t>(v)]);
+  });
+  detail::parallel_chunks(static_cast<std::int64_t>(multi.size()), [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t i = b; i < e; ++i) {
+      // slot = position among the slots of multi-vertex components + the single-vertex slots before it
+      const VertexId v = multi[static_cast<std::size_t>(i)];
+      mem[static_cast<std::size_t>(i + singles_before[static_cast<std::size_t>(p.comp_of[static_cast<std::size_t>(v)])])] = v;
+    }
   });
 }
 
@@ -248,6 +279,7 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   std::vector<std::int64_t> mb;
   std::vector<VertexId> mem;
   component_members(p, mb, mem);
+
   std::vector<std::vector<VertexId>> singles;
   const auto plan = plan_units(p, comps, small_threshold, L.level_unit_begin, singles, mb, mem);
   const std::size_t nu = plan.size();
