@@ -31,6 +31,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
@@ -204,7 +205,20 @@ class SccFinder {
     // a pivot whose reach needs more than kMaxReachLevels BFS levels sits in a
     // deep DAG of small components (config 4), not in a giant SCC: leave it
     // to Tarjan (the result is the same, only the order of work changes)
-    if (!bfs(pivot, alive, fw, false) || !bfs(pivot, alive, bw, true)) return;
+    // The two searches share nothing but read-only inputs and are bound by
+    // memory latency, not by the cores: they run side by side (the backward one
+    // on its own thread; its parallel loops find the pool busy and spawn theirs).
+    // LR_REACH_SERIAL=1 runs them one after the other.
+    bool fw_ok = false, bw_ok = false;
+    if (std::getenv("LR_REACH_SERIAL") != nullptr) {
+      fw_ok = bfs(pivot, alive, fw, false);
+      bw_ok = fw_ok && bfs(pivot, alive, bw, true);
+    } else {
+      std::thread back([&] { bw_ok = bfs(pivot, alive, bw, true); });
+      fw_ok = bfs(pivot, alive, fw, false);
+      back.join();
+    }
+    if (!fw_ok || !bw_ok) return;
     giant_ = pivot;
     // the SCC's members leave the graph: recount live degrees without them
     parallel_chunks(n_, [&](int, std::int64_t b, std::int64_t e) {
