@@ -201,7 +201,11 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr
       emit(u, [&](int k, std::int64_t row, VertexId) { ++cur[at(k, th, row >> kShift)]; });
   });
   std::vector<std::int64_t> bstart(static_cast<std::size_t>(K) * static_cast<std::size_t>(nb + 1), 0);
-  std::vector<uvector<std::uint64_t>> tmp(K);
+  // a bucketed entry is its value and its row inside the bucket: 4 + 2 bytes (the
+  // build is bound by memory traffic; an 8-byte (row, value) pair costs a third more)
+  static_assert(kShift <= 16, "bucket-local rows are 16-bit");
+  std::vector<uvector<std::uint32_t>> tmp(K);
+  std::vector<uvector<std::uint16_t>> tmp_row(K);
   for (int k = 0; k < K; ++k) {  // bucket-major, then thread: stable
     std::int64_t run_total = 0;
     for (std::int64_t b = 0; b < nb; ++b) {
@@ -214,6 +218,7 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr
     }
     bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(nb)] = run_total;
     tmp[static_cast<std::size_t>(k)].resize(static_cast<std::size_t>(run_total));
+    tmp_row[static_cast<std::size_t>(k)].resize(static_cast<std::size_t>(run_total));
     ptr[k].resize(static_cast<std::size_t>(nrows) + 1);  // every entry written below
     col[k].resize(static_cast<std::size_t>(run_total));
   }
@@ -221,8 +226,9 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr
     const std::int64_t b = n_src * th / t, e = n_src * (th + 1) / t;
     for (std::int64_t u = b; u < e; ++u)
       emit(u, [&](int k, std::int64_t row, VertexId v) {
-        tmp[static_cast<std::size_t>(k)][static_cast<std::size_t>(cur[at(k, th, row >> kShift)]++)] =
-            (static_cast<std::uint64_t>(row) << 32) | static_cast<std::uint32_t>(v);
+        const std::size_t at_ = static_cast<std::size_t>(cur[at(k, th, row >> kShift)]++);
+        tmp[static_cast<std::size_t>(k)][at_] = static_cast<std::uint32_t>(v);
+        tmp_row[static_cast<std::size_t>(k)][at_] = static_cast<std::uint16_t>(row & ((std::int64_t{1} << kShift) - 1));
       });
   });
   std::atomic<std::int64_t> next{0};
@@ -237,8 +243,9 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr
       const std::int64_t s1 = bstart[static_cast<std::size_t>(k) * static_cast<std::size_t>(nb + 1) + static_cast<std::size_t>(b) + 1];
       if (r0 >= r1) continue;
       std::fill(cnt.begin(), cnt.begin() + (r1 - r0), 0);
-      const std::uint64_t* src = tmp[static_cast<std::size_t>(k)].data();
-      for (std::int64_t i = s0; i < s1; ++i) ++cnt[static_cast<std::size_t>((src[i] >> 32) - static_cast<std::uint64_t>(r0))];
+      const std::uint32_t* src = tmp[static_cast<std::size_t>(k)].data();
+      const std::uint16_t* srow = tmp_row[static_cast<std::size_t>(k)].data();
+      for (std::int64_t i = s0; i < s1; ++i) ++cnt[srow[i]];
       std::int64_t pos = s0;
       for (std::int64_t r = r0; r < r1; ++r) {
         ptr[k][static_cast<std::size_t>(r)] = pos;
@@ -247,10 +254,7 @@ void bucket_csr(std::int64_t n_src, std::int64_t nrows, Emit&& emit, PtrVec* ptr
         pos += c;
       }
       VertexId* out = col[k].data();
-      for (std::int64_t i = s0; i < s1; ++i) {
-        const std::size_t lr = static_cast<std::size_t>((src[i] >> 32) - static_cast<std::uint64_t>(r0));
-        out[cnt[lr]++] = static_cast<VertexId>(static_cast<std::uint32_t>(src[i]));
-      }
+      for (std::int64_t i = s0; i < s1; ++i) out[cnt[srow[i]]++] = static_cast<VertexId>(src[i]);
     }
   });
   for (int k = 0; k < K; ++k)
