@@ -18,7 +18,6 @@
 #include "levelrank/partition.hpp"
 #include "levelrank/schedule.hpp"
 #include "lr_cuda.h"
-#include "parallel.hpp"
 #include "plan_internal.hpp"
 
 namespace levelrank {
@@ -206,7 +205,6 @@ lr_status lr_plan_build(const lr_graph* gp, int32_t small_threshold, lr_plan** o
     auto plan = std::make_unique<lr_plan>();
     plan->g = &gp->g;
     plan->threshold = small_threshold;
-    detail::ThreadCap cap(static_cast<std::int64_t>(gp->g.vertex_count()) + gp->g.edge_count());
     detail::InEdges in;
     plan->p = detail::find_components_with_in_edges(gp->g, nullptr, in);
     plan->L = detail::build_layout_from(gp->g, plan->p, small_threshold, in);

@@ -14,12 +14,8 @@
 namespace levelrank {
 inline namespace b200 {
 
-namespace detail {
-thread_local int tl_thread_cap = 0;  // 0: none (ThreadCap, parallel.hpp)
-}
-
 int host_threads() {
-  static const int all = [] {
+  static const int t = [] {
     if (const char* e = std::getenv("LR_THREADS")) {
       const int v = std::atoi(e);
       if (v > 0) return v;
@@ -27,7 +23,7 @@ int host_threads() {
     const unsigned h = std::thread::hardware_concurrency();
     return h ? static_cast<int>(std::min(h, 256u)) : 1;
   }();
-  return detail::tl_thread_cap > 0 ? std::min(all, detail::tl_thread_cap) : all;
+  return t;
 }
 
 Graph Graph::from_edges(VertexId n, std::vector<std::pair<VertexId, VertexId>> edges,

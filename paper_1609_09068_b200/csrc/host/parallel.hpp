@@ -30,21 +30,6 @@ struct PhaseClock {
 };
 
 
-// Caps host_threads() for the calling thread while in scope: a graph of a few
-// hundred thousand edges is planned faster by one or two threads than by
-// sixteen waking up for microseconds of work in each of a hundred phases.
-extern thread_local int tl_thread_cap;
-struct ThreadCap {
-  int prev;
-  explicit ThreadCap(std::int64_t work_items) : prev(tl_thread_cap) {
-    const std::int64_t want = std::max<std::int64_t>(1, work_items >> 20);  // ~a million vertices + edges per thread
-    if (want < 256 && (prev == 0 || want < prev)) tl_thread_cap = static_cast<int>(want);
-  }
-  ~ThreadCap() { tl_thread_cap = prev; }
-  ThreadCap(const ThreadCap&) = delete;
-  ThreadCap& operator=(const ThreadCap&) = delete;
-};
-
 // Runs f(i) for i in [0, t) on t threads of the persistent host pool (the
 // caller is thread 0; pool.cpp).
 void pool_run_impl(int t, void (*fn)(void*, int), void* arg);
