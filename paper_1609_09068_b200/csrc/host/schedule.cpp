@@ -7,8 +7,10 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
 #include <numeric>
 #include <stdexcept>
+#include <thread>
 
 #include "parallel.hpp"
 #include "plan_internal.hpp"
@@ -275,10 +277,27 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   const auto& comp_of = p.comp_of;
 
   detail::PhaseClock clk;
-  const auto comps = ordered_components(p, n);
+  // component order and member lists depend only on the partition: side by side
+  // (the second one's parallel loops find the pool busy and spawn their threads)
+  std::vector<VertexId> comps;
+  std::exception_ptr side_error;
+  std::thread side([&] {
+    try {
+      comps = ordered_components(p, n);
+    } catch (...) {
+      side_error = std::current_exception();
+    }
+  });
   std::vector<std::int64_t> mb;
   std::vector<VertexId> mem;
-  component_members(p, mb, mem);
+  try {
+    component_members(p, mb, mem);
+  } catch (...) {
+    side.join();
+    throw;
+  }
+  side.join();
+  if (side_error) std::rethrow_exception(side_error);
 
   std::vector<std::vector<VertexId>> singles;
   const auto plan = plan_units(p, comps, small_threshold, L.level_unit_begin, singles, mb, mem);
