@@ -37,64 +37,115 @@ namespace {
     }                                                                                              \
   } while (0)
 
-// Host -> device copy of a large pageable array (the layout's index arrays are
-// GBs of std::vector storage): the runtime stages such a copy through its own
-// pinned buffer with one thread (~10 GB/s); here four threads fill 32 MB pinned
-// buffers in turn while the previous ones are on the wire (PCIe 5: ~55 GB/s).
-// Small copies and failures to get pinned memory take the plain path.
-static cudaError_t h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  constexpr size_t kChunk = size_t{32} << 20;
-  constexpr int kBufs = 4, kThreads = 4;
-  if (bytes < 2 * kChunk) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
-  struct Stage {
-    void* buf[kBufs] = {};
-    cudaEvent_t ev[kBufs] = {};
-    bool ok = false;
-    Stage() {
-      for (int i = 0; i < kBufs; ++i)
-        if (cudaHostAlloc(&buf[i], kChunk, cudaHostAllocPortable) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
-          cudaGetLastError();
-          return;
-        }
-      ok = true;
-    }
-  };
-  static std::mutex mu;  // one staged copy at a time (the buffers are shared by every context of a device)
-  std::lock_guard<std::mutex> lock(mu);
+// Copies between large pageable host arrays and the device (the layout's index
+// arrays, a caller's std::vector of weights or ranks): the runtime stages such a
+// copy through its own pinned buffer with one thread (~10 GB/s); here four
+// threads move 32 MB pinned buffers in turn while the neighbouring ones are on
+// the wire (PCIe 5: ~55 GB/s).  Small copies, pinned callers and failures to get
+// pinned memory take the plain path.
+namespace {
+constexpr size_t kStageChunk = size_t{32} << 20;
+constexpr int kStageBufs = 4, kStageThreads = 4;
+struct Stage {
+  void* buf[kStageBufs] = {};
+  cudaEvent_t ev[kStageBufs] = {};
+  bool ok = false;
+  Stage() {
+    for (int i = 0; i < kStageBufs; ++i)
+      if (cudaHostAlloc(&buf[i], kStageChunk, cudaHostAllocPortable) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+      }
+    ok = true;
+  }
+};
+std::mutex g_stage_mu;  // one staged copy at a time (the buffers are shared by every context of a device)
+// the current device's staging buffers (events belong to the device that created them); call under g_stage_mu
+Stage* stage_for_device() {
   constexpr int kMaxDev = 64;
-  static std::unique_ptr<Stage> stages[kMaxDev];  // events belong to the device that created them
+  static std::unique_ptr<Stage> stages[kMaxDev];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev)
-    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
   if (!stages[dev]) stages[dev] = std::make_unique<Stage>();
-  Stage& st = *stages[dev];
-  if (!st.ok) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  return stages[dev]->ok ? stages[dev].get() : nullptr;
+}
+void parallel_memcpy(void* dst, const void* src, size_t len) {
+  std::thread th[kStageThreads - 1];
+  const size_t piece = (len + kStageThreads - 1) / kStageThreads;
+  for (int t = 1; t < kStageThreads; ++t)
+    th[t - 1] = std::thread([=] {
+      const size_t lo = std::min(len, piece * t), hi = std::min(len, piece * (t + 1));
+      std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+    });
+  std::memcpy(dst, src, std::min(len, piece));
+  for (auto& t : th) t.join();
+}
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+static cudaError_t h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes < 2 * kStageChunk || host_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  std::lock_guard<std::mutex> lock(g_stage_mu);
+  Stage* st = stage_for_device();
+  if (!st) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
   const char* from = static_cast<const char*>(src);
   char* to = static_cast<char*>(dst);
   cudaError_t e = cudaSuccess;
   size_t i = 0;
-  for (size_t off = 0; off < bytes && e == cudaSuccess; off += kChunk, ++i) {
-    const int b = static_cast<int>(i % kBufs);
-    const size_t len = std::min(kChunk, bytes - off);
-    if (i >= kBufs && (e = cudaEventSynchronize(st.ev[b])) != cudaSuccess) break;
-    std::thread th[kThreads - 1];
-    const size_t piece = (len + kThreads - 1) / kThreads;
-    for (int t = 1; t < kThreads; ++t)
-      th[t - 1] = std::thread([&, t] {
-        const size_t lo = std::min(len, piece * t), hi = std::min(len, piece * (t + 1));
-        std::memcpy(static_cast<char*>(st.buf[b]) + lo, from + off + lo, hi - lo);
-      });
-    std::memcpy(st.buf[b], from + off, std::min(len, piece));
-    for (auto& t : th) t.join();
-    if ((e = cudaMemcpyAsync(to + off, st.buf[b], len, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
-    e = cudaEventRecord(st.ev[b], s);
+  for (size_t off = 0; off < bytes && e == cudaSuccess; off += kStageChunk, ++i) {
+    const int b = static_cast<int>(i % kStageBufs);
+    const size_t len = std::min(kStageChunk, bytes - off);
+    if (i >= kStageBufs && (e = cudaEventSynchronize(st->ev[b])) != cudaSuccess) break;
+    parallel_memcpy(st->buf[b], from + off, len);
+    if ((e = cudaMemcpyAsync(to + off, st->buf[b], len, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+    e = cudaEventRecord(st->ev[b], s);
   }
   // the buffers may be reused by another stream next: drain them before unlocking
-  for (int b = 0; b < kBufs && i > 0; ++b) {
-    const cudaError_t w = cudaEventSynchronize(st.ev[b]);
+  for (int b = 0; b < kStageBufs && b < static_cast<int>(i); ++b) {
+    const cudaError_t w = cudaEventSynchronize(st->ev[b]);
     if (e == cudaSuccess && w != cudaSuccess) e = w;
   }
+  return e;
+}
+
+// device -> pageable host, complete on return
+static cudaError_t d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  auto plain = [&] {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+  };
+  if (bytes < 2 * kStageChunk || host_pinned(dst)) return plain();
+  std::lock_guard<std::mutex> lock(g_stage_mu);
+  Stage* st = stage_for_device();
+  if (!st) return plain();
+  const char* from = static_cast<const char*>(src);
+  char* to = static_cast<char*>(dst);
+  const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
+  cudaError_t e = cudaSuccess;
+  auto drain = [&](size_t j) {  // chunk j: wait for its copy, then move it out of the pinned buffer
+    const int b = static_cast<int>(j % kStageBufs);
+    if ((e = cudaEventSynchronize(st->ev[b])) != cudaSuccess) return;
+    const size_t off = j * kStageChunk;
+    parallel_memcpy(to + off, st->buf[b], std::min(kStageChunk, bytes - off));
+  };
+  for (size_t i = 0; i < nchunks && e == cudaSuccess; ++i) {
+    if (i >= kStageBufs) drain(i - kStageBufs);  // frees buffer i % kStageBufs
+    if (e != cudaSuccess) break;
+    const int b = static_cast<int>(i % kStageBufs);
+    const size_t off = i * kStageChunk;
+    if ((e = cudaMemcpyAsync(st->buf[b], from + off, std::min(kStageChunk, bytes - off), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+    e = cudaEventRecord(st->ev[b], s);
+  }
+  for (size_t j = nchunks > kStageBufs ? nchunks - kStageBufs : 0; j < nchunks && e == cudaSuccess; ++j) drain(j);
+  if (e != cudaSuccess) cudaStreamSynchronize(s);
   return e;
 }
 
@@ -1709,14 +1760,19 @@ lr_status lr_solve(lr_ctx* ctx, const double* w, double c, double tol, double* r
   }
   LR_CUDA_TRY(cudaSetDevice(ctx->device));
   const size_t bytes = static_cast<size_t>(ctx->n) * sizeof(double);
-  if (bytes) LR_CUDA_TRY(cudaMemcpyAsync(ctx->w.p, w, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (bytes) LR_CUDA_TRY(h2d_async(ctx->w.p, w, bytes, ctx->stream));
   if (std::getenv("LR_PROBE_SYNC")) LR_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   const lr_status st = solve_on_device(ctx, ctx->w.p, c, tol, ctx->r3.p, ctx->r1.p, info, unit_iters);
   if (st != LR_OK && st != LR_ENOCONV && st != LR_EDEGEN) return st;
   if (bytes) {
-    LR_CUDA_TRY(cudaMemcpyAsync(r3, ctx->r3.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    if (r1) LR_CUDA_TRY(cudaMemcpyAsync(r1, ctx->r1.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    LR_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (host_pinned(r3) && (!r1 || host_pinned(r1))) {
+      LR_CUDA_TRY(cudaMemcpyAsync(r3, ctx->r3.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      if (r1) LR_CUDA_TRY(cudaMemcpyAsync(r1, ctx->r1.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      LR_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    } else {
+      LR_CUDA_TRY(d2h_sync(r3, ctx->r3.p, bytes, ctx->stream));
+      if (r1) LR_CUDA_TRY(d2h_sync(r1, ctx->r1.p, bytes, ctx->stream));
+    }
   }
   return st;
 }

@@ -43,3 +43,9 @@ print("H2D w", wall(lambda: wd.copy_(wh, non_blocking=True)))
 print("D2H r3", wall(lambda: r3h.copy_(r3d, non_blocking=True)))
 info = eng.solve_ptr(wd.data_ptr(), r3d.data_ptr(), r1d.data_ptr(), False, p)
 print("info", info)
+# pageable host buffers (what a std::vector or numpy caller passes): staged through
+# pinned buffers by lr_solve (LR_LIB pointing at an older build shows the plain path)
+wp = np.full(n, 1.0 / n)
+r3p = np.empty(n)
+print("host solve r3 only, pinned (wall)", wall(lambda: eng.solve_ptr(wh.data_ptr(), r3h.data_ptr(), 0, True, p)))
+print("host solve r3 only, pageable (wall)", wall(lambda: eng.solve_ptr(wp.ctypes.data, r3p.ctypes.data, 0, True, p)))
