@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
 #include <thread>
 #include <vector>
 
@@ -214,9 +215,22 @@ class SccFinder {
       fw_ok = bfs(pivot, alive, fw, false);
       bw_ok = fw_ok && bfs(pivot, alive, bw, true);
     } else {
-      std::thread back([&] { bw_ok = bfs(pivot, alive, bw, true); });
-      fw_ok = bfs(pivot, alive, fw, false);
+      std::exception_ptr back_error;
+      std::thread back([&] {
+        try {
+          bw_ok = bfs(pivot, alive, bw, true);
+        } catch (...) {
+          back_error = std::current_exception();
+        }
+      });
+      try {
+        fw_ok = bfs(pivot, alive, fw, false);
+      } catch (...) {
+        back.join();
+        throw;
+      }
       back.join();
+      if (back_error) std::rethrow_exception(back_error);
     }
     if (!fw_ok || !bw_ok) return;
     giant_ = pivot;
