@@ -205,9 +205,16 @@ lr_status lr_plan_build(const lr_graph* gp, int32_t small_threshold, lr_plan** o
     auto plan = std::make_unique<lr_plan>();
     plan->g = &gp->g;
     plan->threshold = small_threshold;
-    detail::InEdges in;
-    plan->p = detail::find_components_with_in_edges(gp->g, nullptr, in);
-    plan->L = detail::build_layout_from(gp->g, plan->p, small_threshold, in);
+    if (std::getenv("LR_PLAN_PLAIN") != nullptr) {
+      // the public two-call path (own transpose in the layout, every edge's
+      // components looked up): what tests compare the shared-in-edge path with
+      plan->p = find_components(gp->g);
+      plan->L = build_layout(gp->g, plan->p, small_threshold);
+    } else {
+      detail::InEdges in;
+      plan->p = detail::find_components_with_in_edges(gp->g, nullptr, in);
+      plan->L = detail::build_layout_from(gp->g, plan->p, small_threshold, in);
+    }
     *out = plan.release();
   });
 }

@@ -212,3 +212,45 @@ def test_oracle_on_config_golden(lr, oracle):
         res = oracle.graph_from_csr(g.n, off, tgt).compute_pagerank(np.full(g.n, 1.0 / g.n), 0.85, 1e-12, 100)
         assert np.array_equal(res.unit_iters, z[f"cfg{cfg}_unit_iters"])
         np.testing.assert_allclose(res.ranks, z[f"cfg{cfg}_ranks"], rtol=1e-13)
+
+
+def test_layout_shared_in_edges_equals_plain_path(lr, monkeypatch):
+    """The plan's fast path (the partition's in-edge lists and cross-edge bits
+    shared with the layout, giant-SCC shortcuts) against the public two-call
+    path (find_components + build_layout: own transpose, every edge's
+    components looked up) on graphs with a giant SCC, kept and ignored
+    self-loops, trees and chains around it: every layout array equal."""
+    rng = np.random.default_rng(2024)
+    for t in range(8):
+        n = int(rng.integers(30_000, 80_000))
+        m = int(n * rng.uniform(1.0, 3.0))
+        src = rng.integers(0, n, m)
+        dst = np.where(rng.random(m) < 0.6, np.minimum(src + rng.integers(1, 8, m), n - 1), rng.integers(0, n, m))
+        if t % 4 != 3:  # a dense core: one giant SCC with edges in and out of it
+            k = n // (2 + t % 3)
+            src = np.concatenate([src, rng.integers(0, k, 5 * n)])
+            dst = np.concatenate([dst, rng.integers(0, k, 5 * n)])
+            # a hub, so the partition takes its reachability route for the giant SCC
+            hub = rng.integers(0, k, 600)
+            src = np.concatenate([src, np.zeros(300, np.int64), hub[300:]])
+            dst = np.concatenate([dst, hub[:300], np.zeros(300, np.int64)])
+        if t % 2 == 0:
+            loops = rng.integers(0, n, n // 20)
+            src, dst = np.concatenate([src, loops]), np.concatenate([dst, loops])
+        keep = t % 4 in (0, 1)
+        g = lr.Graph.from_edges(n, src=src.astype(np.int32), dst=dst.astype(np.int32), loop_policy=int(keep))
+        th = [100, 2, 100_000][t % 3]
+        monkeypatch.delenv("LR_PLAN_PLAIN", raising=False)
+        fast = lr.Plan(g, th).layout()
+        monkeypatch.setenv("LR_PLAN_PLAIN", "1")
+        plain = lr.Plan(g, th).layout()
+        monkeypatch.delenv("LR_PLAN_PLAIN", raising=False)
+        assert fast.keys() == plain.keys()
+        for k in fast:
+            a, b = fast[k], plain[k]
+            if isinstance(a, np.ndarray):
+                assert np.array_equal(a, b), (t, k)
+            else:
+                assert a == b, (t, k)
+        if t % 4 != 3:
+            assert (fast["unit_kind"] == 3).any() or th == 100_000
