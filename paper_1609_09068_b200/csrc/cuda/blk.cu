@@ -22,13 +22,13 @@ namespace {
 
 // warp per row: key = (row block << sbits) | source row in the unit
 __global__ void k_blk_keys(const long long* __restrict__ iptr, const int* __restrict__ isrc, long long e_begin, int u0,
-                           int R, int BR, int sbits, unsigned long long* __restrict__ keys,
+                           int row0, int R, int BR, int sbits, unsigned long long* __restrict__ keys,
                            unsigned short* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
   const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   for (long long r = w0; r < R; r += nw) {
-    const long long g = u0 + r;
+    const long long g = row0 + r;
     const long long a = iptr[g], b = iptr[g + 1];
     const unsigned long long hi = static_cast<unsigned long long>(r / BR) << sbits;
     const unsigned short d = static_cast<unsigned short>(r % BR);
@@ -44,7 +44,7 @@ __global__ void k_blk_keys(const long long* __restrict__ iptr, const int* __rest
 // the work is split by slots, not by blocks).  With slack > 0 every `slack`
 // instruction rows (32 slots each) of entries are followed by one empty row of
 // dummies (src 0, dst BR): free slots near every entry for k_blk_banks.
-__global__ void k_blk_pack(const long long* __restrict__ iptr, long long e_begin, int u0, int R, int BR,
+__global__ void k_blk_pack(const long long* __restrict__ iptr, long long e_begin, int row0, int R, int BR,
                            const long long* __restrict__ pad_off, int nb, unsigned long long smask,
                            const unsigned long long* __restrict__ keys, const unsigned short* __restrict__ vals,
                            unsigned* __restrict__ esrc, unsigned short* __restrict__ edst, int slack) {
@@ -58,7 +58,7 @@ __global__ void k_blk_pack(const long long* __restrict__ iptr, long long e_begin
       else hi = mid;
     }
     const int r0 = lo * BR, r1 = min(R, r0 + BR);
-    const long long s0 = iptr[u0 + r0] - e_begin, cnt = iptr[u0 + r1] - iptr[u0 + r0];
+    const long long s0 = iptr[row0 + r0] - e_begin, cnt = iptr[row0 + r1] - iptr[row0 + r0];
     long long j = i - pad_off[lo];  // slot in the block's run -> entry of the sorted run, or -1
     if (slack > 0) {
       const long long row = j >> 5, period = slack + 1;
@@ -279,11 +279,11 @@ int bits_for(long long v) {
 
 }  // namespace
 
-cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long e_begin, long long E, int u0, int R,
-                              int BR, const std::vector<long long>& pad_off, int slack, int win, unsigned* esrc,
-                              unsigned short* edst, cudaStream_t s) {
+cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long e_begin, long long E, int u0, int UR,
+                              int row0, int R, int BR, const std::vector<long long>& pad_off, int slack, int win,
+                              unsigned* esrc, unsigned short* edst, cudaStream_t s) {
   const int nb = static_cast<int>(pad_off.size()) - 1;
-  const int sbits = std::max(1, bits_for(R));
+  const int sbits = std::max(1, bits_for(UR));
   const int end_bit = sbits + std::max(1, bits_for(nb));
   unsigned long long *k0 = nullptr, *k1 = nullptr;
   long long* poff = nullptr;
@@ -313,7 +313,7 @@ cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long 
   if ((e = cudaMemcpyAsync(poff, pad_off.data(), pad_off.size() * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return done(e);
   if (E > 0) {
-    k_blk_keys<<<1184, 256, 0, s>>>(iptr, isrc, e_begin, u0, R, BR, sbits, k0, v0);
+    k_blk_keys<<<1184, 256, 0, s>>>(iptr, isrc, e_begin, u0, row0, R, BR, sbits, k0, v0);
     cub::DoubleBuffer<unsigned long long> kb(k0, k1);
     cub::DoubleBuffer<unsigned short> vb(v0, v1);
     if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<std::int64_t>(E), 0, end_bit,
@@ -323,10 +323,10 @@ cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long 
     if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<std::int64_t>(E), 0, end_bit, s)) !=
         cudaSuccess)
       return done(e);
-    k_blk_pack<<<2368, 256, 0, s>>>(iptr, e_begin, u0, R, BR, poff, nb, (1ull << sbits) - 1, kb.Current(),
+    k_blk_pack<<<2368, 256, 0, s>>>(iptr, e_begin, row0, R, BR, poff, nb, (1ull << sbits) - 1, kb.Current(),
                                     vb.Current(), esrc, edst, slack);
   } else {
-    k_blk_pack<<<2368, 256, 0, s>>>(iptr, e_begin, u0, R, BR, poff, nb, (1ull << sbits) - 1, k0, v0, esrc, edst,
+    k_blk_pack<<<2368, 256, 0, s>>>(iptr, e_begin, row0, R, BR, poff, nb, (1ull << sbits) - 1, k0, v0, esrc, edst,
                                     slack);
   }
   if (win > 0) {  // windows never straddle blocks

@@ -207,6 +207,7 @@ struct LevelTasks {
   long long hot_rows = 0, unit_rows = 0;
   int keep_stream = 0;  // L2 priority of the streamed SpMV operands (spmv.cu policy_stream)
   int blk = -1;         // K5: index into lr_ctx::blk (the level's one grid unit by dest-row blocks), or -1
+  std::vector<int> blk_chunks;  // row-sharded: the same per exchange chunk of this rank's shard (-1: K4c)
   // multi-GPU, large levels: rows split over the ranks for the CTA-solved
   // units (world + 1 bounds; empty = every rank solves the whole level)
   std::vector<int> dist_bounds;
@@ -655,32 +656,31 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     return v ? std::atoi(v) : dflt;
   };
   const char* e_on = std::getenv("LR_BLK");
-  if ((e_on && std::atoi(e_on) == 0) || ctx->comm || !spmv_seg()) return LR_OK;
+  if ((e_on && std::atoi(e_on) == 0) || !spmv_seg()) return LR_OK;
   const char* e_min = std::getenv("LR_BLK_MIN_ROWS");
   const long long min_rows = e_min ? std::atoll(e_min) : (1ll << 21);
   const char* e_br = std::getenv("LR_BLK_ROWS");
   const int BR = std::max(32, std::min(e_br ? std::atoi(e_br) : 16384, (kMaxDynSmem / 8) - 64));
   int sms = 0;
   LR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  for (LevelTasks& T : ctx->lt) {
-    if (T.gu1 - T.gu0 != 1) continue;
-    const int u = gstate[static_cast<size_t>(T.gu0)].unit;
-    const int u0 = L->unit_row_begin[u], R = L->unit_row_begin[u + 1] - u0;
-    if (R < min_rows || R <= 0) continue;
-    const long long e_begin = L->iptr[u0], E = L->iptr[u0 + R] - e_begin;
-    // sparse units (config 3's whole-graph baseline: 5.6 in-edges per row) have too
-    // few entries per block for the sorted gathers to share lines: K4c
-    if (E < static_cast<long long>(env_int("LR_BLK_MIN_DEG", 8)) * R) continue;
+  // slots of a block's run: its entries in rows of 32 (one K5 gather
+  // instruction), one empty row after every `slack` rows (free slots for the
+  // bank balance), padded to whole chunks
+  const int slack = std::max(0, env_int("LR_BLK_SLACK", kBlkSlack));
+  int win = env_int("LR_BLK_BANKS", 1) == 0 ? 0 : env_int("LR_BLK_WIN", kBlkWindow);
+  if (win != 0 && win != 256 && win != 1024 && win != 2048 && win != 4096 && win != 8192) win = kBlkWindow;
+  // the layout of dest rows [row0, row0 + R) of the unit [u0, u0 + UR): its index
+  // in ctx->blk, or -1 when the device has no room for it (the layout and its
+  // build -- sort keys, double buffers: ~20 B per in-edge of scratch -- may not
+  // fit next to a graph close to the HBM capacity: those rows keep K4c, which
+  // needs nothing beyond the CSR)
+  auto build_rows = [&](int u0, int UR, int row0, int R, int& index) -> lr_status {
+    index = -1;
+    const long long e_begin = L->iptr[row0], E = L->iptr[row0 + R] - e_begin;
     const int nb = static_cast<int>((static_cast<long long>(R) + BR - 1) / BR);
-    // slots of a block's run: its entries in rows of 32 (one K5 gather
-    // instruction), one empty row after every `slack` rows (free slots for the
-    // bank balance), padded to whole chunks
-    const int slack = std::max(0, env_int("LR_BLK_SLACK", kBlkSlack));
-    int win = env_int("LR_BLK_BANKS", 1) == 0 ? 0 : env_int("LR_BLK_WIN", kBlkWindow);
-    if (win != 0 && win != 256 && win != 1024 && win != 2048 && win != 4096 && win != 8192) win = kBlkWindow;
     std::vector<long long> pad_off(static_cast<size_t>(nb) + 1, 0);
     for (int b = 0; b < nb; ++b) {
-      const long long cnt = L->iptr[u0 + std::min(R, (b + 1) * BR)] - L->iptr[u0 + b * BR];
+      const long long cnt = L->iptr[row0 + std::min(R, (b + 1) * BR)] - L->iptr[row0 + b * BR];
       long long rows = (cnt + 31) / 32;
       if (slack > 0 && rows > 0) rows += (rows - 1) / slack;
       const long long slots = rows * 32;
@@ -704,9 +704,6 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
     }
     // heaviest parts first: the launch's tail is made of the light ones
     std::stable_sort(parts.begin(), parts.end(), [](const BlkPart& x, const BlkPart& y) { return x.n > y.n; });
-    // the layout and its build (sort keys, double buffers: ~20 B per in-edge of
-    // scratch) may not fit next to a graph close to the HBM capacity: that unit
-    // keeps K4c, which needs nothing beyond the CSR
     auto U = std::make_unique<lr_ctx::BlkUnit>();
     auto build = [&]() -> cudaError_t {
       cudaError_t e;
@@ -717,25 +714,56 @@ static lr_status build_blk_units(lr_ctx* ctx, const lr_layout* L, const std::vec
       if ((e = U->bcnt.alloc(static_cast<size_t>(nslots))) != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(U->yacc.p, 0, U->yacc.bytes(), s)) != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(U->bcnt.p, 0, U->bcnt.bytes(), s)) != cudaSuccess) return e;
-      return build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, R, BR, pad_off, slack, win, U->esrc.p,
-                               U->edst.p, s);
+      return build_blk_entries(ctx->iptr.p, ctx->isrc.p, e_begin, E, u0, UR, row0, R, BR, pad_off, slack, win,
+                               U->esrc.p, U->edst.p, s);
     };
     if (const cudaError_t e = build(); e == cudaErrorMemoryAllocation) {
       cudaGetLastError();  // cleared: not sticky
       cudaStreamSynchronize(s);
-      continue;
+      return LR_OK;
     } else {
       LR_CUDA_TRY(e);
     }
-    U->dev = BlkUnitDev{U->esrc.p, U->edst.p, U->parts.p, static_cast<int>(parts.size()), u0, R, BR, U->yacc.p,
-                        U->bcnt.p};
-    T.blk = static_cast<int>(ctx->blk.size());
+    U->dev = BlkUnitDev{U->esrc.p, U->edst.p, U->parts.p, static_cast<int>(parts.size()), u0, UR, row0, R, BR,
+                        U->yacc.p, U->bcnt.p};
+    index = static_cast<int>(ctx->blk.size());
     ctx->blk.push_back(std::move(U));
+    return LR_OK;
+  };
+  for (LevelTasks& T : ctx->lt) {
+    T.blk = -1;
+    T.blk_chunks.clear();
+    if (T.gu1 - T.gu0 != 1) continue;
+    const int u = gstate[static_cast<size_t>(T.gu0)].unit;
+    const int u0 = L->unit_row_begin[u], R = L->unit_row_begin[u + 1] - u0;
+    if (R < min_rows || R <= 0) continue;
+    const long long E = L->iptr[u0 + R] - L->iptr[u0];
+    // sparse units (config 3's whole-graph baseline: 5.6 in-edges per row) have too
+    // few entries per block for the sorted gathers to share lines: K4c
+    if (E < static_cast<long long>(env_int("LR_BLK_MIN_DEG", 8)) * R) continue;
+    bool any = false;
+    if (!ctx->comm) {
+      if (const lr_status bs = build_rows(u0, R, u0, R, T.blk); bs != LR_OK) return bs;
+      any = T.blk >= 0;
+    } else {
+      // row-sharded: one layout per exchange chunk of this rank's shard (a chunk is
+      // one launch, so that its s' rows can travel while the next chunk computes)
+      const std::vector<int>& cuts = ctx->gu_cuts[static_cast<size_t>(T.gu0)];
+      for (int xc = 0; xc < ctx->xchunks; ++xc) {
+        const int c0 = cuts[static_cast<size_t>(ctx->shard * ctx->xchunks + xc)];
+        const int c1 = cuts[static_cast<size_t>(ctx->shard * ctx->xchunks + xc) + 1];
+        int idx = -1;
+        if (c1 > c0)
+          if (const lr_status bs = build_rows(u0, R, c0, c1 - c0, idx); bs != LR_OK) return bs;
+        T.blk_chunks.push_back(idx);
+        any = any || idx >= 0;
+      }
+    }
     // K5 streams its indices evict-first and gathers the pushed vector block after
     // block: a larger evict-last window than K4c's pays (measured at config 5:
     // 0 / 0.3 / 0.6 / 0.85 / 1.0 / 1.3 / 1.6 / 2.0 / 3.0 of L2 -> 4311 / 4978 /
     // 5276 / 5419 / 5451 / 5472 / 5484 / 5479 / 5462 GB/s)
-    if (std::getenv("LR_L2_HOT_FRAC") == nullptr) {
+    if (any && std::getenv("LR_L2_HOT_FRAC") == nullptr) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
       T.hot_rows = std::min<long long>(T.unit_rows, static_cast<long long>(1.6 * l2 / 16.0));
@@ -1292,10 +1320,15 @@ static lr_status chunked_iteration(lr_ctx* ctx, const LevelTasks& T, const Devic
   const std::vector<int>& cuts = ctx->gu_cuts[static_cast<size_t>(T.gu0)];
   for (int j = 0; j < C; ++j) {
     const int b0 = T.bk0 + T.chunk_bk[static_cast<size_t>(j)], b1 = T.bk0 + T.chunk_bk[static_cast<size_t>(j) + 1];
-    launch_grid_iter(L, ctx->blocks.p + b0, ctx->meta.p ? ctx->meta.p + static_cast<size_t>(b0) * 32 : nullptr, b1 - b0,
-                     T.gu0, 1, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p, ctx->heavy_cnt.p, ctx->params.p,
-                     ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p, ctx->status.p, T.hot_begin, T.hot_rows,
-                     T.unit_rows, T.keep_stream, ctx->maxbuf.p, s, j < C - 1 ? 1 : 0);
+    if (static_cast<size_t>(j) < T.blk_chunks.size() && T.blk_chunks[static_cast<size_t>(j)] >= 0)
+      launch_spmv_blk(ctx->blk[static_cast<size_t>(T.blk_chunks[static_cast<size_t>(j)])]->dev, T.gu0, ctx->gstate.p,
+                      ctx->params.p, ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p, ctx->status.p, T.hot_begin,
+                      T.hot_rows, T.unit_rows, s, ctx->maxbuf.p, j < C - 1 ? 1 : 0);
+    else
+      launch_grid_iter(L, ctx->blocks.p + b0, ctx->meta.p ? ctx->meta.p + static_cast<size_t>(b0) * 32 : nullptr, b1 - b0,
+                       T.gu0, 1, ctx->gstate.p, ctx->heavy.p, ctx->heavy_part.p, ctx->heavy_cnt.p, ctx->params.p,
+                       ctx->pf.p, ctx->rank.p, sin, sout, ctx->unit_iters.p, ctx->status.p, T.hot_begin, T.hot_rows,
+                       T.unit_rows, T.keep_stream, ctx->maxbuf.p, s, j < C - 1 ? 1 : 0);
     ++launches;
     LR_CUDA_TRY(cudaEventRecord(ctx->xev[static_cast<size_t>(j)], s));
     LR_CUDA_TRY(cudaStreamWaitEvent(ctx->xstream, ctx->xev[static_cast<size_t>(j)], 0));

@@ -300,9 +300,11 @@ struct BlkUnitDev {
   const unsigned short* edst;
   const BlkPart* parts;
   int nparts;
-  int u0;  // first row of the unit
-  int R;   // rows of the unit
-  int BR;  // rows per block
+  int u0;    // first row of the unit (sources are unit-relative)
+  int UR;    // rows of the unit
+  int row0;  // first dest row of this layout (u0, or a shard chunk's first row)
+  int R;     // dest rows of this layout
+  int BR;    // rows per block
   double* yacc;  // [split blocks][BR]
   int* bcnt;     // [split blocks]
 };
@@ -310,12 +312,15 @@ struct BlkUnitDev {
 // [e_begin, e_begin + E)) sorted by (block, source): block b's run lands at
 // pad_off[b] (host array, NB + 1 entries, multiples of kBlkChunk), one empty row
 // of 32 slots after every `slack` rows, bank-balanced in windows of `win` slots
-cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long e_begin, long long E, int u0, int R,
-                              int BR, const std::vector<long long>& pad_off, int slack, int win, unsigned* esrc,
-                              unsigned short* edst, cudaStream_t s);
+// (row0, R: the dest rows; u0, UR: the unit, whose rows the sources index)
+cudaError_t build_blk_entries(const long long* iptr, const int* isrc, long long e_begin, long long E, int u0, int UR,
+                              int row0, int R, int BR, const std::vector<long long>& pad_off, int slack, int win,
+                              unsigned* esrc, unsigned short* edst, cudaStream_t s);
+// maxbuf / hold: the row-sharded protocol of launch_grid_iter
 void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
                      double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                     int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s);
+                     int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s, double* maxbuf = nullptr,
+                     int hold = 0);
 
 constexpr int kOutBlock = 1024;  // rows per partial sum of the R1 normalisation
 

@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     k_spmv_blk(BlkUnitDev B, int gu, GridUnitState* gs, const SolveParams* __restrict__ p,
                const double* __restrict__ pf, double* __restrict__ rank, const double* __restrict__ s_in,
                double* __restrict__ s_out, long long* unit_iters, DevStatus* st, int hot_begin, unsigned hot_bytes,
-               unsigned unit_bytes) {
+               unsigned unit_bytes, double* maxbuf, int hold) {
   constexpr int kW = kBlkThreads / 32;
   extern __shared__ double y[];  // [BR + 1]
   __shared__ int s_part;
@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   const unsigned ubr = static_cast<unsigned>(B.BR);
   double lmax = 0.0;
   auto finish_row = [&](int r, double v) {
-    const long long g = static_cast<long long>(B.u0) + r;
+    const long long g = static_cast<long long>(B.row0) + r;
     // rank and pf pass through once per iteration: first out of L2
     double rk;
     asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(rk) : "l"(rank + g), "l"(stream));
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         double v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          LR_DCHECK(j[k] < static_cast<unsigned>(B.R) && d[k] <= static_cast<unsigned>(B.BR));
+          LR_DCHECK(j[k] < static_cast<unsigned>(B.UR) && d[k] <= static_cast<unsigned>(B.BR));
           v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
         }
         const int cn = c + kW * kBlkChunk;
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         double v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          LR_DCHECK(j[k] < static_cast<unsigned>(B.R) && d[k] <= static_cast<unsigned>(B.BR));
+          LR_DCHECK(j[k] < static_cast<unsigned>(B.UR) && d[k] <= static_cast<unsigned>(B.BR));
           v[k] = ld_blk_gather<GATHER_L1>(sb + j[k], keep);
         }
 #pragma unroll
@@ -852,7 +852,15 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   if (s_last && threadIdx.x == 0) {
     __threadfence();
     st->next_task = 0;
-    finish_iteration(gs, gu, 1, p, unit_iters, st);
+    if (hold) {  // an earlier chunk of a chunked (multi-GPU) iteration: the maximum keeps accumulating
+      st->ctas_done = 0;
+    } else if (maxbuf) {  // row-sharded: publish the shard max, decide after the all-reduce
+      maxbuf[gu] = bitsd(atomicAdd(&gs[gu].max_bits, 0ull));
+      gs[gu].max_bits = 0ull;
+      st->ctas_done = 0;
+    } else {
+      finish_iteration(gs, gu, 1, p, unit_iters, st);
+    }
   }
 }
 
@@ -974,7 +982,7 @@ void launch_grid_iter(const DeviceLayout& L, const SpmvBlock* tasks, const unsig
 // slower, 3,924 vs 3,952); LR_BLK_PIPE=0 drops the index prefetch.
 void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const SolveParams* p, const double* pf,
                      double* rank, const double* s_in, double* s_out, long long* unit_iters, DevStatus* st,
-                     int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s) {
+                     int hot_begin, long long hot_rows, long long unit_rows, cudaStream_t s, double* maxbuf, int hold) {
   const char* e_l1 = std::getenv("LR_BLK_L1");
   const bool l1 = !(e_l1 && std::atoi(e_l1) == 0);
   const char* e_pipe = std::getenv("LR_BLK_PIPE");
@@ -998,7 +1006,7 @@ void launch_spmv_blk(const BlkUnitDev& B, int gu, GridUnitState* gs, const Solve
   const unsigned hot_bytes = static_cast<unsigned>(hot_rows * 8), unit_bytes = static_cast<unsigned>(unit_rows * 8);
   auto kern = l1 ? (pipe ? k_spmv_blk<1, 1> : k_spmv_blk<1, 0>) : (pipe ? k_spmv_blk<0, 1> : k_spmv_blk<0, 0>);
   kern<<<grid, kBlkThreads, smem, s>>>(B, gu, gs, p, pf, rank, s_in, s_out, unit_iters, st, hot_begin, hot_bytes,
-                                       unit_bytes);
+                                       unit_bytes, maxbuf, hold);
 }
 
 void launch_grid_zero_max(double* maxbuf, int gu0, int ngu, cudaStream_t s) {

@@ -87,3 +87,25 @@ def test_blk_baseline(lr, oracle, monkeypatch, br, part):
     assert res.report["total_iterations"] == rrep["total_iterations"]
     rel = np.abs(res.ranks - ref) / np.maximum(np.abs(ref), 1e-300)
     assert rel.max() <= 1e-10, rel.max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("br,chunks", [(512, 1), (512, 4), (4000, 3), (256, 7)])
+def test_blk_sharded_single_rank(lr, monkeypatch, br, chunks):
+    """K5 in the row-sharded (multi-GPU) path: one layout per exchange chunk of
+    the rank's shard, maxima held until the last chunk and published for the
+    all-reduce -- on a one-rank communicator, against the unsharded K4c solve."""
+    g = lr.config_graph(2, 4)
+    w = np.full(g.n, 1.0 / g.n)
+    monkeypatch.setenv("LR_BLK", "0")
+    r3a, r1a, _, ita = lr.Engine(g).solve(w, lr.SolverParams(0.85, 1e-12))
+    _force(monkeypatch, br, 0)
+    monkeypatch.setenv("LR_XCHG_CHUNKS", str(chunks))
+    eng = lr.Engine(g, rank=0, world=1, nccl_id=lr.nccl_unique_id())
+    assert eng.blk_units() == chunks
+    r3b, r1b, info, itb = eng.solve(w, lr.SolverParams(0.85, 1e-12))
+    assert np.array_equal(ita, itb)
+    assert np.max(np.abs(r3a - r3b) / r3a) <= 1e-13
+    assert np.max(np.abs(r1a - r1b) / r1a) <= 1e-13
+    r3c, _, _, itc = eng.solve(w, lr.SolverParams(0.85, 1e-12))  # a second solve on the same context
+    assert np.array_equal(itb, itc) and np.max(np.abs(r3c - r3b) / r3b) <= 1e-13
