@@ -162,7 +162,7 @@ class SccFinder {
     });
     std::vector<std::int32_t> cur = next.take();
     while (!cur.empty()) {
-      for (const VertexId v : cur) label_[static_cast<std::size_t>(v)] = v;
+      for_items(cur, [&](int, VertexId v) { label_[static_cast<std::size_t>(v)] = v; }, 1 << 16);
       for_items(cur, [&](int th, VertexId v) {
         auto& out = next.parts[static_cast<std::size_t>(th)];
         for (EdgeId k = a_.off[v]; k < a_.off[v + 1]; ++k) {
@@ -187,11 +187,25 @@ class SccFinder {
   void reach_giant() {
     std::int64_t best = -1;
     VertexId pivot = -1;
-    for (VertexId v = 0; v < n_; ++v)
-      if (live(v)) {
-        const std::int64_t s = static_cast<std::int64_t>(din_[static_cast<std::size_t>(v)]) * dout_[static_cast<std::size_t>(v)];
-        if (s > best) best = s, pivot = v;
-      }
+    {  // the first live vertex of largest din * dout (per-thread candidates over ascending ranges, merged in order)
+      const int T = host_threads();
+      std::vector<std::int64_t> tb(static_cast<std::size_t>(T), -1);
+      std::vector<VertexId> tp(static_cast<std::size_t>(T), -1);
+      parallel_chunks(n_, [&](int th, std::int64_t b, std::int64_t e) {
+        std::int64_t lb = -1;
+        VertexId lp = -1;
+        for (std::int64_t vv = b; vv < e; ++vv) {
+          const VertexId v = static_cast<VertexId>(vv);
+          if (!live(v)) continue;
+          const std::int64_t s = static_cast<std::int64_t>(din_[static_cast<std::size_t>(v)]) * dout_[static_cast<std::size_t>(v)];
+          if (s > lb) lb = s, lp = v;
+        }
+        tb[static_cast<std::size_t>(th)] = lb;
+        tp[static_cast<std::size_t>(th)] = lp;
+      });
+      for (int t = 0; t < T; ++t)
+        if (tb[static_cast<std::size_t>(t)] > best) best = tb[static_cast<std::size_t>(t)], pivot = tp[static_cast<std::size_t>(t)];
+    }
     // no hub (a deep DAG of small components, planted SCCs): Tarjan alone
     if (pivot < 0 || best < kMinHubDegreeProduct) return;
     const std::size_t nn = static_cast<std::size_t>(n_);
