@@ -310,6 +310,10 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
   std::vector<std::int64_t> unit_mem_begin(nu + 1, 0);  // into `umem`
   uvector<VertexId> umem(nn);
   {
+    // offsets first (one step per unit), then the members of every unit copied and
+    // numbered in parallel: small units several per task, the giant SCC and the
+    // levels' singleton groups (millions of members each) split over the threads
+    std::vector<const VertexId*> unit_src(nu);
     std::int64_t pos = 0;
     for (std::int32_t li = 0; li < nl; ++li)
       for (std::int32_t ui = L.level_unit_begin[static_cast<std::size_t>(li)];
@@ -317,22 +321,37 @@ Layout build_layout_impl(const Graph& g, const Partition& p, VertexId small_thre
         const UnitPlan& up = plan[static_cast<std::size_t>(ui)];
         unit_mem_begin[static_cast<std::size_t>(ui)] = pos;
         if (up.comp >= 0) {
-          for (std::int64_t j = mb[static_cast<std::size_t>(up.comp)]; j < mb[static_cast<std::size_t>(up.comp) + 1]; ++j)
-            umem[static_cast<std::size_t>(pos++)] = mem[static_cast<std::size_t>(j)];
+          unit_src[static_cast<std::size_t>(ui)] = mem.data() + mb[static_cast<std::size_t>(up.comp)];
+          pos += mb[static_cast<std::size_t>(up.comp) + 1] - mb[static_cast<std::size_t>(up.comp)];
         } else {
-          for (const VertexId v : singles[static_cast<std::size_t>(li)]) umem[static_cast<std::size_t>(pos++)] = v;
+          unit_src[static_cast<std::size_t>(ui)] = singles[static_cast<std::size_t>(li)].data();
+          pos += static_cast<std::int64_t>(singles[static_cast<std::size_t>(li)].size());
         }
       }
     unit_mem_begin[nu] = pos;
-  }
-  detail::parallel_chunks(static_cast<std::int64_t>(nu), [&](int, std::int64_t b, std::int64_t e) {
-    for (std::int64_t u = b; u < e; ++u)
-      for (std::int64_t j = unit_mem_begin[static_cast<std::size_t>(u)]; j < unit_mem_begin[static_cast<std::size_t>(u) + 1]; ++j) {
-        const VertexId v = umem[static_cast<std::size_t>(j)];
+    constexpr std::int64_t kBigUnit = 1 << 18;
+    auto fill = [&](std::int64_t u, std::int64_t j0, std::int64_t j1) {
+      const std::int64_t base = unit_mem_begin[static_cast<std::size_t>(u)];
+      const VertexId* src = unit_src[static_cast<std::size_t>(u)];
+      for (std::int64_t j = j0; j < j1; ++j) {
+        const VertexId v = src[j];
+        umem[static_cast<std::size_t>(base + j)] = v;
         unit_of[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(u);
-        local_of[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(j - unit_mem_begin[static_cast<std::size_t>(u)]);
+        local_of[static_cast<std::size_t>(v)] = static_cast<std::int32_t>(j);
       }
-  }, 1);
+    };
+    detail::parallel_dynamic(static_cast<std::int64_t>(nu), 256, [&](std::int64_t b, std::int64_t e) {
+      for (std::int64_t u = b; u < e; ++u) {
+        const std::int64_t m = unit_mem_begin[static_cast<std::size_t>(u) + 1] - unit_mem_begin[static_cast<std::size_t>(u)];
+        if (m <= kBigUnit) fill(u, 0, m);
+      }
+    });
+    for (std::size_t u = 0; u < nu; ++u) {
+      const std::int64_t m = unit_mem_begin[u + 1] - unit_mem_begin[u];
+      if (m > kBigUnit)
+        detail::parallel_chunks(m, [&](int, std::int64_t b, std::int64_t e) { fill(static_cast<std::int64_t>(u), b, e); });
+    }
+  }
 
   clk.mark("unit_of / local_of");
   // CAC units: Kahn pass of solve_cac (solvers.cpp:43-83) to get each vertex's
